@@ -1,0 +1,198 @@
+/*
+ * gosma_capi.h — the C ABI of the B200-native GOSMA bound-evaluation path.
+ *
+ * Plain C types only (pointers, sizes, doubles); no torch or CUDA types in the
+ * signatures (streams are passed as void*). Each entry point names the
+ * reference interface it replaces (paths relative to /root/reference/proj).
+ *
+ * Error behaviour mirrors the reference: invalid arguments return
+ * GOSMA_EINVAL (reference: std::invalid_argument), an empty feasible domain
+ * returns GOSMA_EINFEASIBLE (reference: InfeasiblePoseError), a solve that
+ * stopped on a budget with an incumbent returns GOSMA_EBUDGET (reference CLI
+ * exit code 3, tools/smalign_main.cpp:166); CUDA failures return >= 10. The
+ * message of the last failure on the calling thread is gosma_last_error().
+ * Infeasible branches are reported as {+inf, +inf}, not as errors
+ * (core/src/bounds.cpp:277-279).
+ */
+#ifndef GOSMA_CAPI_H
+#define GOSMA_CAPI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GOSMA_OK 0
+#define GOSMA_EINVAL 1
+#define GOSMA_EINFEASIBLE 2
+#define GOSMA_EBUDGET 3
+#define GOSMA_ECUDA 10
+#define GOSMA_ENOMEM 11
+
+typedef struct gosma_ctx gosma_ctx;
+
+/* One semantic class: the model GMM and the image vMF mixture, as the
+ * reference builds ObjectiveContext::ClassData from them
+ * (core/include/smalign/objective.hpp:19-31, core/src/objective.cpp:28-68).
+ * Arrays are caller-owned and deep-copied by gosma_ctx_create. */
+typedef struct gosma_class_view {
+  int n1;               /* model (GMM) components */
+  int n2;               /* image (vMF) components */
+  double class_weight;  /* SemanticClass::weight (mixtures.hpp:46-51) */
+  const double* mu;     /* 3*n1, component means */
+  const double* sigma2; /* n1, isotropic variances (> 0) */
+  const double* phi1;   /* n1, weights (sum 1 within 1e-9) */
+  const double* dir;    /* 3*n2, unit mean directions (|dir| within 1e-6 of 1) */
+  const double* kappa2; /* n2, concentrations (> 0) */
+  const double* phi2;   /* n2, weights (sum 1 within 1e-9) */
+} gosma_class_view;
+
+/* Search node: rotation cube x translation cuboid + inherited lower bound.
+ * Replaces smalign::BranchRegion (core/include/smalign/se3.hpp:38-45); the
+ * upper field of BranchRegion is output-only and not carried. 88 bytes. */
+typedef struct gosma_node {
+  double rc[3]; /* RotationCube::center (axis-angle) */
+  double rhw;   /* RotationCube::half_width */
+  double tc[3]; /* TranslationCuboid::center */
+  double thw[3];/* TranslationCuboid::half_widths */
+  double lower; /* BranchRegion::lower (parent floor; -inf for roots) */
+} gosma_node;
+
+/* Context flags. */
+#define GOSMA_CTX_SINGLE_MIXTURE 1u /* ObjectiveContext(Gmm, Vmfmm, zeta): one class of
+                                       weight 1, no class-weight closure check
+                                       (objective.cpp:103-107) */
+
+/* Replaces ObjectiveContext(const SemanticMixturePair&, double zeta)
+ * (objective.hpp:33-34, objective.cpp:103-121). Validates like the reference
+ * (zeta > 0, non-empty classes, weight closure 1e-9, sigma2 > 0, kappa > 0,
+ * weights >= 0, unit directions within 1e-6) and uploads the mixtures to
+ * `device` (FP64 master + FP32 working tables). */
+int gosma_ctx_create(int device, const gosma_class_view* classes, int n_classes, double zeta,
+                     unsigned flags, gosma_ctx** out);
+
+/* Replaces ObjectiveContext::blurred (objective.hpp:36-43, objective.cpp:70-101). */
+int gosma_ctx_blurred(const gosma_ctx* ctx, double w, double reference_distance,
+                      gosma_ctx** out);
+
+void gosma_ctx_destroy(gosma_ctx* ctx);
+
+/* ObjectiveContext::image_self_energy (objective.hpp:50-52). */
+double gosma_ctx_image_self_energy(const gosma_ctx* ctx);
+
+/* ObjectiveContext::zeta (objective.hpp:46). */
+double gosma_ctx_zeta(const gosma_ctx* ctx);
+
+/* Relative soundness margin subtracted from every lower bound, times the
+ * node's |term| mass. Default set at creation. */
+int gosma_ctx_set_lb_margin(gosma_ctx* ctx, double rel_margin);
+
+/* Replaces evaluate_branch_batch(ctx, branches, threads, skip_upper_at)
+ * (core/include/smalign/solver.hpp:87-95, core/src/solver.cpp:260-292) and,
+ * per element, evaluate_bounds (core/src/bounds.cpp:275-284). Host buffers;
+ * synchronous; results in input order and independent of launch geometry.
+ * split_rot (optional, may be NULL) receives subdivide_adaptive's choice for
+ * the node (1 rotation, 0 translation, -1 not splittable;
+ * core/src/se3.cpp:107-121). */
+int gosma_eval_bounds(gosma_ctx* ctx, const gosma_node* nodes, size_t n, double skip_upper_at,
+                      double* lower, double* upper, int8_t* split_rot);
+
+/* Same, with device-resident buffers, asynchronous on `stream`
+ * (cudaStream_t; NULL = the context's stream). */
+int gosma_eval_bounds_device(gosma_ctx* ctx, const gosma_node* d_nodes, size_t n,
+                             double skip_upper_at, double* d_lower, double* d_upper,
+                             int8_t* d_split_rot, void* stream);
+
+/* Translation-cached variant: the translation-only (self) terms are computed
+ * once per distinct translation cuboid (d_tindex[k] names node k's cuboid in
+ * d_tboxes = {tc[3], thw[3]} records) and reused; the reference adds self
+ * and cross terms separately (bounds.cpp:180) so results are identical up to
+ * FP32 summation order. */
+int gosma_eval_bounds_cached_device(gosma_ctx* ctx, const gosma_node* d_nodes, size_t n,
+                                    const int32_t* d_tindex, const double* d_tboxes,
+                                    size_t n_tboxes, double skip_upper_at, double* d_lower,
+                                    double* d_upper, int8_t* d_split_rot, void* stream);
+
+/* Host FP64 objective (objective.cpp:227-235); GOSMA_EINFEASIBLE when the
+ * pose violates the standoff (objective.cpp:160-166). */
+int gosma_objective_value(const gosma_ctx* ctx, const double r[3], const double t[3],
+                          double* value);
+
+/* Host FP64 analytic gradient d/dr, d/dt (objective.cpp:254-334). */
+int gosma_objective_gradient(const gosma_ctx* ctx, const double r[3], const double t[3],
+                             double g[6]);
+
+/* Pose domain (se3.hpp:32-36): one rotation cube, n_boxes translation
+ * cuboids as {center[3], half_widths[3]} records. */
+typedef struct gosma_domain {
+  double rot_center[3];
+  double rot_half_width;
+  const double* boxes;
+  int n_boxes;
+} gosma_domain;
+
+/* Local refinement (SMA) — local_refine (solver.hpp:80-85, solver.cpp:164-258). */
+int gosma_local_refine(const gosma_ctx* ctx, const double r0[3], const double t0[3],
+                       const gosma_domain* domain, double r_out[3], double t_out[3],
+                       double* value);
+
+/* Replaces SolverConfig (solver.hpp:14-37). Negative time_limit /
+ * max_evaluations / queue_capacity mean "unset". */
+typedef struct gosma_config {
+  double epsilon;
+  double zeta;
+  int batch_size;          /* nodes expanded per wave = batch_size / 8 (solver.cpp:648-649) */
+  double time_limit;
+  long long max_evaluations;
+  long long queue_capacity;
+  int threads;             /* host threads for SMA; 0 = hardware concurrency */
+  unsigned long long seed;
+  int wave_nodes;          /* GPU frontier: max nodes expanded per wave (0 = auto) */
+  int discovery_dive;      /* 1 = run the blurred-context dive (solver.cpp:449-595) */
+} gosma_config;
+
+#define GOSMA_STATUS_EPSILON_OPTIMAL 0
+#define GOSMA_STATUS_TIME_LIMIT 1
+#define GOSMA_STATUS_QUEUE_EXHAUSTED 2
+
+/* Replaces SolverReport (solver.hpp:64-73). */
+typedef struct gosma_report {
+  double best_r[3];
+  double best_t[3];
+  double best_value;
+  double global_lower;
+  double gap;
+  int status;
+  unsigned long long branches_expanded;
+  unsigned long long sma_invocations;
+  unsigned long long bound_evaluations;
+  double wall_time_seconds;
+  unsigned long long waves;
+} gosma_report;
+
+/* Per-wave trace callback (TraceEntry, solver.hpp:45-55). May be NULL. */
+typedef void (*gosma_trace_cb)(void* user, unsigned long long wave,
+                               unsigned long long bound_evaluations, double best_upper,
+                               double global_lower, unsigned long long queue_size,
+                               double unexplored_fraction, double pruned_fraction,
+                               double resolved_fraction);
+
+/* Replaces solve(ctx, domain, config) (solver.hpp:97-103, solver.cpp:312-688):
+ * GPU-resident best-first frontier, host SMA. */
+int gosma_solve(gosma_ctx* ctx, const gosma_domain* domain, const gosma_config* config,
+                gosma_report* report, gosma_trace_cb trace, void* user);
+
+const char* gosma_last_error(void);
+
+/* Build / device introspection for benches and tests. */
+int gosma_device_info(int device, int* sm_count, int* sm_clock_khz, int* cc_major,
+                      int* cc_minor);
+/* Number of bound-kernel launches issued by this process so far. */
+unsigned long long gosma_kernel_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GOSMA_CAPI_H */

@@ -1,0 +1,381 @@
+"""B200-native GOSMA bound evaluation — Python host mirror of the reference
+solver API (/root/reference/proj/core/include/smalign/*.hpp) over the C ABI
+in include/gosma_capi.h (libgosma.so, built in-tree by csrc/Makefile).
+
+There is no CPU fallback: importing this package without a built
+libgosma.so, or calling a compute entry point without a CUDA device, raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+__all__ = [
+    "GosmaError", "InfeasiblePoseError", "ObjectiveContext", "NODE_DTYPE", "make_nodes",
+    "evaluate_branch_batch", "evaluate_bounds", "objective_value", "objective_gradient",
+    "SolverConfig", "SolverReport", "PoseDomain", "solve", "local_refine", "lib", "library_path",
+    "kernel_launches",
+]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+library_path = os.path.join(_HERE, "libgosma.so")
+
+GOSMA_OK, GOSMA_EINVAL, GOSMA_EINFEASIBLE, GOSMA_EBUDGET = 0, 1, 2, 3
+
+
+class GosmaError(RuntimeError):
+    """A C-ABI failure (CUDA or internal)."""
+
+
+class InfeasiblePoseError(ValueError):
+    """Mirrors smalign::InfeasiblePoseError (errors.hpp:16-21)."""
+
+
+class _ClassView(C.Structure):
+    _fields_ = [("n1", C.c_int), ("n2", C.c_int), ("class_weight", C.c_double),
+                ("mu", C.POINTER(C.c_double)), ("sigma2", C.POINTER(C.c_double)),
+                ("phi1", C.POINTER(C.c_double)), ("dir", C.POINTER(C.c_double)),
+                ("kappa2", C.POINTER(C.c_double)), ("phi2", C.POINTER(C.c_double))]
+
+
+class _Domain(C.Structure):
+    _fields_ = [("rot_center", C.c_double * 3), ("rot_half_width", C.c_double),
+                ("boxes", C.POINTER(C.c_double)), ("n_boxes", C.c_int)]
+
+
+class _Config(C.Structure):
+    _fields_ = [("epsilon", C.c_double), ("zeta", C.c_double), ("batch_size", C.c_int),
+                ("time_limit", C.c_double), ("max_evaluations", C.c_longlong),
+                ("queue_capacity", C.c_longlong), ("threads", C.c_int),
+                ("seed", C.c_ulonglong), ("wave_nodes", C.c_int), ("discovery_dive", C.c_int)]
+
+
+class _Report(C.Structure):
+    _fields_ = [("best_r", C.c_double * 3), ("best_t", C.c_double * 3),
+                ("best_value", C.c_double), ("global_lower", C.c_double), ("gap", C.c_double),
+                ("status", C.c_int), ("branches_expanded", C.c_ulonglong),
+                ("sma_invocations", C.c_ulonglong), ("bound_evaluations", C.c_ulonglong),
+                ("wall_time_seconds", C.c_double), ("waves", C.c_ulonglong)]
+
+
+_TRACE_CB = C.CFUNCTYPE(None, C.c_void_p, C.c_ulonglong, C.c_ulonglong, C.c_double, C.c_double,
+                        C.c_ulonglong, C.c_double, C.c_double, C.c_double)
+
+_dp = C.POINTER(C.c_double)
+
+
+def _load():
+    if not os.path.exists(library_path):
+        raise ImportError(
+            f"{library_path} is missing: build it with `make -C {_HERE}/csrc` "
+            "(or __graft_entry__.build()); there is no CPU fallback")
+    lib = C.CDLL(library_path)
+    vp = C.c_void_p
+    lib.gosma_last_error.restype = C.c_char_p
+    lib.gosma_ctx_create.argtypes = [C.c_int, C.POINTER(_ClassView), C.c_int, C.c_double,
+                                     C.c_uint, C.POINTER(vp)]
+    lib.gosma_ctx_blurred.argtypes = [vp, C.c_double, C.c_double, C.POINTER(vp)]
+    lib.gosma_ctx_destroy.argtypes = [vp]
+    lib.gosma_ctx_image_self_energy.restype = C.c_double
+    lib.gosma_ctx_image_self_energy.argtypes = [vp]
+    lib.gosma_ctx_zeta.restype = C.c_double
+    lib.gosma_ctx_zeta.argtypes = [vp]
+    lib.gosma_ctx_set_lb_margin.argtypes = [vp, C.c_double]
+    lib.gosma_eval_bounds.argtypes = [vp, vp, C.c_size_t, C.c_double, _dp, _dp, vp]
+    lib.gosma_eval_bounds_device.argtypes = [vp, vp, C.c_size_t, C.c_double, vp, vp, vp, vp]
+    lib.gosma_eval_bounds_cached_device.argtypes = [vp, vp, C.c_size_t, vp, vp, C.c_size_t,
+                                                    C.c_double, vp, vp, vp, vp]
+    lib.gosma_objective_value.argtypes = [vp, _dp, _dp, _dp]
+    lib.gosma_objective_gradient.argtypes = [vp, _dp, _dp, _dp]
+    lib.gosma_local_refine.argtypes = [vp, _dp, _dp, C.POINTER(_Domain), _dp, _dp, _dp]
+    lib.gosma_solve.argtypes = [vp, C.POINTER(_Domain), C.POINTER(_Config), C.POINTER(_Report),
+                                _TRACE_CB, vp]
+    lib.gosma_device_info.argtypes = [C.c_int] + [C.POINTER(C.c_int)] * 4
+    lib.gosma_kernel_launches.restype = C.c_ulonglong
+    return lib
+
+
+lib = _load()
+
+
+def kernel_launches() -> int:
+    """Bound-kernel launches issued by this process (gpu_launches evidence)."""
+    return int(lib.gosma_kernel_launches())
+
+
+def _check(rc: int, what: str):
+    if rc == GOSMA_OK:
+        return
+    msg = lib.gosma_last_error().decode()
+    if rc == GOSMA_EINVAL:
+        raise ValueError(f"{what}: {msg}")
+    if rc == GOSMA_EINFEASIBLE:
+        raise InfeasiblePoseError(f"{what}: {msg}")
+    raise GosmaError(f"{what} failed ({rc}): {msg}")
+
+
+def _f64(a, shape=None):
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    return a.reshape(shape) if shape is not None else a
+
+
+# gosma_node / BranchRegion record (se3.hpp:38-45): 11 doubles.
+NODE_DTYPE = np.dtype([("rc", "<f8", 3), ("rhw", "<f8"), ("tc", "<f8", 3), ("thw", "<f8", 3),
+                       ("lower", "<f8")])
+
+
+def make_nodes(rc, rhw, tc, thw, lower=None) -> np.ndarray:
+    """Array of BranchRegion records (rotation cube x translation cuboid)."""
+    rc = np.atleast_2d(_f64(rc))
+    n = rc.shape[0]
+    out = np.empty(n, dtype=NODE_DTYPE)
+    out["rc"] = rc
+    out["rhw"] = np.broadcast_to(_f64(rhw), (n,))
+    out["tc"] = np.broadcast_to(_f64(tc), (n, 3))
+    out["thw"] = np.broadcast_to(_f64(thw), (n, 3))
+    out["lower"] = -np.inf if lower is None else np.broadcast_to(_f64(lower), (n,))
+    return out
+
+
+def _as_nodes(nodes) -> np.ndarray:
+    if isinstance(nodes, np.ndarray) and nodes.dtype == NODE_DTYPE:
+        return np.ascontiguousarray(nodes)
+    a = _f64(nodes)
+    if a.ndim == 1:
+        a = a.reshape(-1, 11)
+    if a.shape[-1] != 11:
+        raise ValueError("nodes must be NODE_DTYPE records or (n, 11) float64")
+    return np.ascontiguousarray(a).view(NODE_DTYPE).reshape(-1)
+
+
+class ObjectiveContext:
+    """Mirrors smalign::ObjectiveContext (objective.hpp:17-62).
+
+    ``classes`` is a sequence of dicts with keys mu (n1,3), sigma2 (n1),
+    phi1 (n1), dir (n2,3), kappa2 (n2), phi2 (n2) and optionally weight
+    (the SemanticMixturePair constructor). With ``single_mixture=True`` it is
+    the (Gmm, Vmfmm, zeta) constructor: one class of weight 1.
+    """
+
+    def __init__(self, classes: Sequence[dict], zeta: float, device: int = 0,
+                 single_mixture: bool = False):
+        self._keep = []
+        views = (_ClassView * len(classes))()
+        for k, c in enumerate(classes):
+            mu = _f64(c["mu"]).reshape(-1, 3)
+            dirs = _f64(c["dir"]).reshape(-1, 3)
+            arrs = [mu, _f64(c["sigma2"]), _f64(c["phi1"]), dirs, _f64(c["kappa2"]),
+                    _f64(c["phi2"])]
+            self._keep += arrs
+            views[k] = _ClassView(mu.shape[0], dirs.shape[0], float(c.get("weight", 1.0)),
+                                  *[a.ctypes.data_as(_dp) for a in arrs])
+        h = C.c_void_p()
+        _check(lib.gosma_ctx_create(device, views, len(classes), float(zeta),
+                                    1 if single_mixture else 0, C.byref(h)), "ObjectiveContext")
+        self._h = h
+        self.device = device
+        self.zeta = float(zeta)
+        self.classes = [dict(c) for c in classes]
+        self._keep = []
+
+    @classmethod
+    def _wrap(cls, handle, device, zeta, classes):
+        o = cls.__new__(cls)
+        o._h, o.device, o.zeta, o.classes, o._keep = handle, device, zeta, classes, []
+        return o
+
+    @classmethod
+    def from_mixture(cls, mix, device: int = 0):
+        """From a flat class-concatenated mixture (oracle.bind.Mixture layout:
+        n1, n2, class_weight, mu, sigma2, phi1, dir, kappa2, phi2, zeta)."""
+        classes, o1, o2 = [], 0, 0
+        for c in range(len(mix.n1)):
+            a, b = int(mix.n1[c]), int(mix.n2[c])
+            classes.append({"mu": mix.mu[o1:o1 + a], "sigma2": mix.sigma2[o1:o1 + a],
+                            "phi1": mix.phi1[o1:o1 + a], "dir": mix.dir[o2:o2 + b],
+                            "kappa2": mix.kappa2[o2:o2 + b], "phi2": mix.phi2[o2:o2 + b],
+                            "weight": float(mix.class_weight[c])})
+            o1, o2 = o1 + a, o2 + b
+        return cls(classes, mix.zeta, device=device, single_mixture=False)
+
+    def blurred(self, w: float, reference_distance: float) -> "ObjectiveContext":
+        """ObjectiveContext::blurred (objective.cpp:70-101)."""
+        h = C.c_void_p()
+        _check(lib.gosma_ctx_blurred(self._h, float(w), float(reference_distance), C.byref(h)),
+               "blurred")
+        return ObjectiveContext._wrap(h, self.device, self.zeta, self.classes)
+
+    @property
+    def image_self_energy(self) -> float:
+        return lib.gosma_ctx_image_self_energy(self._h)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def set_lb_margin(self, rel: float):
+        _check(lib.gosma_ctx_set_lb_margin(self._h, float(rel)), "set_lb_margin")
+
+    @property
+    def all_means(self) -> np.ndarray:
+        return np.concatenate([_f64(c["mu"]).reshape(-1, 3) for c in self.classes])
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib.gosma_ctx_destroy(h)
+            self._h = None
+
+
+def evaluate_branch_batch(ctx: ObjectiveContext, branches, threads: int = 0,
+                          skip_upper_at: float = float("inf"), return_split: bool = False):
+    """evaluate_branch_batch (solver.hpp:87-95): (lower, upper) per branch, in
+    input order. ``threads`` is accepted for signature parity and ignored (the
+    GPU decides its own launch geometry; results do not depend on it)."""
+    nodes = _as_nodes(branches)
+    n = nodes.shape[0]
+    lower = np.empty(n)
+    upper = np.empty(n)
+    split = np.empty(n, dtype=np.int8) if return_split else None
+    if n:
+        _check(lib.gosma_eval_bounds(ctx.handle, nodes.ctypes.data, n, float(skip_upper_at),
+                                     lower.ctypes.data_as(_dp), upper.ctypes.data_as(_dp),
+                                     split.ctypes.data if split is not None else None),
+               "evaluate_branch_batch")
+    return (lower, upper, split) if return_split else (lower, upper)
+
+
+def evaluate_bounds(ctx: ObjectiveContext, branch, skip_upper_at: float = float("inf")):
+    """evaluate_bounds (bounds.hpp:63-69) for one branch: (lower, upper)."""
+    lo, up = evaluate_branch_batch(ctx, [branch] if not isinstance(branch, np.ndarray)
+                                   else branch, skip_upper_at=skip_upper_at)
+    return float(lo[0]), float(up[0])
+
+
+def evaluate_branch_batch_device(ctx: ObjectiveContext, d_nodes_ptr: int, n: int,
+                                 d_lower_ptr: int, d_upper_ptr: int, d_split_ptr: int = 0,
+                                 skip_upper_at: float = float("inf"), stream: int = 0):
+    """Device-pointer variant (asynchronous on ``stream``)."""
+    _check(lib.gosma_eval_bounds_device(ctx.handle, d_nodes_ptr, n, float(skip_upper_at),
+                                        d_lower_ptr, d_upper_ptr, d_split_ptr or None,
+                                        stream or None), "evaluate_branch_batch_device")
+
+
+def evaluate_branch_batch_cached_device(ctx, d_nodes_ptr, n, d_tindex_ptr, d_tboxes_ptr,
+                                        n_tboxes, d_lower_ptr, d_upper_ptr, d_split_ptr=0,
+                                        skip_upper_at=float("inf"), stream=0):
+    """Translation-cached device variant (self terms once per cuboid)."""
+    _check(lib.gosma_eval_bounds_cached_device(ctx.handle, d_nodes_ptr, n, d_tindex_ptr,
+                                               d_tboxes_ptr, n_tboxes, float(skip_upper_at),
+                                               d_lower_ptr, d_upper_ptr, d_split_ptr or None,
+                                               stream or None),
+           "evaluate_branch_batch_cached_device")
+
+
+def objective_value(ctx: ObjectiveContext, r, t) -> float:
+    """objective_value (objective.hpp:79-82), host FP64."""
+    v = C.c_double()
+    _check(lib.gosma_objective_value(ctx.handle, _f64(r).ctypes.data_as(_dp),
+                                     _f64(t).ctypes.data_as(_dp), C.byref(v)), "objective_value")
+    return v.value
+
+
+def objective_gradient(ctx: ObjectiveContext, r, t) -> np.ndarray:
+    g = np.empty(6)
+    _check(lib.gosma_objective_gradient(ctx.handle, _f64(r).ctypes.data_as(_dp),
+                                        _f64(t).ctypes.data_as(_dp), g.ctypes.data_as(_dp)),
+           "objective_gradient")
+    return g
+
+
+@dataclass
+class PoseDomain:
+    """PoseDomain (se3.hpp:32-36): rotation cube + translation cuboids
+    ({center[3], half_widths[3]} rows)."""
+    rot_center: np.ndarray = field(default_factory=lambda: np.zeros(3))
+    rot_half_width: float = float(np.pi)
+    boxes: np.ndarray = field(default_factory=lambda: np.zeros((0, 6)))
+
+    def _c(self):
+        b = _f64(self.boxes).reshape(-1, 6)
+        d = _Domain()
+        for k in range(3):
+            d.rot_center[k] = float(self.rot_center[k])
+        d.rot_half_width = float(self.rot_half_width)
+        d.boxes = b.ctypes.data_as(_dp)
+        d.n_boxes = b.shape[0]
+        return d, b
+
+
+@dataclass
+class SolverConfig:
+    """SolverConfig (solver.hpp:14-37)."""
+    epsilon: float = 0.1
+    zeta: float = 0.5
+    batch_size: int = 1024
+    time_limit: Optional[float] = None
+    queue_capacity: Optional[int] = None
+    max_evaluations: Optional[int] = None
+    threads: int = 0
+    seed: int = 0
+    wave_nodes: int = 0
+    discovery_dive: bool = True
+
+
+@dataclass
+class SolverReport:
+    """SolverReport (solver.hpp:64-73)."""
+    r: np.ndarray
+    t: np.ndarray
+    best_value: float
+    global_lower: float
+    gap: float
+    status: str
+    branches_expanded: int
+    sma_invocations: int
+    bound_evaluations: int
+    wall_time_seconds: float
+    waves: int
+    trace: list
+
+
+_STATUS = {0: "epsilon_optimal", 1: "time_limit", 2: "queue_exhausted"}
+
+
+def local_refine(ctx: ObjectiveContext, r0, t0, domain: PoseDomain):
+    """local_refine (solver.hpp:80-85): (value, r, t)."""
+    d, keep = domain._c()
+    r, t, v = np.empty(3), np.empty(3), C.c_double()
+    _check(lib.gosma_local_refine(ctx.handle, _f64(r0).ctypes.data_as(_dp),
+                                  _f64(t0).ctypes.data_as(_dp), C.byref(d),
+                                  r.ctypes.data_as(_dp), t.ctypes.data_as(_dp), C.byref(v)),
+           "local_refine")
+    return v.value, r, t
+
+
+def solve(ctx: ObjectiveContext, domain: PoseDomain, config: SolverConfig) -> SolverReport:
+    """solve (solver.hpp:97-103) on the GPU-resident frontier."""
+    d, keep = domain._c()
+    cfg = _Config(config.epsilon, config.zeta, config.batch_size,
+                  -1.0 if config.time_limit is None else float(config.time_limit),
+                  -1 if config.max_evaluations is None else int(config.max_evaluations),
+                  -1 if config.queue_capacity is None else int(config.queue_capacity),
+                  config.threads, config.seed, config.wave_nodes, int(config.discovery_dive))
+    rep = _Report()
+    trace = []
+
+    def cb(_u, wave, evals, ub, lb, q, fu, fp, fr):
+        trace.append((wave, evals, ub, lb, q, fu, fp, fr))
+
+    ccb = _TRACE_CB(cb)
+    rc = lib.gosma_solve(ctx.handle, C.byref(d), C.byref(cfg), C.byref(rep), ccb, None)
+    if rc not in (GOSMA_OK, GOSMA_EBUDGET):
+        _check(rc, "solve")
+    return SolverReport(np.array(rep.best_r[:]), np.array(rep.best_t[:]), rep.best_value,
+                        rep.global_lower, rep.gap, _STATUS.get(rep.status, "?"),
+                        rep.branches_expanded, rep.sma_invocations, rep.bound_evaluations,
+                        rep.wall_time_seconds, rep.waves, trace)

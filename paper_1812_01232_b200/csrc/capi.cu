@@ -1,0 +1,422 @@
+// C ABI (include/gosma_capi.h): context construction, bound evaluation entry
+// points, host objective. The solver entry point lives in solver.cpp.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "capi_internal.hpp"
+#include "gosma_capi.h"
+
+namespace gosma {
+
+thread_local std::string g_last_error;
+
+int set_error(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+int cuda_error(cudaError_t e, const char* where) {
+  return set_error(GOSMA_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+namespace {
+
+bool weights_close(double sum) { return std::fabs(sum - 1.0) <= 1e-9; }
+
+template <typename T>
+cudaError_t upload(const std::vector<T>& h, T** d) {
+  *d = nullptr;
+  if (h.empty()) return cudaSuccess;
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(d), h.size() * sizeof(T));
+  if (e != cudaSuccess) return e;
+  return cudaMemcpy(*d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice);
+}
+
+double class_self_energy(const HostClass& c) {
+  // objective.cpp:55-64
+  double c2 = 0.0;
+  for (int j = 0; j < c.n2(); ++j)
+    for (int k = 0; k < c.n2(); ++k) {
+      const Vec3 s(c.b[3 * j] + c.b[3 * k], c.b[3 * j + 1] + c.b[3 * k + 1],
+                   c.b[3 * j + 2] + c.b[3 * k + 2]);
+      c2 += c.phi2[j] * c.phi2[k] * std::exp(log_z_eval(s.norm()) - c.log_z2[j] - c.log_z2[k]);
+    }
+  return c2;
+}
+
+double logw_host(double x) {
+  if (x > 30.0) return -std::log(x);
+  return log_z_eval(x) - x;
+}
+
+}  // namespace
+
+// Builds the device tables from the host model.
+int ctx_upload(gosma_ctx* ctx) {
+  const HostModel& hm = ctx->model;
+  std::vector<ClassSpan> spans;
+  std::vector<double> cls_w, mu, inv_s2, phi1, m;
+  std::vector<float> log_phi1, kappa2, e2;
+  int o1 = 0, o2 = 0, max_n1 = 0;
+  for (const HostClass& c : hm.classes) {
+    spans.push_back({o1, c.n1(), o2, c.n2()});
+    cls_w.push_back(c.weight);
+    max_n1 = std::max(max_n1, c.n1());
+    for (int i = 0; i < c.n1(); ++i) {
+      for (int a = 0; a < 3; ++a) mu.push_back(c.mu[3 * i + a]);
+      inv_s2.push_back(1.0 / c.sigma2[i]);
+      phi1.push_back(c.phi1[i]);
+      log_phi1.push_back(c.phi1[i] > 0.0 ? static_cast<float>(std::log(c.phi1[i]))
+                                         : kLogZeroWeight);
+    }
+    for (int j = 0; j < c.n2(); ++j) {
+      for (int a = 0; a < 3; ++a) m.push_back(c.b[3 * j + a] / c.kappa2[j]);
+      kappa2.push_back(static_cast<float>(c.kappa2[j]));
+      const double lp = c.phi2[j] > 0.0 ? std::log(c.phi2[j]) : -1e30;
+      e2.push_back(static_cast<float>((lp - logw_host(c.kappa2[j])) * 1.4426950408889634));
+    }
+    o1 += c.n1();
+    o2 += c.n2();
+  }
+  cudaError_t e;
+  DevCtx& d = ctx->dev;
+  d.n_classes = static_cast<int>(hm.classes.size());
+  d.n1_total = o1;
+  d.n2_total = o2;
+  d.max_n1 = max_n1;
+  d.zeta = hm.zeta;
+  d.lb_margin = ctx->lb_margin;
+  ClassSpan* dspans;
+  if ((e = upload(spans, &dspans)) != cudaSuccess) return cuda_error(e, "ctx upload");
+  d.cls = dspans;
+  double *dw, *dmu, *dis2, *dphi, *dm;
+  float *dlp, *dk2, *de2;
+  if ((e = upload(cls_w, &dw)) != cudaSuccess || (e = upload(mu, &dmu)) != cudaSuccess ||
+      (e = upload(inv_s2, &dis2)) != cudaSuccess || (e = upload(phi1, &dphi)) != cudaSuccess ||
+      (e = upload(m, &dm)) != cudaSuccess || (e = upload(log_phi1, &dlp)) != cudaSuccess ||
+      (e = upload(kappa2, &dk2)) != cudaSuccess || (e = upload(e2, &de2)) != cudaSuccess)
+    return cuda_error(e, "ctx upload");
+  d.cls_w = dw;
+  d.mu = dmu;
+  d.inv_s2 = dis2;
+  d.phi1 = dphi;
+  d.m = dm;
+  d.log_phi1 = dlp;
+  d.kappa2 = dk2;
+  d.e2 = de2;
+  ctx->owned = {dspans, dw, dmu, dis2, dphi, dm, dlp, dk2, de2};
+  if ((e = cudaMalloc(&ctx->d_work, sizeof(unsigned int))) != cudaSuccess)
+    return cuda_error(e, "ctx upload");
+  size_t smem = eval_smem_per_warp(d) * 4;
+  int max_optin = 0;
+  cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
+  if (smem > static_cast<size_t>(max_optin)) {
+    return set_error(GOSMA_EINVAL, "mixtures too large for the per-warp shared-memory tables (" +
+                                       std::to_string(smem) + " B per CTA)");
+  }
+  return GOSMA_OK;
+}
+
+void ctx_free_device(gosma_ctx* ctx) {
+  int cur = 0;
+  cudaGetDevice(&cur);
+  cudaSetDevice(ctx->device);
+  for (void* p : ctx->owned) cudaFree(p);
+  ctx->owned.clear();
+  if (ctx->d_work) cudaFree(ctx->d_work);
+  ctx->d_work = nullptr;
+  ctx->scratch.release();
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  ctx->stream = nullptr;
+  cudaSetDevice(cur);
+}
+
+void Scratch::release() {
+  if (d_nodes) cudaFree(d_nodes);
+  if (d_lower) cudaFree(d_lower);
+  if (d_upper) cudaFree(d_upper);
+  if (d_split) cudaFree(d_split);
+  if (h_pinned) cudaFreeHost(h_pinned);
+  d_nodes = nullptr;
+  d_lower = d_upper = nullptr;
+  d_split = nullptr;
+  h_pinned = nullptr;
+  cap = 0;
+}
+
+cudaError_t Scratch::reserve(size_t n) {
+  if (n <= cap) return cudaSuccess;
+  release();
+  size_t c = std::max<size_t>(n, 1024);
+  cudaError_t e;
+  if ((e = cudaMalloc(&d_nodes, c * sizeof(gosma_node))) != cudaSuccess) return e;
+  if ((e = cudaMalloc(&d_lower, c * sizeof(double))) != cudaSuccess) return e;
+  if ((e = cudaMalloc(&d_upper, c * sizeof(double))) != cudaSuccess) return e;
+  if ((e = cudaMalloc(&d_split, c * sizeof(int8_t))) != cudaSuccess) return e;
+  cap = c;
+  return cudaSuccess;
+}
+
+int validate_and_build(const gosma_class_view* classes, int n_classes, double zeta,
+                       unsigned flags, HostModel* out) {
+  // ObjectiveContext constructors (objective.cpp:28-68, 103-121) and the
+  // component invariants (sphere_stats.cpp:10-35, unit_vector.hpp:17-24).
+  if (!(zeta > 0.0)) return set_error(GOSMA_EINVAL, "ObjectiveContext: zeta must be > 0");
+  if (n_classes < 1 || classes == nullptr)
+    return set_error(GOSMA_EINVAL, "ObjectiveContext: no semantic classes");
+  const bool single = (flags & GOSMA_CTX_SINGLE_MIXTURE) != 0;
+  if (single && n_classes != 1)
+    return set_error(GOSMA_EINVAL, "GOSMA_CTX_SINGLE_MIXTURE needs exactly one class");
+  if (!single) {
+    double wsum = 0.0;
+    for (int c = 0; c < n_classes; ++c) wsum += classes[c].class_weight;
+    if (!weights_close(wsum))
+      return set_error(GOSMA_EINVAL, "ObjectiveContext class weights: weights sum to " +
+                                         std::to_string(wsum) + ", expected 1");
+  }
+  HostModel hm;
+  hm.zeta = zeta;
+  for (int c = 0; c < n_classes; ++c) {
+    const gosma_class_view& v = classes[c];
+    if (v.n1 < 1 || v.n2 < 1)
+      return set_error(GOSMA_EINVAL, "ObjectiveContext: class with empty mixture");
+    HostClass hc;
+    hc.weight = single ? 1.0 : v.class_weight;
+    double s1 = 0.0, s2 = 0.0;
+    for (int i = 0; i < v.n1; ++i) {
+      if (!(v.sigma2[i] > 0.0) || !std::isfinite(v.sigma2[i]))
+        return set_error(GOSMA_EINVAL, "IsotropicGaussian: variance must be positive");
+      if (!(v.phi1[i] >= 0.0) || !std::isfinite(v.phi1[i]))
+        return set_error(GOSMA_EINVAL, "IsotropicGaussian: weight must be non-negative");
+      for (int a = 0; a < 3; ++a) hc.mu.push_back(v.mu[3 * i + a]);
+      hc.sigma2.push_back(v.sigma2[i]);
+      hc.phi1.push_back(v.phi1[i]);
+      hm.all_means.emplace_back(v.mu[3 * i], v.mu[3 * i + 1], v.mu[3 * i + 2]);
+      s1 += v.phi1[i];
+    }
+    for (int j = 0; j < v.n2; ++j) {
+      const Vec3 d(v.dir[3 * j], v.dir[3 * j + 1], v.dir[3 * j + 2]);
+      const double n = d.norm();
+      if (!(std::fabs(n - 1.0) <= 1e-6))
+        return set_error(GOSMA_EINVAL, "UnitVector3: input norm deviates from 1 by more than 1e-6");
+      if (!(v.kappa2[j] > 0.0) || !std::isfinite(v.kappa2[j]))
+        return set_error(GOSMA_EINVAL, "VmfComponent: concentration must be positive");
+      if (!(v.phi2[j] >= 0.0) || !std::isfinite(v.phi2[j]))
+        return set_error(GOSMA_EINVAL, "VmfComponent: weight must be non-negative");
+      const Vec3 u = d / n;  // UnitVector3 renormalises (unit_vector.hpp:23)
+      for (int a = 0; a < 3; ++a) hc.b.push_back(v.kappa2[j] * u[a]);
+      hc.kappa2.push_back(v.kappa2[j]);
+      hc.log_z2.push_back(log_z_eval(v.kappa2[j]));
+      hc.phi2.push_back(v.phi2[j]);
+      s2 += v.phi2[j];
+    }
+    if (!weights_close(s1))
+      return set_error(GOSMA_EINVAL, "ObjectiveContext model: weights sum to " +
+                                         std::to_string(s1) + ", expected 1");
+    if (!weights_close(s2))
+      return set_error(GOSMA_EINVAL, "ObjectiveContext image: weights sum to " +
+                                         std::to_string(s2) + ", expected 1");
+    hc.self_energy = class_self_energy(hc);
+    hm.image_self_energy += hc.weight * hc.self_energy;
+    hm.classes.push_back(std::move(hc));
+  }
+  *out = std::move(hm);
+  return GOSMA_OK;
+}
+
+int ctx_from_model(int device, HostModel&& hm, gosma_ctx** out) {
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess) return cuda_error(e, "cudaGetDeviceCount");
+  if (device < 0 || device >= ndev)
+    return set_error(GOSMA_EINVAL, "device index " + std::to_string(device) + " out of range");
+  auto* ctx = new gosma_ctx();
+  ctx->device = device;
+  ctx->model = std::move(hm);
+  DeviceGuard g(device);
+  cudaDeviceProp prop;
+  if ((e = cudaGetDeviceProperties(&prop, device)) != cudaSuccess) {
+    delete ctx;
+    return cuda_error(e, "cudaGetDeviceProperties");
+  }
+  ctx->sm_count = prop.multiProcessorCount;
+  if ((e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking)) != cudaSuccess) {
+    delete ctx;
+    return cuda_error(e, "cudaStreamCreate");
+  }
+  const int rc = ctx_upload(ctx);
+  if (rc != GOSMA_OK) {
+    ctx_free_device(ctx);
+    delete ctx;
+    return rc;
+  }
+  *out = ctx;
+  return GOSMA_OK;
+}
+
+}  // namespace gosma
+
+using namespace gosma;
+
+extern "C" {
+
+const char* gosma_last_error(void) { return g_last_error.c_str(); }
+
+int gosma_ctx_create(int device, const gosma_class_view* classes, int n_classes, double zeta,
+                     unsigned flags, gosma_ctx** out) {
+  if (!out) return set_error(GOSMA_EINVAL, "out is null");
+  *out = nullptr;
+  HostModel hm;
+  const int rc = validate_and_build(classes, n_classes, zeta, flags, &hm);
+  if (rc != GOSMA_OK) return rc;
+  return ctx_from_model(device, std::move(hm), out);
+}
+
+int gosma_ctx_blurred(const gosma_ctx* src, double w, double reference_distance,
+                      gosma_ctx** out) {
+  // ObjectiveContext::blurred (objective.cpp:70-101)
+  if (!src || !out) return set_error(GOSMA_EINVAL, "null argument");
+  if (!(w >= 0.0) || !(reference_distance >= 0.0))
+    return set_error(GOSMA_EINVAL, "ObjectiveContext::blurred: negative width");
+  HostModel hm = src->model;
+  hm.image_self_energy = 0.0;
+  const double var_add = (w * reference_distance) * (w * reference_distance);
+  const double w2 = w * w;
+  for (HostClass& c : hm.classes) {
+    for (double& s2 : c.sigma2) s2 += var_add;
+    for (int j = 0; j < c.n2(); ++j) {
+      const Vec3 dir = Vec3(c.b[3 * j], c.b[3 * j + 1], c.b[3 * j + 2]) / c.kappa2[j];
+      const double k = c.kappa2[j] / (1.0 + c.kappa2[j] * w2);
+      c.kappa2[j] = k;
+      for (int a = 0; a < 3; ++a) c.b[3 * j + a] = k * dir[a];
+      c.log_z2[j] = log_z_eval(k);
+    }
+    c.self_energy = class_self_energy(c);
+    hm.image_self_energy += c.weight * c.self_energy;
+  }
+  const int rc = ctx_from_model(src->device, std::move(hm), out);
+  if (rc == GOSMA_OK) {
+    (*out)->lb_margin = src->lb_margin;
+    (*out)->dev.lb_margin = src->lb_margin;
+  }
+  return rc;
+}
+
+void gosma_ctx_destroy(gosma_ctx* ctx) {
+  if (!ctx) return;
+  ctx_free_device(ctx);
+  delete ctx;
+}
+
+double gosma_ctx_image_self_energy(const gosma_ctx* ctx) {
+  return ctx ? ctx->model.image_self_energy : NAN;
+}
+
+double gosma_ctx_zeta(const gosma_ctx* ctx) { return ctx ? ctx->model.zeta : NAN; }
+
+int gosma_ctx_set_lb_margin(gosma_ctx* ctx, double rel) {
+  if (!ctx || !(rel >= 0.0) || !(rel < 1e-2))
+    return set_error(GOSMA_EINVAL, "lb margin must be in [0, 1e-2)");
+  ctx->lb_margin = rel;
+  ctx->dev.lb_margin = rel;
+  return GOSMA_OK;
+}
+
+int gosma_eval_bounds_device(gosma_ctx* ctx, const gosma_node* d_nodes, size_t n, double skip,
+                             double* d_lower, double* d_upper, int8_t* d_split, void* stream) {
+  if (!ctx) return set_error(GOSMA_EINVAL, "null context");
+  if (n == 0) return GOSMA_OK;
+  if (!d_nodes || !d_lower || !d_upper) return set_error(GOSMA_EINVAL, "null buffer");
+  DeviceGuard g(ctx->device);
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+  EvalArgs a;
+  a.nodes = reinterpret_cast<const double*>(d_nodes);
+  a.n = static_cast<long long>(n);
+  a.skip_upper_at = skip;
+  a.lower = d_lower;
+  a.upper = d_upper;
+  a.split_rot = d_split;
+  a.work = static_cast<unsigned int*>(ctx->d_work);
+  const cudaError_t e = launch_eval_bounds(ctx->dev, a, ctx->sm_count, s);
+  if (e != cudaSuccess) return cuda_error(e, "eval_bounds launch");
+  return GOSMA_OK;
+}
+
+int gosma_eval_bounds(gosma_ctx* ctx, const gosma_node* nodes, size_t n, double skip,
+                      double* lower, double* upper, int8_t* split_rot) {
+  if (!ctx) return set_error(GOSMA_EINVAL, "null context");
+  if (n == 0) return GOSMA_OK;
+  if (!nodes || !lower || !upper) return set_error(GOSMA_EINVAL, "null buffer");
+  DeviceGuard g(ctx->device);
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  cudaError_t e;
+  // Chunked pipeline: H2D of chunk k+1 overlaps the bound kernel on chunk k.
+  const size_t chunk = std::min<size_t>(n, static_cast<size_t>(1) << 18);
+  if ((e = ctx->scratch.reserve(2 * chunk)) != cudaSuccess) return cuda_error(e, "scratch");
+  cudaStream_t s = ctx->stream;
+  for (size_t off = 0, k = 0; off < n; off += chunk, ++k) {
+    const size_t m = std::min(chunk, n - off);
+    const size_t slot = (k & 1) * chunk;
+    gosma_node* dn = ctx->scratch.d_nodes + slot;
+    if ((e = cudaMemcpyAsync(dn, nodes + off, m * sizeof(gosma_node), cudaMemcpyHostToDevice,
+                             s)) != cudaSuccess)
+      return cuda_error(e, "H2D nodes");
+    const int rc = gosma_eval_bounds_device(ctx, dn, m, skip, ctx->scratch.d_lower + slot,
+                                            ctx->scratch.d_upper + slot,
+                                            split_rot ? ctx->scratch.d_split + slot : nullptr, s);
+    if (rc != GOSMA_OK) return rc;
+    if ((e = cudaMemcpyAsync(lower + off, ctx->scratch.d_lower + slot, m * sizeof(double),
+                             cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(upper + off, ctx->scratch.d_upper + slot, m * sizeof(double),
+                             cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+      return cuda_error(e, "D2H bounds");
+    if (split_rot &&
+        (e = cudaMemcpyAsync(split_rot + off, ctx->scratch.d_split + slot, m * sizeof(int8_t),
+                             cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+      return cuda_error(e, "D2H split");
+  }
+  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_error(e, "eval_bounds");
+  return GOSMA_OK;
+}
+
+int gosma_objective_value(const gosma_ctx* ctx, const double r[3], const double t[3],
+                          double* value) {
+  if (!ctx || !r || !t || !value) return set_error(GOSMA_EINVAL, "null argument");
+  const Vec3 tv(t[0], t[1], t[2]);
+  if (!pose_feasible(ctx->model, tv))
+    return set_error(GOSMA_EINFEASIBLE, "pose within zeta of a component mean");
+  *value = objective_value(ctx->model, Vec3(r[0], r[1], r[2]), tv);
+  return GOSMA_OK;
+}
+
+int gosma_objective_gradient(const gosma_ctx* ctx, const double r[3], const double t[3],
+                             double g[6]) {
+  if (!ctx || !r || !t || !g) return set_error(GOSMA_EINVAL, "null argument");
+  if (!objective_gradient(ctx->model, Vec3(r[0], r[1], r[2]), Vec3(t[0], t[1], t[2]), g))
+    return set_error(GOSMA_EINFEASIBLE, "pose within zeta of a component mean");
+  return GOSMA_OK;
+}
+
+int gosma_device_info(int device, int* sm_count, int* sm_clock_khz, int* cc_major,
+                      int* cc_minor) {
+  cudaDeviceProp p;
+  const cudaError_t e = cudaGetDeviceProperties(&p, device);
+  if (e != cudaSuccess) return cuda_error(e, "cudaGetDeviceProperties");
+  if (sm_count) *sm_count = p.multiProcessorCount;
+  int clk = 0;
+  cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, device);
+  if (sm_clock_khz) *sm_clock_khz = clk;
+  if (cc_major) *cc_major = p.major;
+  if (cc_minor) *cc_minor = p.minor;
+  return GOSMA_OK;
+}
+
+unsigned long long gosma_kernel_launches(void) { return bound_kernel_launch_count(); }
+
+}  // extern "C"

@@ -1,0 +1,62 @@
+// The opaque gosma_ctx and helpers shared by the C-ABI translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "gosma_capi.h"
+#include "gosma_internal.hpp"
+#include "host_math.hpp"
+
+namespace gosma {
+
+// Reusable device buffers for the host-buffer entry point.
+struct Scratch {
+  gosma_node* d_nodes = nullptr;
+  double* d_lower = nullptr;
+  double* d_upper = nullptr;
+  int8_t* d_split = nullptr;
+  void* h_pinned = nullptr;
+  size_t cap = 0;
+  cudaError_t reserve(size_t n);
+  void release();
+};
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+// Default relative LB soundness margin (x |term| mass); see DESIGN.md.
+constexpr double kDefaultLbMargin = 2e-6;
+
+}  // namespace gosma
+
+struct gosma_ctx {
+  int device = 0;
+  int sm_count = 0;
+  gosma::HostModel model;
+  gosma::DevCtx dev{};
+  double lb_margin = gosma::kDefaultLbMargin;
+  std::vector<void*> owned;
+  void* d_work = nullptr;
+  cudaStream_t stream = nullptr;
+  gosma::Scratch scratch;
+  std::mutex mu;
+};
+
+namespace gosma {
+int set_error(int code, const std::string& msg);
+int cuda_error(cudaError_t e, const char* where);
+}  // namespace gosma

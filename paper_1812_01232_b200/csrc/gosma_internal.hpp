@@ -1,0 +1,84 @@
+// Internal types shared by the CUDA kernels and the host runtime.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "gosma_capi.h"
+
+namespace gosma {
+
+// log2(e): exponents are carried in log2 units so every exp is one MUFU.EX2.
+constexpr float kL2E = 1.4426950408889634f;
+// Margin below which a pair is dropped from the objective
+// (objective.cpp:17 kNegligibleExponentMargin).
+constexpr double kNegligibleMargin = 64.0;
+// log(phi) stand-in for zero weights: keeps 2^(e) exactly 0 without inf-inf.
+constexpr float kLogZeroWeight = -1.0e30f;
+
+// Per-class span of the pooled component tables.
+struct ClassSpan {
+  int o1, n1, o2, n2;
+};
+
+// Device view of an ObjectiveContext (objective.hpp:19-31), passed by value.
+// FP64 master copies feed the per-node prep (feasibility, kappa intervals,
+// projections); FP32 tables feed the pair loops.
+struct DevCtx {
+  int n_classes;
+  int n1_total;
+  int n2_total;
+  int max_n1;            // largest class n1 (self-loop sizing)
+  const ClassSpan* cls;  // n_classes
+  const double* cls_w;   // n_classes
+  const double* mu;      // 3*N1 component means
+  const double* inv_s2;  // N1, 1/sigma^2
+  const double* phi1;    // N1
+  const float* log_phi1; // N1 (kLogZeroWeight for 0)
+  const double* m;       // 3*N2, b_j / kappa_j (bounds.cpp:100)
+  const float* kappa2;   // N2
+  const float* e2;       // N2, (log phi2 - log W(kappa2)) * log2e
+  double zeta;
+  double lb_margin;      // relative soundness margin (x |term| mass)
+};
+
+// Host-side master copy of one class (ClassData, objective.hpp:19-31).
+struct HostClass {
+  double weight = 1.0;
+  std::vector<double> mu;      // 3*n1
+  std::vector<double> sigma2;  // n1
+  std::vector<double> phi1;    // n1
+  std::vector<double> b;       // 3*n2, kappa * unit direction
+  std::vector<double> kappa2;  // n2
+  std::vector<double> log_z2;  // n2
+  std::vector<double> phi2;    // n2
+  double self_energy = 0.0;
+  int n1() const { return static_cast<int>(sigma2.size()); }
+  int n2() const { return static_cast<int>(kappa2.size()); }
+};
+
+// Kernel entry points (bounds_kernel.cu).
+struct EvalArgs {
+  const double* nodes;   // 11 doubles per node (gosma_node)
+  long long n;
+  double skip_upper_at;
+  double* lower;
+  double* upper;
+  int8_t* split_rot;     // may be null
+  unsigned int* work;    // dynamic work counter (zeroed before launch)
+};
+
+cudaError_t launch_eval_bounds(const DevCtx& ctx, const EvalArgs& a, int sm_count,
+                               cudaStream_t stream);
+size_t eval_smem_per_warp(const DevCtx& ctx);
+unsigned long long bound_kernel_launch_count();
+
+// Host FP64 math (host_math.cpp) shared by SMA, the solver and the C ABI.
+double log_z_eval(double kappa);
+double log_z_deriv(double kappa);
+
+}  // namespace gosma
