@@ -1,0 +1,341 @@
+#!/usr/bin/env python
+"""GOSMA bound-evaluation benchmark (BASELINE.json configs[1]).
+
+One step = one wave of the hot path: evaluate the bounds (LB + UB, skip=+inf)
+of a fixed batch of rotation x translation sub-cubes resident in HBM, then
+(N > 1) exchange the best upper bound with an NCCL min-allreduce, as the
+frontier-sharded solver does every wave. Weak scaling: every rank owns its
+own batch of `--nodes` sub-cubes.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Under torchrun (N > 1) every rank runs one GPU; rank 0 prints one JSON line.
+`--impl reference` times the reference CPU implementation (oracle/_ref: the
+unmodified reference sources compiled in place) on the host cores, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "sub-cube bounds/sec"
+UNIT = "bounds/s"
+L2_FLUSH_BYTES = 256 << 20
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--nodes", type=int, default=1_000_000)
+    p.add_argument("--n1", type=int, default=64)
+    p.add_argument("--n2", type=int, default=32)
+    p.add_argument("--regime", default="realistic", choices=["realistic", "moderate"])
+    p.add_argument("--seed", type=int, default=2026)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=12.0,
+                   help="target CPU work for the cpu_baseline sample")
+    return p.parse_args()
+
+
+def workload_config(a, world):
+    from paper_1812_01232_b200 import synth
+    classes = synth.mixture(a.n1, a.n2, a.regime, seed=a.seed)
+    P = synth.pair_terms_per_node(classes)
+    cfg = {
+        "workload": (f"bound-kernel microbench (BASELINE configs[1]): {a.nodes} rotation x "
+                     f"translation sub-cubes per GPU, {a.n1} GMM x {a.n2} vMF components "
+                     f"(P={P} pair terms/node, LB+UB each), {a.regime} mixture regime, "
+                     "skip_upper_at=+inf; nodes: rotation octree levels 1-6 x torus_cover(3.5,0.5) "
+                     "boxes subdivided 0-3 levels"),
+        "nodes_per_step_per_gpu": a.nodes, "n_gmm": a.n1, "n_vmf": a.n2,
+        "pair_terms_per_node": P, "regime": a.regime, "seed": a.seed,
+        "l2": "flushed before every timed step (256 MiB write; inputs 88 MB < L2)",
+        "parallelism": f"frontier-sharded x{world} (weak), best-UB min-allreduce per step",
+    }
+    return classes, P, cfg
+
+
+class ClockSampler:
+    """NVML clocks / throttle reasons sampled during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001 — clocks are best-effort evidence
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.02)
+
+    def __enter__(self):
+        if self.nv:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        if self.nv:
+            self._stop.set()
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "note": "nvml unavailable"}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def cpu_reference_rate(classes, nodes_np, threads, target_s, max_nodes=None):
+    """Reference CPU evaluate_branch_batch (oracle/_ref) or the C port, on a
+    bounded sample: returns (nodes/s, kind, sample_desc, cores)."""
+    from oracle import bind
+    from paper_1812_01232_b200 import synth
+    mix = bind.Mixture(**synth.to_mixture_arrays(classes, 0.5))
+    arr = nodes_np.view(np.float64).reshape(-1, 11)
+    if bind.reference_available():
+        ev, kind = bind.Reference(mix), "reference"
+        run = lambda x: ev.eval_bounds(x, threads=threads)  # noqa: E731
+    else:
+        ev, kind = bind.Oracle(mix), "port"
+        run = lambda x: ev.eval_bounds(x, threads=threads)  # noqa: E731
+    probe = arr[: max(threads * 4, 32)]
+    t0 = time.perf_counter()
+    run(probe)
+    dt = time.perf_counter() - t0
+    n = int(min(len(arr), max(len(probe), target_s * len(probe) / max(dt, 1e-6))))
+    if max_nodes:
+        n = min(n, max_nodes)
+    t0 = time.perf_counter()
+    run(arr[:n])
+    dt = time.perf_counter() - t0
+    desc = (f"first {n} sub-cubes of the same seeded batch, evaluate_branch_batch("
+            f"threads={threads}, skip=+inf) via {'oracle/_ref (unmodified reference, -O3)' if kind == 'reference' else 'oracle C port'}")
+    return n / dt, kind, desc, threads, dt
+
+
+def run_reference_arm(a):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return 0
+    from paper_1812_01232_b200 import synth  # noqa: F401 (import-only; no GPU work)
+    classes, P, cfg = workload_config(a, world)
+    nodes_np = synth.nodes(a.nodes, seed=a.seed + 1)
+    threads = os.cpu_count() or 1
+    per_step = max(2.0, min(20.0, 150.0 / max(1, a.steps + a.warmup)))
+    rates = []
+    kind = desc = None
+    for s in range(a.warmup + a.steps):
+        r, kind, desc, cores, dt = cpu_reference_rate(classes, nodes_np, threads, per_step)
+        if s >= a.warmup:
+            rates.append(r)
+    value = statistics.median(rates)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * a.nodes / value,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": cfg,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
+                         "sample": desc},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "pair_terms_per_s": value * P,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        return run_reference_arm(a)
+
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+
+    import paper_1812_01232_b200 as g
+    from paper_1812_01232_b200 import synth
+
+    classes, P, cfg = workload_config(a, world)
+    ctx = g.ObjectiveContext(classes, 0.5, device=local)
+    nodes_np = synth.nodes(a.nodes, seed=a.seed + 1 + 7919 * rank)
+    n = a.nodes
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
+    s_ptr = stream.cuda_stream
+    d_nodes = torch.from_numpy(nodes_np.view(np.uint8)).to(dev)
+    d_lo = torch.empty(n, dtype=torch.float64, device=dev)
+    d_up = torch.empty(n, dtype=torch.float64, device=dev)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    best = torch.empty(1, dtype=torch.float64, device=dev)
+
+    def step(timed_events=None):
+        flush.fill_(1.0)
+        if timed_events is not None:
+            timed_events[0].record(stream)
+        g.evaluate_branch_batch_device(ctx, d_nodes.data_ptr(), n, d_lo.data_ptr(),
+                                       d_up.data_ptr(), 0, float("inf"), s_ptr)
+        if timed_events is not None:
+            timed_events[1].record(stream)
+        best.copy_(d_up.min().reshape(1))
+        if world > 1:
+            dist.all_reduce(best, op=dist.ReduceOp.MIN)
+
+    for _ in range(a.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # Pipe peaks at the clocks of this run (MEASURED_PEAKS.json lacks SFU/FMA).
+    mufu_peak, fma_peak = g.calibrate_pipes(local)
+
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(a.steps)]
+    launches0 = g.kernel_launches()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for k in range(a.steps):
+            step(kev[k])
+        e1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = g.kernel_launches() - launches0
+    total_ms = e0.elapsed_time(e1)
+    kern_ms = [s.elapsed_time(t) for s, t in kev]
+    t = torch.tensor([total_ms, statistics.mean(kern_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms, kern_avg_ms = float(t[0]), float(t[1])
+    ms_per_step = total_ms / a.steps
+    value = world * n * a.steps / (total_ms * 1e-3)
+
+    # Sanity: the batch produced finite bounds.
+    lo_h = d_lo.cpu().numpy()
+    assert np.isfinite(lo_h).mean() > 0.5, "bound kernel produced no finite lower bounds"
+
+    # ---- e2e through the public C-ABI call with pinned HOST buffers
+    h_nodes = torch.empty(n * 88, dtype=torch.uint8, pin_memory=True)
+    h_nodes.numpy()[:] = nodes_np.view(np.uint8)
+    h_lo = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    h_up = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    import ctypes as C
+    lo_p = C.cast(h_lo.data_ptr(), C.POINTER(C.c_double))
+    up_p = C.cast(h_up.data_ptr(), C.POINTER(C.c_double))
+
+    def e2e_step():
+        rc = g.lib.gosma_eval_bounds(ctx.handle, h_nodes.data_ptr(), n, float("inf"), lo_p, up_p,
+                                     None)
+        if rc:
+            raise RuntimeError(g.lib.gosma_last_error().decode())
+        return float(h_up.numpy().min())
+
+    for _ in range(2):
+        e2e_step()
+    e2e_steps = max(3, min(a.steps, 10))
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        e2e_step()
+    e2e_s = time.perf_counter() - t0
+    te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = world * n * e2e_steps / float(te[0])
+
+    if rank != 0:
+        dist.destroy_process_group()
+        return 0
+
+    sfu_ops = 8.0 * P * n  # algorithmic SFU ops per launch
+    achieved = sfu_ops / (kern_avg_ms * 1e-3)
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+        except Exception:  # noqa: BLE001
+            traffic = None
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": cfg,
+        "roofline": {"bound": "sfu", "achieved": achieved / 1e9, "peak": mufu_peak / 1e9,
+                     "unit": "Gop/s", "frac": achieved / mufu_peak, "traffic": traffic,
+                     "peak_source": "on-box MUFU ex2 microbenchmark (gosma_calibrate_pipes), "
+                                    "same run; MEASURED_PEAKS.json has no SFU figure",
+                     "algorithmic": "8 SFU ops per pair term (LB 2 sqrt+rcp+log+exp, UB "
+                                    "sqrt+log+exp) x P x nodes per launch",
+                     "kernel_ms": kern_avg_ms,
+                     "fma_peak_tflops": fma_peak / 1e12},
+        "pair_terms_per_s": value * P,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": n * 88,
+                "d2h_bytes_per_step": n * 16,
+                "path": "gosma_eval_bounds (C ABI, pinned host buffers, chunked H2D/kernel/D2H)"},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    if not a.no_cpu_baseline:
+        r, kind, desc, cores, dt = cpu_reference_rate(classes, nodes_np, os.cpu_count() or 1,
+                                                      a.cpu_seconds)
+        line["cpu_baseline"] = {"value": r, "unit": UNIT, "cores": cores, "kind": kind,
+                                "sample": desc, "seconds": dt}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

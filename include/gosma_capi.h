@@ -189,6 +189,9 @@ const char* gosma_last_error(void);
 /* Build / device introspection for benches and tests. */
 int gosma_device_info(int device, int* sm_count, int* sm_clock_khz, int* cc_major,
                       int* cc_minor);
+/* Pipe-throughput microbenchmarks (roofline denominators): MUFU (SFU/XU)
+ * ops/s and FP32 FMA flop/s measured on `device` at its current clocks. */
+int gosma_calibrate_pipes(int device, double* mufu_ops_per_s, double* fma_flops_per_s);
 /* Number of bound-kernel launches issued by this process so far. */
 unsigned long long gosma_kernel_launches(void);
 

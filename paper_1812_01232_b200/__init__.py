@@ -96,6 +96,7 @@ def _load():
                                 _TRACE_CB, vp]
     lib.gosma_device_info.argtypes = [C.c_int] + [C.POINTER(C.c_int)] * 4
     lib.gosma_kernel_launches.restype = C.c_ulonglong
+    lib.gosma_calibrate_pipes.argtypes = [C.c_int, _dp, _dp]
     return lib
 
 
@@ -105,6 +106,20 @@ lib = _load()
 def kernel_launches() -> int:
     """Bound-kernel launches issued by this process (gpu_launches evidence)."""
     return int(lib.gosma_kernel_launches())
+
+
+def calibrate_pipes(device: int = 0):
+    """(MUFU ops/s, FP32 FMA flop/s) measured on the device right now."""
+    m, f = C.c_double(), C.c_double()
+    _check(lib.gosma_calibrate_pipes(device, C.byref(m), C.byref(f)), "calibrate_pipes")
+    return m.value, f.value
+
+
+def device_info(device: int = 0):
+    sm, clk, ma, mi = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+    _check(lib.gosma_device_info(device, C.byref(sm), C.byref(clk), C.byref(ma), C.byref(mi)),
+           "device_info")
+    return {"sm_count": sm.value, "sm_clock_khz": clk.value, "cc": (ma.value, mi.value)}
 
 
 def _check(rc: int, what: str):

@@ -5,25 +5,32 @@
 //   feasibility scan (se3.cpp:94-100)
 //   + branch_lower_core (bounds.cpp:46-183)   -> lower (max'd with parent floor)
 //   + objective_value at feasible_center      -> upper (bounds.cpp:187-214,
-//     objective.cpp:175-235), skipped when lower >= skip_upper_at.
+//     objective.cpp:175-235), +inf when lower >= skip_upper_at.
 // plus subdivide_adaptive's split decision (se3.cpp:107-121), fused because
 // it reuses psi_trans.
 //
 // Work decomposition: one warp per node (persistent warps, dynamic node
 // counter). Lanes first build per-component tables for the node in shared
-// memory (FP64 prep, FP32 results), then sweep the pair terms:
-//   cross  (i, j): lane owns model row i, image column j is a smem broadcast;
-//   self   (i, j): circulant schedule (i, i+d mod n), conflict-free smem rows.
-// LB and UB contributions of a pair share the geometry and one reciprocal.
+// memory, then sweep the pair terms:
+//   cross (i, j): the lane owns model row i (registers), the image column j
+//                 is a shared-memory broadcast;
+//   self  (i, j): circulant schedule (i, i+d mod n) — every unordered pair
+//                 once, lanes read consecutive rows (conflict-free).
+// The LB and UB contributions of a pair share the geometry and one MUFU.RCP.
 //
 // Numerics: every pair ratio is evaluated in the
 // coupled log form the reference uses for its lower bound,
 //   log[Z(K)/(Z(a)Z(b))] = (K-a-b) + log W(K) - log W(a) - log W(b),
-// with the excess K-a-b = -2ab(1-cos)/(K+a+b) and 1-cos / 1+cos taken from
-// half-angle sines and cosines (|u-v|/2, |u+v|/2), which keeps FP32 accurate
-// at concentrations of 1e4-1e5 where log Z(K)-log Z(a)-log Z(b) would cancel
-// catastrophically. Terms are FP32 (MUFU ex2/rsqrt/rcp); per-lane partial sums
-// are flushed to FP64 every row; per-node sums are FP64 warp reductions.
+// with the excess K-a-b = -2ab(1-cos)/(K+a+b) and 1-cos, 1+cos taken from
+// half-angle sines/cosines (|u-v|/2, |u+v|/2 and their angle-addition
+// formulas). This keeps FP32 accurate at concentrations of 1e4-1e5, where
+// log Z(K) - log Z(a) - log Z(b) would cancel catastrophically. For K > 15,
+// W(K) = 1/K to FP32 precision, so exp(... + log W(K)) = 2^(...) * rsqrt(K^2):
+// a pair costs 7 MUFU ops (2 sqrt, 2 rsqrt, 1 rcp, 2 ex2). The rare exact
+// paths (K <= 15, the interior K minimum of the cross LB, the corner maximum
+// of the self LB when cos A < 0) run only for terms that survive FP32
+// underflow. Terms are FP32; per-row partial sums flush to FP64; per-node sums
+// are FP64 warp reductions.
 #include <cuda_runtime.h>
 
 #include <atomic>
@@ -40,6 +47,9 @@ std::atomic<unsigned long long> g_launches{0};
 
 constexpr int kWarpsPerCta = 4;
 constexpr unsigned kFull = 0xffffffffu;
+// Terms whose log2 value is below this flush to zero in FP32 (ftz) even with
+// the largest possible W factor (W <= 2), so their exact paths are skipped.
+constexpr float kNegligibleLog2 = -128.0f;
 
 __device__ __forceinline__ float ex2f(float x) {
   float y;
@@ -56,16 +66,23 @@ __device__ __forceinline__ float rsqf(float x) {
   asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+__device__ __forceinline__ float sqf(float x) {
+  float y;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 __device__ __forceinline__ float lg2f(float x) {
   float y;
   asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
 
-// log W(x) in log2 units, for x <= 15 (W(x) = (1 - e^{-2x})/x, bounds.cpp:18-37).
-// Series below 0.25 keeps relative accuracy where 1 - e^{-2x} cancels.
-__device__ __noinline__ float log2w_small(float x) {
-  float w;
+// log2 W(x) for any x >= 0 (W(x) = (1 - e^{-2x})/x, bounds.cpp:18-37;
+// log W = log_z_eval(x) - x, sphere_stats.cpp:47-56). Past 15 the e^{-2x}
+// correction is below FP32 resolution. The series below 0.25 keeps relative
+// accuracy where 1 - e^{-2x} cancels.
+__device__ __noinline__ float log2w(float x) {
+  if (x > 15.0f) return -lg2f(x);
   if (x < 0.25f) {
     // W/2 = 1 - x + 2x^2/3 - x^3/3 + 2x^4/15 - 2x^5/45 + 4x^6/315 - x^7/315 + 2x^8/2835
     float p = 2.0f / 2835.0f;
@@ -77,47 +94,20 @@ __device__ __noinline__ float log2w_small(float x) {
     p = fmaf(p, x, 2.0f / 3.0f);
     p = fmaf(p, x, -1.0f);
     p = fmaf(p, x, 1.0f);
-    w = 2.0f * p;
-    return lg2f(w);
+    return 1.0f + lg2f(p);
   }
   const float e = ex2f(-2.0f * kL2E * x);
   return lg2f(1.0f - e) - lg2f(x);
 }
 
-// FP64 log W(x) = log_z_eval(x) - x, or -log x past 30 (bounds.cpp:34-37,
-// sphere_stats.cpp:47-56).
-__device__ double logw_d(double x) {
-  if (x > 30.0) return -log(x);
-  double lz;
-  if (x < 1e-4) {
-    lz = log(2.0) + log1p(x * x / 6.0);
-  } else {
-    lz = x + log1p(-exp(-2.0 * x)) - log(x);
-  }
-  return lz - x;
+// Diagonal pair in closed form: phi^2 * (k/2) coth k (bounds.cpp:104-106,
+// objective.cpp:201-203); k >= 1 always, so 1 - e^{-2k} >= 0.86.
+__device__ __forceinline__ float diag_term(float phi, float k) {
+  const float e = ex2f(-2.0f * kL2E * k);
+  return phi * phi * 0.5f * k * (1.0f + e) * rcpf(1.0f - e);
 }
 
-// Half-angle coth term of the diagonal pair: phi^2 * k/2 * coth k
-// (bounds.cpp:104-106, objective.cpp:201-203). k >= 1 always.
-__device__ __forceinline__ double diag_term(double phi, double k) {
-  double c;
-  if (k > 20.0) {
-    c = 1.0;  // coth(20) = 1 + 8.5e-18, below double resolution
-  } else {
-    const double e = exp(-2.0 * k);
-    c = (1.0 + e) / (1.0 - e);
-  }
-  return phi * phi * 0.5 * k * c;
-}
-
-__device__ __forceinline__ double dnorm3(double x, double y, double z) {
-  // Same evaluation order as the reference (x*x + y*y) + z*z, no FMA.
-  return sqrt(__dadd_rn(__dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)), __dmul_rn(z, z)));
-}
-
-__device__ __forceinline__ double shfl_d(double v, int src) {
-  return __shfl_sync(kFull, v, src);
-}
+__device__ __forceinline__ double shfl_d(double v, int src) { return __shfl_sync(kFull, v, src); }
 
 __device__ __forceinline__ double warp_sum_d(double v) {
 #pragma unroll
@@ -125,207 +115,205 @@ __device__ __forceinline__ double warp_sum_d(double v) {
   return v;
 }
 
-// Per-warp shared-memory tables.
-struct WarpTables {
-  float4* r0;  // (ux, uy, uz, klo)           uhat at the cuboid centre
-  float4* r1;  // (khi, eLo, st, ct)          eLo = (log phi - lw(klo)) log2e; psi_t half-angle
-  float4* r2;  // (kst, eUb, sp, cp)          UB kappa at t*, its exponent, half-angle of psi_t+psi_r
-  float4* r3;  // (usx, usy, usz, eHi)        uhat at t*, eHi = (log phi - lw(khi)) log2e
-  float4* c0;  // (qx, qy, qz, k2)            q_j = R0^T m_j
-  float* c1;   // e2 = (log phi2 - lw(k2)) log2e
-};
-
-// Cross terms of one model row against the image columns of its class.
-// Returns (LB cross sum, UB cross sum) in FP32 (caller flushes to FP64).
-template <bool kSame>
-__device__ __forceinline__ void cross_row(const WarpTables& T, int i, int o2, int n2, float& acc_lb,
-                                          float& acc_ub) {
-  const float4 a0 = T.r0[i];
-  const float4 a1 = T.r1[i];
-  const float4 a2 = T.r2[i];
-  const float4 a3 = T.r3[i];
-  const float ux = a0.x, uy = a0.y, uz = a0.z, klo = a0.w;
-  const float khi = a1.x;
-  const float kst = a2.x, eUb = a2.y, sp = a2.z, cp = a2.w;
-  const float eHi = a3.w;
-  float lb = 0.0f, ub = 0.0f;
-#pragma unroll 2
-  for (int j = o2; j < o2 + n2; ++j) {
-    const float4 q = T.c0[j];
-    const float ej = T.c1[j];
-    const float k2 = q.w;
-    // --- geometry at the cuboid centre
-    const float dx = ux - q.x, dy = uy - q.y, dz = uz - q.z;
-    const float x = fminf(fmaf(dx, dx, fmaf(dy, dy, dz * dz)), 4.0f);  // |u - q|^2
-    const float y = 4.0f - x;                                          // |u + q|^2
-    const float rx = rsqf(fmaxf(x, 1e-30f));
-    const float ry = rsqf(fmaxf(y, 1e-30f));
-    const float sth = 0.5f * x * rx;  // sin(theta/2)
-    const float cth = 0.5f * y * ry;  // cos(theta/2)
-    // B = max(0, theta - psi_t - psi_r) (alignment_angle_B, bounds.cpp:143-156)
-    const float sb = fmaf(sth, cp, -cth * sp);
-    const float cb = fmaf(cth, cp, sth * sp);
-    const bool bzero = !(sb > 0.0f);
-    const float omc = bzero ? 0.0f : 2.0f * sb * sb;  // 1 - cos B
-    const float opc = bzero ? 2.0f : 2.0f * cb * cb;  // 1 + cos B
-    // --- LB: excess at the low kappa endpoint, W(K) at K's minimum
-    const float ab = klo * k2;
-    const float amb = klo - k2;
-    const float K2lo = fmaf(amb, amb, 2.0f * ab * opc);
-    const float rKlo = rsqf(fmaxf(K2lo, 1e-30f));
-    const float Klo = K2lo * rKlo;
-    const float D1 = Klo + klo + k2;
-    const float num1 = -2.0f * kL2E * ab * omc;
-    // --- UB: objective at (r0, t*) (class_objective cross loop)
-    float xs, ys;
-    if (kSame) {
-      xs = x;
-      ys = y;
-    } else {
-      const float ex = a3.x - q.x, ey = a3.y - q.y, ez = a3.z - q.z;
-      xs = fminf(fmaf(ex, ex, fmaf(ey, ey, ez * ez)), 4.0f);
-      ys = 4.0f - xs;
-    }
-    const float ab2 = kst * k2;
-    const float amb2 = kst - k2;
-    const float K2u = fmaf(amb2, amb2, ab2 * ys);
-    const float rKu = rsqf(fmaxf(K2u, 1e-30f));
-    const float Ku = K2u * rKu;
-    const float D2 = Ku + kst + k2;
-    const float num2 = -kL2E * ab2 * xs;
-    const float inv = rcpf(D1 * D2);
-    const float ex1 = num1 * D2 * inv;  // (K - a - b) log2e, LB
-    const float ex2 = num2 * D1 * inv;  // (K - a - b) log2e, UB
-    // K's minimum over the kappa interval (vertex case, bounds.cpp:163-173)
-    const float vertex = (omc - 1.0f) * k2;  // -cos B * k2
-    float t1;
-    if (vertex <= klo && Klo > 15.0f) {
-      t1 = ex2f(ex1 + eHi + ej) * rKlo;
-    } else {
-      float kmin;
-      if (vertex <= klo) {
-        kmin = Klo;
-      } else if (vertex >= khi) {
-        const float d = khi - k2;
-        const float kk = fmaf(d, d, 2.0f * khi * k2 * opc);
-        kmin = kk * rsqf(fmaxf(kk, 1e-30f));
-      } else {
-        const float s = omc * opc;
-        kmin = k2 * (s * rsqf(fmaxf(s, 1e-30f)));
-      }
-      const float lw = kmin > 15.0f ? -lg2f(kmin) : log2w_small(kmin);
-      t1 = ex2f(ex1 + lw + eHi + ej);
-    }
-    float t2;
-    if (Ku > 15.0f) {
-      t2 = ex2f(ex2 + eUb + ej) * rKu;
-    } else {
-      t2 = ex2f(ex2 + log2w_small(Ku) + eUb + ej);
-    }
-    // Reference drops pairs with K < a + b - 64 from the objective.
-    t2 = (ex2 < -64.0f * kL2E) ? 0.0f : t2;
-    lb += t1;
-    ub += t2;
-  }
-  acc_lb = lb;
-  acc_ub = ub;
+// sqrt(s) < z with the reference's rounding (Eigen norm() = sqrt of the
+// squared norm): the squared comparison decides unless s is within a relative
+// 1e-12 of z^2, where the correctly rounded sqrt decides.
+__device__ __forceinline__ bool norm_below(double s, double z, double z2) {
+  const double d = s - z2;
+  if (fabs(d) > 1e-12 * z2) return d < 0.0;
+  return sqrt(s) < z;
 }
 
-// One self pair (i < j logically) with row i held in registers.
+// Per-warp shared-memory tables (SoA of float4 rows).
+struct WarpTables {
+  float4* r0;  // (ux, uy, uz, klo)     uhat at the cuboid centre, kappa_lo
+  float4* r1;  // (khi, eLo, st, ct)    eLo = (log phi - log W(klo)) log2e + 1/2; psi_t half-angle
+  float4* r2;  // (kst, eUs, sp, cp)    kappa at t*, (log phi - log W(kst)) log2e + 1/2, psi_t+psi_r half-angle
+  float4* r3;  // (usx, usy, usz, eHi)  uhat at t*, (log phi - log W(khi)) log2e
+  float4* c0;  // (qx, qy, qz, k2)      q_j = R0^T m_j
+  float* c1;   // e2 = (log phi2 - log W(k2)) log2e
+};
+
+struct Row {
+  float ux, uy, uz, klo, khi, kst, eHi, eUb, sp, cp, usx, usy, usz;
+};
+
+// Cross LB exact path: K minimum over the kappa interval (vertex case,
+// bounds.cpp:160-175) with the exact W factor.
+__device__ __noinline__ float cross_lb_exact(float klo, float khi, float k2, float s2, float c2,
+                                             float K1, float e1) {
+  // s2 = 2(1 - cos B), c2 = 2(1 + cos B)
+  const float cosb = 1.0f - 0.5f * s2;
+  const float vertex = -cosb * k2;
+  float kmin;
+  if (vertex <= klo) {
+    kmin = K1;
+  } else if (vertex >= khi) {
+    const float d = khi - k2;
+    kmin = sqf(fmaxf(fmaf(d, d, khi * k2 * c2), 0.0f));
+  } else {
+    kmin = k2 * sqf(0.25f * s2 * c2);  // k2 sin B
+  }
+  return ex2f(e1 + log2w(kmin));
+}
+
+template <bool kSame>
+__device__ __forceinline__ void cross_pair(const Row& r, const float4 q, const float ej, float& l,
+                                           float& u) {
+  const float k2 = q.w;
+  const float dx = r.ux - q.x, dy = r.uy - q.y, dz = r.uz - q.z;
+  const float x = fmaf(dx, dx, fmaf(dy, dy, dz * dz));  // |u - q|^2 = 4 sin^2(theta/2)
+  const float y = fmaxf(4.0f - x, 0.0f);                // |u + q|^2
+  const float sg = sqf(x), gm = sqf(y);                 // 2 sin(theta/2), 2 cos(theta/2)
+  // B = max(0, theta - psi_t - psi_r) (alignment_angle_B, bounds.cpp:143-156)
+  float sbs = fmaf(sg, r.cp, -gm * r.sp);  // 2 sin(B/2)
+  float cbs = fmaf(gm, r.cp, sg * r.sp);   // 2 cos(B/2)
+  const bool bz = !(sbs > 0.0f);
+  sbs = bz ? 0.0f : sbs;
+  cbs = bz ? 2.0f : cbs;
+  const float s2 = sbs * sbs;  // 2(1 - cos B)
+  const float c2 = cbs * cbs;  // 2(1 + cos B)
+  // LB: excess at the low kappa endpoint, W(K) at K's minimum
+  const float ab = r.klo * k2;
+  const float amb = r.klo - k2;
+  const float K2lo = fmaf(amb, amb, ab * c2);
+  const float rK1 = rsqf(K2lo);
+  const float K1 = K2lo * rK1;
+  const float D1 = K1 + r.klo + k2;
+  const float n1 = ab * s2;
+  // UB: objective at (r0, t*) (class_objective cross loop, objective.cpp:212-220)
+  float xs, ys;
+  if (kSame) {
+    xs = x;
+    ys = y;
+  } else {
+    const float ex = r.usx - q.x, ey = r.usy - q.y, ez = r.usz - q.z;
+    xs = fmaf(ex, ex, fmaf(ey, ey, ez * ez));
+    ys = fmaxf(4.0f - xs, 0.0f);
+  }
+  const float ab2 = r.kst * k2;
+  const float amb2 = r.kst - k2;
+  const float K2u = fmaf(amb2, amb2, ab2 * ys);
+  const float rK2 = rsqf(K2u);
+  const float K2 = K2u * rK2;
+  const float D2 = K2 + r.kst + k2;
+  const float n2 = ab2 * xs;
+  const float inv = rcpf(D1 * D2) * -kL2E;
+  const float e1 = fmaf(n1 * D2, inv, r.eHi + ej);  // log2 of the LB term without W(K)
+  const float e2 = fmaf(n2 * D1, inv, r.eUb + ej);  // log2 of the UB term without W(K)
+  float t1 = ex2f(e1) * rK1;
+  float t2 = ex2f(e2) * rK2;
+  if (e1 > kNegligibleLog2 && (-(1.0f - 0.5f * s2) * k2 > r.klo || !(K1 > 15.0f)))
+    t1 = cross_lb_exact(r.klo, r.khi, k2, s2, c2, K1, e1);
+  if (e2 > kNegligibleLog2 && !(K2 > 15.0f)) t2 = ex2f(e2 + log2w(K2));
+  l += t1;
+  u += t2;
+}
+
+// Self LB exact path: K's corner maximum (bounds.cpp:124-137) when cos A < 0
+// or K small.
+__device__ __noinline__ float self_lb_exact(float alo, float ahi, float blo, float bhi, float c2,
+                                            float K2hh, float e1) {
+  const float dll = alo - blo, dlh = alo - bhi, dhl = ahi - blo;
+  const float K2ll = fmaf(dll, dll, alo * blo * c2);
+  const float K2lh = fmaf(dlh, dlh, alo * bhi * c2);
+  const float K2hl = fmaf(dhl, dhl, ahi * blo * c2);
+  const float m = fmaxf(fmaxf(K2ll, K2lh), fmaxf(K2hl, K2hh));
+  return ex2f(e1 + log2w(sqf(fmaxf(m, 0.0f))));
+}
+
 template <bool kSame>
 __device__ __forceinline__ void self_pair(const float4& a0, const float4& a1, const float4& a2,
-                                          const float4& a3, const float4& b0, const float4& b1,
-                                          const float4& b2, const float4& b3, float& lb,
-                                          float& ub) {
-  // --- spread angle A = min(pi, theta + psi_i + psi_j) (bounds.cpp:108-124)
+                                          const float3& a3, const float4& b0, const float4& b1,
+                                          const float4& b2, const float3& b3, float& l,
+                                          float& u) {
+  // spread angle A = min(pi, theta + psi_i + psi_j) (bounds.cpp:108-124)
   const float dx = a0.x - b0.x, dy = a0.y - b0.y, dz = a0.z - b0.z;
-  const float x = fminf(fmaf(dx, dx, fmaf(dy, dy, dz * dz)), 4.0f);
-  const float y = 4.0f - x;
-  const float rx = rsqf(fmaxf(x, 1e-30f));
-  const float ry = rsqf(fmaxf(y, 1e-30f));
-  const float sth = 0.5f * x * rx;
-  const float cth = 0.5f * y * ry;
+  const float x = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+  const float y = fmaxf(4.0f - x, 0.0f);
+  const float sg = sqf(x), gm = sqf(y);
   const float sij = fmaf(a1.z, b1.w, a1.w * b1.z);   // sin((psi_i+psi_j)/2)
   const float cij = fmaf(a1.w, b1.w, -a1.z * b1.z);  // cos((psi_i+psi_j)/2)
-  const float S = fmaf(sth, cij, cth * sij);
-  const float Cc = fmaf(cth, cij, -sth * sij);
-  const bool api = !(cij > 0.0f) || !(Cc > 0.0f);
-  const float omc = api ? 2.0f : 2.0f * S * S;   // 1 - cos A
-  const float opc = api ? 0.0f : 2.0f * Cc * Cc; // 1 + cos A
-  // --- LB: excess at the high corner, W(K) at K's corner maximum
-  const float alo = a0.w, ahi = a1.x, blo = b0.w, bhi = b1.x;
+  float Ss = fmaf(sg, cij, gm * sij);                // 2 sin(A/2)
+  float Cs = fmaf(gm, cij, -sg * sij);               // 2 cos(A/2)
+  const bool api = !(cij > 0.0f) || !(Cs > 0.0f);
+  Ss = api ? 2.0f : Ss;
+  Cs = api ? 0.0f : Cs;
+  const float s2 = Ss * Ss;  // 2(1 - cos A)
+  const float c2 = Cs * Cs;  // 2(1 + cos A)
+  // LB: excess at the high corner, W(K) at K's corner maximum
+  const float ahi = a1.x, bhi = b1.x;
   const float hh = ahi * bhi;
   const float dhh = ahi - bhi;
-  const float K2hh = fmaf(dhh, dhh, 2.0f * hh * opc);
-  const float rKhh = rsqf(fmaxf(K2hh, 1e-30f));
+  const float K2hh = fmaf(dhh, dhh, hh * c2);
+  const float rKhh = rsqf(K2hh);
   const float Khh = K2hh * rKhh;
-  float K2cm = K2hh;
-  float rKcm = rKhh;
-  if (opc < 1.0f) {  // cos A < 0: K^2 need not be monotone in each kappa
-    const float dll = alo - blo, dlh = alo - bhi, dhl = ahi - blo;
-    const float K2ll = fmaf(dll, dll, 2.0f * alo * blo * opc);
-    const float K2lh = fmaf(dlh, dlh, 2.0f * alo * bhi * opc);
-    const float K2hl = fmaf(dhl, dhl, 2.0f * ahi * blo * opc);
-    const float m = fmaxf(fmaxf(K2ll, K2lh), K2hl);
-    if (m > K2hh) {
-      K2cm = m;
-      rKcm = rsqf(fmaxf(m, 1e-30f));
-    }
-  }
   const float D1 = Khh + ahi + bhi;
-  const float num1 = -2.0f * kL2E * hh * omc;
-  // --- UB: objective self pair at t* (objective.cpp:204-209)
+  const float n1 = hh * s2;
+  // UB: objective self pair at t* (objective.cpp:204-209)
   float xs, ys;
   if (kSame) {
     xs = x;
     ys = y;
   } else {
     const float ex = a3.x - b3.x, ey = a3.y - b3.y, ez = a3.z - b3.z;
-    xs = fminf(fmaf(ex, ex, fmaf(ey, ey, ez * ez)), 4.0f);
-    ys = 4.0f - xs;
+    xs = fmaf(ex, ex, fmaf(ey, ey, ez * ez));
+    ys = fmaxf(4.0f - xs, 0.0f);
   }
   const float ka = a2.x, kb = b2.x;
   const float ab2 = ka * kb;
   const float d2 = ka - kb;
   const float K2u = fmaf(d2, d2, ab2 * ys);
-  const float rKu = rsqf(fmaxf(K2u, 1e-30f));
-  const float Ku = K2u * rKu;
-  const float D2 = Ku + ka + kb;
-  const float num2 = -kL2E * ab2 * xs;
-  const float inv = rcpf(D1 * D2);
-  const float ex1 = num1 * D2 * inv;
-  const float ex2 = num2 * D1 * inv;
-  const float Kcm = K2cm * rKcm;
-  float t1;
-  if (Kcm > 15.0f) {
-    t1 = ex2f(ex1 + a1.y + b1.y + 1.0f) * rKcm;  // +1: factor 2 (bounds.cpp:138)
-  } else {
-    t1 = ex2f(ex1 + log2w_small(Kcm) + a1.y + b1.y + 1.0f);
-  }
-  float t2;
-  if (Ku > 15.0f) {
-    t2 = ex2f(ex2 + a2.y + b2.y + 1.0f) * rKu;
-  } else {
-    t2 = ex2f(ex2 + log2w_small(Ku) + a2.y + b2.y + 1.0f);
-  }
-  t2 = (ex2 < -64.0f * kL2E) ? 0.0f : t2;
-  lb += t1;
-  ub += t2;
+  const float rK2 = rsqf(K2u);
+  const float K2 = K2u * rK2;
+  const float D2 = K2 + ka + kb;
+  const float n2 = ab2 * xs;
+  const float inv = rcpf(D1 * D2) * -kL2E;
+  const float e1 = fmaf(n1 * D2, inv, a1.y + b1.y);  // eLo carry +1/2 each: factor 2
+  const float e2 = fmaf(n2 * D1, inv, a2.y + b2.y);  // eUs carry +1/2 each: factor 2
+  float t1 = ex2f(e1) * rKhh;
+  float t2 = ex2f(e2) * rK2;
+  if (e1 > kNegligibleLog2 && (c2 < 2.0f || !(Khh > 15.0f)))
+    t1 = self_lb_exact(a0.w, ahi, b0.w, bhi, c2, K2hh, e1);
+  if (e2 > kNegligibleLog2 && !(K2 > 15.0f)) t2 = ex2f(e2 + log2w(K2));
+  l += t1;
+  u += t2;
+}
+
+__device__ __forceinline__ Row load_row(const WarpTables& T, int i) {
+  const float4 a0 = T.r0[i], a1 = T.r1[i], a2 = T.r2[i], a3 = T.r3[i];
+  Row r;
+  r.ux = a0.x;
+  r.uy = a0.y;
+  r.uz = a0.z;
+  r.klo = a0.w;
+  r.khi = a1.x;
+  r.kst = a2.x;
+  r.eUb = a2.y - 0.5f;
+  r.sp = a2.z;
+  r.cp = a2.w;
+  r.usx = a3.x;
+  r.usy = a3.y;
+  r.usz = a3.z;
+  r.eHi = a3.w;
+  return r;
 }
 
 template <bool kSame>
 __device__ __forceinline__ void class_pairs(const WarpTables& T, const ClassSpan cs, int lane,
-                                            double w, double& lb_self, double& lb_cross,
+                                            float w, double& lb_self, double& lb_cross,
                                             double& ub_self, double& ub_cross) {
   const int n = cs.n1;
   // Cross terms: rows over lanes, columns broadcast.
   for (int base = 0; base < n; base += 32) {
     const int il = base + lane;
     if (il < n) {
-      float l, u;
-      cross_row<kSame>(T, cs.o1 + il, cs.o2, cs.n2, l, u);
-      lb_cross += w * static_cast<double>(l);
-      ub_cross += w * static_cast<double>(u);
+      const Row r = load_row(T, cs.o1 + il);
+      float l = 0.0f, u = 0.0f;
+#pragma unroll 2
+      for (int j = cs.o2; j < cs.o2 + cs.n2; ++j) cross_pair<kSame>(r, T.c0[j], T.c1[j], l, u);
+      lb_cross += static_cast<double>(w * l);
+      ub_cross += static_cast<double>(w * u);
     }
   }
   // Self terms i<j via the circulant schedule: every unordered pair once as
@@ -337,36 +325,64 @@ __device__ __forceinline__ void class_pairs(const WarpTables& T, const ClassSpan
     if (il < n) {
       const int i = cs.o1 + il;
       const float4 a0 = T.r0[i], a1 = T.r1[i], a2 = T.r2[i];
-      const float4 a3 = kSame ? make_float4(0.f, 0.f, 0.f, 0.f) : T.r3[i];
+      float3 a3 = make_float3(0.f, 0.f, 0.f);
+      if (!kSame) a3 = make_float3(T.r3[i].x, T.r3[i].y, T.r3[i].z);
       float l = 0.0f, u = 0.0f;
       int jl = il;
 #pragma unroll 2
       for (int d = 1; d <= dfull; ++d) {
         jl = (jl + 1 == n) ? 0 : jl + 1;
         const int j = cs.o1 + jl;
-        const float4 b0 = T.r0[j], b1 = T.r1[j], b2 = T.r2[j];
-        const float4 b3 = kSame ? make_float4(0.f, 0.f, 0.f, 0.f) : T.r3[j];
-        self_pair<kSame>(a0, a1, a2, a3, b0, b1, b2, b3, l, u);
+        float3 b3 = make_float3(0.f, 0.f, 0.f);
+        if (!kSame) b3 = make_float3(T.r3[j].x, T.r3[j].y, T.r3[j].z);
+        self_pair<kSame>(a0, a1, a2, a3, T.r0[j], T.r1[j], T.r2[j], b3, l, u);
       }
       if (even && il < n / 2) {
-        const int j = cs.o1 + il + n / 2;
-        const float4 b0 = T.r0[j], b1 = T.r1[j], b2 = T.r2[j];
-        const float4 b3 = kSame ? make_float4(0.f, 0.f, 0.f, 0.f) : T.r3[j];
-        self_pair<kSame>(a0, a1, a2, a3, b0, b1, b2, b3, l, u);
+        const int j = i + n / 2;
+        float3 b3 = make_float3(0.f, 0.f, 0.f);
+        if (!kSame) b3 = make_float3(T.r3[j].x, T.r3[j].y, T.r3[j].z);
+        self_pair<kSame>(a0, a1, a2, a3, T.r0[j], T.r1[j], T.r2[j], b3, l, u);
       }
-      lb_self += w * static_cast<double>(l);
-      ub_self += w * static_cast<double>(u);
+      lb_self += static_cast<double>(w * l);
+      ub_self += static_cast<double>(w * u);
     }
   }
 }
 
-__global__ void __launch_bounds__(kWarpsPerCta * 32)
+// Half-angle of psi_trans (se3.cpp:72-92) for a mean outside the cuboid:
+// the vertex with the largest angle to the centre direction is the one with
+// the smallest cosine c_hat . v_hat; returns sin/cos of half that angle as
+// |c_hat - v_hat|/2, |c_hat + v_hat|/2.
+__device__ __forceinline__ void psi_trans_half(float ux, float uy, float uz, float h0, float h1,
+                                               float h2, float cx, float cy, float cz, float& st,
+                                               float& ct) {
+  float best = 2.0f, bx = 0.f, by = 0.f, bz = 0.f;
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    const float vx = ux - ((s & 4) ? h0 : -h0);
+    const float vy = uy - ((s & 2) ? h1 : -h1);
+    const float vz = uz - ((s & 1) ? h2 : -h2);
+    const float rv = rsqf(fmaf(vx, vx, fmaf(vy, vy, vz * vz)));
+    const float cs = fmaf(cx, vx, fmaf(cy, vy, cz * vz)) * rv;
+    if (cs < best) {
+      best = cs;
+      bx = vx * rv;
+      by = vy * rv;
+      bz = vz * rv;
+    }
+  }
+  const float ex = cx - bx, ey = cy - by, ez = cz - bz;
+  const float px = cx + bx, py = cy + by, pz = cz + bz;
+  st = 0.5f * sqf(fmaf(ex, ex, fmaf(ey, ey, ez * ez)));
+  ct = 0.5f * sqf(fmaf(px, px, fmaf(py, py, pz * pz)));
+}
+
+__global__ void __launch_bounds__(kWarpsPerCta * 32, 5)
     eval_bounds_kernel(const DevCtx ctx, const EvalArgs args) {
   extern __shared__ float4 smem4[];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int N1 = ctx.n1_total, N2 = ctx.n2_total;
-  // Per-warp table carve-out.
   const size_t per_warp_f4 = static_cast<size_t>(4 * N1 + N2) + (N2 + 3) / 4;
   float4* base = smem4 + warp * per_warp_f4;
   WarpTables T;
@@ -378,6 +394,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
   T.c1 = reinterpret_cast<float*>(T.c0 + N2);
 
   const double zeta = ctx.zeta;
+  const double zeta2 = zeta * zeta;
   for (;;) {
     long long node = 0;
     if (lane == 0) node = static_cast<long long>(atomicAdd(args.work, 1u));
@@ -400,10 +417,12 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
       bool hit = false;
       if (mi < N1) {
         const double* mu = ctx.mu + 3 * mi;
-        const double f0 = __dadd_rn(fabs(__dsub_rn(mu[0], tc0)), h0);
-        const double f1 = __dadd_rn(fabs(__dsub_rn(mu[1], tc1)), h1);
-        const double f2 = __dadd_rn(fabs(__dsub_rn(mu[2], tc2)), h2);
-        hit = dnorm3(f0, f1, f2) < zeta;
+        const double f0 = fabs(mu[0] - tc0) + h0;
+        const double f1 = fabs(mu[1] - tc1) + h1;
+        const double f2 = fabs(mu[2] - tc2) + h2;
+        hit = norm_below(__dadd_rn(__dadd_rn(__dmul_rn(f0, f0), __dmul_rn(f1, f1)),
+                                   __dmul_rn(f2, f2)),
+                         zeta, zeta2);
       }
       if (__any_sync(kFull, hit)) {
         infeasible = true;
@@ -431,7 +450,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
       for (int r = 0; r < 3; ++r)
 #pragma unroll
         for (int cix = 0; cix < 3; ++cix) {
-          const double k2 = K[3 * r] * K[cix] + K[3 * r + 1] * K[3 + cix] + K[3 * r + 2] * K[6 + cix];
+          const double k2 =
+              K[3 * r] * K[cix] + K[3 * r + 1] * K[3 + cix] + K[3 * r + 2] * K[6 + cix];
           R[3 * r + cix] = ((r == cix ? 1.0 : 0.0) + a * K[3 * r + cix]) + c * k2;
         }
     }
@@ -455,7 +475,11 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
           bool hit = false;
           if (mi < N1) {
             const double* mu = ctx.mu + 3 * mi;
-            hit = dnorm3(__dsub_rn(mu[0], ts0), __dsub_rn(mu[1], ts1), __dsub_rn(mu[2], ts2)) < zeta;
+            const double d0 = __dsub_rn(mu[0], ts0), d1 = __dsub_rn(mu[1], ts1),
+                         d2 = __dsub_rn(mu[2], ts2);
+            hit = norm_below(
+                __dadd_rn(__dadd_rn(__dmul_rn(d0, d0), __dmul_rn(d1, d1)), __dmul_rn(d2, d2)),
+                zeta, zeta2);
           }
           const unsigned bal = __ballot_sync(kFull, hit);
           if (bal) {
@@ -470,7 +494,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
         if (proj == 8) break;
         const double* mu = ctx.mu + 3 * off;
         double d0 = __dsub_rn(ts0, mu[0]), d1 = __dsub_rn(ts1, mu[1]), d2 = __dsub_rn(ts2, mu[2]);
-        const double nn = dnorm3(d0, d1, d2);
+        const double nn =
+            sqrt(__dadd_rn(__dadd_rn(__dmul_rn(d0, d0), __dmul_rn(d1, d1)), __dmul_rn(d2, d2)));
         if (nn > 1e-12) {
           d0 = __ddiv_rn(d0, nn);
           d1 = __ddiv_rn(d1, nn);
@@ -481,9 +506,12 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
           d2 = 0.0;
         }
         const double rad = __dmul_rn(zeta, 1.0 + 1e-9);
-        ts0 = fmin(fmax(__dadd_rn(mu[0], __dmul_rn(d0, rad)), __dsub_rn(tc0, h0)), __dadd_rn(tc0, h0));
-        ts1 = fmin(fmax(__dadd_rn(mu[1], __dmul_rn(d1, rad)), __dsub_rn(tc1, h1)), __dadd_rn(tc1, h1));
-        ts2 = fmin(fmax(__dadd_rn(mu[2], __dmul_rn(d2, rad)), __dsub_rn(tc2, h2)), __dadd_rn(tc2, h2));
+        ts0 = fmin(fmax(__dadd_rn(mu[0], __dmul_rn(d0, rad)), __dsub_rn(tc0, h0)),
+                   __dadd_rn(tc0, h0));
+        ts1 = fmin(fmax(__dadd_rn(mu[1], __dmul_rn(d1, rad)), __dsub_rn(tc1, h1)),
+                   __dadd_rn(tc1, h1));
+        ts2 = fmin(fmax(__dadd_rn(mu[2], __dmul_rn(d2, rad)), __dsub_rn(tc2, h2)),
+                   __dadd_rn(tc2, h2));
       }
     }
     const bool same = (ts0 == tc0) && (ts1 == tc1) && (ts2 == tc2);
@@ -491,65 +519,42 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
     // ---- per-row prep (all classes): kappa interval, psi_t, projections
     double lb_self = 0.0, lb_cross = 0.0, ub_self = 0.0, ub_cross = 0.0;
     float st_max = 0.0f;
+    const float fh0 = static_cast<float>(h0), fh1 = static_cast<float>(h1),
+                fh2 = static_cast<float>(h2);
     for (int c = 0; c < ctx.n_classes; ++c) {
       const ClassSpan cs = ctx.cls[c];
-      const double w = ctx.cls_w[c];
+      const float w = static_cast<float>(ctx.cls_w[c]);
+      float dsl = 0.0f, dsu = 0.0f;
       for (int il = lane; il < cs.n1; il += 32) {
         const int i = cs.o1 + il;
         const double m0 = ctx.mu[3 * i], m1 = ctx.mu[3 * i + 1], m2 = ctx.mu[3 * i + 2];
         const double is2 = ctx.inv_s2[i];
         const double u0 = m0 - tc0, u1 = m1 - tc1, u2 = m2 - tc2;
         const double a0 = fabs(u0), a1 = fabs(u1), a2 = fabs(u2);
-        // point_cuboid_distance (se3.cpp:60-66)
+        // point_cuboid_distance (se3.cpp:60-66); dlo floored at zeta
         const double o0 = fmax(a0 - h0, 0.0), o1 = fmax(a1 - h1, 0.0), o2 = fmax(a2 - h2, 0.0);
-        const double dlo = fmax(sqrt(o0 * o0 + o1 * o1 + o2 * o2), zeta);
+        const double dlo2 = fmax(o0 * o0 + o1 * o1 + o2 * o2, zeta2);
         const double dhi2 = (a0 + h0) * (a0 + h0) + (a1 + h1) * (a1 + h1) + (a2 + h2) * (a2 + h2);
-        const double klo = dlo * dlo * is2 + 1.0;
-        const double khi = dhi2 * is2 + 1.0;
-        const double lphi = static_cast<double>(ctx.log_phi1[i]);
-        const double nrm = sqrt(u0 * u0 + u1 * u1 + u2 * u2);
+        const float klo = static_cast<float>(dlo2 * is2 + 1.0);
+        const float khi = static_cast<float>(dhi2 * is2 + 1.0);
+        const double un2 = u0 * u0 + u1 * u1 + u2 * u2;
         float ux = 1.0f, uy = 0.0f, uz = 0.0f;
-        if (nrm > 1e-12) {
-          const double inv = 1.0 / nrm;
+        if (un2 > 1e-24) {
+          const double inv = rsqrt(un2);
           ux = static_cast<float>(u0 * inv);
           uy = static_cast<float>(u1 * inv);
           uz = static_cast<float>(u2 * inv);
         }
-        // psi_trans (se3.cpp:72-92) as a half-angle: max over the 8 vertices
-        // of |c_hat - v_hat| / 2 = sin(angle / 2).
         float st, ct;
         if (a0 <= h0 && a1 <= h1 && a2 <= h2) {
           st = 1.0f;  // psi_t = pi
           ct = 0.0f;
         } else {
-          const float fu0 = static_cast<float>(u0), fu1 = static_cast<float>(u1),
-                      fu2 = static_cast<float>(u2);
-          const float fh0 = static_cast<float>(h0), fh1 = static_cast<float>(h1),
-                      fh2 = static_cast<float>(h2);
-          float best = -1.0f, bx = 0.f, by = 0.f, bz = 0.f;
-#pragma unroll
-          for (int s = 0; s < 8; ++s) {
-            const float vx = fu0 - ((s & 4) ? fh0 : -fh0);
-            const float vy = fu1 - ((s & 2) ? fh1 : -fh1);
-            const float vz = fu2 - ((s & 1) ? fh2 : -fh2);
-            const float rv = rsqf(fmaxf(fmaf(vx, vx, fmaf(vy, vy, vz * vz)), 1e-37f));
-            const float wx = vx * rv, wy = vy * rv, wz = vz * rv;
-            const float ex = ux - wx, ey = uy - wy, ez = uz - wz;
-            const float d2 = fmaf(ex, ex, fmaf(ey, ey, ez * ez));
-            if (d2 > best) {
-              best = d2;
-              bx = wx;
-              by = wy;
-              bz = wz;
-            }
-          }
-          const float px = ux + bx, py = uy + by, pz = uz + bz;
-          const float e2 = fmaf(px, px, fmaf(py, py, pz * pz));
-          st = 0.5f * sqrtf(fmaxf(best, 0.0f));
-          ct = 0.5f * sqrtf(e2);
+          psi_trans_half(static_cast<float>(u0), static_cast<float>(u1), static_cast<float>(u2),
+                         fh0, fh1, fh2, ux, uy, uz, st, ct);
         }
         st_max = fmaxf(st_max, st);
-        // half-angle of psi_t + psi_r; B = 0 when the sum reaches pi
+        // half-angle of psi_t + psi_r; B = 0 once the sum reaches pi
         float sp = fmaf(st, c_r, ct * s_r);
         float cp = fmaf(ct, c_r, -st * s_r);
         if (!(cp > 0.0f)) {
@@ -558,23 +563,24 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
         }
         // UB projection at t* (project_model, objective.cpp:175-192)
         const double v0 = m0 - ts0, v1 = m1 - ts1, v2 = m2 - ts2;
-        const double dd2 = v0 * v0 + v1 * v1 + v2 * v2;
-        const double dd = sqrt(dd2);
-        const double kst = dd2 * is2 + 1.0;
-        const double id = 1.0 / dd;
-        const double phi = ctx.phi1[i];
-        if (!infeasible) {
-          lb_self += w * diag_term(phi, klo);
-          ub_self += w * diag_term(phi, kst);
-        }
-        const float eLo = static_cast<float>((lphi - logw_d(klo)) * kL2E);
-        const float eHi = static_cast<float>((lphi - logw_d(khi)) * kL2E);
-        const float eUb = static_cast<float>((lphi - logw_d(kst)) * kL2E);
-        T.r0[i] = make_float4(ux, uy, uz, static_cast<float>(klo));
-        T.r1[i] = make_float4(static_cast<float>(khi), eLo, st, ct);
-        T.r2[i] = make_float4(static_cast<float>(kst), eUb, sp, cp);
-        T.r3[i] = make_float4(static_cast<float>(v0 * id), static_cast<float>(v1 * id),
-                              static_cast<float>(v2 * id), eHi);
+        const double vn2 = v0 * v0 + v1 * v1 + v2 * v2;
+        const float kst = static_cast<float>(vn2 * is2 + 1.0);
+        const double iv = rsqrt(vn2);
+        const float lphi = ctx.log_phi1[i];
+        const float phi = static_cast<float>(ctx.phi1[i]);
+        dsl += diag_term(phi, klo);
+        dsu += diag_term(phi, kst);
+        const float lwlo = log2w(klo), lwhi = log2w(khi), lwst = log2w(kst);
+        const float lp2 = lphi * kL2E;
+        T.r0[i] = make_float4(ux, uy, uz, klo);
+        T.r1[i] = make_float4(khi, lp2 - lwlo + 0.5f, st, ct);
+        T.r2[i] = make_float4(kst, lp2 - lwst + 0.5f, sp, cp);
+        T.r3[i] = make_float4(static_cast<float>(v0 * iv), static_cast<float>(v1 * iv),
+                              static_cast<float>(v2 * iv), lp2 - lwhi);
+      }
+      if (!infeasible) {
+        lb_self += static_cast<double>(w * dsl);
+        ub_self += static_cast<double>(w * dsu);
       }
     }
     // split decision (subdivide_adaptive, se3.cpp:107-121)
@@ -613,7 +619,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
     // ---- pair sweeps
     for (int c = 0; c < ctx.n_classes; ++c) {
       const ClassSpan cs = ctx.cls[c];
-      const double w = ctx.cls_w[c];
+      const float w = static_cast<float>(ctx.cls_w[c]);
       if (same) {
         class_pairs<true>(T, cs, lane, w, lb_self, lb_cross, ub_self, ub_cross);
       } else {
