@@ -85,8 +85,11 @@ double gosma_ctx_image_self_energy(const gosma_ctx* ctx);
 /* ObjectiveContext::zeta (objective.hpp:46). */
 double gosma_ctx_zeta(const gosma_ctx* ctx);
 
-/* Relative soundness margin subtracted from every lower bound, times the
- * node's |term| mass. Default set at creation. */
+/* Lower-bound soundness margin. By default every lower
+ * bound has subtracted (a) the kernel's per-term FP32 error estimate and (b)
+ * rel_margin x the node's |term| mass (default 2e-7), so it never exceeds the
+ * FP64 value. rel_margin < 0 selects the raw FP32 core (no margin at all),
+ * for parity diagnostics only. */
 int gosma_ctx_set_lb_margin(gosma_ctx* ctx, double rel_margin);
 
 /* Replaces evaluate_branch_batch(ctx, branches, threads, skip_upper_at)

@@ -47,9 +47,18 @@ std::atomic<unsigned long long> g_launches{0};
 
 constexpr int kWarpsPerCta = 4;
 constexpr unsigned kFull = 0xffffffffu;
-// Terms whose log2 value is below this flush to zero in FP32 (ftz) even with
-// the largest possible W factor (W <= 2), so their exact paths are skipped.
-constexpr float kNegligibleLog2 = -128.0f;
+// Pair exponents (log2) below this leave the term under 2^-45 of its F_i G_j
+// prefactor (<= ~2^34): the exact W paths are skipped for them.
+constexpr float kNegligibleLog2 = -80.0f;
+// FP32 error model of a pair term (relative; unit roundoff u = 2^-24, safety
+// factor 2): exponent error from the B = theta - psi cancellation
+// (kErrAmp * |e/num| * max(x, y)), from the exponent's own operations
+// (kErrExp * |e|), and the term's MUFU/rounding error (kErrTerm). Summed into
+// a per-node margin subtracted from the lower bound.
+constexpr float kU = 5.9604645e-8f;
+constexpr float kErrAmp = 2.0f * 8.0f * kU * 0.6931472f;
+constexpr float kErrExp = 2.0f * 10.0f * kU * 0.6931472f;
+constexpr float kErrTerm = 2.0f * 6.0f * kU;
 
 __device__ __forceinline__ float ex2f(float x) {
   float y;
@@ -126,23 +135,32 @@ __device__ __forceinline__ bool norm_below(double s, double z, double z2) {
 
 // Per-warp shared-memory tables (SoA of float4 rows).
 struct WarpTables {
-  float4* r0;  // (ux, uy, uz, klo)     uhat at the cuboid centre, kappa_lo
-  float4* r1;  // (khi, eLo, st, ct)    eLo = (log phi - log W(klo)) log2e + 1/2; psi_t half-angle
-  float4* r2;  // (kst, eUs, sp, cp)    kappa at t*, (log phi - log W(kst)) log2e + 1/2, psi_t+psi_r half-angle
-  float4* r3;  // (usx, usy, usz, eHi)  uhat at t*, (log phi - log W(khi)) log2e
-  float4* c0;  // (qx, qy, qz, k2)      q_j = R0^T m_j
-  float* c1;   // e2 = (log phi2 - log W(k2)) log2e
+  float4* r0;  // (uhx, uhy, uhz, klo)   uhat at the cuboid centre (FP32 high part), kappa_lo
+  float4* r1;  // (khi, Flo, st, ct)     Flo = phi / W(klo); psi_t half-angle
+  float4* r2;  // (kst, Fst, sp, cp)     kappa at t*, phi / W(kst), half-angle of psi_t + psi_r
+  float4* r3;  // (ulx, uly, ulz, Fhi)   uhat low part (double-float), phi / W(khi)
+  float4* r4;  // (usx, usy, usz, s4)    uhat at t*, s4 = 4 sin^2((psi_t + psi_r)/2)
+  float4* c0;  // (qhx, qhy, qhz, k2)    q_j = R0^T m_j, FP32 high part
+  float4* c1;  // (qlx, qly, qlz, G)     q_j low part, G = phi2 / W(k2)
 };
+// Pair terms are F_i G_j 2^(excess log2e) W(K) (the log W(a), log W(b) and
+// log phi pieces of the reference's log_term, bounds.cpp:136/176, as linear
+// factors): the exponent then only carries the small excess, so FP32 keeps
+// ~1e-7 relative accuracy on the terms that matter. F_i multiplies row sums.
+
+constexpr int kRowF4 = 5;  // float4 per model row
+constexpr int kColF4 = 2;  // float4 per image column
 
 struct Row {
-  float ux, uy, uz, klo, khi, kst, eHi, eUb, sp, cp, usx, usy, usz;
+  float uhx, uhy, uhz, ulx, uly, ulz, klo, khi, kst, Fhi, Fst, cp2, sp2, csp2, s4, c4, usx, usy,
+      usz;
 };
 
 // Cross LB exact path: K minimum over the kappa interval (vertex case,
-// bounds.cpp:160-175) with the exact W factor.
+// bounds.cpp:160-175) with the exact W factor. s2 = 2(1 - cos B),
+// c2 = 2(1 + cos B).
 __device__ __noinline__ float cross_lb_exact(float klo, float khi, float k2, float s2, float c2,
                                              float K1, float e1) {
-  // s2 = 2(1 - cos B), c2 = 2(1 + cos B)
   const float cosb = 1.0f - 0.5f * s2;
   const float vertex = -cosb * k2;
   float kmin;
@@ -157,22 +175,38 @@ __device__ __noinline__ float cross_lb_exact(float klo, float khi, float k2, flo
   return ex2f(e1 + log2w(kmin));
 }
 
+// One cross pair (model row i x image column j). The alignment angle
+// B = max(0, theta - psi_t - psi_r) (alignment_angle_B, bounds.cpp:143-156)
+// enters as 2 sin(B/2) = (x - s4) / (2 sin(theta/2) cos(psi/2) + 2 cos(theta/2) sin(psi/2))
+// with x = |u - q|^2 = 4 sin^2(theta/2) from double-float directions and
+// s4 = 4 sin^2(psi/2) from FP64 per-row prep: the theta ~ psi cancellation
+// happens in x - s4, where both operands carry ~1e-7 relative error, instead
+// of in sin/cos products.
 template <bool kSame>
-__device__ __forceinline__ void cross_pair(const Row& r, const float4 q, const float ej, float& l,
-                                           float& u) {
-  const float k2 = q.w;
-  const float dx = r.ux - q.x, dy = r.uy - q.y, dz = r.uz - q.z;
+__device__ __forceinline__ void cross_pair(const Row& r, const float4 qa, const float4 qb, float& l,
+                                           float& u, float& me) {
+  const float k2 = qa.w;
+  const float dx = (r.uhx - qa.x) + (r.ulx - qb.x);
+  const float dy = (r.uhy - qa.y) + (r.uly - qb.y);
+  const float dz = (r.uhz - qa.z) + (r.ulz - qb.z);
   const float x = fmaf(dx, dx, fmaf(dy, dy, dz * dz));  // |u - q|^2 = 4 sin^2(theta/2)
-  const float y = fmaxf(4.0f - x, 0.0f);                // |u + q|^2
-  const float sg = sqf(x), gm = sqf(y);                 // 2 sin(theta/2), 2 cos(theta/2)
-  // B = max(0, theta - psi_t - psi_r) (alignment_angle_B, bounds.cpp:143-156)
-  float sbs = fmaf(sg, r.cp, -gm * r.sp);  // 2 sin(B/2)
-  float cbs = fmaf(gm, r.cp, sg * r.sp);   // 2 cos(B/2)
-  const bool bz = !(sbs > 0.0f);
-  sbs = bz ? 0.0f : sbs;
-  cbs = bz ? 2.0f : cbs;
-  const float s2 = sbs * sbs;  // 2(1 - cos B)
-  const float c2 = cbs * cbs;  // 2(1 + cos B)
+  // |u + q|^2 = 4 cos^2(theta/2) directly (4 - x cancels near antipodal pairs)
+  const float px = (r.uhx + qa.x) + (r.ulx + qb.x);
+  const float py = (r.uhy + qa.y) + (r.uly + qb.y);
+  const float pz = (r.uhz + qa.z) + (r.ulz + qb.z);
+  const float y = fmaf(px, px, fmaf(py, py, pz * pz));
+  // With sg = 2 sin(theta/2) = sqrt(x), gm = 2 cos(theta/2) = sqrt(y):
+  //   den^2 = (sg cp + gm sp)^2 = x cp^2 + y sp^2 + 2 sg gm cp sp
+  //   c2    = (gm cp + sg sp)^2 = y cp^2 + x sp^2 + 2 sg gm cp sp = 2(1 + cos B)
+  // so one MUFU sqrt (of x*y) serves both.
+  const float m = sqf(x * y) * r.csp2;
+  // 2 sin(B/2) * den = x - 4 sin^2(psi/2) = 4 cos^2(psi/2) - y: take the form
+  // whose operands are small (theta below / above 90 degrees).
+  float num = (x > y) ? (r.c4 - y) : (x - r.s4);
+  const bool bz = !(num > 0.0f);                        // theta <= psi: B = 0
+  num = bz ? 0.0f : num;
+  const float den2 = bz ? 1.0f : fmaf(x, r.cp2, fmaf(y, r.sp2, m));
+  const float c2 = bz ? 4.0f : fmaf(y, r.cp2, fmaf(x, r.sp2, m));
   // LB: excess at the low kappa endpoint, W(K) at K's minimum
   const float ab = r.klo * k2;
   const float amb = r.klo - k2;
@@ -180,16 +214,16 @@ __device__ __forceinline__ void cross_pair(const Row& r, const float4 q, const f
   const float rK1 = rsqf(K2lo);
   const float K1 = K2lo * rK1;
   const float D1 = K1 + r.klo + k2;
-  const float n1 = ab * s2;
   // UB: objective at (r0, t*) (class_objective cross loop, objective.cpp:212-220)
   float xs, ys;
   if (kSame) {
     xs = x;
     ys = y;
   } else {
-    const float ex = r.usx - q.x, ey = r.usy - q.y, ez = r.usz - q.z;
+    const float ex = r.usx - qa.x, ey = r.usy - qa.y, ez = r.usz - qa.z;
+    const float fx = r.usx + qa.x, fy = r.usy + qa.y, fz = r.usz + qa.z;
     xs = fmaf(ex, ex, fmaf(ey, ey, ez * ez));
-    ys = fmaxf(4.0f - xs, 0.0f);
+    ys = fmaf(fx, fx, fmaf(fy, fy, fz * fz));
   }
   const float ab2 = r.kst * k2;
   const float amb2 = r.kst - k2;
@@ -197,17 +231,24 @@ __device__ __forceinline__ void cross_pair(const Row& r, const float4 q, const f
   const float rK2 = rsqf(K2u);
   const float K2 = K2u * rK2;
   const float D2 = K2 + r.kst + k2;
-  const float n2 = ab2 * xs;
-  const float inv = rcpf(D1 * D2) * -kL2E;
-  const float e1 = fmaf(n1 * D2, inv, r.eHi + ej);  // log2 of the LB term without W(K)
-  const float e2 = fmaf(n2 * D1, inv, r.eUb + ej);  // log2 of the UB term without W(K)
+  // excess_LB = -ab (num/den)^2 / D1,  excess_UB = -ab2 xs / D2, one reciprocal
+  const float inv = rcpf(D1 * D2 * den2) * -kL2E;
+  const float g = ab * num * D2 * inv;          // e1 / num
+  const float e1 = g * num;                     // (K - a - b) log2e, LB
+  const float e2 = ab2 * xs * D1 * den2 * inv;  // (K - a - b) log2e, UB
   float t1 = ex2f(e1) * rK1;
   float t2 = ex2f(e2) * rK2;
-  if (e1 > kNegligibleLog2 && (-(1.0f - 0.5f * s2) * k2 > r.klo || !(K1 > 15.0f)))
-    t1 = cross_lb_exact(r.klo, r.khi, k2, s2, c2, K1, e1);
+  // exact paths: K's interior minimum (cos B < -klo/k2) or small K
+  if (e1 > kNegligibleLog2 && (c2 * k2 < 2.0f * (k2 - r.klo) || !(K1 > 15.0f)))
+    t1 = cross_lb_exact(r.klo, r.khi, k2, 4.0f - c2, c2, K1, e1);
   if (e2 > kNegligibleLog2 && !(K2 > 15.0f)) t2 = ex2f(e2 + log2w(K2));
-  l += t1;
-  u += t2;
+  // FP32 error estimate of the LB term (relative): B = theta - psi carries
+  // ~u theta absolute error, amplified in e1 by max(x, y)/num.
+  const float err = fmaf(fabsf(g) * fminf(x, y), kErrAmp, fmaf(fabsf(e1), kErrExp, kErrTerm));
+  const float gt1 = qb.w * t1;  // G_j; F_i is applied to the row sum
+  l += gt1;
+  me = fmaf(gt1, err, me);
+  u = fmaf(qb.w, t2, u);
 }
 
 // Self LB exact path: K's corner maximum (bounds.cpp:124-137) when cos A < 0
@@ -224,23 +265,28 @@ __device__ __noinline__ float self_lb_exact(float alo, float ahi, float blo, flo
 
 template <bool kSame>
 __device__ __forceinline__ void self_pair(const float4& a0, const float4& a1, const float4& a2,
-                                          const float3& a3, const float4& b0, const float4& b1,
-                                          const float4& b2, const float3& b3, float& l,
-                                          float& u) {
-  // spread angle A = min(pi, theta + psi_i + psi_j) (bounds.cpp:108-124)
-  const float dx = a0.x - b0.x, dy = a0.y - b0.y, dz = a0.z - b0.z;
-  const float x = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-  const float y = fmaxf(4.0f - x, 0.0f);
-  const float sg = sqf(x), gm = sqf(y);
+                                          const float3& a3, const float3& al, const float4& b0,
+                                          const float4& b1, const float4& b2, const float3& b3,
+                                          const float3& bl, float& l, float& u, float& me) {
+  // spread angle A = min(pi, theta + psi_i + psi_j) (bounds.cpp:108-124);
+  // directions are double-float (high part in a0/b0, low part in al/bl)
+  const float dx = (a0.x - b0.x) + (al.x - bl.x), dy = (a0.y - b0.y) + (al.y - bl.y),
+              dz = (a0.z - b0.z) + (al.z - bl.z);
+  const float px = (a0.x + b0.x) + (al.x + bl.x), py = (a0.y + b0.y) + (al.y + bl.y),
+              pz = (a0.z + b0.z) + (al.z + bl.z);
+  const float x = fmaf(dx, dx, fmaf(dy, dy, dz * dz));  // |u_i - u_j|^2
+  const float y = fmaf(px, px, fmaf(py, py, pz * pz));  // |u_i + u_j|^2
   const float sij = fmaf(a1.z, b1.w, a1.w * b1.z);   // sin((psi_i+psi_j)/2)
   const float cij = fmaf(a1.w, b1.w, -a1.z * b1.z);  // cos((psi_i+psi_j)/2)
-  float Ss = fmaf(sg, cij, gm * sij);                // 2 sin(A/2)
-  float Cs = fmaf(gm, cij, -sg * sij);               // 2 cos(A/2)
-  const bool api = !(cij > 0.0f) || !(Cs > 0.0f);
-  Ss = api ? 2.0f : Ss;
-  Cs = api ? 0.0f : Cs;
-  const float s2 = Ss * Ss;  // 2(1 - cos A)
-  const float c2 = Cs * Cs;  // 2(1 + cos A)
+  // With sg = sqrt(x) = 2 sin(theta/2), gm = sqrt(y) = 2 cos(theta/2):
+  //   s2 = (sg cij + gm sij)^2 = 2(1 - cos A),  c2 = (gm cij - sg sij)^2 = 2(1 + cos A);
+  // the cross products need only sg gm = sqrt(x y). A = pi once gm cij <= sg sij.
+  const float cij2 = cij * cij, sij2 = sij * sij;
+  const float m = 2.0f * cij * sij * sqf(x * y);
+  const float gc2 = y * cij2;
+  const bool api = !(cij > 0.0f) || !(gc2 > x * sij2);
+  const float s2 = api ? 4.0f : fmaf(x, cij2, fmaf(y, sij2, m));
+  const float c2 = api ? 0.0f : fmaf(x, sij2, gc2 - m);
   // LB: excess at the high corner, W(K) at K's corner maximum
   const float ahi = a1.x, bhi = b1.x;
   const float hh = ahi * bhi;
@@ -257,8 +303,9 @@ __device__ __forceinline__ void self_pair(const float4& a0, const float4& a1, co
     ys = y;
   } else {
     const float ex = a3.x - b3.x, ey = a3.y - b3.y, ez = a3.z - b3.z;
+    const float fx = a3.x + b3.x, fy = a3.y + b3.y, fz = a3.z + b3.z;
     xs = fmaf(ex, ex, fmaf(ey, ey, ez * ez));
-    ys = fmaxf(4.0f - xs, 0.0f);
+    ys = fmaf(fx, fx, fmaf(fy, fy, fz * fz));
   }
   const float ka = a2.x, kb = b2.x;
   const float ab2 = ka * kb;
@@ -269,51 +316,61 @@ __device__ __forceinline__ void self_pair(const float4& a0, const float4& a1, co
   const float D2 = K2 + ka + kb;
   const float n2 = ab2 * xs;
   const float inv = rcpf(D1 * D2) * -kL2E;
-  const float e1 = fmaf(n1 * D2, inv, a1.y + b1.y);  // eLo carry +1/2 each: factor 2
-  const float e2 = fmaf(n2 * D1, inv, a2.y + b2.y);  // eUs carry +1/2 each: factor 2
+  const float e1 = n1 * D2 * inv;
+  const float e2 = n2 * D1 * inv;
   float t1 = ex2f(e1) * rKhh;
   float t2 = ex2f(e2) * rK2;
   if (e1 > kNegligibleLog2 && (c2 < 2.0f || !(Khh > 15.0f)))
     t1 = self_lb_exact(a0.w, ahi, b0.w, bhi, c2, K2hh, e1);
   if (e2 > kNegligibleLog2 && !(K2 > 15.0f)) t2 = ex2f(e2 + log2w(K2));
-  l += t1;
-  u += t2;
+  const float ft1 = b1.y * t1;  // F_j (Flo); 2 F_i is applied to the row sum
+  l += ft1;
+  me = fmaf(ft1, fmaf(fabsf(e1), kErrExp, kErrTerm), me);
+  u = fmaf(b2.y, t2, u);  // F_j (Fst)
 }
 
 __device__ __forceinline__ Row load_row(const WarpTables& T, int i) {
-  const float4 a0 = T.r0[i], a1 = T.r1[i], a2 = T.r2[i], a3 = T.r3[i];
+  const float4 a0 = T.r0[i], a1 = T.r1[i], a2 = T.r2[i], a3 = T.r3[i], a4 = T.r4[i];
   Row r;
-  r.ux = a0.x;
-  r.uy = a0.y;
-  r.uz = a0.z;
+  r.uhx = a0.x;
+  r.uhy = a0.y;
+  r.uhz = a0.z;
   r.klo = a0.w;
   r.khi = a1.x;
   r.kst = a2.x;
-  r.eUb = a2.y - 0.5f;
-  r.sp = a2.z;
-  r.cp = a2.w;
-  r.usx = a3.x;
-  r.usy = a3.y;
-  r.usz = a3.z;
-  r.eHi = a3.w;
+  r.Fst = a2.y;
+  r.sp2 = a2.z * a2.z;
+  r.cp2 = a2.w * a2.w;
+  r.csp2 = 2.0f * a2.z * a2.w;
+  r.c4 = 4.0f * r.cp2;
+  r.ulx = a3.x;
+  r.uly = a3.y;
+  r.ulz = a3.z;
+  r.Fhi = a3.w;
+  r.usx = a4.x;
+  r.usy = a4.y;
+  r.usz = a4.z;
+  r.s4 = a4.w;
   return r;
 }
 
 template <bool kSame>
 __device__ __forceinline__ void class_pairs(const WarpTables& T, const ClassSpan cs, int lane,
                                             float w, double& lb_self, double& lb_cross,
-                                            double& ub_self, double& ub_cross) {
+                                            double& ub_self, double& ub_cross, double& lb_err) {
   const int n = cs.n1;
   // Cross terms: rows over lanes, columns broadcast.
   for (int base = 0; base < n; base += 32) {
     const int il = base + lane;
     if (il < n) {
       const Row r = load_row(T, cs.o1 + il);
-      float l = 0.0f, u = 0.0f;
+      float l = 0.0f, u = 0.0f, me = 0.0f;
 #pragma unroll 2
-      for (int j = cs.o2; j < cs.o2 + cs.n2; ++j) cross_pair<kSame>(r, T.c0[j], T.c1[j], l, u);
-      lb_cross += static_cast<double>(w * l);
-      ub_cross += static_cast<double>(w * u);
+      for (int j = cs.o2; j < cs.o2 + cs.n2; ++j)
+        cross_pair<kSame>(r, T.c0[j], T.c1[j], l, u, me);
+      lb_cross += static_cast<double>(w * r.Fhi * l);
+      lb_err += static_cast<double>(2.0f * w * r.Fhi * me);
+      ub_cross += static_cast<double>(w * r.Fst * u);
     }
   }
   // Self terms i<j via the circulant schedule: every unordered pair once as
@@ -326,55 +383,80 @@ __device__ __forceinline__ void class_pairs(const WarpTables& T, const ClassSpan
       const int i = cs.o1 + il;
       const float4 a0 = T.r0[i], a1 = T.r1[i], a2 = T.r2[i];
       float3 a3 = make_float3(0.f, 0.f, 0.f);
-      if (!kSame) a3 = make_float3(T.r3[i].x, T.r3[i].y, T.r3[i].z);
-      float l = 0.0f, u = 0.0f;
+      if (!kSame) a3 = make_float3(T.r4[i].x, T.r4[i].y, T.r4[i].z);
+      const float3 al = make_float3(T.r3[i].x, T.r3[i].y, T.r3[i].z);
+      float l = 0.0f, u = 0.0f, me = 0.0f;
       int jl = il;
 #pragma unroll 2
       for (int d = 1; d <= dfull; ++d) {
         jl = (jl + 1 == n) ? 0 : jl + 1;
         const int j = cs.o1 + jl;
         float3 b3 = make_float3(0.f, 0.f, 0.f);
-        if (!kSame) b3 = make_float3(T.r3[j].x, T.r3[j].y, T.r3[j].z);
-        self_pair<kSame>(a0, a1, a2, a3, T.r0[j], T.r1[j], T.r2[j], b3, l, u);
+        if (!kSame) b3 = make_float3(T.r4[j].x, T.r4[j].y, T.r4[j].z);
+        const float4 bl = T.r3[j];
+        self_pair<kSame>(a0, a1, a2, a3, al, T.r0[j], T.r1[j], T.r2[j], b3,
+                         make_float3(bl.x, bl.y, bl.z), l, u, me);
       }
       if (even && il < n / 2) {
         const int j = i + n / 2;
         float3 b3 = make_float3(0.f, 0.f, 0.f);
-        if (!kSame) b3 = make_float3(T.r3[j].x, T.r3[j].y, T.r3[j].z);
-        self_pair<kSame>(a0, a1, a2, a3, T.r0[j], T.r1[j], T.r2[j], b3, l, u);
+        if (!kSame) b3 = make_float3(T.r4[j].x, T.r4[j].y, T.r4[j].z);
+        const float4 bl = T.r3[j];
+        self_pair<kSame>(a0, a1, a2, a3, al, T.r0[j], T.r1[j], T.r2[j], b3,
+                         make_float3(bl.x, bl.y, bl.z), l, u, me);
       }
-      lb_self += static_cast<double>(w * l);
-      ub_self += static_cast<double>(w * u);
+      lb_self += static_cast<double>(2.0f * w * a1.y * l);
+      lb_err += static_cast<double>(2.0f * w * a1.y * me);
+      ub_self += static_cast<double>(2.0f * w * a2.y * u);
     }
   }
 }
 
-// Half-angle of psi_trans (se3.cpp:72-92) for a mean outside the cuboid:
-// the vertex with the largest angle to the centre direction is the one with
-// the smallest cosine c_hat . v_hat; returns sin/cos of half that angle as
-// |c_hat - v_hat|/2, |c_hat + v_hat|/2.
-__device__ __forceinline__ void psi_trans_half(float ux, float uy, float uz, float h0, float h1,
-                                               float h2, float cx, float cy, float cz, float& st,
-                                               float& ct) {
-  float best = 2.0f, bx = 0.f, by = 0.f, bz = 0.f;
+// Half-angle of psi_trans (se3.cpp:72-92) for a mean outside the cuboid: the
+// vertex with the largest angle to the centre direction has the smallest
+// cosine c_hat . v_hat. FP32 picks the candidates (every vertex within 1e-6 of
+// the best cosine), FP64 evaluates them: returns sin and cos of half the
+// angle as |c_hat - v_hat|/2 and |c_hat + v_hat|/2.
+__device__ __forceinline__ void psi_trans_half(double u0, double u1, double u2, double h0,
+                                               double h1, double h2, double c0, double c1,
+                                               double c2, double& st, double& ct) {
+  const float fu0 = static_cast<float>(u0), fu1 = static_cast<float>(u1),
+              fu2 = static_cast<float>(u2);
+  const float fh0 = static_cast<float>(h0), fh1 = static_cast<float>(h1),
+              fh2 = static_cast<float>(h2);
+  const float fc0 = static_cast<float>(c0), fc1 = static_cast<float>(c1),
+              fc2 = static_cast<float>(c2);
+  float cosv[8];
+  float best = 2.0f;
 #pragma unroll
   for (int s = 0; s < 8; ++s) {
-    const float vx = ux - ((s & 4) ? h0 : -h0);
-    const float vy = uy - ((s & 2) ? h1 : -h1);
-    const float vz = uz - ((s & 1) ? h2 : -h2);
+    const float vx = fu0 - ((s & 4) ? fh0 : -fh0);
+    const float vy = fu1 - ((s & 2) ? fh1 : -fh1);
+    const float vz = fu2 - ((s & 1) ? fh2 : -fh2);
     const float rv = rsqf(fmaf(vx, vx, fmaf(vy, vy, vz * vz)));
-    const float cs = fmaf(cx, vx, fmaf(cy, vy, cz * vz)) * rv;
-    if (cs < best) {
-      best = cs;
-      bx = vx * rv;
-      by = vy * rv;
-      bz = vz * rv;
+    cosv[s] = fmaf(fc0, vx, fmaf(fc1, vy, fc2 * vz)) * rv;
+    best = fminf(best, cosv[s]);
+  }
+  double bs = -1.0, bc = 0.0;
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    if (cosv[s] <= best + 1e-6f) {
+      const double vx = u0 - ((s & 4) ? h0 : -h0);
+      const double vy = u1 - ((s & 2) ? h1 : -h1);
+      const double vz = u2 - ((s & 1) ? h2 : -h2);
+      const double iv = rsqrt(vx * vx + vy * vy + vz * vz);
+      const double wx = vx * iv, wy = vy * iv, wz = vz * iv;
+      const double ex = c0 - wx, ey = c1 - wy, ez = c2 - wz;
+      const double sd = ex * ex + ey * ey + ez * ez;
+      if (sd > bs) {
+        bs = sd;
+        const double px = c0 + wx, py = c1 + wy, pz = c2 + wz;
+        bc = px * px + py * py + pz * pz;
+      }
     }
   }
-  const float ex = cx - bx, ey = cy - by, ez = cz - bz;
-  const float px = cx + bx, py = cy + by, pz = cz + bz;
-  st = 0.5f * sqf(fmaf(ex, ex, fmaf(ey, ey, ez * ez)));
-  ct = 0.5f * sqf(fmaf(px, px, fmaf(py, py, pz * pz)));
+  st = 0.5 * sqrt(bs);
+  ct = 0.5 * sqrt(bc);
 }
 
 __global__ void __launch_bounds__(kWarpsPerCta * 32, 5)
@@ -383,15 +465,16 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 5)
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int N1 = ctx.n1_total, N2 = ctx.n2_total;
-  const size_t per_warp_f4 = static_cast<size_t>(4 * N1 + N2) + (N2 + 3) / 4;
+  const size_t per_warp_f4 = static_cast<size_t>(kRowF4 * N1 + kColF4 * N2);
   float4* base = smem4 + warp * per_warp_f4;
   WarpTables T;
   T.r0 = base;
   T.r1 = T.r0 + N1;
   T.r2 = T.r1 + N1;
   T.r3 = T.r2 + N1;
-  T.c0 = T.r3 + N1;
-  T.c1 = reinterpret_cast<float*>(T.c0 + N2);
+  T.r4 = T.r3 + N1;
+  T.c0 = T.r4 + N1;
+  T.c1 = T.c0 + N2;
 
   const double zeta = ctx.zeta;
   const double zeta2 = zeta * zeta;
@@ -456,13 +539,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 5)
         }
     }
     const double psi_r = fmin(sqrt(3.0) * rhw, M_PI);
-    float s_r, c_r;
-    {
-      double s, c;
-      sincos(0.5 * psi_r, &s, &c);
-      s_r = static_cast<float>(s);
-      c_r = static_cast<float>(c);
-    }
+    double s_r, c_r;
+    sincos(0.5 * psi_r, &s_r, &c_r);
 
     // ---- feasible_center (bounds.cpp:187-214): t*, warp-cooperative scan
     double ts0 = tc0, ts1 = tc1, ts2 = tc2;
@@ -517,10 +595,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 5)
     const bool same = (ts0 == tc0) && (ts1 == tc1) && (ts2 == tc2);
 
     // ---- per-row prep (all classes): kappa interval, psi_t, projections
-    double lb_self = 0.0, lb_cross = 0.0, ub_self = 0.0, ub_cross = 0.0;
-    float st_max = 0.0f;
-    const float fh0 = static_cast<float>(h0), fh1 = static_cast<float>(h1),
-                fh2 = static_cast<float>(h2);
+    double lb_self = 0.0, lb_cross = 0.0, ub_self = 0.0, ub_cross = 0.0, lb_err = 0.0;
+    double st_max = 0.0;
     for (int c = 0; c < ctx.n_classes; ++c) {
       const ClassSpan cs = ctx.cls[c];
       const float w = static_cast<float>(ctx.cls_w[c]);
@@ -538,54 +614,59 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 5)
         const float klo = static_cast<float>(dlo2 * is2 + 1.0);
         const float khi = static_cast<float>(dhi2 * is2 + 1.0);
         const double un2 = u0 * u0 + u1 * u1 + u2 * u2;
-        float ux = 1.0f, uy = 0.0f, uz = 0.0f;
+        double c0 = 1.0, c1 = 0.0, c2 = 0.0;  // UnitX when the mean is at the centre
         if (un2 > 1e-24) {
           const double inv = rsqrt(un2);
-          ux = static_cast<float>(u0 * inv);
-          uy = static_cast<float>(u1 * inv);
-          uz = static_cast<float>(u2 * inv);
+          c0 = u0 * inv;
+          c1 = u1 * inv;
+          c2 = u2 * inv;
         }
-        float st, ct;
+        double st, ct;
         if (a0 <= h0 && a1 <= h1 && a2 <= h2) {
-          st = 1.0f;  // psi_t = pi
-          ct = 0.0f;
+          st = 1.0;  // psi_t = pi
+          ct = 0.0;
         } else {
-          psi_trans_half(static_cast<float>(u0), static_cast<float>(u1), static_cast<float>(u2),
-                         fh0, fh1, fh2, ux, uy, uz, st, ct);
+          psi_trans_half(u0, u1, u2, h0, h1, h2, c0, c1, c2, st, ct);
         }
-        st_max = fmaxf(st_max, st);
+        st_max = fmax(st_max, st);
         // half-angle of psi_t + psi_r; B = 0 once the sum reaches pi
-        float sp = fmaf(st, c_r, ct * s_r);
-        float cp = fmaf(ct, c_r, -st * s_r);
-        if (!(cp > 0.0f)) {
-          sp = 1.0f;
-          cp = 0.0f;
+        double sp = st * c_r + ct * s_r;
+        double cp = ct * c_r - st * s_r;
+        if (!(cp > 0.0)) {
+          sp = 1.0;
+          cp = 0.0;
         }
         // UB projection at t* (project_model, objective.cpp:175-192)
         const double v0 = m0 - ts0, v1 = m1 - ts1, v2 = m2 - ts2;
         const double vn2 = v0 * v0 + v1 * v1 + v2 * v2;
         const float kst = static_cast<float>(vn2 * is2 + 1.0);
         const double iv = rsqrt(vn2);
-        const float lphi = ctx.log_phi1[i];
         const float phi = static_cast<float>(ctx.phi1[i]);
         dsl += diag_term(phi, klo);
         dsu += diag_term(phi, kst);
-        const float lwlo = log2w(klo), lwhi = log2w(khi), lwst = log2w(kst);
-        const float lp2 = lphi * kL2E;
-        T.r0[i] = make_float4(ux, uy, uz, klo);
-        T.r1[i] = make_float4(khi, lp2 - lwlo + 0.5f, st, ct);
-        T.r2[i] = make_float4(kst, lp2 - lwst + 0.5f, sp, cp);
-        T.r3[i] = make_float4(static_cast<float>(v0 * iv), static_cast<float>(v1 * iv),
-                              static_cast<float>(v2 * iv), lp2 - lwhi);
+        // phi / W(k) = phi * k / (1 - e^{-2k}) (k >= 1)
+        const float Flo = phi * klo * rcpf(1.0f - ex2f(-2.0f * kL2E * klo));
+        const float Fhi = phi * khi * rcpf(1.0f - ex2f(-2.0f * kL2E * khi));
+        const float Fst = phi * kst * rcpf(1.0f - ex2f(-2.0f * kL2E * kst));
+        const float uhx = static_cast<float>(c0), uhy = static_cast<float>(c1),
+                    uhz = static_cast<float>(c2);
+        T.r0[i] = make_float4(uhx, uhy, uhz, klo);
+        T.r1[i] = make_float4(khi, Flo, static_cast<float>(st), static_cast<float>(ct));
+        T.r2[i] = make_float4(kst, Fst, static_cast<float>(sp), static_cast<float>(cp));
+        T.r3[i] = make_float4(static_cast<float>(c0 - uhx), static_cast<float>(c1 - uhy),
+                              static_cast<float>(c2 - uhz), Fhi);
+        T.r4[i] = make_float4(static_cast<float>(v0 * iv), static_cast<float>(v1 * iv),
+                              static_cast<float>(v2 * iv), static_cast<float>(4.0 * sp * sp));
       }
       if (!infeasible) {
         lb_self += static_cast<double>(w * dsl);
+        lb_err += static_cast<double>(w * dsl * kErrTerm);
         ub_self += static_cast<double>(w * dsu);
       }
     }
     // split decision (subdivide_adaptive, se3.cpp:107-121)
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) st_max = fmaxf(st_max, __shfl_xor_sync(kFull, st_max, o));
+    for (int o = 16; o > 0; o >>= 1) st_max = fmax(st_max, __shfl_xor_sync(kFull, st_max, o));
     if (lane == 0 && args.split_rot) {
       const bool rot_ok = rhw > 1e-9;
       const bool trans_ok = fmax(fmax(h0, h1), h2) > 1e-9;
@@ -605,14 +686,17 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 5)
       __syncwarp();
       continue;
     }
-    // ---- per-column prep: q_j = R0^T m_j (bounds.cpp:97-102)
+    // ---- per-column prep: q_j = R0^T m_j (bounds.cpp:97-102), double-float
     for (int j = lane; j < N2; j += 32) {
       const double x0 = ctx.m[3 * j], x1 = ctx.m[3 * j + 1], x2 = ctx.m[3 * j + 2];
-      const float q0 = static_cast<float>(R[0] * x0 + R[3] * x1 + R[6] * x2);
-      const float q1 = static_cast<float>(R[1] * x0 + R[4] * x1 + R[7] * x2);
-      const float q2 = static_cast<float>(R[2] * x0 + R[5] * x1 + R[8] * x2);
-      T.c0[j] = make_float4(q0, q1, q2, ctx.kappa2[j]);
-      T.c1[j] = ctx.e2[j];
+      const double q0 = R[0] * x0 + R[3] * x1 + R[6] * x2;
+      const double q1 = R[1] * x0 + R[4] * x1 + R[7] * x2;
+      const double q2 = R[2] * x0 + R[5] * x1 + R[8] * x2;
+      const float f0 = static_cast<float>(q0), f1 = static_cast<float>(q1),
+                  f2 = static_cast<float>(q2);
+      T.c0[j] = make_float4(f0, f1, f2, ctx.kappa2[j]);
+      T.c1[j] = make_float4(static_cast<float>(q0 - f0), static_cast<float>(q1 - f1),
+                            static_cast<float>(q2 - f2), ctx.g2[j]);
     }
     __syncwarp();
 
@@ -621,19 +705,22 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 5)
       const ClassSpan cs = ctx.cls[c];
       const float w = static_cast<float>(ctx.cls_w[c]);
       if (same) {
-        class_pairs<true>(T, cs, lane, w, lb_self, lb_cross, ub_self, ub_cross);
+        class_pairs<true>(T, cs, lane, w, lb_self, lb_cross, ub_self, ub_cross, lb_err);
       } else {
-        class_pairs<false>(T, cs, lane, w, lb_self, lb_cross, ub_self, ub_cross);
+        class_pairs<false>(T, cs, lane, w, lb_self, lb_cross, ub_self, ub_cross, lb_err);
       }
     }
     lb_self = warp_sum_d(lb_self);
     lb_cross = warp_sum_d(lb_cross);
     ub_self = warp_sum_d(ub_self);
     ub_cross = warp_sum_d(ub_cross);
+    lb_err = warp_sum_d(lb_err);
     if (lane == 0) {
-      // Soundness margin proportional to the |term| mass (all terms >= 0).
+      // Soundness margin: the FP32 error estimate of the terms plus a relative
+      // floor on the |term| mass (all terms >= 0).
       const double mass = lb_self + 2.0 * lb_cross;
-      const double core = (lb_self - 2.0 * lb_cross) - ctx.lb_margin * mass;
+      const double core =
+          (lb_self - 2.0 * lb_cross) - ctx.lb_err_scale * lb_err - ctx.lb_margin * mass;
       const double lo = core < parent_lower ? parent_lower : core;  // std::max(core, lower)
       double up = INFINITY;
       if (!(lo >= args.skip_upper_at) && have_center) up = ub_self - 2.0 * ub_cross;
@@ -647,7 +734,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 5)
 }  // namespace
 
 size_t eval_smem_per_warp(const DevCtx& ctx) {
-  const size_t f4 = static_cast<size_t>(4 * ctx.n1_total + ctx.n2_total) + (ctx.n2_total + 3) / 4;
+  const size_t f4 = static_cast<size_t>(kRowF4 * ctx.n1_total + kColF4 * ctx.n2_total);
   return f4 * sizeof(float4);
 }
 

@@ -78,8 +78,8 @@ int ctx_upload(gosma_ctx* ctx) {
     for (int j = 0; j < c.n2(); ++j) {
       for (int a = 0; a < 3; ++a) m.push_back(c.b[3 * j + a] / c.kappa2[j]);
       kappa2.push_back(static_cast<float>(c.kappa2[j]));
-      const double lp = c.phi2[j] > 0.0 ? std::log(c.phi2[j]) : -1e30;
-      e2.push_back(static_cast<float>((lp - logw_host(c.kappa2[j])) * 1.4426950408889634));
+      const double k = c.kappa2[j];
+      e2.push_back(static_cast<float>(c.phi2[j] * k / -std::expm1(-2.0 * k)));  // phi2 / W(k)
     }
     o1 += c.n1();
     o2 += c.n2();
@@ -92,6 +92,7 @@ int ctx_upload(gosma_ctx* ctx) {
   d.max_n1 = max_n1;
   d.zeta = hm.zeta;
   d.lb_margin = ctx->lb_margin;
+  d.lb_err_scale = 1.0;
   ClassSpan* dspans;
   if ((e = upload(spans, &dspans)) != cudaSuccess) return cuda_error(e, "ctx upload");
   d.cls = dspans;
@@ -109,7 +110,7 @@ int ctx_upload(gosma_ctx* ctx) {
   d.m = dm;
   d.log_phi1 = dlp;
   d.kappa2 = dk2;
-  d.e2 = de2;
+  d.g2 = de2;
   ctx->owned = {dspans, dw, dmu, dis2, dphi, dm, dlp, dk2, de2};
   if ((e = cudaMalloc(&ctx->d_work, sizeof(unsigned int))) != cudaSuccess)
     return cuda_error(e, "ctx upload");
@@ -304,6 +305,7 @@ int gosma_ctx_blurred(const gosma_ctx* src, double w, double reference_distance,
   if (rc == GOSMA_OK) {
     (*out)->lb_margin = src->lb_margin;
     (*out)->dev.lb_margin = src->lb_margin;
+    (*out)->dev.lb_err_scale = src->dev.lb_err_scale;
   }
   return rc;
 }
@@ -321,10 +323,16 @@ double gosma_ctx_image_self_energy(const gosma_ctx* ctx) {
 double gosma_ctx_zeta(const gosma_ctx* ctx) { return ctx ? ctx->model.zeta : NAN; }
 
 int gosma_ctx_set_lb_margin(gosma_ctx* ctx, double rel) {
-  if (!ctx || !(rel >= 0.0) || !(rel < 1e-2))
-    return set_error(GOSMA_EINVAL, "lb margin must be in [0, 1e-2)");
+  if (!ctx || !(rel < 1e-2)) return set_error(GOSMA_EINVAL, "lb margin must be below 1e-2");
+  if (rel < 0.0) {  // raw FP32 core: no error estimate, no floor (parity diagnostics)
+    ctx->lb_margin = 0.0;
+    ctx->dev.lb_margin = 0.0;
+    ctx->dev.lb_err_scale = 0.0;
+    return GOSMA_OK;
+  }
   ctx->lb_margin = rel;
   ctx->dev.lb_margin = rel;
+  ctx->dev.lb_err_scale = 1.0;
   return GOSMA_OK;
 }
 

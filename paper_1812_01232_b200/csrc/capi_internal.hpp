@@ -39,7 +39,7 @@ struct DeviceGuard {
 };
 
 // Default relative LB soundness margin (x |term| mass); see DESIGN.md.
-constexpr double kDefaultLbMargin = 2e-6;
+constexpr double kDefaultLbMargin = 2e-7;
 
 }  // namespace gosma
 

@@ -41,9 +41,10 @@ struct DevCtx {
   const float* log_phi1; // N1 (kLogZeroWeight for 0)
   const double* m;       // 3*N2, b_j / kappa_j (bounds.cpp:100)
   const float* kappa2;   // N2
-  const float* e2;       // N2, (log phi2 - log W(kappa2)) * log2e
+  const float* g2;       // N2, phi2 / W(kappa2), W(k) = (1 - e^{-2k}) / k
   double zeta;
-  double lb_margin;      // relative soundness margin (x |term| mass)
+  double lb_margin;      // relative soundness floor (x |term| mass)
+  double lb_err_scale;   // 1: subtract the FP32 error estimate; 0: raw core (diagnostics)
 };
 
 // Host-side master copy of one class (ClassData, objective.hpp:19-31).

@@ -9,7 +9,7 @@ from oracle.bind import Oracle, Mixture
 def run(regime, n1, n2, n, seed, zeta, kcap=150.0, ncls=1, **kw):
     cls = synth.mixture(n1, n2, regime, seed=seed, kappa_cap=kcap, n_classes=ncls)
     ctx = g.ObjectiveContext(cls, zeta)
-    ctx.set_lb_margin(0.0)
+    ctx.set_lb_margin(-1.0)
     nodes = synth.nodes(n, seed=seed + 1, **kw)
     lo, up, sp = g.evaluate_branch_batch(ctx, nodes, return_split=True)
     o = Oracle(Mixture(**synth.to_mixture_arrays(cls, zeta)))

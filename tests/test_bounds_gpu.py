@@ -1,0 +1,314 @@
+"""Parity of the CUDA bound kernel (through the C ABI) with the oracle and the
+reference's golden vectors.
+
+Tolerance. Pair terms are FP32 (FP64 sums), so
+agreement is stated relative to the node's |term| mass M (sum of |pair
+contributions|, from the oracle):
+  * raw FP32 core (ctx.set_lb_margin(-1)):  |LB - LB_ref| <= 2e-5 M
+    (typically <= 1e-6 M; the bound is set by B = theta - psi at large
+    concentrations, where FP32 resolves B only to ~u*theta),
+  * certified LB (default): the kernel subtracts its own per-term FP32 error
+    estimate + 2e-7 M, so  LB <= LB_ref (sound)  and  LB >= LB_ref - 5e-5 M,
+  * UB: |UB - UB_ref| <= 2e-6 M_ub.
+Infeasible branches ({+inf, +inf}) must match exactly.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from oracle.bind import Mixture, Oracle
+
+pytestmark = pytest.mark.gpu
+
+TOL_RAW = 2e-5
+TOL_CERT = 5e-5
+TOL_UB = 2e-6
+
+
+def mix_classes(mix):
+    classes, o1, o2 = [], 0, 0
+    for c in range(len(mix.n1)):
+        a, b = int(mix.n1[c]), int(mix.n2[c])
+        classes.append({"mu": mix.mu[o1:o1 + a], "sigma2": mix.sigma2[o1:o1 + a],
+                        "phi1": mix.phi1[o1:o1 + a], "dir": mix.dir[o2:o2 + b],
+                        "kappa2": mix.kappa2[o2:o2 + b], "phi2": mix.phi2[o2:o2 + b],
+                        "weight": float(mix.class_weight[c])})
+        o1, o2 = o1 + a, o2 + b
+    return classes
+
+
+def gpu_ctx(g, mix, margin=None):
+    ctx = g.ObjectiveContext(mix_classes(mix), mix.zeta)
+    if margin is not None:
+        ctx.set_lb_margin(margin)
+    return ctx
+
+
+def check_parity(g, mix, nodes, skip=float("inf"), ref=None, check_split=True):
+    nodes = np.ascontiguousarray(nodes, dtype=np.float64).reshape(-1, 11)
+    ctx = gpu_ctx(g, mix)
+    lo, up, split = g.evaluate_branch_batch(ctx, nodes, skip_upper_at=skip, return_split=True)
+    ctx.set_lb_margin(-1.0)
+    raw, _ = g.evaluate_branch_batch(ctx, nodes, skip_upper_at=skip)
+    o = Oracle(mix)
+    rlo, rup, lm, um, rsplit = o.eval_bounds(nodes, skip=skip, threads=8)
+    if ref is not None:  # golden values from the reference itself
+        rlo, rup = np.asarray(ref[0]), np.asarray(ref[1])
+    assert np.array_equal(np.isinf(lo), np.isinf(rlo)), "feasibility pattern differs"
+    f = np.isfinite(rlo)
+    # parent floors (lower = max(core, parent)) make some rows exact
+    err_raw = np.abs(raw[f] - rlo[f])
+    assert np.all(err_raw <= TOL_RAW * lm[f] + 1e-12), \
+        f"raw LB max err/mass {np.max(err_raw / lm[f]):.3e}"
+    assert np.all(lo[f] <= rlo[f] + 1e-9 * lm[f] + 1e-12), "certified LB above the FP64 LB"
+    assert np.all(lo[f] >= rlo[f] - TOL_CERT * lm[f] - 1e-12), \
+        f"certified LB too loose: {np.max((rlo[f] - lo[f]) / lm[f]):.3e}"
+    # the UB is +inf exactly where the LB reaches skip_upper_at or no feasible centre exists
+    assert np.array_equal(np.isinf(up) & ~np.isinf(lo), np.isinf(rup) & ~np.isinf(rlo)) or \
+        np.isfinite(skip), "upper-bound inf pattern differs"
+    fu = np.isfinite(rup) & np.isfinite(up)
+    err_up = np.abs(up[fu] - rup[fu])
+    assert np.all(err_up <= TOL_UB * um[fu] + 1e-12), \
+        f"UB max err/mass {np.max(err_up / um[fu]):.3e}"
+    if check_split:
+        agree = split == rsplit
+        if not agree.all():
+            # only near-ties of psi_r vs max psi_t may differ (FP32 half-angles)
+            for k in np.flatnonzero(~agree):
+                n = nodes[k]
+                psi_r = min(math.sqrt(3) * n[3], math.pi)
+                pt = max(o.psi_trans(n[4:7], n[7:10], m) for m in mix.mu)
+                assert abs(psi_r - pt) < 1e-5, f"split differs away from a tie at node {k}"
+    return lo, up
+
+
+def test_golden_vectors(gosma, golden_bounds):
+    for case in golden_bounds["cases"]:
+        mix = Mixture.from_dict(case["mixture"])
+        for res in case["results"]:
+            check_parity(gosma, mix, np.array(case["nodes"]), skip=res["skip"],
+                         ref=(res["lower"], res["upper"]))
+
+
+def rand_mix(rng, n1, n2, kcap=150.0, zeta=0.2, ncls=1):
+    from tests.golden.make_golden import random_context
+    return random_context(rng, n1, n2, kcap, zeta, n_classes=ncls)
+
+
+def rand_nodes(rng, n):
+    from tests.golden.make_golden import random_nodes
+    return random_nodes(rng, n)
+
+
+@pytest.mark.parametrize("n1,n2,kcap,zeta,ncls", [
+    (4, 3, 40.0, 0.2, 1), (3, 3, 150.0, 0.15, 1), (1, 1, 20.0, 0.2, 1), (33, 17, 150.0, 0.2, 1),
+    (64, 32, 150.0, 0.2, 1), (5, 4, 60.0, 0.2, 3), (2, 7, 1e4, 0.2, 4)])
+def test_moderate_regimes(gosma, n1, n2, kcap, zeta, ncls):
+    rng = np.random.default_rng(1000 + n1 * 7 + n2)
+    check_parity(gosma, rand_mix(rng, n1, n2, kcap, zeta, ncls), rand_nodes(rng, 1500))
+
+
+@pytest.mark.parametrize("n1,n2", [(8, 6), (64, 32), (45, 40), (128, 64)])
+def test_realistic_regime(gosma, n1, n2):
+    from paper_1812_01232_b200 import synth
+    classes = synth.mixture(n1, n2, "realistic", seed=n1 * 31 + n2)
+    mix = Mixture(**synth.to_mixture_arrays(classes, 0.5))
+    nodes = synth.nodes(800, seed=n1 + n2).view(np.float64).reshape(-1, 11)
+    check_parity(gosma, mix, nodes)
+
+
+def test_large_mixtures_config5(gosma):
+    # configs[4]: 256 GMM x 128 vMF (P = 65408)
+    from paper_1812_01232_b200 import synth
+    classes = synth.mixture(256, 128, "realistic", seed=5)
+    mix = Mixture(**synth.to_mixture_arrays(classes, 0.5))
+    nodes = synth.nodes(60, seed=6).view(np.float64).reshape(-1, 11)
+    check_parity(gosma, mix, nodes)
+
+
+def test_extreme_concentrations(gosma):
+    # test_bounds.cpp:161-196: sigma2 = 6.25e-4, kappa2 = 1e5
+    d1 = np.array([0.1, 0.0, 1.0]) / np.linalg.norm([0.1, 0.0, 1.0])
+    d2 = np.array([-0.1, 0.1, 1.0]) / np.linalg.norm([-0.1, 0.1, 1.0])
+    mix = Mixture([2], [2], [1.0], [[0.4, -0.2, 0.1], [-0.5, 0.3, -0.2]], [6.25e-4, 6.25e-4],
+                  [0.5, 0.5], [d1, d2], [1e5, 1e5], [0.5, 0.5], 0.5)
+    rng = np.random.default_rng(97)
+    nodes = np.zeros((1000, 11))
+    nodes[:, 0:3] = rng.uniform(-2, 2, (1000, 3))
+    nodes[:, 3] = rng.uniform(0.1, math.pi, 1000)
+    nodes[:, 4:7] = rng.uniform(-4, 4, (1000, 3))
+    nodes[:, 7:10] = rng.uniform(0.1, 1.0, (1000, 3))
+    nodes[:, 10] = -math.inf
+    lo, up = check_parity(gosma, mix, nodes)
+    f = np.isfinite(lo)
+    assert f.sum() > 300 and np.all(lo[f] <= up[f] + 1e-9)
+
+
+def test_skip_upper_at(gosma):
+    rng = np.random.default_rng(5)
+    mix = rand_mix(rng, 6, 5)
+    nodes = rand_nodes(rng, 500)
+    ctx = gpu_ctx(gosma, mix)
+    lo, up = gosma.evaluate_branch_batch(ctx, nodes)
+    skip = float(np.median(lo[np.isfinite(lo)]))
+    lo2, up2 = gosma.evaluate_branch_batch(ctx, nodes, skip_upper_at=skip)
+    assert np.array_equal(lo, lo2)
+    assert np.all(np.isinf(up2[lo2 >= skip]))
+    keep = lo2 < skip
+    assert np.array_equal(up2[keep], up[keep])
+    check_parity(gosma, mix, nodes, skip=skip)
+
+
+def test_empty_single_and_order_invariance(gosma):
+    rng = np.random.default_rng(6)
+    mix = rand_mix(rng, 7, 4)
+    ctx = gpu_ctx(gosma, mix)
+    lo, up = gosma.evaluate_branch_batch(ctx, np.zeros((0, 11)))
+    assert lo.shape == (0,) and up.shape == (0,)
+    nodes = rand_nodes(rng, 300)
+    lo, up = gosma.evaluate_branch_batch(ctx, nodes)
+    lo_b, up_b = gosma.evaluate_branch_batch(ctx, nodes)
+    assert np.array_equal(lo, lo_b) and np.array_equal(up, up_b)  # deterministic
+    perm = rng.permutation(len(nodes))
+    lo_p, up_p = gosma.evaluate_branch_batch(ctx, nodes[perm])
+    assert np.array_equal(lo_p, lo[perm]) and np.array_equal(up_p, up[perm])  # order-preserving
+    for k in (0, 17, 299):
+        l1, u1 = gosma.evaluate_bounds(ctx, nodes[k])
+        assert l1 == lo[k] and u1 == up[k]  # batch == single evaluation
+
+
+def test_bound_soundness_sampling(gosma):
+    # test_bounds.cpp:312-330: LB <= f(pose) at feasible interior poses
+    rng = np.random.default_rng(42)
+    checked = 0
+    for trial in range(40):
+        mix = rand_mix(rng, 3, 3, 150.0, 0.15)
+        ctx = gpu_ctx(gosma, mix)
+        o = Oracle(mix)
+        nodes = rand_nodes(rng, 20)
+        lo, up = gosma.evaluate_branch_batch(ctx, nodes)
+        for k in range(len(nodes)):
+            if math.isinf(lo[k]):
+                continue
+            assert lo[k] <= up[k] + 1e-9
+            b = nodes[k]
+            for _ in range(10):
+                r = b[0:3] + rng.uniform(-b[3], b[3], 3)
+                t = b[4:7] + rng.uniform(-1, 1, 3) * b[7:10]
+                f = o.objective(r, t)
+                if math.isinf(f):
+                    continue
+                assert lo[k] <= f + 1e-9
+                checked += 1
+    assert checked > 2000
+
+
+def test_children_keep_parent_floor(gosma):
+    # test_bounds.cpp:355-373
+    rng = np.random.default_rng(66)
+    for trial in range(30):
+        mix = rand_mix(rng, 3, 3, 80.0, 0.2)
+        ctx = gpu_ctx(gosma, mix)
+        o = Oracle(mix)
+        parent = rand_nodes(rng, 1)[0]
+        parent[3] = max(parent[3], 0.1)
+        parent[7:10] = np.maximum(parent[7:10], 0.05)
+        plo, _ = gosma.evaluate_branch_batch(ctx, parent[None])
+        if math.isinf(plo[0]):
+            continue
+        _, kids = o.subdivide(parent)
+        kids[:, 10] = -math.inf
+        klo, _ = gosma.evaluate_branch_batch(ctx, kids)
+        _, _, lm, _, _ = o.eval_bounds(parent)
+        assert klo.min() >= plo[0] - TOL_CERT * lm[0] - 1e-9
+
+
+def test_bounds_tighten_as_branch_shrinks(gosma):
+    # test_bounds.cpp:332-353
+    rng = np.random.default_rng(55)
+    mix = rand_mix(rng, 2, 2, 20.0, 0.2)
+    ctx = gpu_ctx(gosma, mix)
+    node = np.array([0.4, -0.2, 0.8, 0.1, 0.3, 0.1, -2.0, 0.1, 0.1, 0.1, -math.inf])
+    gap = math.inf
+    for h in range(11):
+        lo, up = gosma.evaluate_branch_batch(ctx, node[None])
+        gap = up[0] - lo[0]
+        assert gap >= -1e-6
+        node[3] *= 0.5
+        node[7:10] *= 0.5
+    assert gap < 1e-3
+
+
+def test_config2_batch_properties(gosma):
+    """Full-size configs[1] batch: size-independent properties + a sampled parity check."""
+    import torch
+    from paper_1812_01232_b200 import synth
+    classes = synth.mixture(64, 32, "realistic", seed=2026)
+    ctx = gosma.ObjectiveContext(classes, 0.5)
+    n = 1_000_000
+    nodes = synth.nodes(n, seed=2027)
+    d_nodes = torch.from_numpy(nodes.view(np.uint8)).cuda()
+    d_lo = torch.empty(n, dtype=torch.float64, device="cuda")
+    d_up = torch.empty_like(d_lo)
+    d_sp = torch.empty(n, dtype=torch.int8, device="cuda")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        gosma.evaluate_branch_batch_device(ctx, d_nodes.data_ptr(), n, d_lo.data_ptr(),
+                                           d_up.data_ptr(), d_sp.data_ptr(), float("inf"),
+                                           s.cuda_stream)
+    s.synchronize()
+    lo, up, sp = d_lo.cpu().numpy(), d_up.cpu().numpy(), d_sp.cpu().numpy()
+    f = np.isfinite(lo)
+    assert f.mean() > 0.99
+    assert np.all(np.isfinite(up[f]))
+    assert np.all(lo[f] <= up[f] + 1e-6 * np.abs(up[f]) + 1e-9)
+    assert set(np.unique(sp)).issubset({-1, 0, 1})
+    # sampled parity against the oracle
+    rng = np.random.default_rng(0)
+    idx = rng.choice(n, 600, replace=False)
+    mix = Mixture(**synth.to_mixture_arrays(classes, 0.5))
+    o = Oracle(mix)
+    rlo, rup, lm, um, _ = o.eval_bounds(nodes.view(np.float64).reshape(-1, 11)[idx], threads=8)
+    ff = np.isfinite(rlo)
+    assert np.all(lo[idx][ff] <= rlo[ff] + 1e-9 * lm[ff])
+    assert np.all(lo[idx][ff] >= rlo[ff] - TOL_CERT * lm[ff])
+    assert np.all(np.abs(up[idx][ff] - rup[ff]) <= TOL_UB * um[ff])
+
+
+def test_host_objective_matches_golden(gosma, golden_objective):
+    for case in golden_objective["cases"]:
+        mix = Mixture.from_dict(case["mixture"])
+        ctx = gpu_ctx(gosma, mix)
+        assert abs(ctx.image_self_energy - case["self_energy"]) <= 1e-12 * max(1, abs(case["self_energy"]))
+        for p in case["poses"]:
+            if math.isinf(p["f"]):
+                with pytest.raises(gosma.InfeasiblePoseError):
+                    gosma.objective_value(ctx, p["r"], p["t"])
+            else:
+                v = gosma.objective_value(ctx, p["r"], p["t"])
+                assert abs(v - p["f"]) <= 1e-12 * max(1.0, abs(p["f"]))
+
+
+def test_host_gradient_matches_central_differences(gosma):
+    # test_objective.cpp:240-290
+    rng = np.random.default_rng(3)
+    mix = rand_mix(rng, 4, 3, 40.0, 0.05)
+    ctx = gpu_ctx(gosma, mix)
+    for _ in range(10):
+        r = rng.normal(size=3) * 0.5
+        t = rng.normal(size=3) * 0.4
+        try:
+            gr = gosma.objective_gradient(ctx, r, t)
+        except gosma.InfeasiblePoseError:
+            continue
+        x = np.concatenate([r, t])
+        h = 1e-6
+        fd = np.zeros(6)
+        for k in range(6):
+            xp, xm = x.copy(), x.copy()
+            xp[k] += h
+            xm[k] -= h
+            fd[k] = (gosma.objective_value(ctx, xp[:3], xp[3:]) -
+                     gosma.objective_value(ctx, xm[:3], xm[3:])) / (2 * h)
+        assert np.all(np.abs(gr - fd) <= 1e-4 * (1 + np.abs(fd)))
