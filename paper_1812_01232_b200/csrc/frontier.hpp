@@ -1,0 +1,92 @@
+// GPU-resident frontier (frontier.cu): an unordered node pool in HBM with an
+// order-preserving 64-bit key per node (the lower bound); each wave
+// radix-selects the W smallest keys, expands them, and appends the surviving
+// children. Expanded nodes become holes; holes and stale nodes are compacted
+// away when they dominate the pool.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+#include <vector>
+
+#include "gosma_capi.h"
+
+namespace gosma {
+
+constexpr unsigned long long kHoleKey = ~0ull;
+
+struct RouteStats {
+  double pruned_volume = 0.0;
+  double resolved_volume = 0.0;
+  unsigned long long floor_key = ~0ull;  // order key of the min resolved lower bound
+  double scratch = 0.0;
+};
+
+struct ArgMin {
+  unsigned long long key = ~0ull;    // order key of the min upper bound
+  unsigned long long index = ~0ull;  // first child attaining it
+};
+
+unsigned long long host_order_key(double v);
+double key_to_double(unsigned long long k);
+
+struct Frontier {
+  // node pool
+  gosma_node* nodes = nullptr;
+  int8_t* split = nullptr;
+  double* vol = nullptr;
+  unsigned long long* key = nullptr;
+  size_t size = 0;   // slots in use (live + holes + stale)
+  size_t holes = 0;  // expanded slots
+  size_t cap = 0;
+  // selection
+  unsigned int* sel = nullptr;
+  size_t sel_cap = 0;
+  unsigned int* hist = nullptr;  // radix-select histogram (4096 bins)
+  std::vector<unsigned int> h_hist;
+  // children of one wave
+  gosma_node* kids = nullptr;
+  double* kid_lower = nullptr;
+  double* kid_upper = nullptr;
+  int8_t* kid_split = nullptr;
+  double* kid_vol = nullptr;
+  int* keep = nullptr;
+  unsigned int* kept_idx = nullptr;
+  size_t kid_cap = 0;
+  // reductions / scratch
+  RouteStats* stats = nullptr;
+  ArgMin* amin = nullptr;
+  unsigned long long* counter = nullptr;
+  RouteStats* h_stats = nullptr;
+  ArgMin* h_amin = nullptr;
+  unsigned long long* h_counter = nullptr;
+  void* temp = nullptr;
+  size_t temp_bytes = 0;
+
+  cudaError_t reserve(size_t cap_nodes, size_t wave);
+  void release();
+  cudaError_t ensure_temp(size_t bytes);
+  cudaError_t grow(size_t need, cudaStream_t s);
+  // Host upload of initial nodes.
+  cudaError_t upload(const gosma_node* h_nodes, const int8_t* h_split, const double* h_vol,
+                     size_t n, cudaStream_t s);
+  // min key over the pool (kHoleKey if empty)
+  cudaError_t min_key(cudaStream_t s, unsigned long long* out);
+  // selects up to `want` slots with key < limit (the smallest first); writes
+  // their indices to sel, marks them holes, returns the count.
+  cudaError_t select_smallest(size_t want, unsigned long long limit, cudaStream_t s, size_t* n);
+  cudaError_t expand_selected(size_t n_sel, cudaStream_t s);
+  cudaError_t best_child(size_t n_kids, cudaStream_t s, int* index, double* value);
+  // route children against d*, append survivors
+  cudaError_t route_append(size_t n_kids, double dstar, cudaStream_t s, RouteStats* out);
+  // drop holes and nodes with key >= limit; returns the dropped (non-hole) volume
+  cudaError_t compact(unsigned long long limit, cudaStream_t s, double* dropped_volume);
+  // keep the `keep_n` smallest keys (capacity folding); returns folded volume
+  // and the smallest folded lower bound
+  cudaError_t fold_to(size_t keep_n, cudaStream_t s, double* folded_volume, double* folded_min);
+  size_t live_upper_bound() const { return size - holes; }
+};
+
+}  // namespace gosma

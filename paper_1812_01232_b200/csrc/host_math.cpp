@@ -246,3 +246,101 @@ double psi_trans(const Vec3& c, const Vec3& h, const Vec3& p) {
 }
 
 }  // namespace gosma
+
+namespace gosma {
+
+namespace {
+double logw_fp64(double x) { return x > 30.0 ? -std::log(x) : log_z_eval(x) - x; }
+double pair_k64(double a, double b, double c) {
+  return std::sqrt(std::max(0.0, a * a + b * b + 2.0 * c * a * b));
+}
+}  // namespace
+
+double lower_bound_fp64(const HostModel& model, const Vec3& rc, double rhw, const Vec3& tc,
+                        const Vec3& th, double parent_lower) {
+  // FP64 evaluate_bounds lower part (bounds.cpp:46-183, 270-273): used by the
+  // solver for resolved (unsplittable) branches, where the certified floor
+  // should carry no FP32 slack.
+  for (const Vec3& mu : model.all_means)
+    if (point_box_hi(mu, tc, th) < model.zeta) return INFINITY;
+  const Mat3 R0t = rotation_matrix(rc).transpose();
+  const double psi_r = std::min(std::sqrt(3.0) * rhw, M_PI);
+  double total = 0.0;
+  for (const HostClass& c : model.classes) {
+    const int n1 = c.n1(), n2 = c.n2();
+    std::vector<double> klo(n1), khi(n1), lwlo(n1), lwhi(n1), pt(n1), cpt(n1), spt(n1), cps(n1),
+        sps(n1);
+    std::vector<Vec3> uh(n1), q(n2);
+    std::vector<char> bz(n1);
+    for (int i = 0; i < n1; ++i) {
+      const Vec3 mu(c.mu[3 * i], c.mu[3 * i + 1], c.mu[3 * i + 2]);
+      const double dlo = std::max(point_box_lo(mu, tc, th), model.zeta);
+      const double dhi = point_box_hi(mu, tc, th);
+      klo[i] = dlo * dlo / c.sigma2[i] + 1.0;
+      khi[i] = dhi * dhi / c.sigma2[i] + 1.0;
+      lwlo[i] = logw_fp64(klo[i]);
+      lwhi[i] = logw_fp64(khi[i]);
+      const Vec3 u = mu - tc;
+      const double n = u.norm();
+      uh[i] = n > 1e-12 ? u / n : Vec3(1.0, 0.0, 0.0);
+      pt[i] = psi_trans(tc, th, mu);
+      cpt[i] = std::cos(pt[i]);
+      spt[i] = std::sin(pt[i]);
+      const double ps = pt[i] + psi_r;
+      bz[i] = ps >= M_PI;
+      cps[i] = bz[i] ? -1.0 : std::cos(ps);
+      sps[i] = bz[i] ? 0.0 : std::sin(ps);
+    }
+    for (int j = 0; j < n2; ++j)
+      q[j] = R0t * (Vec3(c.b[3 * j], c.b[3 * j + 1], c.b[3 * j + 2]) / c.kappa2[j]);
+    double self_lo = 0.0;
+    for (int i = 0; i < n1; ++i) {
+      self_lo += c.phi1[i] * c.phi1[i] * 0.5 * klo[i] / std::tanh(klo[i]);
+      for (int j = i + 1; j < n1; ++j) {
+        double ca;
+        if (pt[i] + pt[j] >= M_PI) {
+          ca = -1.0;
+        } else {
+          const double cth = std::clamp(uh[i].dot(uh[j]), -1.0, 1.0);
+          const double cpp = cpt[i] * cpt[j] - spt[i] * spt[j];
+          if (cth <= -cpp) {
+            ca = -1.0;
+          } else {
+            const double spp = spt[i] * cpt[j] + cpt[i] * spt[j];
+            ca = cth * cpp - std::sqrt(std::max(0.0, 1.0 - cth * cth)) * spp;
+          }
+        }
+        const double khh = pair_k64(khi[i], khi[j], ca);
+        const double ex = 2.0 * khi[i] * khi[j] * (ca - 1.0) / (khh + khi[i] + khi[j]);
+        const double kcm = std::max(std::max(pair_k64(klo[i], klo[j], ca), pair_k64(klo[i], khi[j], ca)),
+                                    std::max(pair_k64(khi[i], klo[j], ca), khh));
+        self_lo += 2.0 * c.phi1[i] * c.phi1[j] * std::exp(ex + logw_fp64(kcm) - lwlo[i] - lwlo[j]);
+      }
+    }
+    double cross_hi = 0.0;
+    for (int i = 0; i < n1; ++i)
+      for (int j = 0; j < n2; ++j) {
+        double cb;
+        if (bz[i]) {
+          cb = 1.0;
+        } else {
+          const double cth = std::clamp(uh[i].dot(q[j]), -1.0, 1.0);
+          cb = cth >= cps[i] ? 1.0
+                             : cth * cps[i] + std::sqrt(std::max(0.0, 1.0 - cth * cth)) * sps[i];
+        }
+        const double k2 = c.kappa2[j];
+        const double kl = pair_k64(klo[i], k2, cb);
+        const double ex = 2.0 * klo[i] * k2 * (cb - 1.0) / (kl + klo[i] + k2);
+        const double vx = -cb * k2;
+        const double kmin = vx <= klo[i] ? kl
+                                         : (vx >= khi[i] ? pair_k64(khi[i], k2, cb)
+                                                         : k2 * std::sqrt(std::max(0.0, (1.0 - cb) * (1.0 + cb))));
+        cross_hi += c.phi1[i] * c.phi2[j] *
+                    std::exp(ex + logw_fp64(kmin) - lwhi[i] - (c.log_z2[j] - k2));
+      }
+    total += c.weight * (self_lo - 2.0 * cross_hi);
+  }
+  return std::max(total, parent_lower);
+}
+
+}  // namespace gosma

@@ -107,3 +107,9 @@ double point_box_hi(const Vec3& p, const Vec3& c, const Vec3& h);
 double psi_trans(const Vec3& c, const Vec3& h, const Vec3& p);
 
 }  // namespace gosma
+
+namespace gosma {
+// FP64 lower bound of one branch (bounds.cpp:46-183, 270-273); +inf if infeasible.
+double lower_bound_fp64(const HostModel& model, const Vec3& rc, double rhw, const Vec3& tc,
+                        const Vec3& th, double parent_lower);
+}  // namespace gosma
