@@ -563,10 +563,11 @@ cudaError_t Frontier::compact(unsigned long long limit, cudaStream_t s, double* 
   int8_t* s2 = nullptr;
   double* v2 = nullptr;
   unsigned long long* k2 = nullptr;
-  if ((e = cudaMalloc(&n2, cap * sizeof(gosma_node))) != cudaSuccess) return e;
-  if ((e = cudaMalloc(&s2, cap)) != cudaSuccess) return e;
-  if ((e = cudaMalloc(&v2, cap * sizeof(double))) != cudaSuccess) return e;
-  if ((e = cudaMalloc(&k2, cap * 8)) != cudaSuccess) return e;
+  const size_t c = std::max<size_t>(n + n / 4, 1024);  // shrink-to-fit with headroom
+  if ((e = cudaMalloc(&n2, c * sizeof(gosma_node))) != cudaSuccess) return e;
+  if ((e = cudaMalloc(&s2, c)) != cudaSuccess) return e;
+  if ((e = cudaMalloc(&v2, c * sizeof(double))) != cudaSuccess) return e;
+  if ((e = cudaMalloc(&k2, c * 8)) != cudaSuccess) return e;
   if (n)
     gather_pool<<<grid_for(n, 256), 256, 0, s>>>(nodes, split, vol, key, idx, n, n2, s2, v2, k2);
   if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
@@ -580,6 +581,7 @@ cudaError_t Frontier::compact(unsigned long long limit, cudaStream_t s, double* 
   vol = v2;
   key = k2;
   size = n;
+  cap = c;
   holes = 0;
   return cudaGetLastError();
 }

@@ -406,13 +406,25 @@ int gosma_solve(gosma_ctx* ctx, const gosma_domain* domain, const gosma_config* 
       return cuda_error(e, "frontier upload");
   }
 
+  // Device memory budget for the pool: beyond it the worst nodes are folded
+  // into the resolved set (sound; the reference's queue_capacity mechanism).
+  size_t free_b = 0, total_b = 0;
+  cudaMemGetInfo(&free_b, &total_b);
+  const size_t per_node = sizeof(gosma_node) + 1 + 8 + 8;
+  const size_t mem_cap = std::max<size_t>(free_b / 4 / per_node, 16 * wave_nodes);
+  const size_t qcap = cfg.queue_capacity >= 0
+                          ? std::min<size_t>(static_cast<size_t>(cfg.queue_capacity), mem_cap)
+                          : mem_cap;
   int status = GOSMA_STATUS_QUEUE_EXHAUSTED;
   for (;;) {
-    // capacity folding (solver.cpp:433-447)
-    if (cfg.queue_capacity >= 0 &&
-        F.live_upper_bound() > static_cast<size_t>(cfg.queue_capacity)) {
+    // capacity folding (solver.cpp:433-447); the memory budget folds to 3/4
+    if (F.live_upper_bound() > qcap ||
+        F.size + 8 * wave_nodes > (cfg.queue_capacity >= 0 ? ~size_t{0} : mem_cap)) {
+      const size_t target = cfg.queue_capacity >= 0 && static_cast<size_t>(cfg.queue_capacity) <= mem_cap
+                                ? static_cast<size_t>(cfg.queue_capacity)
+                                : mem_cap * 3 / 4 - 8 * wave_nodes;
       double fv = 0.0, fmin = kInf;
-      if ((e = F.fold_to(static_cast<size_t>(cfg.queue_capacity), s, &fv, &fmin)) != cudaSuccess)
+      if ((e = F.fold_to(target, s, &fv, &fmin)) != cudaSuccess)
         return cuda_error(e, "fold");
       resolved_volume += fv;
       floor_lower = std::min(floor_lower, fmin);
