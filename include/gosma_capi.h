@@ -187,6 +187,47 @@ typedef void (*gosma_trace_cb)(void* user, unsigned long long wave,
 int gosma_solve(gosma_ctx* ctx, const gosma_domain* domain, const gosma_config* config,
                 gosma_report* report, gosma_trace_cb trace, void* user);
 
+/* ---- Stepwise solver: the same branch-and-bound as gosma_solve, one wave per
+ * call, so a driver can shard the frontier across GPUs (one rank per GPU) and
+ * exchange the incumbent / frontier minimum between waves.
+ * gosma_solve is exactly: create(rank 0, world 1); loop { status; certify;
+ * stop rules; expand(d* - eps) }. */
+typedef struct gosma_solver gosma_solver;
+
+typedef struct gosma_wave_status {
+  double best_value;       /* local incumbent d* (FP64 objective) */
+  double frontier_min;     /* min lower bound over the local frontier (+inf if empty) */
+  double floor_lower;      /* min lower bound of resolved / folded nodes */
+  unsigned long long live_nodes;
+  unsigned long long bound_evaluations;
+  double pruned_volume, resolved_volume, total_volume;
+  double elapsed_seconds;
+} gosma_wave_status;
+
+/* Rank `rank` of `world` owns translation roots rank, rank + world, ... and
+ * runs wave 0 (+ discovery dive over its sectors). */
+int gosma_solver_create(gosma_ctx* ctx, const gosma_domain* domain, const gosma_config* config,
+                        int rank, int world, gosma_solver** out);
+void gosma_solver_destroy(gosma_solver* solver);
+/* Local statistics for the global certificate max(prev, min(d*, frontier_min,
+ * floor)) (solver.cpp:626-627); applies capacity folding first. */
+int gosma_solver_status(gosma_solver* solver, gosma_wave_status* status);
+/* An incumbent value found elsewhere (another rank): prunes, carries no pose. */
+int gosma_solver_set_incumbent(gosma_solver* solver, double value);
+/* One wave: expand the best nodes with lower < limit (normally d* - eps),
+ * bound the children, update the incumbent (+SMA), route. max_evals > 0 caps
+ * the children evaluated. */
+int gosma_solver_expand(gosma_solver* solver, double limit, unsigned long long max_evals);
+/* Frontier rebalancing: remove up to max_nodes of the best live nodes into
+ * host buffers / add nodes received from another rank. */
+int gosma_solver_export(gosma_solver* solver, size_t max_nodes, gosma_node* nodes, int8_t* split,
+                        double* volume, size_t* n_out);
+int gosma_solver_import(gosma_solver* solver, const gosma_node* nodes, const int8_t* split,
+                        const double* volume, size_t n);
+/* Local incumbent pose / value and counters (global_lower, gap, status are
+ * the driver's). */
+int gosma_solver_result(gosma_solver* solver, gosma_report* report);
+
 const char* gosma_last_error(void);
 
 /* Build / device introspection for benches and tests. */

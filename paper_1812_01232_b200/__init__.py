@@ -62,6 +62,14 @@ class _Report(C.Structure):
                 ("wall_time_seconds", C.c_double), ("waves", C.c_ulonglong)]
 
 
+class _WaveStatus(C.Structure):
+    _fields_ = [("best_value", C.c_double), ("frontier_min", C.c_double),
+                ("floor_lower", C.c_double), ("live_nodes", C.c_ulonglong),
+                ("bound_evaluations", C.c_ulonglong), ("pruned_volume", C.c_double),
+                ("resolved_volume", C.c_double), ("total_volume", C.c_double),
+                ("elapsed_seconds", C.c_double)]
+
+
 _TRACE_CB = C.CFUNCTYPE(None, C.c_void_p, C.c_ulonglong, C.c_ulonglong, C.c_double, C.c_double,
                         C.c_ulonglong, C.c_double, C.c_double, C.c_double)
 
@@ -97,6 +105,15 @@ def _load():
     lib.gosma_device_info.argtypes = [C.c_int] + [C.POINTER(C.c_int)] * 4
     lib.gosma_kernel_launches.restype = C.c_ulonglong
     lib.gosma_calibrate_pipes.argtypes = [C.c_int, _dp, _dp]
+    lib.gosma_solver_create.argtypes = [vp, C.POINTER(_Domain), C.POINTER(_Config), C.c_int,
+                                        C.c_int, C.POINTER(vp)]
+    lib.gosma_solver_destroy.argtypes = [vp]
+    lib.gosma_solver_status.argtypes = [vp, C.POINTER(_WaveStatus)]
+    lib.gosma_solver_set_incumbent.argtypes = [vp, C.c_double]
+    lib.gosma_solver_expand.argtypes = [vp, C.c_double, C.c_ulonglong]
+    lib.gosma_solver_export.argtypes = [vp, C.c_size_t, vp, vp, vp, C.POINTER(C.c_size_t)]
+    lib.gosma_solver_import.argtypes = [vp, vp, vp, vp, C.c_size_t]
+    lib.gosma_solver_result.argtypes = [vp, C.POINTER(_Report)]
     return lib
 
 
@@ -394,3 +411,71 @@ def solve(ctx: ObjectiveContext, domain: PoseDomain, config: SolverConfig) -> So
                         rep.global_lower, rep.gap, _STATUS.get(rep.status, "?"),
                         rep.branches_expanded, rep.sma_invocations, rep.bound_evaluations,
                         rep.wall_time_seconds, rep.waves, trace)
+
+
+def _config_struct(config: SolverConfig) -> _Config:
+    return _Config(config.epsilon, config.zeta, config.batch_size,
+                   -1.0 if config.time_limit is None else float(config.time_limit),
+                   -1 if config.max_evaluations is None else int(config.max_evaluations),
+                   -1 if config.queue_capacity is None else int(config.queue_capacity),
+                   config.threads, config.seed, config.wave_nodes, int(config.discovery_dive))
+
+
+class ShardSolver:
+    """One rank's share of the branch-and-bound (gosma_solver_*): the frontier
+    of the translation roots rank, rank+world, ... on this GPU. Driven by
+    distributed.solve_sharded; world=1 reproduces solve()."""
+
+    def __init__(self, ctx: ObjectiveContext, domain: PoseDomain, config: SolverConfig,
+                 rank: int = 0, world: int = 1):
+        self._ctx = ctx  # keeps the context alive
+        d, self._boxes = domain._c()
+        self._dom = d
+        self.config = config
+        h = C.c_void_p()
+        _check(lib.gosma_solver_create(ctx.handle, C.byref(d), C.byref(_config_struct(config)),
+                                       rank, world, C.byref(h)), "solver_create")
+        self._h = h
+
+    def status(self) -> dict:
+        st = _WaveStatus()
+        _check(lib.gosma_solver_status(self._h, C.byref(st)), "solver_status")
+        return {k: getattr(st, k) for k, _ in _WaveStatus._fields_}
+
+    def set_incumbent(self, value: float):
+        _check(lib.gosma_solver_set_incumbent(self._h, float(value)), "solver_set_incumbent")
+
+    def expand(self, limit: float, max_evals: int = 0):
+        _check(lib.gosma_solver_expand(self._h, float(limit), int(max(0, max_evals))),
+               "solver_expand")
+
+    def export(self, max_nodes: int):
+        nodes = np.empty(max_nodes, dtype=NODE_DTYPE)
+        split = np.empty(max_nodes, dtype=np.int8)
+        vol = np.empty(max_nodes)
+        n = C.c_size_t(0)
+        _check(lib.gosma_solver_export(self._h, max_nodes, nodes.ctypes.data, split.ctypes.data,
+                                       vol.ctypes.data, C.byref(n)), "solver_export")
+        k = n.value
+        return nodes[:k], split[:k], vol[:k]
+
+    def import_(self, nodes, split, vol):
+        nodes = _as_nodes(nodes)
+        split = np.ascontiguousarray(split, dtype=np.int8)
+        vol = np.ascontiguousarray(vol, dtype=np.float64)
+        _check(lib.gosma_solver_import(self._h, nodes.ctypes.data, split.ctypes.data,
+                                       vol.ctypes.data, len(nodes)), "solver_import")
+
+    def result(self) -> dict:
+        rep = _Report()
+        _check(lib.gosma_solver_result(self._h, C.byref(rep)), "solver_result")
+        return {"value": rep.best_value, "r": np.array(rep.best_r[:]),
+                "t": np.array(rep.best_t[:]), "branches_expanded": rep.branches_expanded,
+                "sma_invocations": rep.sma_invocations,
+                "bound_evaluations": rep.bound_evaluations, "waves": rep.waves}
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib.gosma_solver_destroy(h)
+            self._h = None

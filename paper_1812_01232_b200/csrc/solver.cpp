@@ -287,12 +287,145 @@ int gosma_local_refine(const gosma_ctx* ctx, const double* r0, const double* t0,
   return GOSMA_OK;
 }
 
-int gosma_solve(gosma_ctx* ctx, const gosma_domain* domain, const gosma_config* config,
-                gosma_report* report, gosma_trace_cb trace, void* user) {
-  using Clock = std::chrono::steady_clock;
-  const auto t_start = Clock::now();
-  auto elapsed = [&] { return std::chrono::duration<double>(Clock::now() - t_start).count(); };
-  if (!ctx || !domain || !config || !report) return set_error(GOSMA_EINVAL, "null argument");
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Stepwise solver (one object per rank): the single-GPU gosma_solve and the
+// sharded multi-GPU driver (paper_1812_01232_b200/distributed.py) both run
+// status() -> [global exchange] -> expand() waves on it.
+struct gosma_solver {
+  gosma_ctx* ctx = nullptr;
+  Domain dom;
+  gosma_config cfg{};
+  int rank = 0, world = 1;
+  Incumbent inc;
+  double external = kInf;  // best value found by other ranks (prunes, no pose)
+  Frontier F;
+  double total_volume = 0.0, pruned_volume = 0.0, resolved_volume = 0.0;
+  double floor_lower = kInf;
+  unsigned long long evals = 0, expanded = 0, wave = 0;
+  size_t wave_nodes = 0, qcap = 0, mem_cap = 0;
+  std::chrono::steady_clock::time_point t_start;
+  double elapsed() const {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+  }
+  double dstar() const { return std::min(inc.value, external); }
+};
+
+namespace {
+
+int solver_init(gosma_solver* S) {
+  gosma_ctx* ctx = S->ctx;
+  const HostModel& m = ctx->model;
+  const gosma_config& cfg = S->cfg;
+  cudaStream_t s = ctx->stream;
+  // Roots and the measure (solver.cpp:339-368); rank r owns roots r, r+W, ...
+  double total_volume = 0.0;
+  for (const Box& b : S->dom.boxes) {
+    gosma_node n{};
+    n.rhw = S->dom.rot_hw;
+    for (int a = 0; a < 3; ++a) n.thw[a] = b.h[a];
+    total_volume += volume_of(n);
+  }
+  const bool unit_measure = !(total_volume > 0.0);
+  if (unit_measure) total_volume = static_cast<double>(S->dom.boxes.size());
+  S->total_volume = total_volume;
+  std::vector<gosma_node> roots;
+  std::vector<double> root_vol;
+  bool any_feasible = false;
+  for (size_t k = 0; k < S->dom.boxes.size(); ++k) {
+    const Box& b = S->dom.boxes[k];
+    gosma_node n{};
+    for (int a = 0; a < 3; ++a) {
+      n.rc[a] = S->dom.rot_center[a];
+      n.tc[a] = b.c[a];
+      n.thw[a] = b.h[a];
+    }
+    n.rhw = S->dom.rot_hw;
+    n.lower = -kInf;
+    const double v = unit_measure ? 1.0 : volume_of(n);
+    const bool feas = feasible_box(m, b.c, b.h);
+    any_feasible = any_feasible || feas;
+    if (static_cast<int>(k % S->world) != S->rank) continue;
+    if (feas) {
+      roots.push_back(n);
+      root_vol.push_back(v);
+    } else {
+      S->pruned_volume += v;
+    }
+  }
+  if (!any_feasible)
+    return set_error(GOSMA_EINFEASIBLE, "solve: no feasible camera center in the domain");
+  // Wave size: enough children to keep the bound kernel busy for a few ms
+  // (~1.2e8 pair terms per wave), or what the caller asks for.
+  size_t pairs = 0;
+  for (const HostClass& c : m.classes)
+    pairs += static_cast<size_t>(c.n1()) * c.n2() + static_cast<size_t>(c.n1()) * (c.n1() - 1) / 2;
+  S->wave_nodes =
+      cfg.wave_nodes > 0
+          ? static_cast<size_t>(cfg.wave_nodes)
+          : std::min<size_t>(std::max<size_t>(120000000 / std::max<size_t>(pairs, 1), 1024),
+                             1u << 19);
+  cudaError_t e = S->F.reserve(std::max<size_t>(8 * S->wave_nodes, roots.size() * 2 + 16),
+                               S->wave_nodes);
+  if (e != cudaSuccess) return cuda_error(e, "frontier reserve");
+  // Device memory budget for the pool: beyond it the worst nodes fold into the
+  // resolved set (sound; the reference's queue_capacity mechanism).
+  size_t free_b = 0, total_b = 0;
+  cudaMemGetInfo(&free_b, &total_b);
+  const size_t per_node = sizeof(gosma_node) + 1 + 8 + 8;
+  S->mem_cap = std::max<size_t>(free_b / 4 / per_node, 16 * S->wave_nodes);
+  S->qcap = cfg.queue_capacity >= 0
+                ? std::min<size_t>(static_cast<size_t>(cfg.queue_capacity), S->mem_cap)
+                : S->mem_cap;
+  if (roots.empty()) return GOSMA_OK;
+  // Wave 0: the roots (solver.cpp:611-621) + discovery dive.
+  std::vector<double> lo, up;
+  std::vector<int8_t> sp;
+  int rc = eval_host(ctx, roots, kInf, &lo, &up, &sp);
+  if (rc != GOSMA_OK) return rc;
+  S->evals += roots.size();
+  if (cfg.discovery_dive) {
+    rc = discovery_dive(ctx, S->dom, roots, cfg, &S->inc, &S->evals, 0.0);
+    if (rc != GOSMA_OK) return rc;
+  }
+  for (size_t i = 0; i < roots.size(); ++i)
+    if (up[i] < S->inc.value) improve(m, S->dom, roots[i], &S->inc);
+  std::vector<gosma_node> keep;
+  std::vector<int8_t> ks;
+  std::vector<double> kv;
+  for (size_t i = 0; i < roots.size(); ++i) {
+    gosma_node b = roots[i];
+    b.lower = lo[i];
+    if (!(b.lower < S->dstar())) {
+      S->pruned_volume += root_vol[i];
+    } else if (!splittable(b)) {
+      // resolved: FP64 bound, so zero-size domains certify exactly
+      const double l64 = lower_bound_fp64(m, Vec3(b.rc[0], b.rc[1], b.rc[2]), b.rhw,
+                                          Vec3(b.tc[0], b.tc[1], b.tc[2]),
+                                          Vec3(b.thw[0], b.thw[1], b.thw[2]), -kInf);
+      S->resolved_volume += root_vol[i];
+      S->floor_lower = std::min(S->floor_lower, std::max(l64, b.lower));
+    } else {
+      keep.push_back(b);
+      ks.push_back(sp[i]);
+      kv.push_back(root_vol[i]);
+    }
+  }
+  if (!keep.empty() &&
+      (e = S->F.upload(keep.data(), ks.data(), kv.data(), keep.size(), s)) != cudaSuccess)
+    return cuda_error(e, "frontier upload");
+  return GOSMA_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int gosma_solver_create(gosma_ctx* ctx, const gosma_domain* domain, const gosma_config* config,
+                        int rank, int world, gosma_solver** out) {
+  if (!ctx || !domain || !config || !out) return set_error(GOSMA_EINVAL, "null argument");
+  *out = nullptr;
   const gosma_config& cfg = *config;
   // solver.cpp:320-329
   if (!(cfg.epsilon > 0.0)) return set_error(GOSMA_EINVAL, "solve: epsilon must be > 0");
@@ -301,236 +434,242 @@ int gosma_solve(gosma_ctx* ctx, const gosma_domain* domain, const gosma_config* 
     return set_error(GOSMA_EINVAL, "solve: config.zeta differs from the context's standoff radius");
   if (domain->n_boxes < 1 || !domain->boxes)
     return set_error(GOSMA_EINVAL, "solve: empty translation domain");
-  *report = gosma_report{};
-  const HostModel& m = ctx->model;
-  const Domain dom = make_domain(domain);
+  if (world < 1 || rank < 0 || rank >= world) return set_error(GOSMA_EINVAL, "bad rank/world");
+  auto* S = new gosma_solver();
+  S->ctx = ctx;
+  S->dom = make_domain(domain);
+  S->cfg = cfg;
+  S->rank = rank;
+  S->world = world;
+  S->t_start = std::chrono::steady_clock::now();
+  DeviceGuard g(ctx->device);
+  const int rc = solver_init(S);
+  if (rc != GOSMA_OK) {
+    S->F.release();
+    delete S;
+    return rc;
+  }
+  *out = S;
+  return GOSMA_OK;
+}
+
+void gosma_solver_destroy(gosma_solver* S) {
+  if (!S) return;
+  DeviceGuard g(S->ctx->device);
+  S->F.release();
+  delete S;
+}
+
+int gosma_solver_status(gosma_solver* S, gosma_wave_status* st) {
+  if (!S || !st) return set_error(GOSMA_EINVAL, "null argument");
+  DeviceGuard g(S->ctx->device);
+  cudaStream_t s = S->ctx->stream;
+  cudaError_t e;
+  // capacity folding (solver.cpp:433-447); the memory budget folds to 3/4
+  const bool user_cap = S->cfg.queue_capacity >= 0 &&
+                        static_cast<size_t>(S->cfg.queue_capacity) <= S->mem_cap;
+  if (S->F.live_upper_bound() > S->qcap ||
+      (!user_cap && S->F.size + 8 * S->wave_nodes > S->mem_cap)) {
+    const size_t target = user_cap ? static_cast<size_t>(S->cfg.queue_capacity)
+                                   : S->mem_cap * 3 / 4 - 8 * S->wave_nodes;
+    double fv = 0.0, fmin = kInf;
+    if ((e = S->F.fold_to(target, s, &fv, &fmin)) != cudaSuccess) return cuda_error(e, "fold");
+    S->resolved_volume += fv;
+    S->floor_lower = std::min(S->floor_lower, fmin);
+  }
+  unsigned long long kmin = kHoleKey;
+  if ((e = S->F.min_key(s, &kmin)) != cudaSuccess) return cuda_error(e, "frontier min");
+  st->best_value = S->inc.value;
+  st->frontier_min = kmin == kHoleKey ? kInf : key_to_double(kmin);
+  st->floor_lower = S->floor_lower;
+  st->live_nodes = kmin == kHoleKey ? 0 : S->F.live_upper_bound();
+  st->bound_evaluations = S->evals;
+  st->pruned_volume = S->pruned_volume;
+  st->resolved_volume = S->resolved_volume;
+  st->total_volume = S->total_volume;
+  st->elapsed_seconds = S->elapsed();
+  return GOSMA_OK;
+}
+
+int gosma_solver_set_incumbent(gosma_solver* S, double value) {
+  if (!S) return set_error(GOSMA_EINVAL, "null argument");
+  S->external = std::min(S->external, value);
+  return GOSMA_OK;
+}
+
+int gosma_solver_expand(gosma_solver* S, double limit, unsigned long long max_evals) {
+  if (!S) return set_error(GOSMA_EINVAL, "null argument");
+  gosma_ctx* ctx = S->ctx;
   DeviceGuard g(ctx->device);
   cudaStream_t s = ctx->stream;
-
-  // Roots and the measure (solver.cpp:339-368).
-  double total_volume = 0.0;
-  for (const Box& b : dom.boxes) {
-    gosma_node n{};
-    n.rhw = dom.rot_hw;
-    for (int a = 0; a < 3; ++a) n.thw[a] = b.h[a];
-    total_volume += volume_of(n);
-  }
-  const bool unit_measure = !(total_volume > 0.0);
-  if (unit_measure) total_volume = static_cast<double>(dom.boxes.size());
-  double pruned_volume = 0.0, resolved_volume = 0.0, queue_volume = 0.0;
-  double floor_lower = kInf;
-  std::vector<gosma_node> roots;
-  std::vector<double> root_vol;
-  for (const Box& b : dom.boxes) {
-    gosma_node n{};
-    for (int a = 0; a < 3; ++a) {
-      n.rc[a] = dom.rot_center[a];
-      n.tc[a] = b.c[a];
-      n.thw[a] = b.h[a];
-    }
-    n.rhw = dom.rot_hw;
-    n.lower = -kInf;
-    const double v = unit_measure ? 1.0 : volume_of(n);
-    if (feasible_box(m, b.c, b.h)) {
-      roots.push_back(n);
-      root_vol.push_back(v);
-    } else {
-      pruned_volume += v;
+  cudaError_t e;
+  size_t want = S->wave_nodes;
+  if (max_evals > 0) want = std::min<size_t>(want, std::max<unsigned long long>(1, (max_evals + 7) / 8));
+  size_t n_sel = 0;
+  // Expand only nodes that can still matter: lower < limit (= d* - eps).
+  if ((e = S->F.select_smallest(want, host_order_key(limit), s, &n_sel)) != cudaSuccess)
+    return cuda_error(e, "select");
+  if (n_sel == 0) {
+    // Nothing below the limit yet the gap is open (a resolved floor holds the
+    // bound down): keep refining the live nodes, as the reference's heap would.
+    if ((e = S->F.select_smallest(want, host_order_key(S->dstar()), s, &n_sel)) != cudaSuccess)
+      return cuda_error(e, "select");
+    if (n_sel == 0) {  // only stale nodes remain
+      double dropped = 0.0;
+      if ((e = S->F.compact(host_order_key(S->dstar()), s, &dropped)) != cudaSuccess)
+        return cuda_error(e, "compact");
+      S->pruned_volume += dropped;
+      ++S->wave;
+      return GOSMA_OK;
     }
   }
-  if (roots.empty())
-    return set_error(GOSMA_EINFEASIBLE, "solve: no feasible camera center in the domain");
+  const size_t n_kids = n_sel * 8;
+  if ((e = S->F.expand_selected(n_sel, s)) != cudaSuccess) return cuda_error(e, "expand");
+  EvalArgs a;
+  a.nodes = reinterpret_cast<const double*>(S->F.kids);
+  a.n = static_cast<long long>(n_kids);
+  a.skip_upper_at = S->dstar();
+  a.lower = S->F.kid_lower;
+  a.upper = S->F.kid_upper;
+  a.split_rot = S->F.kid_split;
+  a.work = static_cast<unsigned int*>(ctx->d_work);
+  if ((e = launch_eval_bounds(ctx->dev, a, ctx->sm_count, s)) != cudaSuccess)
+    return cuda_error(e, "eval children");
+  S->evals += n_kids;
+  S->expanded += n_sel;
+  int bi = -1;
+  double bu = kInf;
+  if ((e = S->F.best_child(n_kids, s, &bi, &bu)) != cudaSuccess) return cuda_error(e, "argmin");
+  if (bi >= 0 && bu < S->inc.value) {
+    gosma_node b;
+    cudaMemcpy(&b, S->F.kids + bi, sizeof(gosma_node), cudaMemcpyDeviceToHost);
+    improve(ctx->model, S->dom, b, &S->inc);
+  }
+  RouteStats rs;
+  if ((e = S->F.route_append(n_kids, S->dstar(), s, &rs)) != cudaSuccess)
+    return cuda_error(e, "route");
+  S->pruned_volume += rs.pruned_volume;
+  S->resolved_volume += rs.resolved_volume;
+  if (rs.floor_key != ~0ull) S->floor_lower = std::min(S->floor_lower, key_to_double(rs.floor_key));
+  // amortised compaction: drop holes and stale nodes (lower >= d*,
+  // solver.cpp:660-663) once they fill half the pool
+  if (S->F.holes * 2 > S->F.size) {
+    double dropped = 0.0;
+    if ((e = S->F.compact(host_order_key(S->dstar()), s, &dropped)) != cudaSuccess)
+      return cuda_error(e, "compact");
+    S->pruned_volume += dropped;
+  }
+  ++S->wave;
+  return GOSMA_OK;
+}
 
-  Incumbent inc;
-  unsigned long long evals = 0, expanded = 0, wave = 0;
-  double certified = -kInf;
-  auto emit = [&](unsigned long long w, size_t qsize) {
-    if (trace)
-      trace(user, w, evals, inc.value, certified, qsize, queue_volume / total_volume,
-            pruned_volume / total_volume, resolved_volume / total_volume);
-  };
+int gosma_solver_export(gosma_solver* S, size_t max_nodes, gosma_node* nodes, int8_t* split,
+                        double* vol, size_t* n_out) {
+  if (!S || !n_out) return set_error(GOSMA_EINVAL, "null argument");
+  *n_out = 0;
+  if (max_nodes == 0) return GOSMA_OK;
+  DeviceGuard g(S->ctx->device);
+  cudaStream_t s = S->ctx->stream;
+  cudaError_t e;
+  size_t n = 0;
+  max_nodes = std::min(max_nodes, S->F.sel_cap);
+  // hand off the best live nodes (they are the next to expand)
+  if ((e = S->F.select_smallest(max_nodes, host_order_key(S->dstar()), s, &n)) != cudaSuccess)
+    return cuda_error(e, "export select");
+  if (n) {
+    std::vector<unsigned int> idx(n);
+    cudaMemcpy(idx.data(), S->F.sel, n * 4, cudaMemcpyDeviceToHost);
+    for (size_t k = 0; k < n; ++k) {
+      cudaMemcpy(nodes + k, S->F.nodes + idx[k], sizeof(gosma_node), cudaMemcpyDeviceToHost);
+      cudaMemcpy(split + k, S->F.split + idx[k], 1, cudaMemcpyDeviceToHost);
+      cudaMemcpy(vol + k, S->F.vol + idx[k], 8, cudaMemcpyDeviceToHost);
+    }
+  }
+  *n_out = n;
+  return GOSMA_OK;
+}
 
-  // Wave 0: the roots (solver.cpp:611-621).
-  std::vector<double> lo, up;
-  std::vector<int8_t> sp;
-  int rc = eval_host(ctx, roots, kInf, &lo, &up, &sp);
+int gosma_solver_import(gosma_solver* S, const gosma_node* nodes, const int8_t* split,
+                        const double* vol, size_t n) {
+  if (!S) return set_error(GOSMA_EINVAL, "null argument");
+  if (n == 0) return GOSMA_OK;
+  DeviceGuard g(S->ctx->device);
+  const cudaError_t e = S->F.upload(nodes, split, vol, n, S->ctx->stream);
+  if (e != cudaSuccess) return cuda_error(e, "import");
+  return GOSMA_OK;
+}
+
+int gosma_solver_result(gosma_solver* S, gosma_report* report) {
+  if (!S || !report) return set_error(GOSMA_EINVAL, "null argument");
+  *report = gosma_report{};
+  report->best_value = S->inc.value;
+  for (int k = 0; k < 3; ++k) {
+    report->best_r[k] = S->inc.r[k];
+    report->best_t[k] = S->inc.t[k];
+  }
+  report->branches_expanded = S->expanded;
+  report->sma_invocations = S->inc.sma;
+  report->bound_evaluations = S->evals;
+  report->wall_time_seconds = S->elapsed();
+  report->waves = S->wave;
+  return GOSMA_OK;
+}
+
+// solve() (solver.cpp:312-688) on one GPU: status -> stop rules -> expand.
+int gosma_solve(gosma_ctx* ctx, const gosma_domain* domain, const gosma_config* config,
+                gosma_report* report, gosma_trace_cb trace, void* user) {
+  if (!report) return set_error(GOSMA_EINVAL, "null argument");
+  gosma_solver* S = nullptr;
+  int rc = gosma_solver_create(ctx, domain, config, 0, 1, &S);
   if (rc != GOSMA_OK) return rc;
-  evals += roots.size();
-  if (cfg.discovery_dive) {
-    rc = discovery_dive(ctx, dom, roots, cfg, &inc, &evals, 0.0);
-    if (rc != GOSMA_OK) return rc;
-  }
-  for (size_t i = 0; i < roots.size(); ++i) {
-    if (up[i] < inc.value) improve(m, dom, roots[i], &inc);
-  }
-  Frontier F;
-  // Wave size: enough children to keep the bound kernel busy for a few ms
-  // (pair terms per wave ~1e9), but never more than the caller asks for.
-  size_t pairs = 0;
-  for (const HostClass& c : m.classes)
-    pairs += static_cast<size_t>(c.n1()) * c.n2() + static_cast<size_t>(c.n1()) * (c.n1() - 1) / 2;
-  size_t wave_nodes = cfg.wave_nodes > 0
-                          ? static_cast<size_t>(cfg.wave_nodes)
-                          : std::min<size_t>(std::max<size_t>(120000000 / std::max<size_t>(pairs, 1), 1024),
-                                             1u << 19);
-  cudaError_t e = F.reserve(std::max<size_t>(8 * wave_nodes, roots.size() * 2), wave_nodes);
-  if (e != cudaSuccess) return cuda_error(e, "frontier reserve");
-  struct Guard {
-    Frontier* f;
-    ~Guard() { f->release(); }
-  } guard{&F};
-  {
-    std::vector<gosma_node> keep;
-    std::vector<int8_t> ks;
-    std::vector<double> kv;
-    for (size_t i = 0; i < roots.size(); ++i) {
-      gosma_node b = roots[i];
-      b.lower = lo[i];
-      if (!(b.lower < inc.value)) {
-        pruned_volume += root_vol[i];
-      } else if (!splittable(b)) {
-        // resolved: FP64 bound, so zero-size domains certify exactly
-        const double l64 = lower_bound_fp64(m, Vec3(b.rc[0], b.rc[1], b.rc[2]), b.rhw,
-                                            Vec3(b.tc[0], b.tc[1], b.tc[2]),
-                                            Vec3(b.thw[0], b.thw[1], b.thw[2]), -kInf);
-        resolved_volume += root_vol[i];
-        floor_lower = std::min(floor_lower, std::max(l64, b.lower));
-      } else {
-        keep.push_back(b);
-        ks.push_back(sp[i]);
-        kv.push_back(root_vol[i]);
-      }
-    }
-    if (!keep.empty() &&
-        (e = F.upload(keep.data(), ks.data(), kv.data(), keep.size(), s)) != cudaSuccess)
-      return cuda_error(e, "frontier upload");
-  }
-
-  // Device memory budget for the pool: beyond it the worst nodes are folded
-  // into the resolved set (sound; the reference's queue_capacity mechanism).
-  size_t free_b = 0, total_b = 0;
-  cudaMemGetInfo(&free_b, &total_b);
-  const size_t per_node = sizeof(gosma_node) + 1 + 8 + 8;
-  const size_t mem_cap = std::max<size_t>(free_b / 4 / per_node, 16 * wave_nodes);
-  const size_t qcap = cfg.queue_capacity >= 0
-                          ? std::min<size_t>(static_cast<size_t>(cfg.queue_capacity), mem_cap)
-                          : mem_cap;
+  const gosma_config& cfg = *config;
+  double certified = -kInf;
   int status = GOSMA_STATUS_QUEUE_EXHAUSTED;
   for (;;) {
-    // capacity folding (solver.cpp:433-447); the memory budget folds to 3/4
-    if (F.live_upper_bound() > qcap ||
-        F.size + 8 * wave_nodes > (cfg.queue_capacity >= 0 ? ~size_t{0} : mem_cap)) {
-      const size_t target = cfg.queue_capacity >= 0 && static_cast<size_t>(cfg.queue_capacity) <= mem_cap
-                                ? static_cast<size_t>(cfg.queue_capacity)
-                                : mem_cap * 3 / 4 - 8 * wave_nodes;
-      double fv = 0.0, fmin = kInf;
-      if ((e = F.fold_to(target, s, &fv, &fmin)) != cudaSuccess)
-        return cuda_error(e, "fold");
-      resolved_volume += fv;
-      floor_lower = std::min(floor_lower, fmin);
+    gosma_wave_status st;
+    if ((rc = gosma_solver_status(S, &st)) != GOSMA_OK) break;
+    const double dstar = st.best_value;
+    // certified lower bound (solver.cpp:626-627)
+    certified = std::max(certified, std::min(std::min(dstar, st.frontier_min), st.floor_lower));
+    if (trace) {
+      const double queue_volume =
+          std::max(0.0, st.total_volume - st.pruned_volume - st.resolved_volume);
+      trace(user, S->wave, st.bound_evaluations, dstar, certified, st.live_nodes,
+            queue_volume / st.total_volume, st.pruned_volume / st.total_volume,
+            st.resolved_volume / st.total_volume);
     }
-    unsigned long long kmin = kHoleKey;
-    if ((e = F.min_key(s, &kmin)) != cudaSuccess) return cuda_error(e, "frontier min");
-    const bool empty = (kmin == kHoleKey);
-    const double front_min = empty ? kInf : key_to_double(kmin);
-    queue_volume = std::max(0.0, total_volume - pruned_volume - resolved_volume);
-    certified = std::max(certified, std::min(std::min(inc.value, front_min), floor_lower));
-    emit(wave, F.live_upper_bound());
-    if (inc.value - certified <= cfg.epsilon) {
+    // stop rules (solver.cpp:629-645)
+    if (dstar - certified <= cfg.epsilon) {
       status = GOSMA_STATUS_EPSILON_OPTIMAL;
       break;
     }
-    if (empty) {
+    if (st.live_nodes == 0) {
       status = GOSMA_STATUS_QUEUE_EXHAUSTED;
       break;
     }
-    if (cfg.time_limit >= 0.0 && elapsed() >= cfg.time_limit) {
+    if (cfg.time_limit >= 0.0 && st.elapsed_seconds >= cfg.time_limit) {
       status = GOSMA_STATUS_TIME_LIMIT;
       break;
     }
-    if (cfg.max_evaluations >= 0 && evals >= static_cast<unsigned long long>(cfg.max_evaluations)) {
-      status = GOSMA_STATUS_TIME_LIMIT;
-      break;
-    }
-    // Expand only nodes that can still matter: lower < d* - eps (the stop rule
-    // never needs the others expanded).
-    const double limit = inc.value - cfg.epsilon;
-    size_t want = wave_nodes;
-    if (cfg.max_evaluations >= 0) {  // keep within the evaluation budget
-      const unsigned long long left =
-          static_cast<unsigned long long>(cfg.max_evaluations) > evals
-              ? static_cast<unsigned long long>(cfg.max_evaluations) - evals
-              : 0;
-      want = std::min<size_t>(want, std::max<unsigned long long>(1, (left + 7) / 8));
-    }
-    size_t n_sel = 0;
-    if ((e = F.select_smallest(want, host_order_key(limit), s, &n_sel)) != cudaSuccess)
-      return cuda_error(e, "select");
-    if (n_sel == 0) {
-      // Nothing below d* - eps, yet the gap is open (a resolved floor holds the
-      // certified bound down): keep refining the live nodes, as the
-      // reference's heap would, until the queue runs dry.
-      if ((e = F.select_smallest(want, host_order_key(inc.value), s, &n_sel)) != cudaSuccess)
-        return cuda_error(e, "select");
-      if (n_sel == 0) {  // only stale nodes remain
-        double dropped = 0.0;
-        if ((e = F.compact(host_order_key(inc.value), s, &dropped)) != cudaSuccess)
-          return cuda_error(e, "compact");
-        pruned_volume += dropped;
-        continue;
+    unsigned long long left = 0;
+    if (cfg.max_evaluations >= 0) {
+      if (st.bound_evaluations >= static_cast<unsigned long long>(cfg.max_evaluations)) {
+        status = GOSMA_STATUS_TIME_LIMIT;
+        break;
       }
+      left = static_cast<unsigned long long>(cfg.max_evaluations) - st.bound_evaluations;
     }
-    const size_t n_kids = n_sel * 8;
-    if ((e = F.expand_selected(n_sel, s)) != cudaSuccess) return cuda_error(e, "expand");
-    EvalArgs a;
-    a.nodes = reinterpret_cast<const double*>(F.kids);
-    a.n = static_cast<long long>(n_kids);
-    a.skip_upper_at = inc.value;
-    a.lower = F.kid_lower;
-    a.upper = F.kid_upper;
-    a.split_rot = F.kid_split;
-    a.work = static_cast<unsigned int*>(ctx->d_work);
-    if ((e = launch_eval_bounds(ctx->dev, a, ctx->sm_count, s)) != cudaSuccess)
-      return cuda_error(e, "eval children");
-    evals += n_kids;
-    expanded += n_sel;
-    int bi = -1;
-    double bu = kInf;
-    if ((e = F.best_child(n_kids, s, &bi, &bu)) != cudaSuccess) return cuda_error(e, "argmin");
-    if (bi >= 0 && bu < inc.value) {
-      gosma_node b;
-      cudaMemcpy(&b, F.kids + bi, sizeof(gosma_node), cudaMemcpyDeviceToHost);
-      improve(m, dom, b, &inc);
-    }
-    RouteStats rs;
-    if ((e = F.route_append(n_kids, inc.value, s, &rs)) != cudaSuccess)
-      return cuda_error(e, "route");
-    pruned_volume += rs.pruned_volume;
-    resolved_volume += rs.resolved_volume;
-    if (rs.floor_key != ~0ull) floor_lower = std::min(floor_lower, key_to_double(rs.floor_key));
-    // amortised compaction: drop holes and stale nodes (lower >= d*,
-    // solver.cpp:660-663) once they fill half the pool
-    if (F.holes * 2 > F.size) {
-      double dropped = 0.0;
-      if ((e = F.compact(host_order_key(inc.value), s, &dropped)) != cudaSuccess)
-        return cuda_error(e, "compact");
-      pruned_volume += dropped;
-    }
-    ++wave;
+    if ((rc = gosma_solver_expand(S, dstar - cfg.epsilon, left)) != GOSMA_OK) break;
   }
-  report->best_value = inc.value;
-  for (int k = 0; k < 3; ++k) {
-    report->best_r[k] = inc.r[k];
-    report->best_t[k] = inc.t[k];
+  if (rc != GOSMA_OK) {
+    gosma_solver_destroy(S);
+    return rc;
   }
+  gosma_solver_result(S, report);
   report->global_lower = certified;
-  report->gap = inc.value - certified;
+  report->gap = report->best_value - certified;
   report->status = status;
-  report->branches_expanded = expanded;
-  report->sma_invocations = inc.sma;
-  report->bound_evaluations = evals;
-  report->wall_time_seconds = elapsed();
-  report->waves = wave;
+  gosma_solver_destroy(S);
   return status == GOSMA_STATUS_TIME_LIMIT ? GOSMA_EBUDGET : GOSMA_OK;
 }
 

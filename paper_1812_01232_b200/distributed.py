@@ -1,0 +1,204 @@
+"""Frontier-sharded branch-and-bound across GPUs.
+
+One process per GPU (torchrun), one ``ShardSolver`` per rank owning the
+translation roots rank, rank+world, ... Every wave:
+
+1. each rank reports {d*_local, min(frontier min, resolved floor)};
+2. one min-allreduce (NCCL over NVLink for CUDA tensors, gloo on CPU) gives the
+   global incumbent and the global frontier minimum;
+3. certified = max(prev, min(d*, global min)) (solver.cpp:626-627); the stop
+   rules (solver.cpp:629-645) are evaluated identically on every rank;
+4. the global d* is pushed into every shard (it prunes there, soundly);
+5. each shard expands its best nodes below d* - eps;
+6. every ``rebalance_every`` waves the live-frontier sizes are all-gathered and,
+   when max/min exceeds ``imbalance``, donors hand their best nodes to
+   receivers (point-to-point, deterministic pairing).
+
+The shard interface (status / set_incumbent / expand / export / import_ /
+result) is duck-typed, so the exchange logic is tested on CPU with gloo and a
+host-side toy shard (tests/test_distributed.py).
+"""
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+import numpy as np
+
+try:
+    import torch
+    import torch.distributed as dist
+except ImportError:  # pragma: no cover - torch is part of the image
+    torch = None
+    dist = None
+
+
+@dataclass
+class ShardedReport:
+    best_value: float
+    global_lower: float
+    gap: float
+    status: str
+    r: np.ndarray
+    t: np.ndarray
+    bound_evaluations: int
+    waves: int
+    migrated_nodes: int
+    wall_time_seconds: float
+    trace: List[tuple] = field(default_factory=list)
+
+
+class Comm:
+    """Collectives of the driver over a torch.distributed process group."""
+
+    def __init__(self, device=None, group=None):
+        self.group = group
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.device = device if device is not None else torch.device("cpu")
+
+    def _t(self, values, dtype=torch.float64):
+        return torch.tensor(values, dtype=dtype, device=self.device)
+
+    def allreduce(self, values, op="min"):
+        t = self._t(values)
+        if self.world > 1:
+            dist.all_reduce(t, op={"min": dist.ReduceOp.MIN, "max": dist.ReduceOp.MAX,
+                                   "sum": dist.ReduceOp.SUM}[op], group=self.group)
+        return t.cpu().numpy()
+
+    def allgather(self, value: float):
+        t = self._t([value])
+        if self.world == 1:
+            return t.cpu().numpy()
+        out = [torch.empty_like(t) for _ in range(self.world)]
+        dist.all_gather(out, t, group=self.group)
+        return torch.cat(out).cpu().numpy()
+
+    def send_array(self, arr: np.ndarray, dst: int):
+        t = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float64)).to(self.device)
+        n = self._t([t.shape[0]], torch.int64)
+        dist.send(n, dst, group=self.group)
+        if t.shape[0]:
+            dist.send(t.reshape(-1), dst, group=self.group)
+
+    def recv_array(self, src: int, width: int) -> np.ndarray:
+        n = self._t([0], torch.int64)
+        dist.recv(n, src, group=self.group)
+        k = int(n.item())
+        if k == 0:
+            return np.zeros((0, width))
+        t = torch.empty(k * width, dtype=torch.float64, device=self.device)
+        dist.recv(t, src, group=self.group)
+        return t.cpu().numpy().reshape(k, width)
+
+
+def plan_rebalance(counts, imbalance: float = 1.5, min_move: int = 1):
+    """Deterministic transfer plan [(src, dst, n)] that moves the live-frontier
+    sizes toward their mean when max/min exceeds ``imbalance``. Pure function:
+    every rank computes the same plan from the all-gathered counts."""
+    counts = [int(c) for c in counts]
+    world = len(counts)
+    if world < 2:
+        return []
+    hi, lo = max(counts), min(counts)
+    if hi < min_move or hi <= imbalance * max(lo, 1):
+        return []
+    mean = sum(counts) / world
+    donors = [[r, c - int(math.floor(mean))] for r, c in enumerate(counts) if c > mean]
+    takers = [[r, int(math.ceil(mean)) - c] for r, c in enumerate(counts) if c < mean]
+    plan = []
+    di = ti = 0
+    while di < len(donors) and ti < len(takers):
+        n = min(donors[di][1], takers[ti][1])
+        if n >= min_move:
+            plan.append((donors[di][0], takers[ti][0], n))
+        donors[di][1] -= n
+        takers[ti][1] -= n
+        if donors[di][1] <= 0:
+            di += 1
+        if takers[ti][1] <= 0:
+            ti += 1
+    return plan
+
+
+NODE_WIDTH = 13  # 11 node doubles + volume + split flag
+
+
+def _pack(nodes, split, vol):
+    a = np.empty((len(nodes), NODE_WIDTH))
+    if len(nodes):
+        a[:, :11] = np.asarray(nodes).view(np.float64).reshape(-1, 11)
+        a[:, 11] = vol
+        a[:, 12] = split
+    return a
+
+
+def _unpack(a):
+    nodes = np.ascontiguousarray(a[:, :11])
+    return nodes, a[:, 12].astype(np.int8), np.ascontiguousarray(a[:, 11])
+
+
+def solve_sharded(shard, epsilon: float, comm: Comm, time_limit: Optional[float] = None,
+                  max_evaluations: Optional[int] = None, rebalance_every: int = 4,
+                  imbalance: float = 1.5, max_migrate: int = 65536,
+                  trace: bool = True) -> ShardedReport:
+    """Runs the sharded branch-and-bound to the certified gap ``epsilon``."""
+    t0 = time.perf_counter()
+    certified = -math.inf
+    status = "queue_exhausted"
+    wave = 0
+    migrated = 0
+    tr = []
+    while True:
+        st = shard.status()
+        local_min = min(st["frontier_min"], st["floor_lower"])
+        mins = comm.allreduce([st["best_value"], local_min], "min")
+        dstar, gmin = float(mins[0]), float(mins[1])
+        sums = comm.allreduce([float(st["live_nodes"]), float(st["bound_evaluations"])], "sum")
+        live, evals = int(sums[0]), int(sums[1])
+        elapsed = float(comm.allreduce([time.perf_counter() - t0], "max")[0])
+        certified = max(certified, min(dstar, gmin))
+        if trace:
+            tr.append((wave, evals, dstar, certified, live))
+        if dstar - certified <= epsilon:
+            status = "epsilon_optimal"
+            break
+        if live == 0:
+            status = "queue_exhausted"
+            break
+        if time_limit is not None and elapsed >= time_limit:
+            status = "time_limit"
+            break
+        if max_evaluations is not None and evals >= max_evaluations:
+            status = "time_limit"
+            break
+        shard.set_incumbent(dstar)
+        budget = 0
+        if max_evaluations is not None:
+            budget = max(1, (max_evaluations - evals) // comm.world)
+        shard.expand(dstar - epsilon, budget)
+        wave += 1
+        if comm.world > 1 and rebalance_every > 0 and wave % rebalance_every == 0:
+            counts = comm.allgather(float(shard.status()["live_nodes"]))
+            for src, dst, n in plan_rebalance(counts, imbalance):
+                n = min(n, max_migrate)
+                if comm.rank == src:
+                    comm.send_array(_pack(*shard.export(n)), dst)
+                elif comm.rank == dst:
+                    nodes, split, vol = _unpack(comm.recv_array(src, NODE_WIDTH))
+                    shard.import_(nodes, split, vol)
+                migrated += n
+    # The rank holding the best incumbent publishes its pose.
+    res = shard.result()
+    best = comm.allreduce([res["value"]], "min")[0]
+    owner = comm.allreduce([comm.rank if res["value"] == best else comm.world], "min")[0]
+    pose = np.concatenate([res["r"], res["t"]]) if comm.rank == owner else np.zeros(6)
+    pose = comm.allreduce(list(pose), "sum")
+    evals = int(comm.allreduce([float(res["bound_evaluations"])], "sum")[0])
+    return ShardedReport(best_value=float(best), global_lower=certified,
+                         gap=float(best) - certified, status=status, r=pose[:3], t=pose[3:],
+                         bound_evaluations=evals, waves=wave, migrated_nodes=migrated,
+                         wall_time_seconds=time.perf_counter() - t0, trace=tr)

@@ -1,0 +1,159 @@
+"""GPU-resident solve() against the reference's solver tests
+(proj/tests/test_solver.cpp, test_bench.cpp) and golden runs of the
+unmodified reference (tests/golden/solver_golden.json)."""
+import math
+
+import numpy as np
+import pytest
+
+from oracle.bind import Mixture, Oracle
+
+pytestmark = pytest.mark.gpu
+
+
+def zr(k):
+    return (math.exp(k) - math.exp(-k)) / k
+
+
+def toy_ctx(g, var=1.0, k2=5.0, zeta=0.5):
+    return g.ObjectiveContext([{"mu": [[0, 0, 2]], "sigma2": [var], "phi1": [1.0],
+                                "dir": [[0, 0, 1]], "kappa2": [k2], "phi2": [1.0]}], zeta,
+                              single_mixture=True)
+
+
+def box_domain(g, rot_hw, trans_hw, tc=(0, 0, 0)):
+    return g.PoseDomain(np.zeros(3), rot_hw, np.array([[*tc, trans_hw, trans_hw, trans_hw]], float))
+
+
+def check_invariants(r, eps):
+    assert r.gap >= -1e-9
+    assert (r.status == "epsilon_optimal") == (r.gap <= eps)
+    prev_u, prev_l = math.inf, -math.inf
+    for (_w, _e, ub, lb, _q, fu, fp, fr) in r.trace:
+        assert ub <= prev_u + 1e-15 and lb >= prev_l - 1e-15
+        prev_u, prev_l = ub, lb
+        assert abs(fu + fp + fr - 1.0) <= 1e-9
+
+
+def test_degenerate_single_pose_domain(gosma):
+    # test_solver.cpp:90-103
+    ctx = toy_ctx(gosma)
+    dom = box_domain(gosma, 0.0, 0.0, (0.1, -0.2, 0.3))
+    r = gosma.solve(ctx, dom, gosma.SolverConfig(epsilon=1e-6, zeta=0.5))
+    f = gosma.objective_value(ctx, [0, 0, 0], [0.1, -0.2, 0.3])
+    assert r.best_value == f
+    assert abs(r.gap) <= 1e-6 and r.status == "epsilon_optimal"
+    check_invariants(r, 1e-6)
+
+
+def test_aligned_toy_optimum(gosma, golden_solver):
+    # test_solver.cpp:105-140 + the reference's own run of it
+    ctx = toy_ctx(gosma, var=4.0, k2=2.0)
+    dom = box_domain(gosma, 0.4, 0.4, (0.05, -0.03, 0.02))
+    r = gosma.solve(ctx, dom, gosma.SolverConfig(epsilon=0.3, zeta=0.5, max_evaluations=3000000))
+    fstar = -zr(4.0) / zr(2.0) ** 2
+    assert r.status == "epsilon_optimal"
+    assert abs(r.best_value - fstar) <= 1e-6 and r.best_value >= fstar - 1e-9
+    assert r.global_lower <= fstar + 1e-9
+    from paper_1812_01232_b200.host import rotation_matrix
+    cam = rotation_matrix(r.r) @ (np.array([0, 0, 2.0]) - r.t)
+    assert abs(np.linalg.norm(cam) - 2.0) < 0.01
+    assert math.acos(min(1.0, cam[2] / np.linalg.norm(cam))) < 0.01
+    assert r.sma_invocations > 0 and r.branches_expanded > 0
+    check_invariants(r, 0.3)
+    ref = golden_solver["solves"][0]
+    assert abs(r.best_value - ref["best_value"]) <= 1e-9
+    assert abs(r.global_lower - ref["global_lower"]) <= 1e-3
+
+
+def test_matches_grid_oracle_on_toy_pair(gosma, golden_solver):
+    # test_bench.cpp:222-239: LB <= grid min, d* <= grid min + eps
+    s = golden_solver["solves"][1]
+    mix = Mixture.from_dict(s["mixture"])
+    ctx = gosma.ObjectiveContext([{"mu": mix.mu, "sigma2": mix.sigma2, "phi1": mix.phi1,
+                                   "dir": mix.dir, "kappa2": mix.kappa2, "phi2": mix.phi2}],
+                                 mix.zeta, single_mixture=True)
+    dom = gosma.PoseDomain(np.zeros(3), s["rot_hw"], np.array(s["boxes"]))
+    r = gosma.solve(ctx, dom, gosma.SolverConfig(epsilon=0.05, zeta=mix.zeta, batch_size=256,
+                                                 max_evaluations=60000))
+    o = Oracle(mix)
+    axes_r = np.linspace(-0.3, 0.3, 7)
+    b = s["boxes"][0]
+    best = math.inf
+    for a in axes_r:
+        for bb in axes_r:
+            for c in axes_r:
+                for x in np.linspace(b[0] - b[3], b[0] + b[3], 7):
+                    for y in np.linspace(b[1] - b[4], b[1] + b[4], 7):
+                        for z in np.linspace(b[2] - b[5], b[2] + b[5], 7):
+                            best = min(best, o.objective([a, bb, c], [x, y, z]))
+    assert r.global_lower <= best + 1e-9
+    assert r.best_value <= best + 0.05
+    # the reference reaches the same incumbent within eps under the same budget
+    assert abs(r.best_value - s["best_value"]) <= 0.05
+    check_invariants(r, 0.05)
+
+
+def test_validation_and_infeasible_domain(gosma):
+    # test_solver.cpp:261-279
+    ctx = toy_ctx(gosma)
+    dom = box_domain(gosma, 0.2, 0.2)
+    with pytest.raises(ValueError):
+        gosma.solve(ctx, dom, gosma.SolverConfig(epsilon=0.0, zeta=0.5))
+    with pytest.raises(ValueError):
+        gosma.solve(ctx, dom, gosma.SolverConfig(batch_size=0, zeta=0.5))
+    with pytest.raises(ValueError):
+        gosma.solve(ctx, dom, gosma.SolverConfig(zeta=0.25))
+    dead = box_domain(gosma, 0.1, 0.05, (0, 0, 2))
+    with pytest.raises(gosma.InfeasiblePoseError):
+        gosma.solve(ctx, dead, gosma.SolverConfig(zeta=0.5))
+
+
+def test_budgets_and_capacity_folding(gosma):
+    # test_solver.cpp:197-259
+    rng = np.random.default_rng(909)
+    mu = rng.normal(size=(2, 3)) + np.array([0, 0, 2.5])
+    d = rng.normal(size=(2, 3)) + np.array([0, 0, 2.0])
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    ctx = gosma.ObjectiveContext([{"mu": mu, "sigma2": rng.uniform(0.4, 1.2, 2), "phi1": [.5, .5],
+                                   "dir": d, "kappa2": rng.uniform(3, 12, 2), "phi2": [.5, .5]}],
+                                 0.3, single_mixture=True)
+    dom = box_domain(gosma, 0.8, 0.8)
+    rb = gosma.solve(ctx, dom, gosma.SolverConfig(epsilon=1e-9, zeta=0.3, max_evaluations=1))
+    assert rb.status == "time_limit" and math.isfinite(rb.best_value)
+    check_invariants(rb, 1e-9)
+    rt = gosma.solve(ctx, dom, gosma.SolverConfig(epsilon=1e-9, zeta=0.3, time_limit=0.0))
+    assert rt.status == "time_limit" and math.isfinite(rt.best_value)
+    rc = gosma.solve(ctx, box_domain(gosma, 0.6, 0.6),
+                     gosma.SolverConfig(epsilon=0.05, zeta=0.3, batch_size=64, queue_capacity=16,
+                                        max_evaluations=30000, wave_nodes=8))
+    assert math.isfinite(rc.best_value) and rc.global_lower <= rc.best_value + 1e-9
+    check_invariants(rc, 0.05)
+
+
+def test_local_refine(gosma):
+    # test_solver.cpp:233-279
+    ctx = toy_ctx(gosma)
+    dom = box_domain(gosma, 0.4, 0.4)
+    fstar = -zr(10.0) / zr(5.0) ** 2
+    v, r, t = gosma.local_refine(ctx, [0, 0, 0], [0, 0, 0], dom)
+    assert v <= gosma.objective_value(ctx, [0, 0, 0], [0, 0, 0]) + 1e-12
+    v, r, t = gosma.local_refine(ctx, [0.03, -0.04, 0.02], [-0.03, 0.05, 0.02], dom)
+    assert abs(v - fstar) <= 1e-9 * abs(fstar)
+    assert np.linalg.norm(gosma.objective_gradient(ctx, r, t)) < 1e-6
+    corner = box_domain(gosma, 0.05, 0.05, (0.3, 0.3, -0.4))
+    v, r, t = gosma.local_refine(ctx, [0, 0, 0], [0.3, 0.3, -0.4], corner)
+    assert np.max(np.abs(t - np.array([0.3, 0.3, -0.4]))) <= 0.05 + 1e-12
+    assert np.max(np.abs(r)) <= 0.05 + 1e-12
+
+
+def test_sharded_driver_single_rank_equals_solve(gosma):
+    from paper_1812_01232_b200.distributed import Comm, solve_sharded
+    ctx = toy_ctx(gosma, var=4.0, k2=2.0)
+    dom = box_domain(gosma, 0.4, 0.4, (0.05, -0.03, 0.02))
+    cfg = gosma.SolverConfig(epsilon=0.3, zeta=0.5)
+    shard = gosma.ShardSolver(ctx, dom, cfg, 0, 1)
+    rep = solve_sharded(shard, 0.3, Comm())
+    ref = gosma.solve(ctx, dom, cfg)
+    assert rep.status == "epsilon_optimal"
+    assert abs(rep.best_value - ref.best_value) <= 1e-9
