@@ -153,7 +153,7 @@ constexpr int kColF4 = 2;  // float4 per image column
 
 struct Row {
   float uhx, uhy, uhz, ulx, uly, ulz, klo, khi, kst, Fhi, Fst, cp2, sp2, csp2, s4, c4, usx, usy,
-      usz;
+      usz, klo2;
 };
 
 // Cross LB exact path: K minimum over the kappa interval (vertex case,
@@ -184,7 +184,7 @@ __device__ __noinline__ float cross_lb_exact(float klo, float khi, float k2, flo
 // of in sin/cos products.
 template <bool kSame>
 __device__ __forceinline__ void cross_pair(const Row& r, const float4 qa, const float4 qb, float& l,
-                                           float& u, float& me) {
+                                           float& u, float& ma, float& mb) {
   const float k2 = qa.w;
   const float dx = (r.uhx - qa.x) + (r.ulx - qb.x);
   const float dy = (r.uhy - qa.y) + (r.uly - qb.y);
@@ -238,16 +238,21 @@ __device__ __forceinline__ void cross_pair(const Row& r, const float4 qa, const 
   const float e2 = ab2 * xs * D1 * den2 * inv;  // (K - a - b) log2e, UB
   float t1 = ex2f(e1) * rK1;
   float t2 = ex2f(e2) * rK2;
-  // exact paths: K's interior minimum (cos B < -klo/k2) or small K
-  if (e1 > kNegligibleLog2 && (c2 * k2 < 2.0f * (k2 - r.klo) || !(K1 > 15.0f)))
-    t1 = cross_lb_exact(r.klo, r.khi, k2, 4.0f - c2, c2, K1, e1);
-  if (e2 > kNegligibleLog2 && !(K2 > 15.0f)) t2 = ex2f(e2 + log2w(K2));
-  // FP32 error estimate of the LB term (relative): B = theta - psi carries
-  // ~u theta absolute error, amplified in e1 by max(x, y)/num.
-  const float err = fmaf(fabsf(g) * fminf(x, y), kErrAmp, fmaf(fabsf(e1), kErrExp, kErrTerm));
+  // exact paths (one rarely-taken branch): K's interior minimum
+  // (cos B < -klo/k2, i.e. c2 k2 + 2 klo < 2 k2) or small K
+  const bool s1 = e1 > kNegligibleLog2 && (fmaf(c2, k2, r.klo2) < k2 + k2 || !(K1 > 15.0f));
+  const bool s2 = e2 > kNegligibleLog2 && !(K2 > 15.0f);
+  if (s1 | s2) {
+    if (s1) t1 = cross_lb_exact(r.klo, r.khi, k2, 4.0f - c2, c2, K1, e1);
+    if (s2) t2 = ex2f(e2 + log2w(K2));
+  }
+  // FP32 error estimate of the LB term: B = theta - psi
+  // carries ~u theta absolute error, amplified in e1 by min(x, y)/num (the
+  // operand used); accumulated as sum t |e1/num| min(x,y) and sum t |e1|.
   const float gt1 = qb.w * t1;  // G_j; F_i is applied to the row sum
   l += gt1;
-  me = fmaf(gt1, err, me);
+  ma = fmaf(gt1, fabsf(g) * fminf(x, y), ma);
+  mb = fmaf(gt1, fabsf(e1), mb);
   u = fmaf(qb.w, t2, u);
 }
 
@@ -325,7 +330,7 @@ __device__ __forceinline__ void self_pair(const float4& a0, const float4& a1, co
   if (e2 > kNegligibleLog2 && !(K2 > 15.0f)) t2 = ex2f(e2 + log2w(K2));
   const float ft1 = b1.y * t1;  // F_j (Flo); 2 F_i is applied to the row sum
   l += ft1;
-  me = fmaf(ft1, fmaf(fabsf(e1), kErrExp, kErrTerm), me);
+  me = fmaf(ft1, fabsf(e1), me);
   u = fmaf(b2.y, t2, u);  // F_j (Fst)
 }
 
@@ -336,6 +341,7 @@ __device__ __forceinline__ Row load_row(const WarpTables& T, int i) {
   r.uhy = a0.y;
   r.uhz = a0.z;
   r.klo = a0.w;
+  r.klo2 = 2.0f * a0.w;
   r.khi = a1.x;
   r.kst = a2.x;
   r.Fst = a2.y;
@@ -354,22 +360,23 @@ __device__ __forceinline__ Row load_row(const WarpTables& T, int i) {
   return r;
 }
 
-template <bool kSame>
+template <bool kSame, bool kCross, bool kSelf>
 __device__ __forceinline__ void class_pairs(const WarpTables& T, const ClassSpan cs, int lane,
                                             float w, double& lb_self, double& lb_cross,
                                             double& ub_self, double& ub_cross, double& lb_err) {
   const int n = cs.n1;
   // Cross terms: rows over lanes, columns broadcast.
-  for (int base = 0; base < n; base += 32) {
+  for (int base = 0; kCross && base < n; base += 32) {
     const int il = base + lane;
     if (il < n) {
       const Row r = load_row(T, cs.o1 + il);
-      float l = 0.0f, u = 0.0f, me = 0.0f;
+      float l = 0.0f, u = 0.0f, ma = 0.0f, mb = 0.0f;
 #pragma unroll 2
       for (int j = cs.o2; j < cs.o2 + cs.n2; ++j)
-        cross_pair<kSame>(r, T.c0[j], T.c1[j], l, u, me);
+        cross_pair<kSame>(r, T.c0[j], T.c1[j], l, u, ma, mb);
       lb_cross += static_cast<double>(w * r.Fhi * l);
-      lb_err += static_cast<double>(2.0f * w * r.Fhi * me);
+      lb_err += static_cast<double>(
+          2.0f * w * r.Fhi * fmaf(ma, kErrAmp, fmaf(mb, kErrExp, l * kErrTerm)));
       ub_cross += static_cast<double>(w * r.Fst * u);
     }
   }
@@ -377,7 +384,7 @@ __device__ __forceinline__ void class_pairs(const WarpTables& T, const ClassSpan
   // (i, i+d mod n), d = 1..(n-1)/2, plus d = n/2 for i < n/2 when n is even.
   const int dfull = (n - 1) / 2;
   const bool even = (n % 2) == 0;
-  for (int base = 0; base < n; base += 32) {
+  for (int base = 0; kSelf && base < n; base += 32) {
     const int il = base + lane;
     if (il < n) {
       const int i = cs.o1 + il;
@@ -406,7 +413,7 @@ __device__ __forceinline__ void class_pairs(const WarpTables& T, const ClassSpan
                          make_float3(bl.x, bl.y, bl.z), l, u, me);
       }
       lb_self += static_cast<double>(2.0f * w * a1.y * l);
-      lb_err += static_cast<double>(2.0f * w * a1.y * me);
+      lb_err += static_cast<double>(2.0f * w * a1.y * fmaf(me, kErrExp, l * kErrTerm));
       ub_self += static_cast<double>(2.0f * w * a2.y * u);
     }
   }
@@ -459,7 +466,13 @@ __device__ __forceinline__ void psi_trans_half(double u0, double u1, double u2, 
   ct = 0.5 * sqrt(bc);
 }
 
-__global__ void __launch_bounds__(kWarpsPerCta * 32, 5)
+// kMode: kModeFull = every term per node; kSelfOnly = per distinct translation
+// cuboid, the translation-only (self + diagonal) sums; kCrossCached = per node,
+// the cross terms plus the cached self sums of the node's cuboid.
+enum { kModeFull = 0, kSelfOnly = 1, kCrossCached = 2 };
+
+template <int kMode>
+__global__ void __launch_bounds__(kWarpsPerCta * 32, 6)
     eval_bounds_kernel(const DevCtx ctx, const EvalArgs args) {
   extern __shared__ float4 smem4[];
   const int lane = threadIdx.x & 31;
@@ -658,7 +671,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 5)
         T.r4[i] = make_float4(static_cast<float>(v0 * iv), static_cast<float>(v1 * iv),
                               static_cast<float>(v2 * iv), static_cast<float>(4.0 * sp * sp));
       }
-      if (!infeasible) {
+      if (!infeasible && kMode != kCrossCached) {
         lb_self += static_cast<double>(w * dsl);
         lb_err += static_cast<double>(w * dsl * kErrTerm);
         ub_self += static_cast<double>(w * dsu);
@@ -667,7 +680,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 5)
     // split decision (subdivide_adaptive, se3.cpp:107-121)
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) st_max = fmax(st_max, __shfl_xor_sync(kFull, st_max, o));
-    if (lane == 0 && args.split_rot) {
+    if (kMode != kSelfOnly && lane == 0 && args.split_rot) {
       const bool rot_ok = rhw > 1e-9;
       const bool trans_ok = fmax(fmax(h0, h1), h2) > 1e-9;
       int8_t sr;
@@ -680,14 +693,20 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 5)
     }
     if (infeasible) {
       if (lane == 0) {
-        args.lower[node] = INFINITY;
-        args.upper[node] = INFINITY;
+        if (kMode == kSelfOnly) {
+          double* o = args.self_out + 4 * node;
+          o[0] = o[1] = o[2] = 0.0;
+          o[3] = 1.0;  // infeasible
+        } else {
+          args.lower[node] = INFINITY;
+          args.upper[node] = INFINITY;
+        }
       }
       __syncwarp();
       continue;
     }
     // ---- per-column prep: q_j = R0^T m_j (bounds.cpp:97-102), double-float
-    for (int j = lane; j < N2; j += 32) {
+    for (int j = lane; kMode != kSelfOnly && j < N2; j += 32) {
       const double x0 = ctx.m[3 * j], x1 = ctx.m[3 * j + 1], x2 = ctx.m[3 * j + 2];
       const double q0 = R[0] * x0 + R[3] * x1 + R[6] * x2;
       const double q1 = R[1] * x0 + R[4] * x1 + R[7] * x2;
@@ -704,10 +723,11 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 5)
     for (int c = 0; c < ctx.n_classes; ++c) {
       const ClassSpan cs = ctx.cls[c];
       const float w = static_cast<float>(ctx.cls_w[c]);
+      constexpr bool kC = kMode != kSelfOnly, kS = kMode != kCrossCached;
       if (same) {
-        class_pairs<true>(T, cs, lane, w, lb_self, lb_cross, ub_self, ub_cross, lb_err);
+        class_pairs<true, kC, kS>(T, cs, lane, w, lb_self, lb_cross, ub_self, ub_cross, lb_err);
       } else {
-        class_pairs<false>(T, cs, lane, w, lb_self, lb_cross, ub_self, ub_cross, lb_err);
+        class_pairs<false, kC, kS>(T, cs, lane, w, lb_self, lb_cross, ub_self, ub_cross, lb_err);
       }
     }
     lb_self = warp_sum_d(lb_self);
@@ -715,6 +735,23 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 5)
     ub_self = warp_sum_d(ub_self);
     ub_cross = warp_sum_d(ub_cross);
     lb_err = warp_sum_d(lb_err);
+    if (kMode == kSelfOnly) {
+      if (lane == 0) {
+        double* o = args.self_out + 4 * node;
+        o[0] = lb_self;
+        o[1] = ub_self;
+        o[2] = lb_err;
+        o[3] = have_center ? 0.0 : 2.0;  // 2: no feasible centre (upper = +inf)
+      }
+      __syncwarp();
+      continue;
+    }
+    if (kMode == kCrossCached) {  // the cuboid's translation-only sums
+      const double* o = args.self_out + 4 * static_cast<long long>(args.tindex[node]);
+      lb_self = o[0];
+      ub_self = o[1];
+      lb_err += o[2];
+    }
     if (lane == 0) {
       // Soundness margin: the FP32 error estimate of the terms plus a relative
       // floor on the |term| mass (all terms >= 0).
@@ -738,20 +775,23 @@ size_t eval_smem_per_warp(const DevCtx& ctx) {
   return f4 * sizeof(float4);
 }
 
-cudaError_t launch_eval_bounds(const DevCtx& ctx, const EvalArgs& a, int sm_count,
-                               cudaStream_t stream) {
+namespace {
+
+template <int kMode>
+cudaError_t launch_mode(const DevCtx& ctx, const EvalArgs& a, int sm_count,
+                        cudaStream_t stream) {
   if (a.n <= 0) return cudaSuccess;
   const size_t smem = eval_smem_per_warp(ctx) * kWarpsPerCta;
   static size_t configured = 0;
   if (smem > 48 * 1024 && smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(eval_bounds_kernel,
+    cudaError_t e = cudaFuncSetAttribute(eval_bounds_kernel<kMode>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     configured = smem;
   }
   int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, eval_bounds_kernel,
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, eval_bounds_kernel<kMode>,
                                                                 kWarpsPerCta * 32, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
@@ -760,11 +800,53 @@ cudaError_t launch_eval_bounds(const DevCtx& ctx, const EvalArgs& a, int sm_coun
   if (grid > need) grid = need;
   e = cudaMemsetAsync(a.work, 0, sizeof(unsigned int), stream);
   if (e != cudaSuccess) return e;
-  eval_bounds_kernel<<<static_cast<unsigned>(grid), kWarpsPerCta * 32, smem, stream>>>(ctx, a);
+  eval_bounds_kernel<kMode>
+      <<<static_cast<unsigned>(grid), kWarpsPerCta * 32, smem, stream>>>(ctx, a);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }
 
+}  // namespace
+
+cudaError_t launch_eval_bounds(const DevCtx& ctx, const EvalArgs& a, int sm_count,
+                               cudaStream_t stream) {
+  return launch_mode<kModeFull>(ctx, a, sm_count, stream);
+}
+
+cudaError_t launch_eval_self(const DevCtx& ctx, const EvalArgs& a, int sm_count,
+                             cudaStream_t stream) {
+  return launch_mode<kSelfOnly>(ctx, a, sm_count, stream);
+}
+
+cudaError_t launch_eval_cross_cached(const DevCtx& ctx, const EvalArgs& a, int sm_count,
+                                     cudaStream_t stream) {
+  return launch_mode<kCrossCached>(ctx, a, sm_count, stream);
+}
+
+
 unsigned long long bound_kernel_launch_count() { return g_launches.load(); }
+
+namespace {
+// {tc[3], thw[3]} cuboid records -> node records for the self kernel (the
+// rotation part does not enter the translation-only sums).
+__global__ void boxes_to_nodes(const double* boxes, size_t n, gosma_node* out) {
+  const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  gosma_node b{};
+  for (int a = 0; a < 3; ++a) {
+    b.tc[a] = boxes[6 * i + a];
+    b.thw[a] = boxes[6 * i + 3 + a];
+  }
+  b.lower = -INFINITY;
+  out[i] = b;
+}
+}  // namespace
+
+cudaError_t boxes_as_nodes(const double* d_boxes, size_t n, gosma_node* d_out,
+                           cudaStream_t stream) {
+  if (n == 0) return cudaSuccess;
+  boxes_to_nodes<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(d_boxes, n, d_out);
+  return cudaGetLastError();
+}
 
 }  // namespace gosma

@@ -132,6 +132,11 @@ void ctx_free_device(gosma_ctx* ctx) {
   ctx->owned.clear();
   if (ctx->d_work) cudaFree(ctx->d_work);
   ctx->d_work = nullptr;
+  cudaFree(ctx->d_cache_nodes);
+  cudaFree(ctx->d_cache_self);
+  ctx->d_cache_nodes = nullptr;
+  ctx->d_cache_self = nullptr;
+  ctx->cache_cap = 0;
   ctx->scratch.release();
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   ctx->stream = nullptr;
@@ -353,6 +358,51 @@ int gosma_eval_bounds_device(gosma_ctx* ctx, const gosma_node* d_nodes, size_t n
   a.work = static_cast<unsigned int*>(ctx->d_work);
   const cudaError_t e = launch_eval_bounds(ctx->dev, a, ctx->sm_count, s);
   if (e != cudaSuccess) return cuda_error(e, "eval_bounds launch");
+  return GOSMA_OK;
+}
+
+int gosma_eval_bounds_cached_device(gosma_ctx* ctx, const gosma_node* d_nodes, size_t n,
+                                    const int32_t* d_tindex, const double* d_tboxes,
+                                    size_t n_tboxes, double skip, double* d_lower,
+                                    double* d_upper, int8_t* d_split, void* stream) {
+  if (!ctx) return set_error(GOSMA_EINVAL, "null context");
+  if (n == 0) return GOSMA_OK;
+  if (!d_nodes || !d_tindex || !d_tboxes || !d_lower || !d_upper || n_tboxes == 0)
+    return set_error(GOSMA_EINVAL, "null buffer");
+  DeviceGuard g(ctx->device);
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+  cudaError_t e;
+  if (n_tboxes > ctx->cache_cap) {
+    cudaFree(ctx->d_cache_nodes);
+    cudaFree(ctx->d_cache_self);
+    ctx->d_cache_nodes = nullptr;
+    ctx->d_cache_self = nullptr;
+    if ((e = cudaMalloc(&ctx->d_cache_nodes, n_tboxes * sizeof(gosma_node))) != cudaSuccess ||
+        (e = cudaMalloc(&ctx->d_cache_self, n_tboxes * 4 * sizeof(double))) != cudaSuccess)
+      return cuda_error(e, "cache alloc");
+    ctx->cache_cap = n_tboxes;
+  }
+  if ((e = boxes_as_nodes(d_tboxes, n_tboxes, ctx->d_cache_nodes, s)) != cudaSuccess)
+    return cuda_error(e, "boxes");
+  EvalArgs a;
+  a.nodes = reinterpret_cast<const double*>(ctx->d_cache_nodes);
+  a.n = static_cast<long long>(n_tboxes);
+  a.skip_upper_at = skip;
+  a.lower = nullptr;
+  a.upper = nullptr;
+  a.split_rot = nullptr;
+  a.work = static_cast<unsigned int*>(ctx->d_work);
+  a.self_out = ctx->d_cache_self;
+  if ((e = launch_eval_self(ctx->dev, a, ctx->sm_count, s)) != cudaSuccess)
+    return cuda_error(e, "self kernel");
+  a.nodes = reinterpret_cast<const double*>(d_nodes);
+  a.n = static_cast<long long>(n);
+  a.lower = d_lower;
+  a.upper = d_upper;
+  a.split_rot = d_split;
+  a.tindex = d_tindex;
+  if ((e = launch_eval_cross_cached(ctx->dev, a, ctx->sm_count, s)) != cudaSuccess)
+    return cuda_error(e, "cross kernel");
   return GOSMA_OK;
 }
 

@@ -51,6 +51,9 @@ struct gosma_ctx {
   double lb_margin = gosma::kDefaultLbMargin;
   std::vector<void*> owned;
   void* d_work = nullptr;
+  gosma_node* d_cache_nodes = nullptr;  // translation-cached mode scratch
+  double* d_cache_self = nullptr;
+  size_t cache_cap = 0;
   cudaStream_t stream = nullptr;
   gosma::Scratch scratch;
   std::mutex mu;

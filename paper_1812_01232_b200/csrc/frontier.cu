@@ -79,8 +79,12 @@ __global__ void mark_holes(unsigned long long* key, const unsigned int* sel, siz
 }
 
 // subdivide_adaptive (se3.cpp:107-147): 8 children per selected node.
+// With `toff` set, also emits the wave's distinct translation cuboids for the
+// translation-cached bound kernels: a rotation split keeps the parent's cuboid
+// for all 8 children (one slot), a translation split makes 8 new ones.
 __global__ void expand(const gosma_node* front, const int8_t* split, const double* vol,
-                       const unsigned int* sel, size_t n_sel, gosma_node* kids, double* kid_vol) {
+                       const unsigned int* sel, size_t n_sel, gosma_node* kids, double* kid_vol,
+                       const unsigned int* toff, int* tidx, gosma_node* tnodes) {
   const size_t t = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
   if (t >= n_sel * 8) return;
   const size_t p = sel[t / 8];
@@ -104,6 +108,19 @@ __global__ void expand(const gosma_node* front, const int8_t* split, const doubl
   }
   kids[t] = k;  // lower inherited: the parent's bound is valid on any subset
   kid_vol[t] = vol[p] / 8.0;
+  if (toff) {
+    const bool rot = split[p] == 1;
+    const unsigned slot = toff[t / 8] + (rot ? 0u : static_cast<unsigned>(c));
+    tidx[t] = static_cast<int>(slot);
+    if (!rot || c == 0) tnodes[slot] = k;
+  }
+}
+
+__global__ void cuboid_counts(const int8_t* split, const unsigned int* sel, size_t n_sel,
+                              unsigned int* cnt) {
+  const size_t k = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+  if (k < n_sel) cnt[k] = split[sel[k]] == 1 ? 1u : 8u;
+  if (k == n_sel) cnt[k] = 0u;
 }
 
 // Route evaluated children (solver.cpp:396-405).
@@ -233,7 +250,11 @@ cudaError_t Frontier::reserve(size_t cap_nodes, size_t wave) {
   }
   if (wave > sel_cap) {
     cudaFree(sel);
+    cudaFree(tcnt);
+    cudaFree(toff);
     if ((e = cudaMalloc(&sel, wave * 4)) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&tcnt, (wave + 1) * 4)) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&toff, (wave + 1) * 4)) != cudaSuccess) return e;
     sel_cap = wave;
   }
   const size_t nk = wave * 8;
@@ -245,6 +266,12 @@ cudaError_t Frontier::reserve(size_t cap_nodes, size_t wave) {
     cudaFree(kid_vol);
     cudaFree(keep);
     cudaFree(kept_idx);
+    cudaFree(tidx);
+    cudaFree(tnodes);
+    cudaFree(tself);
+    if ((e = cudaMalloc(&tidx, nk * 4)) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&tnodes, nk * sizeof(gosma_node))) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&tself, nk * 4 * sizeof(double))) != cudaSuccess) return e;
     if ((e = cudaMalloc(&kids, nk * sizeof(gosma_node))) != cudaSuccess) return e;
     if ((e = cudaMalloc(&kid_lower, nk * 8)) != cudaSuccess) return e;
     if ((e = cudaMalloc(&kid_upper, nk * 8)) != cudaSuccess) return e;
@@ -281,6 +308,15 @@ void Frontier::release() {
   cudaFree(kid_vol);
   cudaFree(keep);
   cudaFree(kept_idx);
+  cudaFree(tcnt);
+  cudaFree(toff);
+  cudaFree(tidx);
+  cudaFree(tnodes);
+  cudaFree(tself);
+  tcnt = toff = nullptr;
+  tidx = nullptr;
+  tnodes = nullptr;
+  tself = nullptr;
   cudaFree(stats);
   cudaFree(amin);
   cudaFree(counter);
@@ -473,7 +509,29 @@ cudaError_t Frontier::select_smallest(size_t want, unsigned long long limit, cud
 
 cudaError_t Frontier::expand_selected(size_t n_sel, cudaStream_t s) {
   if (n_sel == 0) return cudaSuccess;
-  expand<<<grid_for(n_sel * 8, 256), 256, 0, s>>>(nodes, split, vol, sel, n_sel, kids, kid_vol);
+  expand<<<grid_for(n_sel * 8, 256), 256, 0, s>>>(nodes, split, vol, sel, n_sel, kids, kid_vol,
+                                                   nullptr, nullptr, nullptr);
+  return cudaGetLastError();
+}
+
+cudaError_t Frontier::expand_selected_cached(size_t n_sel, cudaStream_t s, size_t* n_cuboids) {
+  *n_cuboids = 0;
+  if (n_sel == 0) return cudaSuccess;
+  cuboid_counts<<<grid_for(n_sel + 1, 256), 256, 0, s>>>(split, sel, n_sel, tcnt);
+  size_t need = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, need, tcnt, toff, static_cast<int>(n_sel + 1), s);
+  cudaError_t e = ensure_temp(need);
+  if (e != cudaSuccess) return e;
+  cub::DeviceScan::ExclusiveSum(temp, need, tcnt, toff, static_cast<int>(n_sel + 1), s);
+  expand<<<grid_for(n_sel * 8, 256), 256, 0, s>>>(nodes, split, vol, sel, n_sel, kids, kid_vol,
+                                                   toff, tidx, tnodes);
+  unsigned int total = 0;
+  if ((e = cudaMemcpyAsync(h_counter, toff + n_sel, sizeof(unsigned int),
+                           cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+    return e;
+  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+  std::memcpy(&total, h_counter, sizeof(unsigned int));
+  *n_cuboids = total;
   return cudaGetLastError();
 }
 

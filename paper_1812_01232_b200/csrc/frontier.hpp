@@ -55,6 +55,12 @@ struct Frontier {
   int* keep = nullptr;
   unsigned int* kept_idx = nullptr;
   size_t kid_cap = 0;
+  // distinct translation cuboids of one wave (translation-cached bounds)
+  unsigned int* tcnt = nullptr;  // per selected parent: 1 (rotation split) or 8
+  unsigned int* toff = nullptr;  // exclusive scan of tcnt (n_sel + 1 entries)
+  int* tidx = nullptr;           // child -> cuboid slot
+  gosma_node* tnodes = nullptr;  // cuboid slots (translation part used)
+  double* tself = nullptr;       // 4 doubles per cuboid: self LB, self UB, err, flag
   // reductions / scratch
   RouteStats* stats = nullptr;
   ArgMin* amin = nullptr;
@@ -78,6 +84,7 @@ struct Frontier {
   // their indices to sel, marks them holes, returns the count.
   cudaError_t select_smallest(size_t want, unsigned long long limit, cudaStream_t s, size_t* n);
   cudaError_t expand_selected(size_t n_sel, cudaStream_t s);
+  cudaError_t expand_selected_cached(size_t n_sel, cudaStream_t s, size_t* n_cuboids);
   cudaError_t best_child(size_t n_kids, cudaStream_t s, int* index, double* value);
   // route children against d*, append survivors
   cudaError_t route_append(size_t n_kids, double dstar, cudaStream_t s, RouteStats* out);

@@ -71,11 +71,23 @@ struct EvalArgs {
   double* upper;
   int8_t* split_rot;     // may be null
   unsigned int* work;    // dynamic work counter (zeroed before launch)
+  // translation-cached modes: per-cuboid {lb_self, ub_self, lb_err, flag}
+  double* self_out = nullptr;
+  const int32_t* tindex = nullptr;  // node -> cuboid (cross-cached mode)
 };
 
 cudaError_t launch_eval_bounds(const DevCtx& ctx, const EvalArgs& a, int sm_count,
                                cudaStream_t stream);
+// Translation-cached evaluation: self sums once per cuboid (a.nodes are the
+// cuboids as nodes, a.self_out receives 4 doubles each), then cross terms per
+// node with a.tindex mapping nodes to cuboids.
+cudaError_t launch_eval_self(const DevCtx& ctx, const EvalArgs& a, int sm_count,
+                             cudaStream_t stream);
+cudaError_t launch_eval_cross_cached(const DevCtx& ctx, const EvalArgs& a, int sm_count,
+                                     cudaStream_t stream);
 size_t eval_smem_per_warp(const DevCtx& ctx);
+cudaError_t boxes_as_nodes(const double* d_boxes, size_t n, gosma_node* d_out,
+                           cudaStream_t stream);
 unsigned long long bound_kernel_launch_count();
 
 // Host FP64 math (host_math.cpp) shared by SMA, the solver and the C ABI.

@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <atomic>
 #include <chrono>
 #include <cmath>
@@ -305,6 +306,10 @@ struct gosma_solver {
   double floor_lower = kInf;
   unsigned long long evals = 0, expanded = 0, wave = 0;
   size_t wave_nodes = 0, qcap = 0, mem_cap = 0;
+  // translation-cached child bounds (GOSMA_FULL_KERNEL=1 selects the single
+  // full kernel, for A/B measurements)
+  bool cached = std::getenv("GOSMA_FULL_KERNEL") == nullptr;
+  unsigned long long cuboid_evals = 0;
   std::chrono::steady_clock::time_point t_start;
   double elapsed() const {
     return std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
@@ -524,16 +529,32 @@ int gosma_solver_expand(gosma_solver* S, double limit, unsigned long long max_ev
     }
   }
   const size_t n_kids = n_sel * 8;
-  if ((e = S->F.expand_selected(n_sel, s)) != cudaSuccess) return cuda_error(e, "expand");
   EvalArgs a;
+  a.work = static_cast<unsigned int*>(ctx->d_work);
+  a.skip_upper_at = S->dstar();
+  if (S->cached) {
+    // Translation-cached bounds: the self sums once per distinct cuboid
+    // (rotation-split siblings share theirs), then the cross sums per child.
+    size_t n_cub = 0;
+    if ((e = S->F.expand_selected_cached(n_sel, s, &n_cub)) != cudaSuccess)
+      return cuda_error(e, "expand");
+    a.nodes = reinterpret_cast<const double*>(S->F.tnodes);
+    a.n = static_cast<long long>(n_cub);
+    a.self_out = S->F.tself;
+    if ((e = launch_eval_self(ctx->dev, a, ctx->sm_count, s)) != cudaSuccess)
+      return cuda_error(e, "eval cuboids");
+    a.tindex = S->F.tidx;
+    S->cuboid_evals += n_cub;
+  } else if ((e = S->F.expand_selected(n_sel, s)) != cudaSuccess) {
+    return cuda_error(e, "expand");
+  }
   a.nodes = reinterpret_cast<const double*>(S->F.kids);
   a.n = static_cast<long long>(n_kids);
-  a.skip_upper_at = S->dstar();
   a.lower = S->F.kid_lower;
   a.upper = S->F.kid_upper;
   a.split_rot = S->F.kid_split;
-  a.work = static_cast<unsigned int*>(ctx->d_work);
-  if ((e = launch_eval_bounds(ctx->dev, a, ctx->sm_count, s)) != cudaSuccess)
+  if ((e = (S->cached ? launch_eval_cross_cached(ctx->dev, a, ctx->sm_count, s)
+                      : launch_eval_bounds(ctx->dev, a, ctx->sm_count, s))) != cudaSuccess)
     return cuda_error(e, "eval children");
   S->evals += n_kids;
   S->expanded += n_sel;
@@ -673,10 +694,5 @@ int gosma_solve(gosma_ctx* ctx, const gosma_domain* domain, const gosma_config* 
   return status == GOSMA_STATUS_TIME_LIMIT ? GOSMA_EBUDGET : GOSMA_OK;
 }
 
-int gosma_eval_bounds_cached_device(gosma_ctx*, const gosma_node*, size_t, const int32_t*,
-                                    const double*, size_t, double, double*, double*, int8_t*,
-                                    void*) {
-  return set_error(GOSMA_EINVAL, "gosma_eval_bounds_cached_device: not built yet");
-}
 
 }  // extern "C"

@@ -276,6 +276,85 @@ def test_config2_batch_properties(gosma):
     assert np.all(np.abs(up[idx][ff] - rup[ff]) <= TOL_UB * um[ff])
 
 
+def _cached_vs_full(gosma, classes, zeta, nodes, tboxes, tindex, skip=float("inf")):
+    import torch
+    ctx = gosma.ObjectiveContext(classes, zeta)
+    n = len(nodes)
+    d_nodes = torch.from_numpy(np.ascontiguousarray(nodes).view(np.uint8)).cuda()
+    d_tb = torch.from_numpy(np.ascontiguousarray(tboxes, dtype=np.float64)).cuda()
+    d_ti = torch.from_numpy(np.ascontiguousarray(tindex, dtype=np.int32)).cuda()
+    outs = []
+    s = torch.cuda.Stream()
+    for cached in (False, True):
+        d_lo = torch.empty(n, dtype=torch.float64, device="cuda")
+        d_up = torch.empty_like(d_lo)
+        d_sp = torch.empty(n, dtype=torch.int8, device="cuda")
+        with torch.cuda.stream(s):
+            if cached:
+                gosma.evaluate_branch_batch_cached_device(
+                    ctx, d_nodes.data_ptr(), n, d_ti.data_ptr(), d_tb.data_ptr(), len(tboxes),
+                    d_lo.data_ptr(), d_up.data_ptr(), d_sp.data_ptr(), skip, s.cuda_stream)
+            else:
+                gosma.evaluate_branch_batch_device(ctx, d_nodes.data_ptr(), n, d_lo.data_ptr(),
+                                                   d_up.data_ptr(), d_sp.data_ptr(), skip,
+                                                   s.cuda_stream)
+        s.synchronize()
+        outs.append((d_lo.cpu().numpy(), d_up.cpu().numpy(), d_sp.cpu().numpy()))
+    return outs
+
+
+@pytest.mark.parametrize("n1,n2,ncls", [(8, 6, 1), (64, 32, 1), (33, 17, 3)])
+def test_translation_cached_mode_equals_full(gosma, n1, n2, ncls):
+    """Self terms once per translation cuboid (rotation-split siblings share it),
+    cross terms per node: the same bounds as the full kernel. Only the FP64
+    summation split of the error estimate differs, so the tolerance is 1e-12
+    of the mass (relative), far below TOL_RAW."""
+    from paper_1812_01232_b200 import synth
+    classes = synth.mixture(n1, n2, "realistic", seed=n1 + 5 * n2, n_classes=ncls)
+    base = synth.nodes(400, seed=n1 * n2).view(np.float64).reshape(-1, 11)
+    rng = np.random.default_rng(n1)
+    # 400 cuboids, each shared by 1..8 rotation cells
+    reps = rng.integers(1, 9, len(base))
+    tindex = np.repeat(np.arange(len(base)), reps).astype(np.int32)
+    nodes = base[tindex].copy()
+    nodes[:, 0:3] += rng.uniform(-0.3, 0.3, (len(nodes), 3))
+    nodes[:, 3] *= rng.uniform(0.3, 1.0, len(nodes))
+    perm = rng.permutation(len(nodes))  # the index map need not be monotone
+    nodes, tindex = nodes[perm], tindex[perm]
+    tboxes = base[:, 4:10]
+    (lo, up, sp), (clo, cup, csp) = _cached_vs_full(gosma, classes, 0.5, nodes, tboxes, tindex)
+    assert np.array_equal(np.isinf(lo), np.isinf(clo))
+    f = np.isfinite(lo)
+    scale = np.abs(lo[f]) + np.abs(up[f]) + 1.0
+    assert np.all(np.abs(lo[f] - clo[f]) <= 1e-12 * scale)
+    fu = np.isfinite(up)
+    assert np.array_equal(fu, np.isfinite(cup))
+    assert np.all(np.abs(up[fu] - cup[fu]) <= 1e-12 * (np.abs(up[fu]) + 1.0))
+    assert np.array_equal(sp, csp)
+    # and against the FP64 oracle (certified LB sound, UB within TOL_UB)
+    mix = Mixture(**synth.to_mixture_arrays(classes, 0.5))
+    rlo, rup, lm, um, _ = Oracle(mix).eval_bounds(nodes, threads=8)
+    ff = np.isfinite(rlo)
+    assert np.all(clo[ff] <= rlo[ff] + 1e-9 * lm[ff])
+    assert np.all(clo[ff] >= rlo[ff] - TOL_CERT * lm[ff])
+    fu = ff & np.isfinite(rup)
+    assert np.all(np.abs(cup[fu] - rup[fu]) <= TOL_UB * um[fu] + 1e-12)
+
+
+def test_translation_cached_mode_skip(gosma):
+    from paper_1812_01232_b200 import synth
+    classes = synth.mixture(16, 8, "realistic", seed=3)
+    base = synth.nodes(200, seed=4).view(np.float64).reshape(-1, 11)
+    tindex = np.arange(len(base), dtype=np.int32)
+    (lo, up, _), _ = _cached_vs_full(gosma, classes, 0.5, base, base[:, 4:10], tindex)
+    skip = float(np.median(lo[np.isfinite(lo)]))
+    (lo2, up2, _), (clo, cup, _) = _cached_vs_full(gosma, classes, 0.5, base, base[:, 4:10],
+                                                    tindex, skip)
+    assert np.all(np.isinf(cup[clo >= skip]))
+    keep = np.isfinite(up2)
+    assert np.array_equal(keep, np.isfinite(cup))
+
+
 def test_host_objective_matches_golden(gosma, golden_objective):
     for case in golden_objective["cases"]:
         mix = Mixture.from_dict(case["mixture"])
