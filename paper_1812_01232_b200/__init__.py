@@ -22,7 +22,8 @@ __all__ = [
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-library_path = os.path.join(_HERE, "libgosma.so")
+# GOSMA_LIBRARY selects an alternative in-tree build (kernel-variant A/B runs).
+library_path = os.environ.get("GOSMA_LIBRARY") or os.path.join(_HERE, "libgosma.so")
 
 GOSMA_OK, GOSMA_EINVAL, GOSMA_EINFEASIBLE, GOSMA_EBUDGET = 0, 1, 2, 3
 

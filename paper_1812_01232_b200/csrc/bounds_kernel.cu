@@ -133,15 +133,17 @@ __device__ __forceinline__ bool norm_below(double s, double z, double z2) {
   return sqrt(s) < z;
 }
 
-// Per-warp shared-memory tables (SoA of float4 rows).
+// Per-warp shared-memory tables: one record of kRowF4 float4 per model row
+// (80 B: conflict-free when lanes read consecutive rows) and kColF4 float4 per
+// image column (broadcast), so a row or column costs one address.
 struct WarpTables {
-  float4* r0;  // (uhx, uhy, uhz, klo)   uhat at the cuboid centre (FP32 high part), kappa_lo
-  float4* r1;  // (khi, Flo, st, ct)     Flo = phi / W(klo); psi_t half-angle
-  float4* r2;  // (kst, Fst, sp, cp)     kappa at t*, phi / W(kst), half-angle of psi_t + psi_r
-  float4* r3;  // (ulx, uly, ulz, Fhi)   uhat low part (double-float), phi / W(khi)
-  float4* r4;  // (usx, usy, usz, s4)    uhat at t*, s4 = 4 sin^2((psi_t + psi_r)/2)
-  float4* c0;  // (qhx, qhy, qhz, k2)    q_j = R0^T m_j, FP32 high part
-  float4* c1;  // (qlx, qly, qlz, G)     q_j low part, G = phi2 / W(k2)
+  float4* row;  // [0] (uhx, uhy, uhz, klo)   uhat at the cuboid centre (FP32 high part), kappa_lo
+                // [1] (khi, Flo, st, ct)     Flo = phi / W(klo); psi_t half-angle
+                // [2] (kst, Fst, sp, cp)     kappa at t*, phi / W(kst), half-angle of psi_t + psi_r
+                // [3] (ulx, uly, ulz, Fhi)   uhat low part (double-float), phi / W(khi)
+                // [4] (usx, usy, usz, s4)    uhat at t*, s4 = 4 sin^2((psi_t + psi_r)/2)
+  float4* col;  // [0] (qhx, qhy, qhz, k2)    q_j = R0^T m_j, FP32 high part
+                // [1] (qlx, qly, qlz, G)     q_j low part, G = phi2 / W(k2)
 };
 // Pair terms are F_i G_j 2^(excess log2e) W(K) (the log W(a), log W(b) and
 // log phi pieces of the reference's log_term, bounds.cpp:136/176, as linear
@@ -335,7 +337,8 @@ __device__ __forceinline__ void self_pair(const float4& a0, const float4& a1, co
 }
 
 __device__ __forceinline__ Row load_row(const WarpTables& T, int i) {
-  const float4 a0 = T.r0[i], a1 = T.r1[i], a2 = T.r2[i], a3 = T.r3[i], a4 = T.r4[i];
+  const float4* p = T.row + i * kRowF4;
+  const float4 a0 = p[0], a1 = p[1], a2 = p[2], a3 = p[3], a4 = p[4];
   Row r;
   r.uhx = a0.x;
   r.uhy = a0.y;
@@ -373,7 +376,7 @@ __device__ __forceinline__ void class_pairs(const WarpTables& T, const ClassSpan
       float l = 0.0f, u = 0.0f, ma = 0.0f, mb = 0.0f;
 #pragma unroll 2
       for (int j = cs.o2; j < cs.o2 + cs.n2; ++j)
-        cross_pair<kSame>(r, T.c0[j], T.c1[j], l, u, ma, mb);
+        cross_pair<kSame>(r, T.col[j * kColF4], T.col[j * kColF4 + 1], l, u, ma, mb);
       lb_cross += static_cast<double>(w * r.Fhi * l);
       lb_err += static_cast<double>(
           2.0f * w * r.Fhi * fmaf(ma, kErrAmp, fmaf(mb, kErrExp, l * kErrTerm)));
@@ -388,10 +391,11 @@ __device__ __forceinline__ void class_pairs(const WarpTables& T, const ClassSpan
     const int il = base + lane;
     if (il < n) {
       const int i = cs.o1 + il;
-      const float4 a0 = T.r0[i], a1 = T.r1[i], a2 = T.r2[i];
+      const float4* pa = T.row + i * kRowF4;
+      const float4 a0 = pa[0], a1 = pa[1], a2 = pa[2], av3 = pa[3];
       float3 a3 = make_float3(0.f, 0.f, 0.f);
-      if (!kSame) a3 = make_float3(T.r4[i].x, T.r4[i].y, T.r4[i].z);
-      const float3 al = make_float3(T.r3[i].x, T.r3[i].y, T.r3[i].z);
+      if (!kSame) a3 = make_float3(pa[4].x, pa[4].y, pa[4].z);
+      const float3 al = make_float3(av3.x, av3.y, av3.z);
       float l = 0.0f, u = 0.0f, me = 0.0f;
       int jl = il;
 #pragma unroll 2
@@ -399,17 +403,19 @@ __device__ __forceinline__ void class_pairs(const WarpTables& T, const ClassSpan
         jl = (jl + 1 == n) ? 0 : jl + 1;
         const int j = cs.o1 + jl;
         float3 b3 = make_float3(0.f, 0.f, 0.f);
-        if (!kSame) b3 = make_float3(T.r4[j].x, T.r4[j].y, T.r4[j].z);
-        const float4 bl = T.r3[j];
-        self_pair<kSame>(a0, a1, a2, a3, al, T.r0[j], T.r1[j], T.r2[j], b3,
+        const float4* pb = T.row + j * kRowF4;
+        if (!kSame) b3 = make_float3(pb[4].x, pb[4].y, pb[4].z);
+        const float4 bl = pb[3];
+        self_pair<kSame>(a0, a1, a2, a3, al, pb[0], pb[1], pb[2], b3,
                          make_float3(bl.x, bl.y, bl.z), l, u, me);
       }
       if (even && il < n / 2) {
         const int j = i + n / 2;
         float3 b3 = make_float3(0.f, 0.f, 0.f);
-        if (!kSame) b3 = make_float3(T.r4[j].x, T.r4[j].y, T.r4[j].z);
-        const float4 bl = T.r3[j];
-        self_pair<kSame>(a0, a1, a2, a3, al, T.r0[j], T.r1[j], T.r2[j], b3,
+        const float4* pb = T.row + j * kRowF4;
+        if (!kSame) b3 = make_float3(pb[4].x, pb[4].y, pb[4].z);
+        const float4 bl = pb[3];
+        self_pair<kSame>(a0, a1, a2, a3, al, pb[0], pb[1], pb[2], b3,
                          make_float3(bl.x, bl.y, bl.z), l, u, me);
       }
       lb_self += static_cast<double>(2.0f * w * a1.y * l);
@@ -472,7 +478,10 @@ __device__ __forceinline__ void psi_trans_half(double u0, double u1, double u2, 
 enum { kModeFull = 0, kSelfOnly = 1, kCrossCached = 2 };
 
 template <int kMode>
-__global__ void __launch_bounds__(kWarpsPerCta * 32, 6)
+#ifndef GOSMA_MIN_BLOCKS
+#define GOSMA_MIN_BLOCKS 6
+#endif
+__global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
     eval_bounds_kernel(const DevCtx ctx, const EvalArgs args) {
   extern __shared__ float4 smem4[];
   const int lane = threadIdx.x & 31;
@@ -481,13 +490,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 6)
   const size_t per_warp_f4 = static_cast<size_t>(kRowF4 * N1 + kColF4 * N2);
   float4* base = smem4 + warp * per_warp_f4;
   WarpTables T;
-  T.r0 = base;
-  T.r1 = T.r0 + N1;
-  T.r2 = T.r1 + N1;
-  T.r3 = T.r2 + N1;
-  T.r4 = T.r3 + N1;
-  T.c0 = T.r4 + N1;
-  T.c1 = T.c0 + N2;
+  T.row = base;
+  T.col = base + kRowF4 * N1;
 
   const double zeta = ctx.zeta;
   const double zeta2 = zeta * zeta;
@@ -663,13 +667,14 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 6)
         const float Fst = phi * kst * rcpf(1.0f - ex2f(-2.0f * kL2E * kst));
         const float uhx = static_cast<float>(c0), uhy = static_cast<float>(c1),
                     uhz = static_cast<float>(c2);
-        T.r0[i] = make_float4(uhx, uhy, uhz, klo);
-        T.r1[i] = make_float4(khi, Flo, static_cast<float>(st), static_cast<float>(ct));
-        T.r2[i] = make_float4(kst, Fst, static_cast<float>(sp), static_cast<float>(cp));
-        T.r3[i] = make_float4(static_cast<float>(c0 - uhx), static_cast<float>(c1 - uhy),
-                              static_cast<float>(c2 - uhz), Fhi);
-        T.r4[i] = make_float4(static_cast<float>(v0 * iv), static_cast<float>(v1 * iv),
-                              static_cast<float>(v2 * iv), static_cast<float>(4.0 * sp * sp));
+        float4* pr = T.row + i * kRowF4;
+        pr[0] = make_float4(uhx, uhy, uhz, klo);
+        pr[1] = make_float4(khi, Flo, static_cast<float>(st), static_cast<float>(ct));
+        pr[2] = make_float4(kst, Fst, static_cast<float>(sp), static_cast<float>(cp));
+        pr[3] = make_float4(static_cast<float>(c0 - uhx), static_cast<float>(c1 - uhy),
+                            static_cast<float>(c2 - uhz), Fhi);
+        pr[4] = make_float4(static_cast<float>(v0 * iv), static_cast<float>(v1 * iv),
+                            static_cast<float>(v2 * iv), static_cast<float>(4.0 * sp * sp));
       }
       if (!infeasible && kMode != kCrossCached) {
         lb_self += static_cast<double>(w * dsl);
@@ -713,8 +718,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 6)
       const double q2 = R[2] * x0 + R[5] * x1 + R[8] * x2;
       const float f0 = static_cast<float>(q0), f1 = static_cast<float>(q1),
                   f2 = static_cast<float>(q2);
-      T.c0[j] = make_float4(f0, f1, f2, ctx.kappa2[j]);
-      T.c1[j] = make_float4(static_cast<float>(q0 - f0), static_cast<float>(q1 - f1),
+      T.col[j * kColF4] = make_float4(f0, f1, f2, ctx.kappa2[j]);
+      T.col[j * kColF4 + 1] = make_float4(static_cast<float>(q0 - f0), static_cast<float>(q1 - f1),
                             static_cast<float>(q2 - f2), ctx.g2[j]);
     }
     __syncwarp();

@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <atomic>
 #include <chrono>
@@ -310,6 +311,17 @@ struct gosma_solver {
   // full kernel, for A/B measurements)
   bool cached = std::getenv("GOSMA_FULL_KERNEL") == nullptr;
   unsigned long long cuboid_evals = 0;
+  // GOSMA_PROFILE=1: synchronising per-phase wall times, printed on destroy
+  bool profile = std::getenv("GOSMA_PROFILE") != nullptr;
+  double phase[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  std::chrono::steady_clock::time_point lap_t;
+  void lap(int k, cudaStream_t s) {
+    if (!profile) return;
+    cudaStreamSynchronize(s);
+    const auto now = std::chrono::steady_clock::now();
+    if (k >= 0) phase[k] += std::chrono::duration<double>(now - lap_t).count();
+    lap_t = now;
+  }
   std::chrono::steady_clock::time_point t_start;
   double elapsed() const {
     return std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
@@ -460,6 +472,14 @@ int gosma_solver_create(gosma_ctx* ctx, const gosma_domain* domain, const gosma_
 
 void gosma_solver_destroy(gosma_solver* S) {
   if (!S) return;
+  if (S->profile) {
+    static const char* kName[8] = {"status", "select", "expand+self", "eval", "best+improve",
+                                   "route", "compact", "other"};
+    std::fprintf(stderr, "[gosma profile] waves %llu evals %llu cuboids %llu:", S->wave, S->evals,
+                 S->cuboid_evals);
+    for (int k = 0; k < 8; ++k) std::fprintf(stderr, " %s %.3fs", kName[k], S->phase[k]);
+    std::fprintf(stderr, "\n");
+  }
   DeviceGuard g(S->ctx->device);
   S->F.release();
   delete S;
@@ -470,6 +490,12 @@ int gosma_solver_status(gosma_solver* S, gosma_wave_status* st) {
   DeviceGuard g(S->ctx->device);
   cudaStream_t s = S->ctx->stream;
   cudaError_t e;
+  S->lap(-1, s);
+  struct LapAtExit {
+    gosma_solver* S;
+    cudaStream_t s;
+    ~LapAtExit() { S->lap(0, s); }
+  } lap_at_exit{S, s};
   // capacity folding (solver.cpp:433-447); the memory budget folds to 3/4
   const bool user_cap = S->cfg.queue_capacity >= 0 &&
                         static_cast<size_t>(S->cfg.queue_capacity) <= S->mem_cap;
@@ -511,6 +537,7 @@ int gosma_solver_expand(gosma_solver* S, double limit, unsigned long long max_ev
   size_t want = S->wave_nodes;
   if (max_evals > 0) want = std::min<size_t>(want, std::max<unsigned long long>(1, (max_evals + 7) / 8));
   size_t n_sel = 0;
+  S->lap(-1, s);
   // Expand only nodes that can still matter: lower < limit (= d* - eps).
   if ((e = S->F.select_smallest(want, host_order_key(limit), s, &n_sel)) != cudaSuccess)
     return cuda_error(e, "select");
@@ -529,6 +556,7 @@ int gosma_solver_expand(gosma_solver* S, double limit, unsigned long long max_ev
     }
   }
   const size_t n_kids = n_sel * 8;
+  S->lap(1, s);
   EvalArgs a;
   a.work = static_cast<unsigned int*>(ctx->d_work);
   a.skip_upper_at = S->dstar();
@@ -545,6 +573,7 @@ int gosma_solver_expand(gosma_solver* S, double limit, unsigned long long max_ev
       return cuda_error(e, "eval cuboids");
     a.tindex = S->F.tidx;
     S->cuboid_evals += n_cub;
+    S->lap(2, s);
   } else if ((e = S->F.expand_selected(n_sel, s)) != cudaSuccess) {
     return cuda_error(e, "expand");
   }
@@ -556,6 +585,7 @@ int gosma_solver_expand(gosma_solver* S, double limit, unsigned long long max_ev
   if ((e = (S->cached ? launch_eval_cross_cached(ctx->dev, a, ctx->sm_count, s)
                       : launch_eval_bounds(ctx->dev, a, ctx->sm_count, s))) != cudaSuccess)
     return cuda_error(e, "eval children");
+  S->lap(3, s);
   S->evals += n_kids;
   S->expanded += n_sel;
   int bi = -1;
@@ -566,12 +596,14 @@ int gosma_solver_expand(gosma_solver* S, double limit, unsigned long long max_ev
     cudaMemcpy(&b, S->F.kids + bi, sizeof(gosma_node), cudaMemcpyDeviceToHost);
     improve(ctx->model, S->dom, b, &S->inc);
   }
+  S->lap(4, s);
   RouteStats rs;
   if ((e = S->F.route_append(n_kids, S->dstar(), s, &rs)) != cudaSuccess)
     return cuda_error(e, "route");
   S->pruned_volume += rs.pruned_volume;
   S->resolved_volume += rs.resolved_volume;
   if (rs.floor_key != ~0ull) S->floor_lower = std::min(S->floor_lower, key_to_double(rs.floor_key));
+  S->lap(5, s);
   // amortised compaction: drop holes and stale nodes (lower >= d*,
   // solver.cpp:660-663) once they fill half the pool
   if (S->F.holes * 2 > S->F.size) {
@@ -580,6 +612,7 @@ int gosma_solver_expand(gosma_solver* S, double limit, unsigned long long max_ev
       return cuda_error(e, "compact");
     S->pruned_volume += dropped;
   }
+  S->lap(6, s);
   ++S->wave;
   return GOSMA_OK;
 }
