@@ -479,7 +479,7 @@ enum { kModeFull = 0, kSelfOnly = 1, kCrossCached = 2 };
 
 template <int kMode>
 #ifndef GOSMA_MIN_BLOCKS
-#define GOSMA_MIN_BLOCKS 6
+#define GOSMA_MIN_BLOCKS 7
 #endif
 __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
     eval_bounds_kernel(const DevCtx ctx, const EvalArgs args) {
@@ -724,7 +724,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
     }
     __syncwarp();
 
-    // ---- pair sweeps
+    // ---- pair sweeps (GOSMA_PREP_ONLY: times the per-node prep alone)
+#ifndef GOSMA_PREP_ONLY
     for (int c = 0; c < ctx.n_classes; ++c) {
       const ClassSpan cs = ctx.cls[c];
       const float w = static_cast<float>(ctx.cls_w[c]);
@@ -735,6 +736,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
         class_pairs<false, kC, kS>(T, cs, lane, w, lb_self, lb_cross, ub_self, ub_cross, lb_err);
       }
     }
+#endif
     lb_self = warp_sum_d(lb_self);
     lb_cross = warp_sum_d(lb_cross);
     ub_self = warp_sum_d(ub_self);
