@@ -36,6 +36,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 
 #include "gosma_internal.hpp"
 
@@ -116,11 +117,18 @@ __device__ __forceinline__ float diag_term(float phi, float k) {
   return phi * phi * 0.5f * k * (1.0f + e) * rcpf(1.0f - e);
 }
 
-__device__ __forceinline__ double shfl_d(double v, int src) { return __shfl_sync(kFull, v, src); }
+// Lane groups: a group of kG lanes (32, 16 or 8) evaluates one node; small
+// mixtures (max class n1 <= 16 / 8) run 2 or 4 nodes per warp so the row
+// lanes stay busy. `gm` is the group's lane mask.
+template <int kG>
+__device__ __forceinline__ double shfl_d(unsigned gm, double v, int src) {
+  return __shfl_sync(gm, v, src, kG);
+}
 
-__device__ __forceinline__ double warp_sum_d(double v) {
+template <int kG>
+__device__ __forceinline__ double group_sum_d(unsigned gm, double v) {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  for (int o = kG / 2; o > 0; o >>= 1) v += __shfl_xor_sync(gm, v, o, kG);
   return v;
 }
 
@@ -363,13 +371,13 @@ __device__ __forceinline__ Row load_row(const WarpTables& T, int i) {
   return r;
 }
 
-template <bool kSame, bool kCross, bool kSelf>
+template <int kG, bool kSame, bool kCross, bool kSelf>
 __device__ __forceinline__ void class_pairs(const WarpTables& T, const ClassSpan cs, int lane,
                                             float w, double& lb_self, double& lb_cross,
                                             double& ub_self, double& ub_cross, double& lb_err) {
   const int n = cs.n1;
   // Cross terms: rows over lanes, columns broadcast.
-  for (int base = 0; kCross && base < n; base += 32) {
+  for (int base = 0; kCross && base < n; base += kG) {
     const int il = base + lane;
     if (il < n) {
       const Row r = load_row(T, cs.o1 + il);
@@ -387,7 +395,7 @@ __device__ __forceinline__ void class_pairs(const WarpTables& T, const ClassSpan
   // (i, i+d mod n), d = 1..(n-1)/2, plus d = n/2 for i < n/2 when n is even.
   const int dfull = (n - 1) / 2;
   const bool even = (n % 2) == 0;
-  for (int base = 0; kSelf && base < n; base += 32) {
+  for (int base = 0; kSelf && base < n; base += kG) {
     const int il = base + lane;
     if (il < n) {
       const int i = cs.o1 + il;
@@ -477,18 +485,21 @@ __device__ __forceinline__ void psi_trans_half(double u0, double u1, double u2, 
 // the cross terms plus the cached self sums of the node's cuboid.
 enum { kModeFull = 0, kSelfOnly = 1, kCrossCached = 2 };
 
-template <int kMode>
 #ifndef GOSMA_MIN_BLOCKS
 #define GOSMA_MIN_BLOCKS 7
 #endif
+template <int kMode, int kG>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
     eval_bounds_kernel(const DevCtx ctx, const EvalArgs args) {
   extern __shared__ float4 smem4[];
-  const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
+  const int wl = threadIdx.x & 31;
+  const int lane = wl & (kG - 1);  // lane within the group
+  const int gbase = wl & ~(kG - 1);
+  const unsigned gm = kG == 32 ? kFull : (((1u << kG) - 1u) << gbase);
+  const int group = static_cast<int>(threadIdx.x) / kG;
   const int N1 = ctx.n1_total, N2 = ctx.n2_total;
   const size_t per_warp_f4 = static_cast<size_t>(kRowF4 * N1 + kColF4 * N2);
-  float4* base = smem4 + warp * per_warp_f4;
+  float4* base = smem4 + group * per_warp_f4;
   WarpTables T;
   T.row = base;
   T.col = base + kRowF4 * N1;
@@ -498,21 +509,26 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
   for (;;) {
     long long node = 0;
     if (lane == 0) node = static_cast<long long>(atomicAdd(args.work, 1u));
-    node = __shfl_sync(kFull, node, 0);
+    node = __shfl_sync(gm, node, 0, kG);
     if (node >= args.n) break;
 
     // ---- node fetch (gosma_node: rc[3], rhw, tc[3], thw[3], lower)
-    double v = 0.0;
+    double v = 0.0, v2 = 0.0;
     if (lane < 11) v = args.nodes[node * 11 + lane];
-    const double rc0 = shfl_d(v, 0), rc1 = shfl_d(v, 1), rc2 = shfl_d(v, 2);
-    const double rhw = shfl_d(v, 3);
-    const double tc0 = shfl_d(v, 4), tc1 = shfl_d(v, 5), tc2 = shfl_d(v, 6);
-    const double h0 = shfl_d(v, 7), h1 = shfl_d(v, 8), h2 = shfl_d(v, 9);
-    const double parent_lower = shfl_d(v, 10);
+    if (kG < 11 && lane < 11 - kG) v2 = args.nodes[node * 11 + kG + lane];
+    auto fetch = [&](int k) {
+      if (kG < 11 && k >= kG) return shfl_d<kG>(gm, v2, k - kG);
+      return shfl_d<kG>(gm, v, k);
+    };
+    const double rc0 = fetch(0), rc1 = fetch(1), rc2 = fetch(2);
+    const double rhw = fetch(3);
+    const double tc0 = fetch(4), tc1 = fetch(5), tc2 = fetch(6);
+    const double h0 = fetch(7), h1 = fetch(8), h2 = fetch(9);
+    const double parent_lower = fetch(10);
 
     // ---- feasibility scan (feasible_wrt_zeta, se3.cpp:94-100)
     bool infeasible = false;
-    for (int mb = 0; mb < N1; mb += 32) {
+    for (int mb = 0; mb < N1; mb += kG) {
       const int mi = mb + lane;
       bool hit = false;
       if (mi < N1) {
@@ -524,7 +540,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
                                    __dmul_rn(f2, f2)),
                          zeta, zeta2);
       }
-      if (__any_sync(kFull, hit)) {
+      if (__any_sync(gm, hit)) {
         infeasible = true;
         break;
       }
@@ -565,7 +581,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
     if (!infeasible) {
       for (int proj = 0; proj <= 8; ++proj) {
         int off = -1;
-        for (int mb = 0; mb < N1; mb += 32) {
+        for (int mb = 0; mb < N1; mb += kG) {
           const int mi = mb + lane;
           bool hit = false;
           if (mi < N1) {
@@ -576,7 +592,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
                 __dadd_rn(__dadd_rn(__dmul_rn(d0, d0), __dmul_rn(d1, d1)), __dmul_rn(d2, d2)),
                 zeta, zeta2);
           }
-          const unsigned bal = __ballot_sync(kFull, hit);
+          const unsigned bal = __ballot_sync(gm, hit) >> gbase;
           if (bal) {
             off = mb + __ffs(bal) - 1;
             break;
@@ -618,7 +634,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
       const ClassSpan cs = ctx.cls[c];
       const float w = static_cast<float>(ctx.cls_w[c]);
       float dsl = 0.0f, dsu = 0.0f;
-      for (int il = lane; il < cs.n1; il += 32) {
+      for (int il = lane; il < cs.n1; il += kG) {
         const int i = cs.o1 + il;
         const double m0 = ctx.mu[3 * i], m1 = ctx.mu[3 * i + 1], m2 = ctx.mu[3 * i + 2];
         const double is2 = ctx.inv_s2[i];
@@ -684,7 +700,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
     }
     // split decision (subdivide_adaptive, se3.cpp:107-121)
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) st_max = fmax(st_max, __shfl_xor_sync(kFull, st_max, o));
+    for (int o = kG / 2; o > 0; o >>= 1)
+      st_max = fmax(st_max, __shfl_xor_sync(gm, st_max, o, kG));
     if (kMode != kSelfOnly && lane == 0 && args.split_rot) {
       const bool rot_ok = rhw > 1e-9;
       const bool trans_ok = fmax(fmax(h0, h1), h2) > 1e-9;
@@ -707,11 +724,11 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
           args.upper[node] = INFINITY;
         }
       }
-      __syncwarp();
+      __syncwarp(gm);
       continue;
     }
     // ---- per-column prep: q_j = R0^T m_j (bounds.cpp:97-102), double-float
-    for (int j = lane; kMode != kSelfOnly && j < N2; j += 32) {
+    for (int j = lane; kMode != kSelfOnly && j < N2; j += kG) {
       const double x0 = ctx.m[3 * j], x1 = ctx.m[3 * j + 1], x2 = ctx.m[3 * j + 2];
       const double q0 = R[0] * x0 + R[3] * x1 + R[6] * x2;
       const double q1 = R[1] * x0 + R[4] * x1 + R[7] * x2;
@@ -722,7 +739,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
       T.col[j * kColF4 + 1] = make_float4(static_cast<float>(q0 - f0), static_cast<float>(q1 - f1),
                             static_cast<float>(q2 - f2), ctx.g2[j]);
     }
-    __syncwarp();
+    __syncwarp(gm);
 
     // ---- pair sweeps (GOSMA_PREP_ONLY: times the per-node prep alone)
 #ifndef GOSMA_PREP_ONLY
@@ -731,17 +748,19 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
       const float w = static_cast<float>(ctx.cls_w[c]);
       constexpr bool kC = kMode != kSelfOnly, kS = kMode != kCrossCached;
       if (same) {
-        class_pairs<true, kC, kS>(T, cs, lane, w, lb_self, lb_cross, ub_self, ub_cross, lb_err);
+        class_pairs<kG, true, kC, kS>(T, cs, lane, w, lb_self, lb_cross, ub_self, ub_cross,
+                                      lb_err);
       } else {
-        class_pairs<false, kC, kS>(T, cs, lane, w, lb_self, lb_cross, ub_self, ub_cross, lb_err);
+        class_pairs<kG, false, kC, kS>(T, cs, lane, w, lb_self, lb_cross, ub_self, ub_cross,
+                                       lb_err);
       }
     }
 #endif
-    lb_self = warp_sum_d(lb_self);
-    lb_cross = warp_sum_d(lb_cross);
-    ub_self = warp_sum_d(ub_self);
-    ub_cross = warp_sum_d(ub_cross);
-    lb_err = warp_sum_d(lb_err);
+    lb_self = group_sum_d<kG>(gm, lb_self);
+    lb_cross = group_sum_d<kG>(gm, lb_cross);
+    ub_self = group_sum_d<kG>(gm, ub_self);
+    ub_cross = group_sum_d<kG>(gm, ub_cross);
+    lb_err = group_sum_d<kG>(gm, lb_err);
     if (kMode == kSelfOnly) {
       if (lane == 0) {
         double* o = args.self_out + 4 * node;
@@ -750,7 +769,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
         o[2] = lb_err;
         o[3] = have_center ? 0.0 : 2.0;  // 2: no feasible centre (upper = +inf)
       }
-      __syncwarp();
+      __syncwarp(gm);
       continue;
     }
     if (kMode == kCrossCached) {  // the cuboid's translation-only sums
@@ -771,7 +790,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
       args.lower[node] = lo;
       args.upper[node] = up;
     }
-    __syncwarp();
+    __syncwarp(gm);
   }
 }
 
@@ -784,33 +803,62 @@ size_t eval_smem_per_warp(const DevCtx& ctx) {
 
 namespace {
 
-template <int kMode>
-cudaError_t launch_mode(const DevCtx& ctx, const EvalArgs& a, int sm_count,
-                        cudaStream_t stream) {
-  if (a.n <= 0) return cudaSuccess;
-  const size_t smem = eval_smem_per_warp(ctx) * kWarpsPerCta;
+// Lanes per node: 8 / 16 when every class has at most that many model rows
+// and the per-group tables stay small (GOSMA_GROUP=32 forces whole warps).
+int group_lanes(const DevCtx& ctx) {
+  static const int forced = [] {
+    const char* e = std::getenv("GOSMA_GROUP");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (forced == 8 || forced == 16 || forced == 32) return forced;
+  const size_t table = eval_smem_per_warp(ctx);
+  for (int g : {8, 16}) {
+    if (ctx.max_n1 <= g && table * kWarpsPerCta * (32 / g) <= 64 * 1024) return g;
+  }
+  return 32;
+}
+
+template <int kMode, int kG>
+cudaError_t launch_group(const DevCtx& ctx, const EvalArgs& a, int sm_count,
+                         cudaStream_t stream) {
+  constexpr int kGroupsPerCta = kWarpsPerCta * (32 / kG);
+  const size_t smem = eval_smem_per_warp(ctx) * kGroupsPerCta;
   static size_t configured = 0;
   if (smem > 48 * 1024 && smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(eval_bounds_kernel<kMode>,
+    cudaError_t e = cudaFuncSetAttribute(eval_bounds_kernel<kMode, kG>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     configured = smem;
   }
   int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, eval_bounds_kernel<kMode>,
-                                                                kWarpsPerCta * 32, smem);
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      &per_sm, eval_bounds_kernel<kMode, kG>, kWarpsPerCta * 32, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   long long grid = static_cast<long long>(per_sm) * sm_count;
-  const long long need = (a.n + kWarpsPerCta - 1) / kWarpsPerCta;
+  const long long need = (a.n + kGroupsPerCta - 1) / kGroupsPerCta;
   if (grid > need) grid = need;
   e = cudaMemsetAsync(a.work, 0, sizeof(unsigned int), stream);
   if (e != cudaSuccess) return e;
-  eval_bounds_kernel<kMode>
+  eval_bounds_kernel<kMode, kG>
       <<<static_cast<unsigned>(grid), kWarpsPerCta * 32, smem, stream>>>(ctx, a);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
+}
+
+template <int kMode>
+cudaError_t launch_mode(const DevCtx& ctx, const EvalArgs& a, int sm_count,
+                        cudaStream_t stream) {
+  if (a.n <= 0) return cudaSuccess;
+  switch (group_lanes(ctx)) {
+    case 8:
+      return launch_group<kMode, 8>(ctx, a, sm_count, stream);
+    case 16:
+      return launch_group<kMode, 16>(ctx, a, sm_count, stream);
+    default:
+      return launch_group<kMode, 32>(ctx, a, sm_count, stream);
+  }
 }
 
 }  // namespace

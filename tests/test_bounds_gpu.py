@@ -103,13 +103,15 @@ def rand_nodes(rng, n):
 
 @pytest.mark.parametrize("n1,n2,kcap,zeta,ncls", [
     (4, 3, 40.0, 0.2, 1), (3, 3, 150.0, 0.15, 1), (1, 1, 20.0, 0.2, 1), (33, 17, 150.0, 0.2, 1),
-    (64, 32, 150.0, 0.2, 1), (5, 4, 60.0, 0.2, 3), (2, 7, 1e4, 0.2, 4)])
+    (64, 32, 150.0, 0.2, 1), (5, 4, 60.0, 0.2, 3), (2, 7, 1e4, 0.2, 4),
+    # 16- and 8-lane groups (several nodes per warp) incl. mixed class sizes
+    (12, 10, 150.0, 0.2, 1), (16, 16, 150.0, 0.2, 1), (9, 3, 150.0, 0.2, 2), (8, 40, 150.0, 0.2, 1)])
 def test_moderate_regimes(gosma, n1, n2, kcap, zeta, ncls):
     rng = np.random.default_rng(1000 + n1 * 7 + n2)
     check_parity(gosma, rand_mix(rng, n1, n2, kcap, zeta, ncls), rand_nodes(rng, 1500))
 
 
-@pytest.mark.parametrize("n1,n2", [(8, 6), (64, 32), (45, 40), (128, 64)])
+@pytest.mark.parametrize("n1,n2", [(8, 6), (12, 12), (64, 32), (45, 40), (128, 64)])
 def test_realistic_regime(gosma, n1, n2):
     from paper_1812_01232_b200 import synth
     classes = synth.mixture(n1, n2, "realistic", seed=n1 * 31 + n2)
