@@ -227,6 +227,9 @@ int gosma_solver_import(gosma_solver* solver, const gosma_node* nodes, const int
 /* Local incumbent pose / value and counters (global_lower, gap, status are
  * the driver's). */
 int gosma_solver_result(gosma_solver* solver, gosma_report* report);
+/* Volume still held by the live frontier (a full pass over the pool; for the
+ * ledger check total = pruned + resolved + live, solver.cpp:597-608). */
+int gosma_solver_live_volume(gosma_solver* solver, double* volume);
 
 const char* gosma_last_error(void);
 

@@ -115,6 +115,7 @@ def _load():
     lib.gosma_solver_export.argtypes = [vp, C.c_size_t, vp, vp, vp, C.POINTER(C.c_size_t)]
     lib.gosma_solver_import.argtypes = [vp, vp, vp, vp, C.c_size_t]
     lib.gosma_solver_result.argtypes = [vp, C.POINTER(_Report)]
+    lib.gosma_solver_live_volume.argtypes = [vp, _dp]
     return lib
 
 
@@ -442,6 +443,12 @@ class ShardSolver:
         st = _WaveStatus()
         _check(lib.gosma_solver_status(self._h, C.byref(st)), "solver_status")
         return {k: getattr(st, k) for k, _ in _WaveStatus._fields_}
+
+    def live_volume(self) -> float:
+        """Volume of the live frontier (ledger check: total = pruned + resolved + live)."""
+        v = C.c_double()
+        _check(lib.gosma_solver_live_volume(self._h, C.byref(v)), "solver_live_volume")
+        return v.value
 
     def set_incumbent(self, value: float):
         _check(lib.gosma_solver_set_incumbent(self._h, float(value)), "solver_set_incumbent")

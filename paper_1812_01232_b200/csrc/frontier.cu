@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdint>
 #include <cstring>
 
@@ -45,16 +46,16 @@ inline unsigned grid_cap(size_t n, unsigned block) {
 
 // Histogram of digit (key >> shift) & mask among keys < limit whose bits above
 // `prefix_shift` equal `prefix` (prefix_shift 64: no prefix).
-__global__ void digit_hist(const unsigned long long* key, size_t n, unsigned long long limit,
-                           int shift, int bits, unsigned long long prefix, int prefix_shift,
-                           unsigned int* hist) {
+__global__ void digit_hist(const unsigned long long* key, const unsigned int* idx, size_t n,
+                           unsigned long long limit, int shift, int bits,
+                           unsigned long long prefix, int prefix_shift, unsigned int* hist) {
   __shared__ unsigned int sh[kBins];
   const int nb = 1 << bits;
   for (int b = threadIdx.x; b < nb; b += blockDim.x) sh[b] = 0;
   __syncthreads();
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<size_t>(gridDim.x) * blockDim.x) {
-    const unsigned long long k = key[i];
+    const unsigned long long k = idx ? key[idx[i]] : key[i];
     if (k >= limit) continue;
     if (prefix_shift < 64 && (k >> prefix_shift) != prefix) continue;
     atomicAdd(&sh[(k >> shift) & static_cast<unsigned long long>(nb - 1)], 1u);
@@ -72,6 +73,38 @@ struct KeyBelow {
     return k >= lo && k < hi;
   }
 };
+
+// Appended children (slot < end, read on the device) whose key is below tau.
+struct NewCandidate {
+  const unsigned long long* key;
+  unsigned long long tau;
+  size_t base;
+  const unsigned long long* count;  // appended children (int in the low word)
+  __device__ __forceinline__ bool operator()(const unsigned int& i) const {
+    return i < base + static_cast<size_t>(*reinterpret_cast<const int*>(count)) && key[i] < tau;
+  }
+};
+
+struct NotHole {
+  const unsigned long long* key;
+  __device__ __forceinline__ bool operator()(const unsigned int& i) const {
+    return key[i] != kHoleKey;
+  }
+};
+
+__global__ void min_key_gather(const unsigned long long* key, const unsigned int* idx, size_t n,
+                               unsigned long long* out) {
+  typedef cub::BlockReduce<unsigned long long, 256> BR;
+  __shared__ typename BR::TempStorage tmp;
+  unsigned long long best = kHoleKey;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const unsigned long long k = key[idx[i]];
+    if (k < best) best = k;
+  }
+  const unsigned long long r = BR(tmp).Reduce(best, cub::Min());
+  if (threadIdx.x == 0 && r != kHoleKey) atomicMin(out, r);
+}
 
 __global__ void mark_holes(unsigned long long* key, const unsigned int* sel, size_t n) {
   const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
@@ -173,6 +206,19 @@ __global__ void append_kids(const gosma_node* kids, const int8_t* ksplit, const 
   dkey[i] = order_key(nd.lower);
 }
 
+__global__ void append_kids_counted(const gosma_node* kids, const int8_t* ksplit,
+                                    const double* kvol, const unsigned int* idx,
+                                    const unsigned long long* count, gosma_node* dst,
+                                    int8_t* dsplit, double* dvol, unsigned long long* dkey) {
+  const size_t k = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+  if (k >= static_cast<size_t>(*reinterpret_cast<const int*>(count))) return;
+  const gosma_node nd = kids[idx[k]];
+  dst[k] = nd;
+  dsplit[k] = ksplit[idx[k]];
+  dvol[k] = kvol[idx[k]];
+  dkey[k] = order_key(nd.lower);
+}
+
 __global__ void gather_pool(const gosma_node* src, const int8_t* ssplit, const double* svol,
                             const unsigned long long* skey, const unsigned int* idx, size_t n,
                             gosma_node* dst, int8_t* dsplit, double* dvol,
@@ -184,6 +230,64 @@ __global__ void gather_pool(const gosma_node* src, const int8_t* ssplit, const d
   dsplit[i] = ssplit[k];
   dvol[i] = svol[k];
   dkey[i] = skey[k];
+}
+
+// Marks stale slots (key >= limit) as holes and sums their volume.
+__global__ void drop_stale(unsigned long long* key, const double* vol, size_t n,
+                           unsigned long long limit, double* out) {
+  typedef cub::BlockReduce<double, 256> BR;
+  __shared__ typename BR::TempStorage tmp;
+  double acc = 0.0;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const unsigned long long k = key[i];
+    if (k != kHoleKey && k >= limit) {
+      acc += vol[i];
+      key[i] = kHoleKey;
+    }
+  }
+  const double sum = BR(tmp).Sum(acc);
+  if (threadIdx.x == 0 && sum != 0.0) atomicAdd(out, sum);
+}
+
+// Live (non-hole) slots at index >= live and holes at index < live.
+struct TailLive {
+  const unsigned long long* key;
+  unsigned int live;
+  __device__ __forceinline__ bool operator()(const unsigned int& i) const {
+    return i >= live && key[i] != kHoleKey;
+  }
+};
+struct HeadHole {
+  const unsigned long long* key;
+  unsigned int live;
+  __device__ __forceinline__ bool operator()(const unsigned int& i) const {
+    return i < live && key[i] == kHoleKey;
+  }
+};
+
+__global__ void count_live(const unsigned long long* key, size_t n, unsigned long long* out) {
+  typedef cub::BlockReduce<unsigned long long, 256> BR;
+  __shared__ typename BR::TempStorage tmp;
+  unsigned long long c = 0;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    c += key[i] != kHoleKey ? 1 : 0;
+  const unsigned long long sum = BR(tmp).Sum(c);
+  if (threadIdx.x == 0 && sum) atomicAdd(out, sum);
+}
+
+// Moves the live tail into the head holes (in place, order not preserved).
+__global__ void move_tail(gosma_node* nodes, int8_t* split, double* vol, unsigned long long* key,
+                          const unsigned int* dst, const unsigned int* src,
+                          const unsigned long long* count) {
+  const size_t k = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+  if (k >= static_cast<size_t>(*reinterpret_cast<const int*>(count))) return;
+  const unsigned int d = dst[k], s = src[k];
+  nodes[d] = nodes[s];
+  split[d] = split[s];
+  vol[d] = vol[s];
+  key[d] = key[s];
 }
 
 // Sum of volumes of non-hole slots with key >= limit.
@@ -199,6 +303,20 @@ __global__ void dropped_volume(const unsigned long long* key, const double* vol,
   }
   const double s = BR(tmp).Sum(acc);
   if (threadIdx.x == 0 && s != 0.0) atomicAdd(out, s);
+}
+
+__global__ void min_key_at_least(const unsigned long long* key, size_t n,
+                                 unsigned long long tau, unsigned long long* out) {
+  typedef cub::BlockReduce<unsigned long long, 256> BR;
+  __shared__ typename BR::TempStorage tmp;
+  unsigned long long best = kHoleKey;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const unsigned long long k = key[i];
+    if (k >= tau && k < best) best = k;
+  }
+  const unsigned long long r = BR(tmp).Reduce(best, cub::Min());
+  if (threadIdx.x == 0 && r != kHoleKey) atomicMin(out, r);
 }
 
 __global__ void min_upper_key(const double* upper, size_t n, ArgMin* out) {
@@ -317,6 +435,18 @@ void Frontier::release() {
   tidx = nullptr;
   tnodes = nullptr;
   tself = nullptr;
+  cudaFree(bsel);
+  bsel = nullptr;
+  bsel_cap = 0;
+  cudaFree(cidx);
+  cidx = nullptr;
+  cidx_cap = 0;
+  cudaFree(cand);
+  cudaFree(cand_tmp);
+  cand = cand_tmp = nullptr;
+  cand_n = cand_cap = 0;
+  tau = 0;
+  known_min = 0;
   cudaFree(stats);
   cudaFree(amin);
   cudaFree(counter);
@@ -350,6 +480,7 @@ cudaError_t Frontier::ensure_temp(size_t bytes) {
   if (bytes <= temp_bytes) return cudaSuccess;
   cudaFree(temp);
   temp = nullptr;
+  bytes = std::max(bytes, temp_bytes + temp_bytes / 2);  // geometric growth
   const cudaError_t e = cudaMalloc(&temp, bytes);
   if (e == cudaSuccess) temp_bytes = bytes;
   return e;
@@ -357,7 +488,9 @@ cudaError_t Frontier::ensure_temp(size_t bytes) {
 
 cudaError_t Frontier::grow(size_t need, cudaStream_t s) {
   if (need <= cap) return cudaSuccess;
-  const size_t c = std::max(need, 2 * cap);
+  // geometric growth (x4); past half the budget, straight to the budget
+  size_t c = std::max(need, 4 * cap);
+  if (cap_limit && c > cap_limit / 2) c = std::max(need, cap_limit);
   gosma_node* n2 = nullptr;
   int8_t* s2 = nullptr;
   double* v2 = nullptr;
@@ -392,6 +525,8 @@ cudaError_t Frontier::upload(const gosma_node* h_nodes, const int8_t* h_split,
   if ((e = grow(size + n, s)) != cudaSuccess) return e;
   std::vector<unsigned long long> k(n);
   for (size_t i = 0; i < n; ++i) k[i] = host_order_key(h_nodes[i].lower);
+  known_min = 0;  // imported keys may lie below the cached minimum
+  tau = 0;
   cudaMemcpyAsync(nodes + size, h_nodes, n * sizeof(gosma_node), cudaMemcpyHostToDevice, s);
   cudaMemcpyAsync(split + size, h_split, n, cudaMemcpyHostToDevice, s);
   cudaMemcpyAsync(vol + size, h_vol, n * sizeof(double), cudaMemcpyHostToDevice, s);
@@ -405,40 +540,67 @@ cudaError_t Frontier::min_key(cudaStream_t s, unsigned long long* out) {
     *out = kHoleKey;
     return cudaSuccess;
   }
+  cudaError_t e;
+  // every live key below tau is a candidate: their minimum is the pool minimum
+  if (tau != 0 && (cand_n > 0 || tau == kHoleKey)) {
+    unsigned long long init = kHoleKey;
+    std::memcpy(h_counter, &init, 8);
+    if ((e = cudaMemcpyAsync(counter, h_counter, 8, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+      return e;
+    if (cand_n) min_key_gather<<<grid_cap(cand_n, 256), 256, 0, s>>>(key, cand, cand_n, counter);
+    cudaMemcpyAsync(h_counter, counter, 8, cudaMemcpyDeviceToHost, s);
+    e = cudaStreamSynchronize(s);
+    *out = h_counter[0];
+    if (e == cudaSuccess && (*out != kHoleKey || tau == kHoleKey)) {
+      if (*out != kHoleKey) known_min = *out;
+      return cudaSuccess;
+    }
+    if (e != cudaSuccess) return e;
+  }
   size_t need = 0;
   cub::DeviceReduce::Min(nullptr, need, key, counter, static_cast<int>(size), s);
-  cudaError_t e = ensure_temp(need);
+  e = ensure_temp(need);
   if (e != cudaSuccess) return e;
   cub::DeviceReduce::Min(temp, need, key, counter, static_cast<int>(size), s);
   cudaMemcpyAsync(h_counter, counter, 8, cudaMemcpyDeviceToHost, s);
   e = cudaStreamSynchronize(s);
   *out = h_counter[0];
+  if (e == cudaSuccess && *out != kHoleKey) known_min = *out;
   return e;
 }
 
-cudaError_t Frontier::select_smallest(size_t want, unsigned long long limit, cudaStream_t s,
-                                      size_t* n_out) {
-  *n_out = 0;
-  if (size == 0 || want == 0) return cudaSuccess;
-  want = std::min(want, sel_cap);
+// Radix descent over 12-bit digit histograms: the largest bin boundary lo
+// with count(key < lo) = below <= want (refined until below >= fill * want or
+// the digits run out), and hi = the end of the boundary bin (capped at limit).
+cudaError_t Frontier::descend(size_t want, unsigned long long limit, double fill, cudaStream_t s,
+                              unsigned long long* lo, unsigned long long* hi, size_t* below_out,
+                              size_t* bin_out, const unsigned int* idx, size_t n_items) {
   // Digit schedule over the 64-bit key: 12,12,12,12,12,4 bits.
-  static const int kShift[6] = {52, 40, 28, 16, 4, 0};
-  static const int kBits[6] = {12, 12, 12, 12, 12, 4};
-  unsigned long long prefix = 0, lo_key = 0, hi_key = limit;
+  // Every live key lies in [known_min, limit): the digits start below their
+  // common high bits (one 12-bit level usually resolves a wave).
+  int pshift = 64;  // bits >= pshift are fixed to `prefix` (64: none)
+  unsigned long long prefix = 0;
+  if (known_min > 0 && known_min < limit) {
+    const unsigned long long x = known_min ^ (limit - 1);
+    pshift = std::max(12, x ? 64 - __builtin_clzll(x) : 0);
+    prefix = pshift >= 64 ? 0ull : (known_min >> pshift);
+  }
+  unsigned long long lo_key = 0, hi_key = limit;
   size_t below = 0;  // count of keys < lo_key
+  size_t bin = 0;    // count of keys in [lo_key, hi_key)
   cudaError_t e;
-  for (int lvl = 0; lvl < 6; ++lvl) {
-    const int shift = kShift[lvl], bits = kBits[lvl];
-    const int pshift = shift + bits;  // bits above this digit form the prefix
+  while (pshift > 0) {
+    const int bits = std::min(12, pshift);
+    const int shift = pshift - bits;
     if ((e = cudaMemsetAsync(hist, 0, kBins * 4, s)) != cudaSuccess) return e;
-    digit_hist<<<grid_cap(size, 256), 256, 0, s>>>(key, size, limit, shift, bits, prefix,
-                                                   lvl == 0 ? 64 : pshift, hist);
+    digit_hist<<<grid_cap(n_items, 256), 256, 0, s>>>(key, idx, n_items, limit, shift, bits,
+                                                      prefix, pshift, hist);
     const int nb = 1 << bits;
     if ((e = cudaMemcpyAsync(h_hist.data(), hist, nb * 4, cudaMemcpyDeviceToHost, s)) !=
         cudaSuccess)
       return e;
     if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
-    const unsigned long long base = (lvl == 0) ? 0ull : (prefix << pshift);
+    const unsigned long long base = pshift >= 64 ? 0ull : (prefix << pshift);
     size_t cum = below;
     int b = 0;
     for (; b < nb; ++b) {
@@ -446,63 +608,162 @@ cudaError_t Frontier::select_smallest(size_t want, unsigned long long limit, cud
       cum += h_hist[b];
     }
     if (b == nb) {  // everything under this prefix fits
-      if (lvl == 0) {
-        lo_key = hi_key = limit;
-      } else {
-        const unsigned long long end = base + (1ull << pshift);
-        lo_key = hi_key = (end == 0 || end > limit) ? limit : end;
-      }
+      const unsigned long long end = pshift >= 64 ? 0ull : base + (1ull << pshift);
+      lo_key = hi_key = (end == 0 || end > limit) ? limit : end;
       below = cum;
+      bin = 0;
       break;
     }
+    bin = h_hist[b];
     lo_key = base + (static_cast<unsigned long long>(b) << shift);
     const unsigned long long end = lo_key + (1ull << shift);
     hi_key = (end == 0 || end > limit) ? limit : end;
     below = cum;
-    if (below >= want / 2 || lvl == 5) break;
-    prefix = (lvl == 0 ? 0ull : (prefix << bits)) | static_cast<unsigned long long>(b);
+    if (static_cast<double>(below) >= fill * static_cast<double>(want) || shift == 0) break;
+    prefix = (pshift >= 64 ? 0ull : (prefix << bits)) | static_cast<unsigned long long>(b);
+    pshift = shift;
   }
-  // keys < lo_key (count `below` <= want), then fill from [lo_key, hi_key)
-  cub::CountingInputIterator<unsigned int> it(0);
-  size_t need = 0;
-  KeyBelow p1{key, 0ull, lo_key};
-  cub::DeviceSelect::If(nullptr, need, it, sel, counter, static_cast<int>(size), p1, s);
-  if ((e = ensure_temp(need)) != cudaSuccess) return e;
-  size_t n1 = 0;
-  if (below > 0) {
-    cub::DeviceSelect::If(temp, need, it, sel, counter, static_cast<int>(size), p1, s);
-    cudaMemcpyAsync(h_counter, counter, 8, cudaMemcpyDeviceToHost, s);
-    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
-    n1 = static_cast<size_t>(*reinterpret_cast<int*>(h_counter));
+  *lo = lo_key;
+  *hi = hi_key;
+  *below_out = below;
+  if (bin_out) *bin_out = bin;
+  return cudaSuccess;
+}
+
+// Candidate list: the pool indices of every live key below tau (tau = 0:
+// invalid, kHoleKey: the list holds the whole live pool). Waves select from
+// it, so a wave touches O(candidates) memory instead of the whole pool.
+cudaError_t Frontier::rebuild_candidates(size_t want_total, cudaStream_t s) {
+  ++rebuilds;
+  tau = 0;
+  cand_n = 0;
+  if (size == 0) {
+    tau = kHoleKey;
+    return cudaSuccess;
   }
-  size_t n2 = 0;
-  if (n1 < want && hi_key > lo_key) {
-    // fill from the boundary bin, chunked through kept_idx (kid_cap slots)
-    KeyBelow p2{key, lo_key, hi_key};
-    size_t done = 0;
-    while (done < size && n1 + n2 < want) {
-      const size_t chunk = std::min(size - done, kid_cap);
-      cub::CountingInputIterator<unsigned int> it2(static_cast<unsigned int>(done));
-      size_t need2 = 0;
-      cub::DeviceSelect::If(nullptr, need2, it2, kept_idx, counter, static_cast<int>(chunk), p2,
-                            s);
-      if ((e = ensure_temp(need2)) != cudaSuccess) return e;
-      cub::DeviceSelect::If(temp, need2, it2, kept_idx, counter, static_cast<int>(chunk), p2, s);
-      cudaMemcpyAsync(h_counter, counter, 8, cudaMemcpyDeviceToHost, s);
-      if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
-      const size_t got = static_cast<size_t>(*reinterpret_cast<int*>(h_counter));
-      const size_t take = std::min(got, want - n1 - n2);
-      if (take)
-        cudaMemcpyAsync(sel + n1 + n2, kept_idx, take * 4, cudaMemcpyDeviceToDevice, s);
-      n2 += take;
-      done += chunk;
+  unsigned long long lo = 0, hi = kHoleKey;
+  size_t below = 0, bin = 0;
+  cudaError_t e = descend(want_total, kHoleKey, 0.5, s, &lo, &hi, &below, &bin, nullptr, size);
+  if (e != cudaSuccess) return e;
+  const unsigned long long t = below > 0 ? lo : hi;  // massive ties: keep the boundary bin
+  const size_t count = below > 0 ? below : bin;
+  const size_t cap_need = count + 16 * std::max<size_t>(sel_cap, 1);
+  if (cap_need > cand_cap) {
+    cudaFree(cand);
+    cudaFree(cand_tmp);
+    cand = cand_tmp = nullptr;
+    if ((e = cudaMalloc(&cand, cap_need * 4)) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&cand_tmp, cap_need * 4)) != cudaSuccess) return e;
+    cand_cap = cap_need;
+  }
+  if (count) {
+    cub::CountingInputIterator<unsigned int> it(0);
+    KeyBelow p{key, 0ull, t};
+    size_t need = 0;
+    cub::DeviceSelect::If(nullptr, need, it, cand, counter, static_cast<int>(size), p, s);
+    if ((e = ensure_temp(need)) != cudaSuccess) return e;
+    cub::DeviceSelect::If(temp, need, it, cand, counter, static_cast<int>(size), p, s);
+  }
+  cand_n = count;
+  tau = t;
+  return cudaGetLastError();
+}
+
+namespace {
+struct SubTimer {
+  Frontier* F;
+  cudaStream_t s;
+  std::chrono::steady_clock::time_point t;
+  SubTimer(Frontier* f, cudaStream_t st) : F(f), s(st) {
+    if (F->prof) {
+      cudaStreamSynchronize(s);
+      t = std::chrono::steady_clock::now();
     }
   }
+  void lap(int k) {
+    if (!F->prof) return;
+    cudaStreamSynchronize(s);
+    const auto now = std::chrono::steady_clock::now();
+    F->t_sub[k] += std::chrono::duration<double>(now - t).count();
+    t = now;
+  }
+};
+}  // namespace
+
+cudaError_t Frontier::select_smallest(size_t want, unsigned long long limit, cudaStream_t s,
+                                      size_t* n_out) {
+  SubTimer tm(this, s);
+  *n_out = 0;
+  if (size == 0 || want == 0) return cudaSuccess;
+  want = std::min(want, sel_cap);
+  cudaError_t e;
+  const size_t target = std::max<size_t>(8 * want, size_t(1) << 20);
+  if (tau == 0 && (e = rebuild_candidates(target, s)) != cudaSuccess) return e;
+  tm.lap(0);
+  unsigned long long lo_key = 0, hi_key = limit;
+  size_t below = 0, bin_count = 0;
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    if (cand_n == 0) {
+      lo_key = hi_key = limit;
+      below = bin_count = 0;
+    } else if ((e = descend(want, limit, 0.5, s, &lo_key, &hi_key, &below, &bin_count, cand,
+                            cand_n)) != cudaSuccess) {
+      return e;
+    }
+    // too few candidates below the limit while the pool may hold more: refill
+    const bool short_of_want = hi_key == lo_key && below < want;
+    if (attempt == 0 && short_of_want && tau < limit && tau != kHoleKey) {
+      tm.lap(1);
+      if ((e = rebuild_candidates(target, s)) != cudaSuccess) return e;
+      tm.lap(0);
+      continue;
+    }
+    break;
+  }
+  tm.lap(1);
+  // candidates with key < lo_key (count `below` <= want), then the first ones
+  // (in candidate order) of the boundary bin [lo_key, hi_key); both counts are
+  // known from the histograms, so the stable selections need no host sync.
+  size_t need = 0;
+  KeyBelow p1{key, 0ull, lo_key};
+  cub::DeviceSelect::If(nullptr, need, cand, sel, counter, static_cast<int>(cand_n), p1, s);
+  if ((e = ensure_temp(need)) != cudaSuccess) return e;
+  const size_t n1 = below;
+  if (n1 > 0) cub::DeviceSelect::If(temp, need, cand, sel, counter, static_cast<int>(cand_n), p1, s);
+  size_t n2 = 0;
+  if (n1 < want && hi_key > lo_key && bin_count > 0) {
+    n2 = std::min(want - n1, bin_count);
+    if (bin_count > bsel_cap) {
+      cudaFree(bsel);
+      bsel = nullptr;
+      const size_t c = std::max(bin_count, 2 * bsel_cap);
+      if ((e = cudaMalloc(&bsel, c * 4)) != cudaSuccess) return e;
+      bsel_cap = c;
+    }
+    KeyBelow p2{key, lo_key, hi_key};
+    cub::DeviceSelect::If(temp, need, cand, bsel, counter, static_cast<int>(cand_n), p2, s);
+    if ((e = cudaMemcpyAsync(sel + n1, bsel, n2 * 4, cudaMemcpyDeviceToDevice, s)) !=
+        cudaSuccess)
+      return e;
+  }
   const size_t n = n1 + n2;
+  max_bin = std::max(max_bin, bin_count);
+  max_cand = std::max(max_cand, cand_n);
+  tm.lap(2);
   if (n) {
     mark_holes<<<grid_for(n, 256), 256, 0, s>>>(key, sel, n);
     holes += n;
+    // drop the expanded slots from the candidate list
+    NotHole ph{key};
+    size_t need2 = 0;
+    cub::DeviceSelect::If(nullptr, need2, cand, cand_tmp, counter, static_cast<int>(cand_n), ph,
+                          s);
+    if ((e = ensure_temp(need2)) != cudaSuccess) return e;
+    cub::DeviceSelect::If(temp, need2, cand, cand_tmp, counter, static_cast<int>(cand_n), ph, s);
+    std::swap(cand, cand_tmp);
+    cand_n -= n;
   }
+  tm.lap(3);
   *n_out = n;
   return cudaGetLastError();
 }
@@ -558,12 +819,16 @@ cudaError_t Frontier::best_child(size_t n_kids, cudaStream_t s, int* index, doub
 
 cudaError_t Frontier::route_append(size_t n_kids, double dstar, cudaStream_t s,
                                    RouteStats* out) {
+  SubTimer tm(this, s);
   cudaError_t e;
   RouteStats zero;
-  if ((e = cudaMemcpyAsync(stats, &zero, sizeof(RouteStats), cudaMemcpyHostToDevice, s)) !=
+  std::memcpy(h_stats, &zero, sizeof(RouteStats));
+  if ((e = cudaMemcpyAsync(stats, h_stats, sizeof(RouteStats), cudaMemcpyHostToDevice, s)) !=
       cudaSuccess)
     return e;
-  size_t kept = 0;
+  // room for every child, so the append needs no host round trip
+  if ((e = grow(size + n_kids, s)) != cudaSuccess) return e;
+  tm.lap(4);
   if (n_kids) {
     route<<<grid_for(n_kids, 256), 256, 0, s>>>(kids, kid_lower, kid_split, kid_vol, n_kids,
                                                 dstar, keep, stats);
@@ -574,74 +839,102 @@ cudaError_t Frontier::route_append(size_t n_kids, double dstar, cudaStream_t s,
     if ((e = ensure_temp(need)) != cudaSuccess) return e;
     cub::DeviceSelect::Flagged(temp, need, it, keep, kept_idx, counter, static_cast<int>(n_kids),
                                s);
-    if ((e = cudaMemcpyAsync(h_counter, counter, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
-      return e;
-    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
-    kept = static_cast<size_t>(*reinterpret_cast<int*>(h_counter));
-    if ((e = grow(size + kept, s)) != cudaSuccess) return e;
-    if (kept) {
-      append_kids<<<grid_for(kept, 256), 256, 0, s>>>(kids, kid_split, kid_vol, kept_idx, kept,
-                                                      nodes + size, split + size, vol + size,
-                                                      key + size);
+    append_kids_counted<<<grid_for(n_kids, 256), 256, 0, s>>>(
+        kids, kid_split, kid_vol, kept_idx, counter, nodes + size, split + size, vol + size,
+        key + size);
+    if (tau != 0 && cand_n + n_kids > cand_cap) tau = 0;  // list full: rebuild next wave
+    if (tau != 0) {
+      // appended children below tau join the candidate list (count -> counter[1])
+      cub::CountingInputIterator<unsigned int> ia(static_cast<unsigned int>(size));
+      NewCandidate pc{key, tau, size, counter};
+      size_t need2 = 0;
+      cub::DeviceSelect::If(nullptr, need2, ia, cand + cand_n, counter + 1,
+                            static_cast<int>(n_kids), pc, s);
+      if ((e = ensure_temp(need2)) != cudaSuccess) return e;
+      cub::DeviceSelect::If(temp, need2, ia, cand + cand_n, counter + 1, static_cast<int>(n_kids),
+                            pc, s);
     }
+    if ((e = cudaMemcpyAsync(h_counter, counter, 16, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+      return e;
   }
   if ((e = cudaMemcpyAsync(h_stats, stats, sizeof(RouteStats), cudaMemcpyDeviceToHost, s)) !=
       cudaSuccess)
     return e;
   if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+  tm.lap(5);
   *out = *h_stats;
-  size += kept;
+  if (n_kids) {
+    size += static_cast<size_t>(*reinterpret_cast<int*>(h_counter));
+    if (tau != 0) cand_n += static_cast<size_t>(*reinterpret_cast<int*>(h_counter + 1));
+  }
   return cudaGetLastError();
 }
 
+// Drops holes and stale nodes (key >= limit) in place: stale slots become
+// holes (their volume is returned), then the live tail is moved into the head
+// holes; no reallocation, traffic proportional to the moved nodes.
 cudaError_t Frontier::compact(unsigned long long limit, cudaStream_t s, double* dropped) {
   *dropped = 0.0;
   if (size == 0) return cudaSuccess;
   cudaError_t e;
   RouteStats zero;
-  if ((e = cudaMemcpyAsync(stats, &zero, sizeof(RouteStats), cudaMemcpyHostToDevice, s)) !=
+  std::memcpy(h_stats, &zero, sizeof(RouteStats));
+  if ((e = cudaMemcpyAsync(stats, h_stats, sizeof(RouteStats), cudaMemcpyHostToDevice, s)) !=
       cudaSuccess)
     return e;
-  dropped_volume<<<grid_cap(size, 256), 256, 0, s>>>(key, vol, size, limit, &stats->scratch);
-  // surviving slots: key < limit (holes carry the maximal key)
-  unsigned int* idx = nullptr;
-  if ((e = cudaMalloc(&idx, size * 4)) != cudaSuccess) return e;
-  cub::CountingInputIterator<unsigned int> it(0);
-  KeyBelow p{key, 0ull, limit};
-  size_t need = 0;
-  cub::DeviceSelect::If(nullptr, need, it, idx, counter, static_cast<int>(size), p, s);
-  if ((e = ensure_temp(need)) != cudaSuccess) return e;
-  cub::DeviceSelect::If(temp, need, it, idx, counter, static_cast<int>(size), p, s);
+  if ((e = cudaMemsetAsync(counter, 0, 16, s)) != cudaSuccess) return e;
+  if (limit < kHoleKey)
+    drop_stale<<<grid_cap(size, 256), 256, 0, s>>>(key, vol, size, limit, &stats->scratch);
+  count_live<<<grid_cap(size, 256), 256, 0, s>>>(key, size, counter);
   cudaMemcpyAsync(h_counter, counter, 8, cudaMemcpyDeviceToHost, s);
   cudaMemcpyAsync(h_stats, stats, sizeof(RouteStats), cudaMemcpyDeviceToHost, s);
   if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
-  const size_t n = static_cast<size_t>(*reinterpret_cast<int*>(h_counter));
+  const size_t live = static_cast<size_t>(h_counter[0]);
   *dropped = h_stats->scratch;
-  gosma_node* n2 = nullptr;
-  int8_t* s2 = nullptr;
-  double* v2 = nullptr;
-  unsigned long long* k2 = nullptr;
-  const size_t c = std::max<size_t>(n + n / 4, 1024);  // shrink-to-fit with headroom
-  if ((e = cudaMalloc(&n2, c * sizeof(gosma_node))) != cudaSuccess) return e;
-  if ((e = cudaMalloc(&s2, c)) != cudaSuccess) return e;
-  if ((e = cudaMalloc(&v2, c * sizeof(double))) != cudaSuccess) return e;
-  if ((e = cudaMalloc(&k2, c * 8)) != cudaSuccess) return e;
-  if (n)
-    gather_pool<<<grid_for(n, 256), 256, 0, s>>>(nodes, split, vol, key, idx, n, n2, s2, v2, k2);
-  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
-  cudaFree(idx);
-  cudaFree(nodes);
-  cudaFree(split);
-  cudaFree(vol);
-  cudaFree(key);
-  nodes = n2;
-  split = s2;
-  vol = v2;
-  key = k2;
-  size = n;
-  cap = c;
+  // holes below `live` and live slots at or above it are equally many (<= m)
+  const size_t m = size - live;
+  if (live > 0 && m > 0) {
+    if (2 * m > cidx_cap) {
+      cudaFree(cidx);
+      cidx = nullptr;
+      if ((e = cudaMalloc(&cidx, 2 * m * 4)) != cudaSuccess) return e;
+      cidx_cap = 2 * m;
+    }
+    cub::CountingInputIterator<unsigned int> it(0);
+    const HeadHole ph{key, static_cast<unsigned int>(live)};
+    const TailLive pt{key, static_cast<unsigned int>(live)};
+    size_t need = 0, need2 = 0;
+    cub::DeviceSelect::If(nullptr, need, it, cidx, counter, static_cast<int>(live), ph, s);
+    cub::DeviceSelect::If(nullptr, need2, it + live, cidx + m, counter + 1,
+                          static_cast<int>(size - live), pt, s);
+    if ((e = ensure_temp(std::max(need, need2))) != cudaSuccess) return e;
+    cub::DeviceSelect::If(temp, need, it, cidx, counter, static_cast<int>(live), ph, s);
+    cub::DeviceSelect::If(temp, need2, it + live, cidx + m, counter + 1,
+                          static_cast<int>(size - live), pt, s);
+    move_tail<<<grid_for(m, 256), 256, 0, s>>>(nodes, split, vol, key, cidx, cidx + m, counter);
+  }
+  size = live;
   holes = 0;
+  tau = 0;  // slots moved: the candidate list is rebuilt on the next selection
   return cudaGetLastError();
+}
+
+// enforce_capacity (solver.cpp:433-447): keeps the ~keep_n best live nodes
+// and folds the rest into the resolved set; their volume and minimum lower
+// bound are returned (the caller adds them to the ledger and floor_lower).
+cudaError_t Frontier::live_volume(cudaStream_t s, double* out) {
+  *out = 0.0;
+  if (size == 0) return cudaSuccess;
+  RouteStats zero;
+  std::memcpy(h_stats, &zero, sizeof(RouteStats));
+  cudaError_t e = cudaMemcpyAsync(stats, h_stats, sizeof(RouteStats), cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return e;
+  // live = non-hole keys >= 0: dropped_volume with limit 0 sums every live slot
+  dropped_volume<<<grid_cap(size, 256), 256, 0, s>>>(key, vol, size, 0ull, &stats->scratch);
+  cudaMemcpyAsync(h_stats, stats, sizeof(RouteStats), cudaMemcpyDeviceToHost, s);
+  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+  *out = h_stats->scratch;
+  return cudaSuccess;
 }
 
 cudaError_t Frontier::fold_to(size_t keep_n, cudaStream_t s, double* folded_volume,
@@ -651,43 +944,25 @@ cudaError_t Frontier::fold_to(size_t keep_n, cudaStream_t s, double* folded_volu
   double none = 0.0;
   cudaError_t e = compact(kHoleKey, s, &none);  // drop holes: the pool is live nodes only
   if (e != cudaSuccess || size <= keep_n) return e;
-  // full sort of the keys (rare path)
-  unsigned long long *k0 = nullptr, *k1 = nullptr;
-  unsigned int *i0 = nullptr, *i1 = nullptr;
-  if ((e = cudaMalloc(&k0, size * 8)) != cudaSuccess) return e;
-  if ((e = cudaMalloc(&k1, size * 8)) != cudaSuccess) return e;
-  if ((e = cudaMalloc(&i0, size * 4)) != cudaSuccess) return e;
-  if ((e = cudaMalloc(&i1, size * 4)) != cudaSuccess) return e;
-  cudaMemcpyAsync(k0, key, size * 8, cudaMemcpyDeviceToDevice, s);
-  std::vector<unsigned int> iota(size);
-  for (size_t i = 0; i < size; ++i) iota[i] = static_cast<unsigned int>(i);
-  cudaMemcpyAsync(i0, iota.data(), size * 4, cudaMemcpyHostToDevice, s);
-  cub::DoubleBuffer<unsigned long long> kb(k0, k1);
-  cub::DoubleBuffer<unsigned int> vb(i0, i1);
-  size_t need = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, need, kb, vb, static_cast<int>(size), 0, 64, s);
-  if ((e = ensure_temp(need)) != cudaSuccess) return e;
-  cub::DeviceRadixSort::SortPairs(temp, need, kb, vb, static_cast<int>(size), 0, 64, s);
-  unsigned long long kmin = 0;
-  std::vector<unsigned int> ord(size);
-  std::vector<double> hv(size);
-  cudaMemcpyAsync(&kmin, kb.Current() + keep_n, 8, cudaMemcpyDeviceToHost, s);
-  cudaMemcpyAsync(ord.data(), vb.Current(), size * 4, cudaMemcpyDeviceToHost, s);
-  cudaMemcpyAsync(hv.data(), vol, size * 8, cudaMemcpyDeviceToHost, s);
+  unsigned long long lo = 0, hi = kHoleKey;
+  size_t below = 0;
+  if ((e = descend(keep_n, kHoleKey, 0.9, s, &lo, &hi, &below, nullptr, nullptr, size)) !=
+      cudaSuccess)
+    return e;
+  // fold every key >= tau; with massive ties below the first boundary keep the bin
+  const unsigned long long cut = below > 0 ? lo : hi;
+  if (cut >= kHoleKey) return cudaSuccess;
+  unsigned long long kmin = kHoleKey;
+  if ((e = cudaMemcpyAsync(counter, &kmin, 8, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+    return e;
+  min_key_at_least<<<grid_cap(size, 256), 256, 0, s>>>(key, size, cut, counter);
+  if ((e = cudaMemcpyAsync(h_counter, counter, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+    return e;
   if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
-  double fv = 0.0;
-  for (size_t i = keep_n; i < size; ++i) fv += hv[ord[i]];
-  *folded_volume = fv;
+  kmin = h_counter[0];
+  if (kmin == kHoleKey) return cudaSuccess;
   *folded_min = key_to_double(kmin);
-  const size_t nf = size - keep_n;
-  mark_holes<<<grid_for(nf, 256), 256, 0, s>>>(key, vb.Current() + keep_n, nf);
-  holes += nf;
-  e = compact(kHoleKey, s, &none);
-  cudaFree(k0);
-  cudaFree(k1);
-  cudaFree(i0);
-  cudaFree(i1);
-  return e;
+  return compact(cut, s, folded_volume);
 }
 
 }  // namespace gosma

@@ -41,10 +41,27 @@ struct Frontier {
   size_t size = 0;   // slots in use (live + holes + stale)
   size_t holes = 0;  // expanded slots
   size_t cap = 0;
+  size_t cap_limit = 0;  // memory budget in nodes (0: none)
   // selection
   unsigned int* sel = nullptr;
   size_t sel_cap = 0;
   unsigned int* hist = nullptr;  // radix-select histogram (4096 bins)
+  unsigned int* bsel = nullptr;  // boundary-bin candidates of a selection
+  size_t bsel_cap = 0;
+  unsigned int* cidx = nullptr;  // compaction move lists (holes, live tail)
+  size_t cidx_cap = 0;
+  // a lower bound of the smallest live key (set by min_key; keys only rise
+  // through selection/append, so it stays valid until an import)
+  unsigned long long known_min = 0;
+  // candidate list: pool indices of all live keys < tau (0: invalid)
+  unsigned int* cand = nullptr;
+  unsigned int* cand_tmp = nullptr;
+  size_t cand_n = 0, cand_cap = 0;
+  unsigned long long tau = 0;
+  unsigned long long rebuilds = 0;  // candidate-list rebuilds (profiling)
+  bool prof = false;                // synchronising sub-phase timers
+  double t_sub[6] = {0, 0, 0, 0, 0, 0};  // rebuild, descend, pick, list; grow, route
+  size_t max_bin = 0, max_cand = 0;
   std::vector<unsigned int> h_hist;
   // children of one wave
   gosma_node* kids = nullptr;
@@ -82,6 +99,10 @@ struct Frontier {
   cudaError_t min_key(cudaStream_t s, unsigned long long* out);
   // selects up to `want` slots with key < limit (the smallest first); writes
   // their indices to sel, marks them holes, returns the count.
+  cudaError_t descend(size_t want, unsigned long long limit, double fill, cudaStream_t s,
+                      unsigned long long* lo, unsigned long long* hi, size_t* below,
+                      size_t* bin, const unsigned int* idx, size_t n_items);
+  cudaError_t rebuild_candidates(size_t want_total, cudaStream_t s);
   cudaError_t select_smallest(size_t want, unsigned long long limit, cudaStream_t s, size_t* n);
   cudaError_t expand_selected(size_t n_sel, cudaStream_t s);
   cudaError_t expand_selected_cached(size_t n_sel, cudaStream_t s, size_t* n_cuboids);
@@ -94,6 +115,7 @@ struct Frontier {
   // and the smallest folded lower bound
   cudaError_t fold_to(size_t keep_n, cudaStream_t s, double* folded_volume, double* folded_min);
   size_t live_upper_bound() const { return size - holes; }
+  cudaError_t live_volume(cudaStream_t s, double* out);
 };
 
 }  // namespace gosma

@@ -333,6 +333,7 @@ namespace {
 
 int solver_init(gosma_solver* S) {
   gosma_ctx* ctx = S->ctx;
+  S->F.prof = S->profile;
   const HostModel& m = ctx->model;
   const gosma_config& cfg = S->cfg;
   cudaStream_t s = ctx->stream;
@@ -392,6 +393,7 @@ int solver_init(gosma_solver* S) {
   cudaMemGetInfo(&free_b, &total_b);
   const size_t per_node = sizeof(gosma_node) + 1 + 8 + 8;
   S->mem_cap = std::max<size_t>(free_b / 4 / per_node, 16 * S->wave_nodes);
+  S->F.cap_limit = S->mem_cap;
   S->qcap = cfg.queue_capacity >= 0
                 ? std::min<size_t>(static_cast<size_t>(cfg.queue_capacity), S->mem_cap)
                 : S->mem_cap;
@@ -475,10 +477,14 @@ void gosma_solver_destroy(gosma_solver* S) {
   if (S->profile) {
     static const char* kName[8] = {"status", "select", "expand+self", "eval", "best+improve",
                                    "route", "compact", "other"};
-    std::fprintf(stderr, "[gosma profile] waves %llu evals %llu cuboids %llu:", S->wave, S->evals,
-                 S->cuboid_evals);
+    std::fprintf(stderr, "[gosma profile] waves %llu evals %llu cuboids %llu rebuilds %llu pool %zu:",
+                 S->wave, S->evals, S->cuboid_evals, S->F.rebuilds, S->F.size);
     for (int k = 0; k < 8; ++k) std::fprintf(stderr, " %s %.3fs", kName[k], S->phase[k]);
-    std::fprintf(stderr, "\n");
+    std::fprintf(stderr,
+                 " | select: rebuild %.3fs descend %.3fs pick %.3fs list %.3fs (max bin %zu, "
+                 "max list %zu) | route: grow %.3fs rest %.3fs\n",
+                 S->F.t_sub[0], S->F.t_sub[1], S->F.t_sub[2], S->F.t_sub[3], S->F.max_bin,
+                 S->F.max_cand, S->F.t_sub[4], S->F.t_sub[5]);
   }
   DeviceGuard g(S->ctx->device);
   S->F.release();
@@ -650,6 +656,14 @@ int gosma_solver_import(gosma_solver* S, const gosma_node* nodes, const int8_t* 
   DeviceGuard g(S->ctx->device);
   const cudaError_t e = S->F.upload(nodes, split, vol, n, S->ctx->stream);
   if (e != cudaSuccess) return cuda_error(e, "import");
+  return GOSMA_OK;
+}
+
+int gosma_solver_live_volume(gosma_solver* S, double* volume) {
+  if (!S || !volume) return set_error(GOSMA_EINVAL, "null argument");
+  DeviceGuard g(S->ctx->device);
+  const cudaError_t e = S->F.live_volume(S->ctx->stream, volume);
+  if (e != cudaSuccess) return cuda_error(e, "live volume");
   return GOSMA_OK;
 }
 
