@@ -188,3 +188,33 @@ def test_volume_ledger_is_conserved_over_waves(gosma):
             shard.expand(st["best_value"] - 0.1)
         # the certified lower bound never decreases
         assert all(b >= a - 1e-12 for a, b in zip(lows, lows[1:]))
+
+
+def test_sharded_driver_over_nccl_world1(gosma):
+    """The sharded driver's collectives on a CUDA tensor over an NCCL process
+    group (world size 1 here: one GPU per gpurun box); the multi-rank exchange
+    logic itself is covered with gloo in tests/test_distributed.py."""
+    import os
+    import socket
+    import torch
+    import torch.distributed as dist
+    from paper_1812_01232_b200.distributed import Comm, solve_sharded
+    if dist.is_initialized():
+        pytest.skip("a process group already exists")
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        ctx = toy_ctx(gosma, var=4.0, k2=2.0)
+        dom = box_domain(gosma, 0.4, 0.4, (0.05, -0.03, 0.02))
+        cfg = gosma.SolverConfig(epsilon=0.3, zeta=0.5)
+        rep = solve_sharded(gosma.ShardSolver(ctx, dom, cfg, 0, 1), 0.3,
+                            Comm(device=torch.device("cuda", 0)))
+        assert rep.status == "epsilon_optimal"
+        assert abs(rep.best_value - gosma.solve(ctx, dom, cfg).best_value) <= 1e-9
+    finally:
+        dist.destroy_process_group()
