@@ -139,6 +139,13 @@ void ctx_free_device(gosma_ctx* ctx) {
   ctx->cache_cap = 0;
   ctx->scratch.release();
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  if (ctx->h2d_stream) cudaStreamDestroy(ctx->h2d_stream);
+  if (ctx->d2h_stream) cudaStreamDestroy(ctx->d2h_stream);
+  for (cudaEvent_t& ev : ctx->pipe_ev) {
+    if (ev) cudaEventDestroy(ev);
+    ev = nullptr;
+  }
+  ctx->h2d_stream = ctx->d2h_stream = nullptr;
   ctx->stream = nullptr;
   cudaSetDevice(cur);
 }
@@ -414,32 +421,64 @@ int gosma_eval_bounds(gosma_ctx* ctx, const gosma_node* nodes, size_t n, double 
   DeviceGuard g(ctx->device);
   std::lock_guard<std::mutex> lock(ctx->mu);
   cudaError_t e;
-  // Chunked pipeline: H2D of chunk k+1 overlaps the bound kernel on chunk k.
-  const size_t chunk = std::min<size_t>(n, static_cast<size_t>(1) << 18);
+  // Three-stream pipeline over two device slots: H2D of chunk k+1 (copy-in
+  // stream) and D2H of chunk k-1 (copy-out stream) overlap the bound kernel on
+  // chunk k (compute stream). Overlap needs pinned host buffers; pageable ones
+  // still work (the copies then serialise).
+  const size_t chunk = std::min<size_t>(n, static_cast<size_t>(1) << 17);
   if ((e = ctx->scratch.reserve(2 * chunk)) != cudaSuccess) return cuda_error(e, "scratch");
-  cudaStream_t s = ctx->stream;
-  for (size_t off = 0, k = 0; off < n; off += chunk, ++k) {
-    const size_t m = std::min(chunk, n - off);
-    const size_t slot = (k & 1) * chunk;
-    gosma_node* dn = ctx->scratch.d_nodes + slot;
-    if ((e = cudaMemcpyAsync(dn, nodes + off, m * sizeof(gosma_node), cudaMemcpyHostToDevice,
-                             s)) != cudaSuccess)
-      return cuda_error(e, "H2D nodes");
-    const int rc = gosma_eval_bounds_device(ctx, dn, m, skip, ctx->scratch.d_lower + slot,
-                                            ctx->scratch.d_upper + slot,
-                                            split_rot ? ctx->scratch.d_split + slot : nullptr, s);
-    if (rc != GOSMA_OK) return rc;
-    if ((e = cudaMemcpyAsync(lower + off, ctx->scratch.d_lower + slot, m * sizeof(double),
-                             cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
-        (e = cudaMemcpyAsync(upper + off, ctx->scratch.d_upper + slot, m * sizeof(double),
-                             cudaMemcpyDeviceToHost, s)) != cudaSuccess)
-      return cuda_error(e, "D2H bounds");
-    if (split_rot &&
-        (e = cudaMemcpyAsync(split_rot + off, ctx->scratch.d_split + slot, m * sizeof(int8_t),
-                             cudaMemcpyDeviceToHost, s)) != cudaSuccess)
-      return cuda_error(e, "D2H split");
+  if (!ctx->h2d_stream) {
+    if ((e = cudaStreamCreateWithFlags(&ctx->h2d_stream, cudaStreamNonBlocking)) != cudaSuccess ||
+        (e = cudaStreamCreateWithFlags(&ctx->d2h_stream, cudaStreamNonBlocking)) != cudaSuccess)
+      return cuda_error(e, "pipeline streams");
+    for (cudaEvent_t& ev : ctx->pipe_ev)
+      if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess)
+        return cuda_error(e, "pipeline events");
   }
-  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_error(e, "eval_bounds");
+  cudaStream_t ks = ctx->stream, hs = ctx->h2d_stream, ds = ctx->d2h_stream;
+  cudaEvent_t* h2d_done = ctx->pipe_ev;      // [slot]
+  cudaEvent_t* k_done = ctx->pipe_ev + 2;    // [slot]
+  cudaEvent_t* d2h_done = ctx->pipe_ev + 4;  // [slot]
+  // the compute stream may hold earlier work on these slots
+  if ((e = cudaEventRecord(k_done[0], ks)) != cudaSuccess) return cuda_error(e, "event");
+  cudaEventRecord(k_done[1], ks);
+  cudaEventRecord(d2h_done[0], ks);
+  cudaEventRecord(d2h_done[1], ks);
+  const size_t nchunks = (n + chunk - 1) / chunk;
+  auto h2d = [&](size_t k) -> cudaError_t {
+    const size_t off = k * chunk, m = std::min(chunk, n - off), slot = k & 1;
+    cudaStreamWaitEvent(hs, k_done[slot], 0);  // the kernel of chunk k-2 has read the slot
+    cudaError_t err = cudaMemcpyAsync(ctx->scratch.d_nodes + slot * chunk, nodes + off,
+                                      m * sizeof(gosma_node), cudaMemcpyHostToDevice, hs);
+    if (err == cudaSuccess) err = cudaEventRecord(h2d_done[slot], hs);
+    return err;
+  };
+  if ((e = h2d(0)) != cudaSuccess) return cuda_error(e, "H2D nodes");
+  for (size_t k = 0; k < nchunks; ++k) {
+    const size_t off = k * chunk, m = std::min(chunk, n - off), slot = k & 1;
+    if (k + 1 < nchunks && (e = h2d(k + 1)) != cudaSuccess) return cuda_error(e, "H2D nodes");
+    cudaStreamWaitEvent(ks, h2d_done[slot], 0);
+    cudaStreamWaitEvent(ks, d2h_done[slot], 0);  // chunk k-2's bounds have left the slot
+    double* dl = ctx->scratch.d_lower + slot * chunk;
+    double* du = ctx->scratch.d_upper + slot * chunk;
+    int8_t* dsp = split_rot ? ctx->scratch.d_split + slot * chunk : nullptr;
+    const int rc = gosma_eval_bounds_device(ctx, ctx->scratch.d_nodes + slot * chunk, m, skip,
+                                            dl, du, dsp, ks);
+    if (rc != GOSMA_OK) return rc;
+    cudaEventRecord(k_done[slot], ks);
+    cudaStreamWaitEvent(ds, k_done[slot], 0);
+    if ((e = cudaMemcpyAsync(lower + off, dl, m * sizeof(double), cudaMemcpyDeviceToHost, ds)) !=
+            cudaSuccess ||
+        (e = cudaMemcpyAsync(upper + off, du, m * sizeof(double), cudaMemcpyDeviceToHost, ds)) !=
+            cudaSuccess)
+      return cuda_error(e, "D2H bounds");
+    if (split_rot && (e = cudaMemcpyAsync(split_rot + off, dsp, m * sizeof(int8_t),
+                                          cudaMemcpyDeviceToHost, ds)) != cudaSuccess)
+      return cuda_error(e, "D2H split");
+    cudaEventRecord(d2h_done[slot], ds);
+  }
+  if ((e = cudaStreamSynchronize(ds)) != cudaSuccess) return cuda_error(e, "eval_bounds");
+  if ((e = cudaStreamSynchronize(ks)) != cudaSuccess) return cuda_error(e, "eval_bounds");
   return GOSMA_OK;
 }
 

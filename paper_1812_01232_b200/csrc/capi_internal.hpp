@@ -55,6 +55,10 @@ struct gosma_ctx {
   double* d_cache_self = nullptr;
   size_t cache_cap = 0;
   cudaStream_t stream = nullptr;
+  // host-buffer pipeline (gosma_eval_bounds): copy-in / copy-out streams and
+  // per-slot events (H2D done, kernel done, D2H done) x 2 slots
+  cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
+  cudaEvent_t pipe_ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   gosma::Scratch scratch;
   std::mutex mu;
 };

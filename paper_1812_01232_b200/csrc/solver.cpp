@@ -405,8 +405,10 @@ int solver_init(gosma_solver* S) {
   if (rc != GOSMA_OK) return rc;
   S->evals += roots.size();
   if (cfg.discovery_dive) {
+    const auto t0 = std::chrono::steady_clock::now();
     rc = discovery_dive(ctx, S->dom, roots, cfg, &S->inc, &S->evals, 0.0);
     if (rc != GOSMA_OK) return rc;
+    S->phase[7] += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   }
   for (size_t i = 0; i < roots.size(); ++i)
     if (up[i] < S->inc.value) improve(m, S->dom, roots[i], &S->inc);
@@ -476,7 +478,7 @@ void gosma_solver_destroy(gosma_solver* S) {
   if (!S) return;
   if (S->profile) {
     static const char* kName[8] = {"status", "select", "expand+self", "eval", "best+improve",
-                                   "route", "compact", "other"};
+                                   "route", "compact", "dive"};
     std::fprintf(stderr, "[gosma profile] waves %llu evals %llu cuboids %llu rebuilds %llu pool %zu:",
                  S->wave, S->evals, S->cuboid_evals, S->F.rebuilds, S->F.size);
     for (int k = 0; k < 8; ++k) std::fprintf(stderr, " %s %.3fs", kName[k], S->phase[k]);

@@ -393,3 +393,27 @@ def test_host_gradient_matches_central_differences(gosma):
             fd[k] = (gosma.objective_value(ctx, xp[:3], xp[3:]) -
                      gosma.objective_value(ctx, xm[:3], xm[3:])) / (2 * h)
         assert np.all(np.abs(gr - fd) <= 1e-4 * (1 + np.abs(fd)))
+
+
+def test_host_pipeline_matches_device_path(gosma):
+    """gosma_eval_bounds (host buffers, 3-stream chunked pipeline, several
+    chunks incl. a ragged last one) equals the device-resident call exactly."""
+    import torch
+    from paper_1812_01232_b200 import synth
+    classes = synth.mixture(16, 12, "realistic", seed=77)
+    ctx = gosma.ObjectiveContext(classes, 0.5)
+    n = 3 * (1 << 17) + 12345
+    nodes = synth.nodes(n, seed=78)
+    lo, up, sp = gosma.evaluate_branch_batch(ctx, nodes, return_split=True)
+    d_nodes = torch.from_numpy(nodes.view(np.uint8)).cuda()
+    d_lo = torch.empty(n, dtype=torch.float64, device="cuda")
+    d_up = torch.empty_like(d_lo)
+    d_sp = torch.empty(n, dtype=torch.int8, device="cuda")
+    s = torch.cuda.Stream()
+    gosma.evaluate_branch_batch_device(ctx, d_nodes.data_ptr(), n, d_lo.data_ptr(),
+                                       d_up.data_ptr(), d_sp.data_ptr(), float("inf"),
+                                       s.cuda_stream)
+    s.synchronize()
+    assert np.array_equal(lo, d_lo.cpu().numpy())
+    assert np.array_equal(up, d_up.cpu().numpy())
+    assert np.array_equal(sp, d_sp.cpu().numpy())
