@@ -236,6 +236,41 @@ const char* gosma_last_error(void);
 /* Build / device introspection for benches and tests. */
 int gosma_device_info(int device, int* sm_count, int* sm_clock_khz, int* cc_major,
                       int* cc_minor);
+/* ---- Mixture construction (host C++; mixtures.hpp:55-98) ------------------
+ * Replaces smalign::build_semantic_mixtures (mixtures.cpp:269-362) and the
+ * DP-means clusterers it uses (mixtures.cpp:49-182); bit-identical results. */
+typedef struct gosma_mixtures gosma_mixtures;
+
+/* points: 3*n_points doubles; bearings: 3*n_bearings doubles, each within 1e-6
+ * of unit length (UnitVector3, renormalised). point_labels / bearing_labels:
+ * one C string per element, or both NULL (a single class "all"). weight_labels
+ * / weights: n_weights class weights (LabeledPointSet class_weights), or NULL
+ * for uniform weights. Invalid input -> GOSMA_EINVAL with the reference's
+ * message. */
+int gosma_mixtures_build(const double* points, const char* const* point_labels,
+                         size_t n_points, const double* bearings,
+                         const char* const* bearing_labels, size_t n_bearings, double lambda_p,
+                         double lambda_f, const char* const* weight_labels,
+                         const double* weights, size_t n_weights, gosma_mixtures** out);
+int gosma_mixtures_class_count(const gosma_mixtures* m);
+/* Class k (in the reference's order: sorted class ids) as a view usable with
+ * gosma_ctx_create; the arrays are owned by m. */
+int gosma_mixtures_class(const gosma_mixtures* m, int k, gosma_class_view* view,
+                         const char** id);
+int gosma_mixtures_warning_count(const gosma_mixtures* m);
+const char* gosma_mixtures_warning(const gosma_mixtures* m, int k);
+void gosma_mixtures_destroy(gosma_mixtures* m);
+
+/* dp_means / dp_vmf_means (mixtures.cpp:49-182). assignment: n ints; centers:
+ * 3*centers_cap doubles; shuffle (0/1) + seed = the optional shuffle seed;
+ * *iterations = length of the objective history. */
+int gosma_dp_means(const double* points, size_t n, double lambda_p, int shuffle,
+                   unsigned long long seed, int* assignment, double* centers, size_t centers_cap,
+                   size_t* n_centers, int* iterations);
+int gosma_dp_vmf_means(const double* bearings, size_t n, double lambda_f, int shuffle,
+                       unsigned long long seed, int* assignment, double* centers,
+                       size_t centers_cap, size_t* n_centers, int* iterations);
+
 /* Pipe-throughput microbenchmarks (roofline denominators): MUFU (SFU/XU)
  * ops/s and FP32 FMA flop/s measured on `device` at its current clocks. */
 int gosma_calibrate_pipes(int device, double* mufu_ops_per_s, double* fma_flops_per_s);

@@ -315,3 +315,71 @@ def reference_torus_cover(major=3.5, minor=0.5, cap=1024):
     boxes = np.zeros((cap, 6))
     n = lib.ref_torus_cover(major, minor, _d(boxes), cap)
     return boxes[:n].copy()
+
+
+def _cstrs(labels):
+    if labels is None:
+        return None, None
+    enc = [str(x).encode() for x in labels]
+    arr = (C.c_char_p * len(enc))(*enc)
+    return arr, enc
+
+
+def reference_dp_means(points, lam, seed=None, vmf=False, cap=100000):
+    """dp_means / dp_vmf_means of the reference: (assignment, centers, iterations)."""
+    lib = C.CDLL(REF_SO)
+    fn = lib.ref_dp_vmf_means if vmf else lib.ref_dp_means
+    fn.argtypes = [_dp, C.c_long, C.c_double, C.c_int, C.c_ulonglong, _ip, _dp, C.c_long,
+                   C.POINTER(C.c_long), _ip]
+    lib.ref_last_error.restype = C.c_char_p
+    p = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 3)
+    n = len(p)
+    asg = np.zeros(n, dtype=np.int32)
+    cen = np.zeros((min(cap, max(n, 1)), 3))
+    nc, it = C.c_long(0), np.zeros(1, dtype=np.int32)
+    rc = fn(_d(p), n, float(lam), int(seed is not None), int(seed or 0), _i(asg), _d(cen),
+            len(cen), C.byref(nc), _i(it))
+    if rc != 0:
+        raise ValueError(lib.ref_last_error().decode())
+    return asg, cen[:nc.value].copy(), int(it[0])
+
+
+def reference_build_mixtures(points, bearings, lambda_p, lambda_f, point_labels=None,
+                             bearing_labels=None, class_weights=None, cap_classes=256,
+                             cap_comp=100000):
+    """build_semantic_mixtures of the reference: (classes, warnings); classes
+    are dicts {id, weight, mu, sigma2, phi1, dir, kappa2, phi2}."""
+    lib = C.CDLL(REF_SO)
+    lib.ref_build_mixtures.restype = C.c_int
+    lib.ref_last_error.restype = C.c_char_p
+    p = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 3)
+    b = np.ascontiguousarray(bearings, dtype=np.float64).reshape(-1, 3)
+    pl, _k1 = _cstrs(point_labels)
+    bl, _k2 = _cstrs(bearing_labels)
+    wl, _k3 = _cstrs(list(class_weights) if class_weights else None)
+    w = np.array([class_weights[k] for k in class_weights], float) if class_weights else None
+    n1 = np.zeros(cap_classes, dtype=np.int32)
+    n2 = np.zeros(cap_classes, dtype=np.int32)
+    cw = np.zeros(cap_classes)
+    mu, dr = np.zeros((cap_comp, 3)), np.zeros((cap_comp, 3))
+    s2, p1, k2, p2 = (np.zeros(cap_comp) for _ in range(4))
+    ids = C.create_string_buffer(1 << 16)
+    warns = C.create_string_buffer(1 << 16)
+    nc = lib.ref_build_mixtures(_d(p), pl, C.c_long(len(p)), _d(b), bl, C.c_long(len(b)),
+                                C.c_double(lambda_p), C.c_double(lambda_f), wl,
+                                None if w is None else _d(w), C.c_long(0 if w is None else len(w)),
+                                cap_classes, cap_comp, _i(n1), _i(n2), _d(cw), _d(mu), _d(s2),
+                                _d(p1), _d(dr), _d(k2), _d(p2), ids, len(ids), warns, len(warns))
+    if nc < 0:
+        raise ValueError(lib.ref_last_error().decode())
+    names = ids.value.decode().split("\n")[:nc]
+    out, o1, o2 = [], 0, 0
+    for c in range(nc):
+        a, bb = int(n1[c]), int(n2[c])
+        out.append({"id": names[c], "weight": float(cw[c]), "mu": mu[o1:o1 + a].copy(),
+                    "sigma2": s2[o1:o1 + a].copy(), "phi1": p1[o1:o1 + a].copy(),
+                    "dir": dr[o2:o2 + bb].copy(), "kappa2": k2[o2:o2 + bb].copy(),
+                    "phi2": p2[o2:o2 + bb].copy()})
+        o1, o2 = o1 + a, o2 + bb
+    warnings = [x for x in warns.value.decode().split("\n") if x]
+    return out, warnings

@@ -7,6 +7,9 @@
 // Node records use the product ABI layout (include/gosma_capi.h gosma_node):
 //   {rc[3], rhw, tc[3], thw[3], lower}  (11 doubles)
 #include <chrono>
+#include <cstdio>
+#include <map>
+#include <optional>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -374,6 +377,112 @@ int ref_torus_cover(double major, double minor, double* boxes, int cap) {
     return n;
   } catch (const std::exception& e) {
     return -fail(e, 1);
+  }
+}
+
+// dp_means / dp_vmf_means (mixtures.cpp:49-182) of the reference.
+int ref_dp_means(const double* pts, long n, double lambda, int shuffle, unsigned long long seed,
+                 int* assignment, double* centers, long cap, long* n_centers, int* iters) {
+  try {
+    std::vector<Eigen::Vector3d> p(n);
+    for (long i = 0; i < n; ++i) p[i] = Eigen::Vector3d(pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]);
+    const Clustering c = dp_means(p, lambda, shuffle ? std::optional<std::uint64_t>(seed)
+                                                     : std::nullopt);
+    *n_centers = static_cast<long>(c.centers.size());
+    *iters = static_cast<int>(c.objective_history.size());
+    for (long i = 0; i < n; ++i) assignment[i] = c.assignment[i];
+    for (long k = 0; k < *n_centers && k < cap; ++k)
+      for (int a = 0; a < 3; ++a) centers[3 * k + a] = c.centers[k][a];
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e, 1);
+  }
+}
+
+int ref_dp_vmf_means(const double* dirs, long n, double lambda, int shuffle,
+                     unsigned long long seed, int* assignment, double* centers, long cap,
+                     long* n_centers, int* iters) {
+  try {
+    std::vector<UnitVector3> b;
+    for (long i = 0; i < n; ++i)
+      b.emplace_back(Eigen::Vector3d(dirs[3 * i], dirs[3 * i + 1], dirs[3 * i + 2]));
+    const Clustering c = dp_vmf_means(b, lambda, shuffle ? std::optional<std::uint64_t>(seed)
+                                                         : std::nullopt);
+    *n_centers = static_cast<long>(c.centers.size());
+    *iters = static_cast<int>(c.objective_history.size());
+    for (long i = 0; i < n; ++i) assignment[i] = c.assignment[i];
+    for (long k = 0; k < *n_centers && k < cap; ++k)
+      for (int a = 0; a < 3; ++a) centers[3 * k + a] = c.centers[k][a];
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e, 1);
+  }
+}
+
+// build_semantic_mixtures (mixtures.cpp:269-362) with string labels (NULL:
+// unlabeled) and optional class weights. Outputs are flattened over classes in
+// result order; per class: n1, n2, weight, id (into ids, '\n'-separated), then
+// warnings ('\n'-separated). Returns the class count (or -1 on error).
+int ref_build_mixtures(const double* pts, const char* const* plab, long np, const double* dirs,
+                       const char* const* blab, long nb, double lambda_p, double lambda_f,
+                       const char* const* wlab, const double* w, long nw, int cap_classes,
+                       int cap_comp, int* n1, int* n2, double* cls_w, double* mu, double* sigma2,
+                       double* phi1, double* dir, double* kappa2, double* phi2, char* ids,
+                       long ids_cap, char* warnings, long warn_cap) {
+  try {
+    LabeledPointSet ps;
+    LabeledBearingSet bs;
+    for (long i = 0; i < np; ++i)
+      ps.points.emplace_back(pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]);
+    for (long i = 0; i < nb; ++i)
+      bs.bearings.emplace_back(Eigen::Vector3d(dirs[3 * i], dirs[3 * i + 1], dirs[3 * i + 2]));
+    if (plab)
+      for (long i = 0; i < np; ++i) ps.labels.emplace_back(plab[i]);
+    if (blab)
+      for (long i = 0; i < nb; ++i) bs.labels.emplace_back(blab[i]);
+    std::optional<std::map<std::string, double>> cw;
+    if (w) {
+      cw.emplace();
+      for (long k = 0; k < nw; ++k) (*cw)[wlab[k]] = w[k];
+    }
+    const SemanticMixturePair pair = build_semantic_mixtures(ps, bs, lambda_p, lambda_f, cw);
+    const int nc = static_cast<int>(pair.classes.size());
+    if (nc > cap_classes) {
+      g_err = "capacity";
+      return -1;
+    }
+    std::string idcat, wcat;
+    long o1 = 0, o2 = 0;
+    for (int c = 0; c < nc; ++c) {
+      const auto& cls = pair.classes[c];
+      n1[c] = static_cast<int>(cls.gmm.components.size());
+      n2[c] = static_cast<int>(cls.vmfmm.components.size());
+      cls_w[c] = cls.weight;
+      if (o1 + n1[c] > cap_comp || o2 + n2[c] > cap_comp) {
+        g_err = "capacity";
+        return -1;
+      }
+      for (const auto& g : cls.gmm.components) {
+        for (int a = 0; a < 3; ++a) mu[3 * o1 + a] = g.mean[a];
+        sigma2[o1] = g.variance;
+        phi1[o1] = g.weight;
+        ++o1;
+      }
+      for (const auto& v : cls.vmfmm.components) {
+        for (int a = 0; a < 3; ++a) dir[3 * o2 + a] = v.mean_direction.vec()[a];
+        kappa2[o2] = v.concentration;
+        phi2[o2] = v.weight;
+        ++o2;
+      }
+      idcat += cls.id + "\n";
+    }
+    for (const auto& s : pair.warnings) wcat += s + "\n";
+    std::snprintf(ids, ids_cap, "%s", idcat.c_str());
+    std::snprintf(warnings, warn_cap, "%s", wcat.c_str());
+    return nc;
+  } catch (const std::exception& e) {
+    fail(e, 1);
+    return -1;
   }
 }
 

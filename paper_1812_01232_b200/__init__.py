@@ -116,6 +116,20 @@ def _load():
     lib.gosma_solver_import.argtypes = [vp, vp, vp, vp, C.c_size_t]
     lib.gosma_solver_result.argtypes = [vp, C.POINTER(_Report)]
     lib.gosma_solver_live_volume.argtypes = [vp, _dp]
+    cpp = C.POINTER(C.c_char_p)
+    lib.gosma_mixtures_build.argtypes = [_dp, cpp, C.c_size_t, _dp, cpp, C.c_size_t, C.c_double,
+                                         C.c_double, cpp, _dp, C.c_size_t, C.POINTER(vp)]
+    lib.gosma_mixtures_class_count.argtypes = [vp]
+    lib.gosma_mixtures_class.argtypes = [vp, C.c_int, C.POINTER(_ClassView),
+                                         C.POINTER(C.c_char_p)]
+    lib.gosma_mixtures_warning_count.argtypes = [vp]
+    lib.gosma_mixtures_warning.argtypes = [vp, C.c_int]
+    lib.gosma_mixtures_warning.restype = C.c_char_p
+    lib.gosma_mixtures_destroy.argtypes = [vp]
+    for fn in (lib.gosma_dp_means, lib.gosma_dp_vmf_means):
+        fn.argtypes = [_dp, C.c_size_t, C.c_double, C.c_int, C.c_ulonglong,
+                       C.POINTER(C.c_int), _dp, C.c_size_t, C.POINTER(C.c_size_t),
+                       C.POINTER(C.c_int)]
     return lib
 
 
@@ -487,3 +501,75 @@ class ShardSolver:
         if h:
             lib.gosma_solver_destroy(h)
             self._h = None
+
+
+# ---- mixture construction (host C++; mixtures.hpp:55-98) ---------------------
+
+def _labels(labels, n):
+    if labels is None:
+        return None, None
+    enc = [str(x).encode() for x in labels]
+    if len(enc) != n:
+        raise ValueError("build_semantic_mixtures: label count mismatch")
+    return (C.c_char_p * len(enc))(*enc), enc
+
+
+def _clustering(fn, data, lam, shuffle_seed, what):
+    x = _f64(data).reshape(-1, 3)
+    n = len(x)
+    asg = np.zeros(n, dtype=np.int32)
+    cen = np.zeros((max(n, 1), 3))
+    nc, it = C.c_size_t(0), C.c_int(0)
+    _check(fn(x.ctypes.data_as(_dp), n, float(lam), int(shuffle_seed is not None),
+              int(shuffle_seed or 0), asg.ctypes.data_as(C.POINTER(C.c_int)),
+              cen.ctypes.data_as(_dp), len(cen), C.byref(nc), C.byref(it)), what)
+    return asg, cen[:nc.value].copy(), it.value
+
+
+def dp_means(points, lambda_p: float, shuffle_seed: Optional[int] = None):
+    """dp_means (mixtures.cpp:49-109): (assignment, centers, iterations)."""
+    return _clustering(lib.gosma_dp_means, points, lambda_p, shuffle_seed, "dp_means")
+
+
+def dp_vmf_means(bearings, lambda_f: float, shuffle_seed: Optional[int] = None):
+    """dp_vmf_means (mixtures.cpp:111-182): (assignment, centers, iterations)."""
+    return _clustering(lib.gosma_dp_vmf_means, bearings, lambda_f, shuffle_seed, "dp_vmf_means")
+
+
+def build_semantic_mixtures(points, bearings, lambda_p: float, lambda_f: float,
+                            point_labels=None, bearing_labels=None, class_weights=None):
+    """build_semantic_mixtures (mixtures.cpp:269-362): returns (classes,
+    warnings); each class is a dict {id, weight, mu, sigma2, phi1, dir, kappa2,
+    phi2} accepted by ObjectiveContext."""
+    p = _f64(points).reshape(-1, 3)
+    b = _f64(bearings).reshape(-1, 3)
+    pl, _k1 = _labels(point_labels, len(p))
+    bl, _k2 = _labels(bearing_labels, len(b))
+    wl = w = None
+    keep = None
+    if class_weights is not None:
+        keys = list(class_weights)
+        wl, keep = _labels(keys, len(keys))
+        w = np.array([float(class_weights[k]) for k in keys])
+    h = C.c_void_p()
+    _check(lib.gosma_mixtures_build(p.ctypes.data_as(_dp), pl, len(p), b.ctypes.data_as(_dp), bl,
+                                    len(b), float(lambda_p), float(lambda_f), wl,
+                                    None if w is None else w.ctypes.data_as(_dp),
+                                    0 if w is None else len(w), C.byref(h)),
+           "build_semantic_mixtures")
+    try:
+        classes = []
+        for k in range(lib.gosma_mixtures_class_count(h)):
+            v, cid = _ClassView(), C.c_char_p()
+            _check(lib.gosma_mixtures_class(h, k, C.byref(v), C.byref(cid)), "mixtures_class")
+            a, bb = v.n1, v.n2
+            arr = lambda ptr, m: np.ctypeslib.as_array(ptr, shape=(m,)).copy()  # noqa: E731
+            classes.append({"id": cid.value.decode(), "weight": v.class_weight,
+                            "mu": arr(v.mu, 3 * a).reshape(-1, 3), "sigma2": arr(v.sigma2, a),
+                            "phi1": arr(v.phi1, a), "dir": arr(v.dir, 3 * bb).reshape(-1, 3),
+                            "kappa2": arr(v.kappa2, bb), "phi2": arr(v.phi2, bb)})
+        warnings = [lib.gosma_mixtures_warning(h, k).decode()
+                    for k in range(lib.gosma_mixtures_warning_count(h))]
+    finally:
+        lib.gosma_mixtures_destroy(h)
+    return classes, warnings

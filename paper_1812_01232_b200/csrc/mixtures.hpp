@@ -1,0 +1,67 @@
+// Mixture construction (host C++, off the hot path per the north star):
+// DP-means / DP-vMF-means clustering and the semantic mixture pair, following
+// core/src/mixtures.cpp:49-362 of the reference step for step (same visit
+// order, same floating-point expression order), so results are bit-identical.
+#pragma once
+
+#include <cstdint>
+#include <map>
+#include <optional>
+#include <string>
+#include <vector>
+
+#include "host_math.hpp"
+
+namespace gosma {
+namespace mix {
+
+struct Clustering {
+  std::vector<int> assignment;
+  std::vector<Vec3> centers;
+  std::vector<double> objective_history;
+};
+
+struct Gaussian {
+  Vec3 mean;
+  double variance;
+  double weight;
+};
+
+struct Vmf {
+  Vec3 direction;
+  double concentration;
+  double weight;
+};
+
+struct SemanticClass {
+  std::string id;
+  double weight = 1.0;
+  std::vector<Gaussian> gmm;
+  std::vector<Vmf> vmfmm;
+};
+
+struct SemanticMixturePair {
+  std::vector<SemanticClass> classes;
+  std::vector<std::string> warnings;
+};
+
+// UnitVector3(v) (unit_vector.hpp:16-23): accepts |v| within 1e-6 of 1 and
+// renormalises; throws std::invalid_argument otherwise.
+Vec3 unit_vector(const Vec3& v);
+
+Clustering dp_means(const std::vector<Vec3>& points, double lambda_p,
+                    std::optional<std::uint64_t> shuffle_seed = std::nullopt);
+Clustering dp_vmf_means(const std::vector<Vec3>& bearings, double lambda_f,
+                        std::optional<std::uint64_t> shuffle_seed = std::nullopt);
+std::vector<Gaussian> fit_gaussian_components(const std::vector<std::vector<Vec3>>& clusters,
+                                              double sigma2_min);
+std::vector<Vmf> fit_vmf_components(const std::vector<std::vector<Vec3>>& clusters,
+                                    double kappa_min = 1e-3, double kappa_max = 1e5);
+SemanticMixturePair build_semantic_mixtures(
+    const std::vector<Vec3>& points, const std::vector<std::string>& point_labels,
+    const std::vector<Vec3>& bearings, const std::vector<std::string>& bearing_labels,
+    double lambda_p, double lambda_f,
+    const std::optional<std::map<std::string, double>>& class_weights = std::nullopt);
+
+}  // namespace mix
+}  // namespace gosma
