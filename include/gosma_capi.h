@@ -236,6 +236,12 @@ const char* gosma_last_error(void);
 /* Build / device introspection for benches and tests. */
 int gosma_device_info(int device, int* sm_count, int* sm_clock_khz, int* cc_major,
                       int* cc_minor);
+/* Batched objective_value + objective_gradient (objective.cpp:175-334) on the
+ * GPU in FP64 (kernel K6, the local refiner's evaluator): poses = n x {r[3],
+ * t[3]}; f[n] (+inf where the pose is within zeta of a mean) and g[6n]
+ * ({d/dr, d/dt}, zero where infeasible). Synchronous. */
+int gosma_objective_batch(gosma_ctx* ctx, const double* poses, size_t n, double* f, double* g);
+
 /* ---- Mixture construction (host C++; mixtures.hpp:55-98) ------------------
  * Replaces smalign::build_semantic_mixtures (mixtures.cpp:269-362) and the
  * DP-means clusterers it uses (mixtures.cpp:49-182); bit-identical results. */

@@ -116,6 +116,7 @@ def _load():
     lib.gosma_solver_import.argtypes = [vp, vp, vp, vp, C.c_size_t]
     lib.gosma_solver_result.argtypes = [vp, C.POINTER(_Report)]
     lib.gosma_solver_live_volume.argtypes = [vp, _dp]
+    lib.gosma_objective_batch.argtypes = [vp, _dp, C.c_size_t, _dp, _dp]
     cpp = C.POINTER(C.c_char_p)
     lib.gosma_mixtures_build.argtypes = [_dp, cpp, C.c_size_t, _dp, cpp, C.c_size_t, C.c_double,
                                          C.c_double, cpp, _dp, C.c_size_t, C.POINTER(vp)]
@@ -330,6 +331,18 @@ def objective_value(ctx: ObjectiveContext, r, t) -> float:
     _check(lib.gosma_objective_value(ctx.handle, _f64(r).ctypes.data_as(_dp),
                                      _f64(t).ctypes.data_as(_dp), C.byref(v)), "objective_value")
     return v.value
+
+
+def objective_batch(ctx: ObjectiveContext, poses):
+    """objective_value + objective_gradient for n poses {r[3], t[3]} on the GPU
+    (FP64 batched kernel): (f[n], g[n, 6]); f = +inf where infeasible."""
+    x = _f64(poses).reshape(-1, 6)
+    f = np.empty(len(x))
+    g = np.empty((len(x), 6))
+    _check(lib.gosma_objective_batch(ctx.handle, x.ctypes.data_as(_dp), len(x),
+                                     f.ctypes.data_as(_dp), g.ctypes.data_as(_dp)),
+           "objective_batch")
+    return f, g
 
 
 def objective_gradient(ctx: ObjectiveContext, r, t) -> np.ndarray:

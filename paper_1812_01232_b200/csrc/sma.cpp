@@ -7,6 +7,8 @@
 // start.
 #include "sma.hpp"
 
+#include "objective_device.hpp"
+
 #include <algorithm>
 #include <cmath>
 #include <deque>
@@ -36,19 +38,50 @@ V6 axpy(const V6& x, double a, const V6& d) {
 Vec3 head(const V6& x) { return Vec3(x[0], x[1], x[2]); }
 Vec3 tail(const V6& x) { return Vec3(x[3], x[4], x[5]); }
 
-// objective with infeasible poses mapped to +inf (solver.cpp:37-43)
-double safe_value(const HostModel& m, const V6& x) { return objective_value(m, head(x), tail(x)); }
-
-V6 gradient(const HostModel& m, const V6& x) {
-  V6 g;
-  double gg[6];
-  if (!objective_gradient(m, head(x), tail(x), gg)) {
-    g.fill(0.0);
-    return g;
+// Objective with infeasible poses mapped to +inf (solver.cpp:37-43) and its
+// gradient (zero when infeasible), from the host model or the GPU batcher; the
+// GPU path returns value and gradient together, so the last point is cached.
+class Objective {
+ public:
+  explicit Objective(const SmaEval& ev) : ev_(ev) {}
+  const HostModel& model() const { return *ev_.m; }
+  double value(const V6& x) {
+    if (!ev_.gate) return objective_value(*ev_.m, head(x), tail(x));
+    fetch(x);
+    return f_;
   }
-  for (int k = 0; k < 6; ++k) g[k] = gg[k];
-  return g;
-}
+  V6 grad(const V6& x) {
+    if (!ev_.gate) {
+      V6 g;
+      double gg[6];
+      if (!objective_gradient(*ev_.m, head(x), tail(x), gg)) {
+        g.fill(0.0);
+        return g;
+      }
+      for (int k = 0; k < 6; ++k) g[k] = gg[k];
+      return g;
+    }
+    fetch(x);
+    return g_;
+  }
+
+ private:
+  void fetch(const V6& x) {
+    if (have_ && x == x_) return;
+    ObjRequest r{};
+    for (int k = 0; k < 6; ++k) r.x[k] = x[k];
+    r.model = ev_.model;
+    double gg[6];
+    ev_.gate->eval(r, &f_, gg);
+    for (int k = 0; k < 6; ++k) g_[k] = gg[k];
+    x_ = x;
+    have_ = true;
+  }
+  SmaEval ev_;
+  bool have_ = false;
+  V6 x_{}, g_{};
+  double f_ = 0.0;
+};
 
 // clamp_to_domain (solver.cpp:48-95)
 bool clamp_to_domain(const HostModel& m, const Domain& dom, V6* x) {
@@ -100,10 +133,10 @@ struct LineSearch {
 };
 
 // wolfe_search (solver.cpp:105-160)
-LineSearch wolfe(const HostModel& m, const V6& x, const V6& d, double f0, double g0) {
+LineSearch wolfe(Objective& m, const V6& x, const V6& d, double f0, double g0) {
   const double c1 = 1e-4, c2 = 0.9, alpha_max = 1e3;
-  auto phi = [&](double a) { return safe_value(m, axpy(x, a, d)); };
-  auto dphi = [&](double a) { return dot6(gradient(m, axpy(x, a, d)), d); };
+  auto phi = [&](double a) { return m.value(axpy(x, a, d)); };
+  auto dphi = [&](double a) { return dot6(m.grad(axpy(x, a, d)), d); };
   LineSearch best;
   auto consider = [&](double a, double v) {
     if (v <= f0 + c1 * a * g0 && v < best.value) {
@@ -147,18 +180,25 @@ LineSearch wolfe(const HostModel& m, const V6& x, const V6& d, double f0, double
 }  // namespace
 
 RefineResult local_refine(const HostModel& m, const Vec3& r0, const Vec3& t0, const Domain& dom) {
+  SmaEval ev;
+  ev.m = &m;
+  return local_refine(ev, r0, t0, dom);
+}
+
+RefineResult local_refine(const SmaEval& ev, const Vec3& r0, const Vec3& t0, const Domain& dom) {
+  Objective m(ev);
   const int kMaxIt = 200, kMem = 10;
   const double kGradTol = 1e-6;
   RefineResult best;
   V6 x = {r0[0], r0[1], r0[2], t0[0], t0[1], t0[2]};
-  best.value = safe_value(m, x);
+  best.value = m.value(x);
   best.r = r0;
   best.t = t0;
   if (!std::isfinite(best.value)) return best;
   auto offer = [&](const V6& xx, double fx) {
     V6 p = xx;
-    if (!clamp_to_domain(m, dom, &p)) return;
-    const double fp = (p == xx) ? fx : safe_value(m, p);
+    if (!clamp_to_domain(m.model(), dom, &p)) return;
+    const double fp = (p == xx) ? fx : m.value(p);
     if (fp < best.value) {
       best.value = fp;
       best.r = head(p);
@@ -167,7 +207,7 @@ RefineResult local_refine(const HostModel& m, const Vec3& r0, const Vec3& t0, co
   };
   double fx = best.value;
   offer(x, fx);
-  V6 g = gradient(m, x);
+  V6 g = m.grad(x);
   std::deque<V6> S, Y;
   std::deque<double> Rho;
   for (int it = 0; it < kMaxIt; ++it) {
@@ -200,7 +240,7 @@ RefineResult local_refine(const HostModel& m, const Vec3& r0, const Vec3& t0, co
     const LineSearch ls = wolfe(m, x, d, fx, dg);
     if (!(ls.alpha > 0.0) || !std::isfinite(ls.value)) break;
     const V6 xn = axpy(x, ls.alpha, d);
-    const V6 gn = gradient(m, xn);
+    const V6 gn = m.grad(xn);
     V6 s, y;
     for (int k = 0; k < 6; ++k) {
       s[k] = xn[k] - x[k];
@@ -227,7 +267,7 @@ RefineResult local_refine(const HostModel& m, const Vec3& r0, const Vec3& t0, co
       x[0] = w[0];
       x[1] = w[1];
       x[2] = w[2];
-      g = gradient(m, x);
+      g = m.grad(x);
       S.clear();
       Y.clear();
       Rho.clear();

@@ -17,12 +17,15 @@
 #include <chrono>
 #include <cmath>
 #include <limits>
+#include <memory>
 #include <mutex>
+#include <string>
 #include <thread>
 #include <vector>
 
 #include "capi_internal.hpp"
 #include "frontier.hpp"
+#include "objective_device.hpp"
 #include "sma.hpp"
 
 using namespace gosma;
@@ -82,9 +85,30 @@ struct Incumbent {
   unsigned long long sma = 0;
 };
 
+// Pair terms of a model (the refiner's cost per evaluation).
+size_t model_pairs(const HostModel& m) {
+  size_t p = 0;
+  for (const HostClass& c : m.classes)
+    p += static_cast<size_t>(c.n1()) * c.n2() + static_cast<size_t>(c.n1()) * (c.n1() - 1) / 2;
+  return p;
+}
+
+// Refinements run their objective on the GPU (batched FP64 kernel K6) once a
+// host evaluation gets expensive; GOSMA_SMA=host|gpu overrides.
+bool gpu_sma(const HostModel& m) {
+  static const int forced = [] {
+    const char* e = std::getenv("GOSMA_SMA");
+    if (!e) return -1;
+    return std::string(e) == "gpu" ? 1 : (std::string(e) == "host" ? 0 : -1);
+  }();
+  if (forced >= 0) return forced == 1;
+  return model_pairs(m) >= 512;
+}
+
 // process_wave's incumbent update (solver.cpp:409-431) for one improving
 // branch: FP64 objective at the feasible centre, then SMA from there.
-void improve(const HostModel& m, const Domain& dom, const gosma_node& b, Incumbent* inc) {
+void improve(const HostModel& m, const Domain& dom, const gosma_node& b, Incumbent* inc,
+             BatchGate* gate = nullptr) {
   Vec3 t;
   if (!feasible_center(m, Vec3(b.tc[0], b.tc[1], b.tc[2]), Vec3(b.thw[0], b.thw[1], b.thw[2]),
                        &t))
@@ -95,7 +119,11 @@ void improve(const HostModel& m, const Domain& dom, const gosma_node& b, Incumbe
   inc->value = f;
   inc->r = r;
   inc->t = t;
-  const RefineResult rr = local_refine(m, r, t, dom);
+  SmaEval ev;
+  ev.m = &m;
+  ev.gate = gate;
+  RefineResult rr = local_refine(ev, r, t, dom);
+  if (gate) rr.value = objective_value(m, rr.r, rr.t);  // d* is always the host FP64 value
   ++inc->sma;
   if (rr.value < inc->value) {
     inc->value = rr.value;
@@ -233,30 +261,61 @@ int discovery_dive(gosma_ctx* ctx, const Domain& dom, const std::vector<gosma_no
   const HostModel h1 = blurred_model(m, 0.01, dbar);
   std::vector<RefineResult> res(best.size());
   std::vector<char> ok(best.size(), 0);
-  std::atomic<size_t> next{0};
-  unsigned nthreads = cfg.threads > 0 ? cfg.threads : std::max(1u, std::thread::hardware_concurrency());
-  nthreads = std::min<unsigned>(nthreads, static_cast<unsigned>(best.size()));
-  auto work = [&] {
-    for (;;) {
-      const size_t s = next.fetch_add(1);
-      if (s >= best.size()) return;
-      if (!std::isfinite(best[s].value)) continue;
-      Vec3 t;
-      const gosma_node& b = best[s].b;
-      if (!feasible_center(hc, Vec3(b.tc[0], b.tc[1], b.tc[2]), Vec3(b.thw[0], b.thw[1], b.thw[2]),
-                           &t))
-        continue;
-      RefineResult r = local_refine(hc, Vec3(b.rc[0], b.rc[1], b.rc[2]), t, dom);
-      r = local_refine(h3, r.r, r.t, dom);
-      r = local_refine(h1, r.r, r.t, dom);
-      res[s] = local_refine(m, r.r, r.t, dom);
-      ok[s] = 1;
+  auto ladder = [&](size_t s, BatchGate* gate) {
+    if (!std::isfinite(best[s].value)) return;
+    Vec3 t;
+    const gosma_node& b = best[s].b;
+    if (!feasible_center(hc, Vec3(b.tc[0], b.tc[1], b.tc[2]), Vec3(b.thw[0], b.thw[1], b.thw[2]),
+                         &t))
+      return;
+    const HostModel* stage[4] = {&hc, &h3, &h1, &m};
+    RefineResult r;
+    r.r = Vec3(b.rc[0], b.rc[1], b.rc[2]);
+    r.t = t;
+    for (int k = 0; k < 4; ++k) {
+      SmaEval ev;
+      ev.m = stage[k];
+      ev.gate = gate;
+      ev.model = k;
+      r = local_refine(ev, r.r, r.t, dom);
     }
+    if (gate) r.value = objective_value(m, r.r, r.t);  // incumbents are host FP64 values
+    res[s] = r;
+    ok[s] = 1;
   };
-  std::vector<std::thread> pool;
-  for (unsigned k = 0; k + 1 < nthreads; ++k) pool.emplace_back(work);
-  work();
-  for (auto& th : pool) th.join();
+  std::unique_ptr<DeviceObjective> dobj;
+  if (gpu_sma(m)) {
+    dobj = std::make_unique<DeviceObjective>(ctx->device,
+                                             std::vector<const HostModel*>{&hc, &h3, &h1, &m});
+    if (!dobj->ok()) dobj.reset();
+  }
+  if (dobj) {
+    // one host thread per start; their evaluations share GPU launches
+    BatchGate gate(dobj.get(), static_cast<int>(best.size()));
+    std::vector<std::thread> pool;
+    for (size_t s = 0; s < best.size(); ++s)
+      pool.emplace_back([&, s] {
+        ladder(s, &gate);
+        gate.leave();
+      });
+    for (auto& th : pool) th.join();
+  } else {
+    std::atomic<size_t> next{0};
+    unsigned nthreads =
+        cfg.threads > 0 ? cfg.threads : std::max(1u, std::thread::hardware_concurrency());
+    nthreads = std::min<unsigned>(nthreads, static_cast<unsigned>(best.size()));
+    auto work = [&] {
+      for (;;) {
+        const size_t s = next.fetch_add(1);
+        if (s >= best.size()) return;
+        ladder(s, nullptr);
+      }
+    };
+    std::vector<std::thread> pool;
+    for (unsigned k = 0; k + 1 < nthreads; ++k) pool.emplace_back(work);
+    work();
+    for (auto& th : pool) th.join();
+  }
   for (size_t s = 0; s < best.size(); ++s) {
     if (!ok[s]) continue;
     inc->sma += 4;
@@ -310,6 +369,9 @@ struct gosma_solver {
   // translation-cached child bounds (GOSMA_FULL_KERNEL=1 selects the single
   // full kernel, for A/B measurements)
   bool cached = std::getenv("GOSMA_FULL_KERNEL") == nullptr;
+  // GPU objective for incumbent refinements (large mixtures, see gpu_sma)
+  std::unique_ptr<DeviceObjective> sma_dev;
+  std::unique_ptr<BatchGate> sma_gate;
   unsigned long long cuboid_evals = 0;
   // GOSMA_PROFILE=1: synchronising per-phase wall times, printed on destroy
   bool profile = std::getenv("GOSMA_PROFILE") != nullptr;
@@ -334,6 +396,14 @@ namespace {
 int solver_init(gosma_solver* S) {
   gosma_ctx* ctx = S->ctx;
   S->F.prof = S->profile;
+  if (gpu_sma(ctx->model)) {
+    S->sma_dev = std::make_unique<DeviceObjective>(
+        ctx->device, std::vector<const HostModel*>{&ctx->model});
+    if (S->sma_dev->ok())
+      S->sma_gate = std::make_unique<BatchGate>(S->sma_dev.get(), 1);
+    else
+      S->sma_dev.reset();
+  }
   const HostModel& m = ctx->model;
   const gosma_config& cfg = S->cfg;
   cudaStream_t s = ctx->stream;
@@ -382,7 +452,7 @@ int solver_init(gosma_solver* S) {
   S->wave_nodes =
       cfg.wave_nodes > 0
           ? static_cast<size_t>(cfg.wave_nodes)
-          : std::min<size_t>(std::max<size_t>(120000000 / std::max<size_t>(pairs, 1), 1024),
+          : std::min<size_t>(std::max<size_t>(300000000 / std::max<size_t>(pairs, 1), 1024),
                              1u << 19);
   cudaError_t e = S->F.reserve(std::max<size_t>(8 * S->wave_nodes, roots.size() * 2 + 16),
                                S->wave_nodes);
@@ -411,7 +481,7 @@ int solver_init(gosma_solver* S) {
     S->phase[7] += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   }
   for (size_t i = 0; i < roots.size(); ++i)
-    if (up[i] < S->inc.value) improve(m, S->dom, roots[i], &S->inc);
+    if (up[i] < S->inc.value) improve(m, S->dom, roots[i], &S->inc, S->sma_gate.get());
   std::vector<gosma_node> keep;
   std::vector<int8_t> ks;
   std::vector<double> kv;
@@ -602,7 +672,7 @@ int gosma_solver_expand(gosma_solver* S, double limit, unsigned long long max_ev
   if (bi >= 0 && bu < S->inc.value) {
     gosma_node b;
     cudaMemcpy(&b, S->F.kids + bi, sizeof(gosma_node), cudaMemcpyDeviceToHost);
-    improve(ctx->model, S->dom, b, &S->inc);
+    improve(ctx->model, S->dom, b, &S->inc, S->sma_gate.get());
   }
   S->lap(4, s);
   RouteStats rs;
@@ -658,6 +728,25 @@ int gosma_solver_import(gosma_solver* S, const gosma_node* nodes, const int8_t* 
   DeviceGuard g(S->ctx->device);
   const cudaError_t e = S->F.upload(nodes, split, vol, n, S->ctx->stream);
   if (e != cudaSuccess) return cuda_error(e, "import");
+  return GOSMA_OK;
+}
+
+int gosma_objective_batch(gosma_ctx* ctx, const double* poses, size_t n, double* f, double* g) {
+  if (!ctx) return set_error(GOSMA_EINVAL, "null context");
+  if (n == 0) return GOSMA_OK;
+  if (!poses || !f || !g) return set_error(GOSMA_EINVAL, "null buffer");
+  DeviceObjective dev(ctx->device, {&ctx->model});
+  if (!dev.ok()) return set_error(GOSMA_ECUDA, "objective kernel setup failed");
+  std::vector<ObjRequest> req(n);
+  for (size_t k = 0; k < n; ++k) {
+    for (int a = 0; a < 6; ++a) req[k].x[a] = poses[6 * k + a];
+    req[k].model = 0;
+  }
+  std::vector<double> fv, gv;
+  const cudaError_t e = dev.evaluate(req, &fv, &gv);
+  if (e != cudaSuccess) return cuda_error(e, "objective batch");
+  std::copy(fv.begin(), fv.end(), f);
+  std::copy(gv.begin(), gv.end(), g);
   return GOSMA_OK;
 }
 

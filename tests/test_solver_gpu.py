@@ -2,6 +2,7 @@
 (proj/tests/test_solver.cpp, test_bench.cpp) and golden runs of the
 unmodified reference (tests/golden/solver_golden.json)."""
 import math
+import os
 
 import numpy as np
 import pytest
@@ -218,3 +219,54 @@ def test_sharded_driver_over_nccl_world1(gosma):
         assert abs(rep.best_value - gosma.solve(ctx, dom, cfg).best_value) <= 1e-9
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n1,n2,ncls", [(5, 4, 1), (40, 24, 1), (20, 12, 3)])
+def test_gpu_objective_batch_matches_host_fp64(gosma, n1, n2, ncls):
+    """K6 (batched FP64 objective + gradient, the refiner's GPU evaluator)
+    against the host FP64 objective_value / objective_gradient."""
+    from paper_1812_01232_b200 import synth
+    classes = synth.mixture(n1, n2, "moderate", seed=n1 + 3 * n2, kappa_cap=150.0,
+                            n_classes=ncls)
+    ctx = gosma.ObjectiveContext(classes, 0.5)
+    rng = np.random.default_rng(n1)
+    poses = np.concatenate([rng.uniform(-2.5, 2.5, (200, 3)), rng.uniform(-4, 4, (200, 3))], 1)
+    poses[:5, 3:] = ctx.all_means[:5] + 0.01  # inside a standoff ball: infeasible
+    f, g = gosma.objective_batch(ctx, poses)
+    for k, p in enumerate(poses):
+        try:
+            fh = gosma.objective_value(ctx, p[:3], p[3:])
+            gh = gosma.objective_gradient(ctx, p[:3], p[3:])
+        except gosma.InfeasiblePoseError:
+            assert math.isinf(f[k]) and np.all(g[k] == 0.0)
+            continue
+        assert abs(f[k] - fh) <= 1e-10 * (1.0 + abs(fh)), (k, f[k], fh)
+        assert np.all(np.abs(g[k] - gh) <= 1e-8 * (1.0 + np.abs(gh).max())), (k, g[k], gh)
+
+
+def test_gpu_refiner_matches_host_refiner(gosma):
+    """The discovery dive's SMA ladder on the GPU evaluator (auto for large
+    mixtures) reaches the same incumbent as the host refiner (GOSMA_SMA=host,
+    run in a subprocess: the switch is read once per process)."""
+    import json
+    import subprocess
+    import sys
+    code = r"""
+import json, numpy as np, paper_1812_01232_b200 as g
+from paper_1812_01232_b200 import synth
+cls = synth.mixture(40, 24, "moderate", seed=9, kappa_cap=150.0)
+ctx = g.ObjectiveContext(cls, 0.5)
+dom = g.PoseDomain(np.zeros(3), 1.0, np.array([[0.0, 0.0, -3.0, 0.5, 0.5, 0.5]]))
+r = g.solve(ctx, dom, g.SolverConfig(epsilon=0.01, zeta=0.5, time_limit=0.0))
+print(json.dumps({"v": r.best_value, "r": list(r.r), "t": list(r.t), "sma": r.sma_invocations}))
+"""
+    out = {}
+    for mode in ("gpu", "host"):
+        env = dict(os.environ, GOSMA_SMA=mode)
+        p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                           cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                           timeout=600)
+        assert p.returncode == 0, p.stderr[-2000:]
+        out[mode] = json.loads(p.stdout.strip().splitlines()[-1])
+    assert out["gpu"]["sma"] == out["host"]["sma"] > 0
+    assert abs(out["gpu"]["v"] - out["host"]["v"]) <= 1e-7 * (1.0 + abs(out["host"]["v"]))
