@@ -779,8 +779,12 @@ int gosma_solve(gosma_ctx* ctx, const gosma_domain* domain, const gosma_config* 
                 gosma_report* report, gosma_trace_cb trace, void* user) {
   if (!report) return set_error(GOSMA_EINVAL, "null argument");
   gosma_solver* S = nullptr;
+  const auto tc0 = std::chrono::steady_clock::now();
   int rc = gosma_solver_create(ctx, domain, config, 0, 1, &S);
   if (rc != GOSMA_OK) return rc;
+  if (S->profile)
+    std::fprintf(stderr, "[gosma profile] create %.3fs\n",
+                 std::chrono::duration<double>(std::chrono::steady_clock::now() - tc0).count());
   const gosma_config& cfg = *config;
   double certified = -kInf;
   int status = GOSMA_STATUS_QUEUE_EXHAUSTED;
@@ -828,7 +832,12 @@ int gosma_solve(gosma_ctx* ctx, const gosma_domain* domain, const gosma_config* 
   report->global_lower = certified;
   report->gap = report->best_value - certified;
   report->status = status;
+  const auto td0 = std::chrono::steady_clock::now();
+  const bool prof = S->profile;
   gosma_solver_destroy(S);
+  if (prof)
+    std::fprintf(stderr, "[gosma profile] destroy %.3fs\n",
+                 std::chrono::duration<double>(std::chrono::steady_clock::now() - td0).count());
   return status == GOSMA_STATUS_TIME_LIMIT ? GOSMA_EBUDGET : GOSMA_OK;
 }
 
