@@ -19,6 +19,7 @@
 #include <chrono>
 #include <cstdint>
 #include <cstring>
+#include <mutex>
 
 #include "frontier.hpp"
 
@@ -27,6 +28,41 @@ namespace gosma {
 namespace {
 
 constexpr int kBins = 4096;
+
+// Frontier buffers come from the device's stream-ordered pool (cudaMallocAsync)
+// with a release threshold, so a solver's multi-GB pool is recycled by the
+// next solve instead of being unmapped and remapped (cudaFree of tens of GB
+// costs tenths of a second). Allocation is synchronised before first use and
+// a free waits for the device, as cudaFree would.
+void ensure_pool_retention() {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) return;
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    unsigned long long keep = total_b / 3;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  });
+}
+
+template <typename T>
+cudaError_t dmalloc(T** p, size_t bytes) {
+  ensure_pool_retention();
+  void* v = nullptr;
+  cudaError_t e = cudaMallocAsync(&v, bytes, 0);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(0);
+  *p = static_cast<T*>(v);
+  return e;
+}
+
+void dfree(void* p) {
+  if (!p) return;
+  cudaDeviceSynchronize();  // like cudaFree: no kernel on any stream still uses p
+  cudaFreeAsync(p, 0);
+}
 
 __host__ __device__ __forceinline__ unsigned long long order_key_bits(unsigned long long b) {
   return (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
@@ -360,50 +396,50 @@ double key_to_double(unsigned long long k) {
 cudaError_t Frontier::reserve(size_t cap_nodes, size_t wave) {
   cudaError_t e = cudaSuccess;
   if (cap_nodes > cap) {
-    if ((e = cudaMalloc(&nodes, cap_nodes * sizeof(gosma_node))) != cudaSuccess) return e;
-    if ((e = cudaMalloc(&split, cap_nodes)) != cudaSuccess) return e;
-    if ((e = cudaMalloc(&vol, cap_nodes * sizeof(double))) != cudaSuccess) return e;
-    if ((e = cudaMalloc(&key, cap_nodes * 8)) != cudaSuccess) return e;
+    if ((e = dmalloc(&nodes, cap_nodes * sizeof(gosma_node))) != cudaSuccess) return e;
+    if ((e = dmalloc(&split, cap_nodes)) != cudaSuccess) return e;
+    if ((e = dmalloc(&vol, cap_nodes * sizeof(double))) != cudaSuccess) return e;
+    if ((e = dmalloc(&key, cap_nodes * 8)) != cudaSuccess) return e;
     cap = cap_nodes;
   }
   if (wave > sel_cap) {
-    cudaFree(sel);
-    cudaFree(tcnt);
-    cudaFree(toff);
-    if ((e = cudaMalloc(&sel, wave * 4)) != cudaSuccess) return e;
-    if ((e = cudaMalloc(&tcnt, (wave + 1) * 4)) != cudaSuccess) return e;
-    if ((e = cudaMalloc(&toff, (wave + 1) * 4)) != cudaSuccess) return e;
+    dfree(sel);
+    dfree(tcnt);
+    dfree(toff);
+    if ((e = dmalloc(&sel, wave * 4)) != cudaSuccess) return e;
+    if ((e = dmalloc(&tcnt, (wave + 1) * 4)) != cudaSuccess) return e;
+    if ((e = dmalloc(&toff, (wave + 1) * 4)) != cudaSuccess) return e;
     sel_cap = wave;
   }
   const size_t nk = wave * 8;
   if (nk > kid_cap) {
-    cudaFree(kids);
-    cudaFree(kid_lower);
-    cudaFree(kid_upper);
-    cudaFree(kid_split);
-    cudaFree(kid_vol);
-    cudaFree(keep);
-    cudaFree(kept_idx);
-    cudaFree(tidx);
-    cudaFree(tnodes);
-    cudaFree(tself);
-    if ((e = cudaMalloc(&tidx, nk * 4)) != cudaSuccess) return e;
-    if ((e = cudaMalloc(&tnodes, nk * sizeof(gosma_node))) != cudaSuccess) return e;
-    if ((e = cudaMalloc(&tself, nk * 4 * sizeof(double))) != cudaSuccess) return e;
-    if ((e = cudaMalloc(&kids, nk * sizeof(gosma_node))) != cudaSuccess) return e;
-    if ((e = cudaMalloc(&kid_lower, nk * 8)) != cudaSuccess) return e;
-    if ((e = cudaMalloc(&kid_upper, nk * 8)) != cudaSuccess) return e;
-    if ((e = cudaMalloc(&kid_split, nk)) != cudaSuccess) return e;
-    if ((e = cudaMalloc(&kid_vol, nk * 8)) != cudaSuccess) return e;
-    if ((e = cudaMalloc(&keep, nk * 4)) != cudaSuccess) return e;
-    if ((e = cudaMalloc(&kept_idx, nk * 4)) != cudaSuccess) return e;
+    dfree(kids);
+    dfree(kid_lower);
+    dfree(kid_upper);
+    dfree(kid_split);
+    dfree(kid_vol);
+    dfree(keep);
+    dfree(kept_idx);
+    dfree(tidx);
+    dfree(tnodes);
+    dfree(tself);
+    if ((e = dmalloc(&tidx, nk * 4)) != cudaSuccess) return e;
+    if ((e = dmalloc(&tnodes, nk * sizeof(gosma_node))) != cudaSuccess) return e;
+    if ((e = dmalloc(&tself, nk * 4 * sizeof(double))) != cudaSuccess) return e;
+    if ((e = dmalloc(&kids, nk * sizeof(gosma_node))) != cudaSuccess) return e;
+    if ((e = dmalloc(&kid_lower, nk * 8)) != cudaSuccess) return e;
+    if ((e = dmalloc(&kid_upper, nk * 8)) != cudaSuccess) return e;
+    if ((e = dmalloc(&kid_split, nk)) != cudaSuccess) return e;
+    if ((e = dmalloc(&kid_vol, nk * 8)) != cudaSuccess) return e;
+    if ((e = dmalloc(&keep, nk * 4)) != cudaSuccess) return e;
+    if ((e = dmalloc(&kept_idx, nk * 4)) != cudaSuccess) return e;
     kid_cap = nk;
   }
   if (!stats) {
-    if ((e = cudaMalloc(&stats, sizeof(RouteStats))) != cudaSuccess) return e;
-    if ((e = cudaMalloc(&amin, sizeof(ArgMin))) != cudaSuccess) return e;
-    if ((e = cudaMalloc(&counter, 2 * sizeof(unsigned long long))) != cudaSuccess) return e;
-    if ((e = cudaMalloc(&hist, kBins * sizeof(unsigned int))) != cudaSuccess) return e;
+    if ((e = dmalloc(&stats, sizeof(RouteStats))) != cudaSuccess) return e;
+    if ((e = dmalloc(&amin, sizeof(ArgMin))) != cudaSuccess) return e;
+    if ((e = dmalloc(&counter, 2 * sizeof(unsigned long long))) != cudaSuccess) return e;
+    if ((e = dmalloc(&hist, kBins * sizeof(unsigned int))) != cudaSuccess) return e;
     if ((e = cudaMallocHost(&h_stats, sizeof(RouteStats))) != cudaSuccess) return e;
     if ((e = cudaMallocHost(&h_amin, sizeof(ArgMin))) != cudaSuccess) return e;
     if ((e = cudaMallocHost(&h_counter, 2 * sizeof(unsigned long long))) != cudaSuccess) return e;
@@ -413,44 +449,44 @@ cudaError_t Frontier::reserve(size_t cap_nodes, size_t wave) {
 }
 
 void Frontier::release() {
-  cudaFree(nodes);
-  cudaFree(split);
-  cudaFree(vol);
-  cudaFree(key);
-  cudaFree(sel);
-  cudaFree(hist);
-  cudaFree(kids);
-  cudaFree(kid_lower);
-  cudaFree(kid_upper);
-  cudaFree(kid_split);
-  cudaFree(kid_vol);
-  cudaFree(keep);
-  cudaFree(kept_idx);
-  cudaFree(tcnt);
-  cudaFree(toff);
-  cudaFree(tidx);
-  cudaFree(tnodes);
-  cudaFree(tself);
+  dfree(nodes);
+  dfree(split);
+  dfree(vol);
+  dfree(key);
+  dfree(sel);
+  dfree(hist);
+  dfree(kids);
+  dfree(kid_lower);
+  dfree(kid_upper);
+  dfree(kid_split);
+  dfree(kid_vol);
+  dfree(keep);
+  dfree(kept_idx);
+  dfree(tcnt);
+  dfree(toff);
+  dfree(tidx);
+  dfree(tnodes);
+  dfree(tself);
   tcnt = toff = nullptr;
   tidx = nullptr;
   tnodes = nullptr;
   tself = nullptr;
-  cudaFree(bsel);
+  dfree(bsel);
   bsel = nullptr;
   bsel_cap = 0;
-  cudaFree(cidx);
+  dfree(cidx);
   cidx = nullptr;
   cidx_cap = 0;
-  cudaFree(cand);
-  cudaFree(cand_tmp);
+  dfree(cand);
+  dfree(cand_tmp);
   cand = cand_tmp = nullptr;
   cand_n = cand_cap = 0;
   tau = 0;
   known_min = 0;
-  cudaFree(stats);
-  cudaFree(amin);
-  cudaFree(counter);
-  cudaFree(temp);
+  dfree(stats);
+  dfree(amin);
+  dfree(counter);
+  dfree(temp);
   cudaFreeHost(h_stats);
   cudaFreeHost(h_amin);
   cudaFreeHost(h_counter);
@@ -478,10 +514,10 @@ void Frontier::release() {
 
 cudaError_t Frontier::ensure_temp(size_t bytes) {
   if (bytes <= temp_bytes) return cudaSuccess;
-  cudaFree(temp);
+  dfree(temp);
   temp = nullptr;
   bytes = std::max(bytes, temp_bytes + temp_bytes / 2);  // geometric growth
-  const cudaError_t e = cudaMalloc(&temp, bytes);
+  const cudaError_t e = dmalloc(&temp, bytes);
   if (e == cudaSuccess) temp_bytes = bytes;
   return e;
 }
@@ -496,10 +532,10 @@ cudaError_t Frontier::grow(size_t need, cudaStream_t s) {
   double* v2 = nullptr;
   unsigned long long* k2 = nullptr;
   cudaError_t e;
-  if ((e = cudaMalloc(&n2, c * sizeof(gosma_node))) != cudaSuccess) return e;
-  if ((e = cudaMalloc(&s2, c)) != cudaSuccess) return e;
-  if ((e = cudaMalloc(&v2, c * sizeof(double))) != cudaSuccess) return e;
-  if ((e = cudaMalloc(&k2, c * 8)) != cudaSuccess) return e;
+  if ((e = dmalloc(&n2, c * sizeof(gosma_node))) != cudaSuccess) return e;
+  if ((e = dmalloc(&s2, c)) != cudaSuccess) return e;
+  if ((e = dmalloc(&v2, c * sizeof(double))) != cudaSuccess) return e;
+  if ((e = dmalloc(&k2, c * 8)) != cudaSuccess) return e;
   if (size) {
     cudaMemcpyAsync(n2, nodes, size * sizeof(gosma_node), cudaMemcpyDeviceToDevice, s);
     cudaMemcpyAsync(s2, split, size, cudaMemcpyDeviceToDevice, s);
@@ -507,10 +543,10 @@ cudaError_t Frontier::grow(size_t need, cudaStream_t s) {
     cudaMemcpyAsync(k2, key, size * 8, cudaMemcpyDeviceToDevice, s);
   }
   if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
-  cudaFree(nodes);
-  cudaFree(split);
-  cudaFree(vol);
-  cudaFree(key);
+  dfree(nodes);
+  dfree(split);
+  dfree(vol);
+  dfree(key);
   nodes = n2;
   split = s2;
   vol = v2;
@@ -649,11 +685,11 @@ cudaError_t Frontier::rebuild_candidates(size_t want_total, cudaStream_t s) {
   const size_t count = below > 0 ? below : bin;
   const size_t cap_need = count + 16 * std::max<size_t>(sel_cap, 1);
   if (cap_need > cand_cap) {
-    cudaFree(cand);
-    cudaFree(cand_tmp);
+    dfree(cand);
+    dfree(cand_tmp);
     cand = cand_tmp = nullptr;
-    if ((e = cudaMalloc(&cand, cap_need * 4)) != cudaSuccess) return e;
-    if ((e = cudaMalloc(&cand_tmp, cap_need * 4)) != cudaSuccess) return e;
+    if ((e = dmalloc(&cand, cap_need * 4)) != cudaSuccess) return e;
+    if ((e = dmalloc(&cand_tmp, cap_need * 4)) != cudaSuccess) return e;
     cand_cap = cap_need;
   }
   if (count) {
@@ -734,10 +770,10 @@ cudaError_t Frontier::select_smallest(size_t want, unsigned long long limit, cud
   if (n1 < want && hi_key > lo_key && bin_count > 0) {
     n2 = std::min(want - n1, bin_count);
     if (bin_count > bsel_cap) {
-      cudaFree(bsel);
+      dfree(bsel);
       bsel = nullptr;
       const size_t c = std::max(bin_count, 2 * bsel_cap);
-      if ((e = cudaMalloc(&bsel, c * 4)) != cudaSuccess) return e;
+      if ((e = dmalloc(&bsel, c * 4)) != cudaSuccess) return e;
       bsel_cap = c;
     }
     KeyBelow p2{key, lo_key, hi_key};
@@ -895,9 +931,9 @@ cudaError_t Frontier::compact(unsigned long long limit, cudaStream_t s, double* 
   const size_t m = size - live;
   if (live > 0 && m > 0) {
     if (2 * m > cidx_cap) {
-      cudaFree(cidx);
+      dfree(cidx);
       cidx = nullptr;
-      if ((e = cudaMalloc(&cidx, 2 * m * 4)) != cudaSuccess) return e;
+      if ((e = dmalloc(&cidx, 2 * m * 4)) != cudaSuccess) return e;
       cidx_cap = 2 * m;
     }
     cub::CountingInputIterator<unsigned int> it(0);
