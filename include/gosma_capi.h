@@ -236,6 +236,11 @@ const char* gosma_last_error(void);
 /* Build / device introspection for benches and tests. */
 int gosma_device_info(int device, int* sm_count, int* sm_clock_khz, int* cc_major,
                       int* cc_minor);
+/* Frontier memory comes from the device's stream-ordered pool and is kept
+ * (up to a third of the device memory) for the next solve; this returns the
+ * cached, unused part to the driver. */
+int gosma_release_cached_memory(int device);
+
 /* Batched objective_value + objective_gradient (objective.cpp:175-334) on the
  * GPU in FP64 (kernel K6, the local refiner's evaluator): poses = n x {r[3],
  * t[3]}; f[n] (+inf where the pose is within zeta of a mean) and g[6n]

@@ -117,6 +117,7 @@ def _load():
     lib.gosma_solver_result.argtypes = [vp, C.POINTER(_Report)]
     lib.gosma_solver_live_volume.argtypes = [vp, _dp]
     lib.gosma_objective_batch.argtypes = [vp, _dp, C.c_size_t, _dp, _dp]
+    lib.gosma_release_cached_memory.argtypes = [C.c_int]
     cpp = C.POINTER(C.c_char_p)
     lib.gosma_mixtures_build.argtypes = [_dp, cpp, C.c_size_t, _dp, cpp, C.c_size_t, C.c_double,
                                          C.c_double, cpp, _dp, C.c_size_t, C.POINTER(vp)]
@@ -331,6 +332,11 @@ def objective_value(ctx: ObjectiveContext, r, t) -> float:
     _check(lib.gosma_objective_value(ctx.handle, _f64(r).ctypes.data_as(_dp),
                                      _f64(t).ctypes.data_as(_dp), C.byref(v)), "objective_value")
     return v.value
+
+
+def release_cached_memory(device: int = 0):
+    """Returns the solver's cached frontier memory (stream-ordered pool) to the driver."""
+    _check(lib.gosma_release_cached_memory(device), "release_cached_memory")
 
 
 def objective_batch(ctx: ObjectiveContext, poses):

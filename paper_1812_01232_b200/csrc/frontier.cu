@@ -1002,3 +1002,15 @@ cudaError_t Frontier::fold_to(size_t keep_n, cudaStream_t s, double* folded_volu
 }
 
 }  // namespace gosma
+
+extern "C" int gosma_release_cached_memory(int device) {
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) != cudaSuccess) return GOSMA_ECUDA;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  cudaSetDevice(device);
+  cudaDeviceSynchronize();
+  const cudaError_t e = cudaMemPoolTrimTo(pool, 0);
+  cudaSetDevice(cur);
+  return e == cudaSuccess ? GOSMA_OK : GOSMA_ECUDA;
+}
