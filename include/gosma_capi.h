@@ -92,6 +92,19 @@ double gosma_ctx_zeta(const gosma_ctx* ctx);
  * for parity diagnostics only. */
 int gosma_ctx_set_lb_margin(gosma_ctx* ctx, double rel_margin);
 
+/* Branch + bound in one call (the solver's wave step): the 8 children of each
+ * parent, subdivide_adaptive (se3.cpp:107-147) with the given split flags
+ * (d_split[i] = 1 rotation, 0 translation: the flag gosma_eval_bounds returns
+ * for the parent), are bounded; child c of parent i is slot 8i+c of d_lower /
+ * d_upper / d_child_split. Rotation-split parents evaluate their cuboid's
+ * prologue and self sums once for all 8 children. Children inherit the
+ * parent's lower field as their floor. Device pointers, asynchronous on
+ * `stream`; results equal gosma_eval_bounds_device on the explicit children
+ * to 1e-12 of the |term| mass. */
+int gosma_eval_children_device(gosma_ctx* ctx, const gosma_node* d_parents, const int8_t* d_split,
+                               size_t n, double skip_upper_at, double* d_lower, double* d_upper,
+                               int8_t* d_child_split, void* stream);
+
 /* Replaces evaluate_branch_batch(ctx, branches, threads, skip_upper_at)
  * (core/include/smalign/solver.hpp:87-95, core/src/solver.cpp:260-292) and,
  * per element, evaluate_bounds (core/src/bounds.cpp:275-284). Host buffers;

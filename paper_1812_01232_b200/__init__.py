@@ -117,6 +117,8 @@ def _load():
     lib.gosma_solver_result.argtypes = [vp, C.POINTER(_Report)]
     lib.gosma_solver_live_volume.argtypes = [vp, _dp]
     lib.gosma_objective_batch.argtypes = [vp, _dp, C.c_size_t, _dp, _dp]
+    lib.gosma_eval_children_device.argtypes = [vp, vp, vp, C.c_size_t, C.c_double, vp, vp, vp,
+                                               vp]
     lib.gosma_release_cached_memory.argtypes = [C.c_int]
     cpp = C.POINTER(C.c_char_p)
     lib.gosma_mixtures_build.argtypes = [_dp, cpp, C.c_size_t, _dp, cpp, C.c_size_t, C.c_double,
@@ -324,6 +326,16 @@ def evaluate_branch_batch_cached_device(ctx, d_nodes_ptr, n, d_tindex_ptr, d_tbo
                                                d_lower_ptr, d_upper_ptr, d_split_ptr or None,
                                                stream or None),
            "evaluate_branch_batch_cached_device")
+
+
+def evaluate_children_device(ctx, d_parents_ptr, d_split_ptr, n, d_lower_ptr, d_upper_ptr,
+                             d_child_split_ptr=0, skip_upper_at=float("inf"), stream=0):
+    """Branch + bound: bounds of the 8 subdivide_adaptive children of each
+    parent (slot 8i+c), rotation-split parents sharing their cuboid work."""
+    _check(lib.gosma_eval_children_device(ctx.handle, d_parents_ptr, d_split_ptr, n,
+                                          float(skip_upper_at), d_lower_ptr, d_upper_ptr,
+                                          d_child_split_ptr or None, stream or None),
+           "evaluate_children_device")
 
 
 def objective_value(ctx: ObjectiveContext, r, t) -> float:

@@ -482,8 +482,62 @@ __device__ __forceinline__ void psi_trans_half(double u0, double u1, double u2, 
 
 // kMode: kModeFull = every term per node; kSelfOnly = per distinct translation
 // cuboid, the translation-only (self + diagonal) sums; kCrossCached = per node,
-// the cross terms plus the cached self sums of the node's cuboid.
-enum { kModeFull = 0, kSelfOnly = 1, kCrossCached = 2 };
+// the cross terms plus the cached self sums of the node's cuboid; kSiblings =
+// per rotation-split parent: the cuboid prologue and self sums once, then the
+// cross sums of its 8 children (subdivide_adaptive, se3.cpp:124-131).
+enum { kModeFull = 0, kSelfOnly = 1, kCrossCached = 2, kSiblings = 3 };
+
+// Rodrigues R0 = rotation_matrix(rc) (se3.cpp:21-31), FP64.
+__device__ __forceinline__ void rodrigues(double rc0, double rc1, double rc2, double R[9]) {
+  const double th2 = rc0 * rc0 + rc1 * rc1 + rc2 * rc2;
+  double a, c;
+  if (th2 < 1e-16) {
+    a = 1.0;
+    c = 0.5;
+  } else {
+    const double th = sqrt(th2);
+    double s, co;
+    sincos(th, &s, &co);
+    a = s / th;
+    c = (1.0 - co) / th2;
+  }
+  const double K[9] = {0.0, -rc2, rc1, rc2, 0.0, -rc0, -rc1, rc0, 0.0};
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int cix = 0; cix < 3; ++cix) {
+      const double k2 = K[3 * r] * K[cix] + K[3 * r + 1] * K[3 + cix] + K[3 * r + 2] * K[6 + cix];
+      R[3 * r + cix] = ((r == cix ? 1.0 : 0.0) + a * K[3 * r + cix]) + c * k2;
+    }
+}
+
+// Half-angle of psi_t + psi_r per row (B = 0 once the sum reaches pi) from the
+// FP64 psi_t half-angles: the rotation-dependent row fields.
+__device__ __forceinline__ void half_angles(double st, double ct, double s_r, double c_r,
+                                            double& sp, double& cp) {
+  sp = st * c_r + ct * s_r;
+  cp = ct * c_r - st * s_r;
+  if (!(cp > 0.0)) {
+    sp = 1.0;
+    cp = 0.0;
+  }
+}
+
+// q_j = R0^T m_j (bounds.cpp:97-102), double-float columns.
+__device__ __forceinline__ void column_prep(const WarpTables& T, const DevCtx& ctx, int lane,
+                                            int step, const double R[9]) {
+  for (int j = lane; j < ctx.n2_total; j += step) {
+    const double x0 = ctx.m[3 * j], x1 = ctx.m[3 * j + 1], x2 = ctx.m[3 * j + 2];
+    const double q0 = R[0] * x0 + R[3] * x1 + R[6] * x2;
+    const double q1 = R[1] * x0 + R[4] * x1 + R[7] * x2;
+    const double q2 = R[2] * x0 + R[5] * x1 + R[8] * x2;
+    const float f0 = static_cast<float>(q0), f1 = static_cast<float>(q1),
+                f2 = static_cast<float>(q2);
+    T.col[j * kColF4] = make_float4(f0, f1, f2, ctx.kappa2[j]);
+    T.col[j * kColF4 + 1] = make_float4(static_cast<float>(q0 - f0), static_cast<float>(q1 - f1),
+                                        static_cast<float>(q2 - f2), ctx.g2[j]);
+  }
+}
 
 #ifndef GOSMA_MIN_BLOCKS
 #define GOSMA_MIN_BLOCKS 7
@@ -498,11 +552,12 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
   const unsigned gm = kG == 32 ? kFull : (((1u << kG) - 1u) << gbase);
   const int group = static_cast<int>(threadIdx.x) / kG;
   const int N1 = ctx.n1_total, N2 = ctx.n2_total;
-  const size_t per_warp_f4 = static_cast<size_t>(kRowF4 * N1 + kColF4 * N2);
+  const size_t per_warp_f4 = static_cast<size_t>((kRowF4 + 1) * N1 + kColF4 * N2);
   float4* base = smem4 + group * per_warp_f4;
   WarpTables T;
   T.row = base;
   T.col = base + kRowF4 * N1;
+  double2* stct = reinterpret_cast<double2*>(T.col + kColF4 * N2);  // FP64 psi_t half-angles
 
   const double zeta = ctx.zeta;
   const double zeta2 = zeta * zeta;
@@ -511,6 +566,15 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
     if (lane == 0) node = static_cast<long long>(atomicAdd(args.work, 1u));
     node = __shfl_sync(gm, node, 0, kG);
     if (node >= args.n) break;
+    // item lists: full mode over a subset (node = slot); siblings: the item
+    // is a selection index k, the parent the pool slot sel[k], the outputs
+    // are children 8k .. 8k+7
+    long long item = node;
+    if (args.item_index) node = args.item_index[node];
+    if (kMode == kSiblings) {
+      item = node;
+      node = args.sel[node];
+    }
 
     // ---- node fetch (gosma_node: rc[3], rhw, tc[3], thw[3], lower)
     double v = 0.0, v2 = 0.0;
@@ -548,32 +612,12 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
 
     // ---- rotation: R0 = rotation_matrix(rc) (se3.cpp:21-31), psi_r (se3.cpp:68-70)
     double R[9];
-    {
-      const double th2 = rc0 * rc0 + rc1 * rc1 + rc2 * rc2;
-      double a, c;
-      if (th2 < 1e-16) {
-        a = 1.0;
-        c = 0.5;
-      } else {
-        const double th = sqrt(th2);
-        double s, co;
-        sincos(th, &s, &co);
-        a = s / th;
-        c = (1.0 - co) / th2;
-      }
-      const double K[9] = {0.0, -rc2, rc1, rc2, 0.0, -rc0, -rc1, rc0, 0.0};
-#pragma unroll
-      for (int r = 0; r < 3; ++r)
-#pragma unroll
-        for (int cix = 0; cix < 3; ++cix) {
-          const double k2 =
-              K[3 * r] * K[cix] + K[3 * r + 1] * K[3 + cix] + K[3 * r + 2] * K[6 + cix];
-          R[3 * r + cix] = ((r == cix ? 1.0 : 0.0) + a * K[3 * r + cix]) + c * k2;
-        }
+    double s_r = 0.0, c_r = 1.0;
+    if (kMode != kSiblings) {
+      rodrigues(rc0, rc1, rc2, R);
+      const double psi_r = fmin(sqrt(3.0) * rhw, M_PI);
+      sincos(0.5 * psi_r, &s_r, &c_r);
     }
-    const double psi_r = fmin(sqrt(3.0) * rhw, M_PI);
-    double s_r, c_r;
-    sincos(0.5 * psi_r, &s_r, &c_r);
 
     // ---- feasible_center (bounds.cpp:187-214): t*, warp-cooperative scan
     double ts0 = tc0, ts1 = tc1, ts2 = tc2;
@@ -662,13 +706,9 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
           psi_trans_half(u0, u1, u2, h0, h1, h2, c0, c1, c2, st, ct);
         }
         st_max = fmax(st_max, st);
-        // half-angle of psi_t + psi_r; B = 0 once the sum reaches pi
-        double sp = st * c_r + ct * s_r;
-        double cp = ct * c_r - st * s_r;
-        if (!(cp > 0.0)) {
-          sp = 1.0;
-          cp = 0.0;
-        }
+        stct[i] = make_double2(st, ct);
+        double sp, cp;
+        half_angles(st, ct, s_r, c_r, sp, cp);
         // UB projection at t* (project_model, objective.cpp:175-192)
         const double v0 = m0 - ts0, v1 = m1 - ts1, v2 = m2 - ts2;
         const double vn2 = v0 * v0 + v1 * v1 + v2 * v2;
@@ -702,6 +742,99 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
 #pragma unroll
     for (int o = kG / 2; o > 0; o >>= 1)
       st_max = fmax(st_max, __shfl_xor_sync(gm, st_max, o, kG));
+    if constexpr (kMode == kSiblings) {
+      // one cuboid, 8 rotation children: self sums once, then per child
+      const double hr = 0.5 * rhw;
+      const bool trans_ok = fmax(fmax(h0, h1), h2) > 1e-9;
+      double sl_self = lb_self, su_self = ub_self, se_self = lb_err;
+      if (!infeasible) {
+        __syncwarp(gm);
+        for (int c = 0; c < ctx.n_classes; ++c) {
+          const ClassSpan cs = ctx.cls[c];
+          const float w = static_cast<float>(ctx.cls_w[c]);
+          double dl = 0.0, du = 0.0;
+          if (same) {
+            class_pairs<kG, true, false, true>(T, cs, lane, w, sl_self, dl, su_self, du, se_self);
+          } else {
+            class_pairs<kG, false, false, true>(T, cs, lane, w, sl_self, dl, su_self, du,
+                                                se_self);
+          }
+        }
+        sl_self = group_sum_d<kG>(gm, sl_self);
+        su_self = group_sum_d<kG>(gm, su_self);
+        se_self = group_sum_d<kG>(gm, se_self);
+      }
+      for (int ch = 0; ch < 8; ++ch) {
+        const long long slot = 8 * item + ch;
+        const int sx = (ch & 4) ? 1 : -1, sy = (ch & 2) ? 1 : -1, sz = (ch & 1) ? 1 : -1;
+        // the child exactly as the expand kernel builds it (k.rc[a] += h * s)
+        const double crc0 = rc0 + hr * sx, crc1 = rc1 + hr * sy, crc2 = rc2 + hr * sz;
+        const double psi_c = fmin(sqrt(3.0) * hr, M_PI);
+        double cs_r, cc_r;
+        sincos(0.5 * psi_c, &cs_r, &cc_r);
+        if (lane == 0 && args.split_rot) {
+          const bool rot_ok = hr > 1e-9;
+          int8_t sr;
+          if (!rot_ok && !trans_ok) {
+            sr = -1;
+          } else {
+            sr = (rot_ok && (!trans_ok || cs_r >= st_max)) ? 1 : 0;
+          }
+          args.split_rot[slot] = sr;
+        }
+        if (infeasible) {
+          if (lane == 0) {
+            args.lower[slot] = INFINITY;
+            args.upper[slot] = INFINITY;
+          }
+          continue;
+        }
+        double Rc[9];
+        rodrigues(crc0, crc1, crc2, Rc);
+        __syncwarp(gm);
+        for (int c = 0; c < ctx.n_classes; ++c) {
+          const ClassSpan cs = ctx.cls[c];
+          for (int il = lane; il < cs.n1; il += kG) {
+            const int i = cs.o1 + il;
+            const double2 sc = stct[i];
+            double sp, cp;
+            half_angles(sc.x, sc.y, cs_r, cc_r, sp, cp);
+            float4* pr = T.row + i * kRowF4;
+            pr[2].z = static_cast<float>(sp);
+            pr[2].w = static_cast<float>(cp);
+            pr[4].w = static_cast<float>(4.0 * sp * sp);
+          }
+        }
+        column_prep(T, ctx, lane, kG, Rc);
+        __syncwarp(gm);
+        double lcr = 0.0, ucr = 0.0, ecr = 0.0, dl = 0.0, du = 0.0;
+        for (int c = 0; c < ctx.n_classes; ++c) {
+          const ClassSpan cs = ctx.cls[c];
+          const float w = static_cast<float>(ctx.cls_w[c]);
+          if (same) {
+            class_pairs<kG, true, true, false>(T, cs, lane, w, dl, lcr, du, ucr, ecr);
+          } else {
+            class_pairs<kG, false, true, false>(T, cs, lane, w, dl, lcr, du, ucr, ecr);
+          }
+        }
+        lcr = group_sum_d<kG>(gm, lcr);
+        ucr = group_sum_d<kG>(gm, ucr);
+        ecr = group_sum_d<kG>(gm, ecr);
+        if (lane == 0) {
+          const double mass = sl_self + 2.0 * lcr;
+          const double core = (sl_self - 2.0 * lcr) - ctx.lb_err_scale * (se_self + ecr) -
+                              ctx.lb_margin * mass;
+          const double lo = core < parent_lower ? parent_lower : core;
+          double up = INFINITY;
+          if (!(lo >= args.skip_upper_at) && have_center) up = su_self - 2.0 * ucr;
+          args.lower[slot] = lo;
+          args.upper[slot] = up;
+        }
+        __syncwarp(gm);
+      }
+      __syncwarp(gm);
+      continue;
+    }
     if (kMode != kSelfOnly && lane == 0 && args.split_rot) {
       const bool rot_ok = rhw > 1e-9;
       const bool trans_ok = fmax(fmax(h0, h1), h2) > 1e-9;
@@ -728,17 +861,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
       continue;
     }
     // ---- per-column prep: q_j = R0^T m_j (bounds.cpp:97-102), double-float
-    for (int j = lane; kMode != kSelfOnly && j < N2; j += kG) {
-      const double x0 = ctx.m[3 * j], x1 = ctx.m[3 * j + 1], x2 = ctx.m[3 * j + 2];
-      const double q0 = R[0] * x0 + R[3] * x1 + R[6] * x2;
-      const double q1 = R[1] * x0 + R[4] * x1 + R[7] * x2;
-      const double q2 = R[2] * x0 + R[5] * x1 + R[8] * x2;
-      const float f0 = static_cast<float>(q0), f1 = static_cast<float>(q1),
-                  f2 = static_cast<float>(q2);
-      T.col[j * kColF4] = make_float4(f0, f1, f2, ctx.kappa2[j]);
-      T.col[j * kColF4 + 1] = make_float4(static_cast<float>(q0 - f0), static_cast<float>(q1 - f1),
-                            static_cast<float>(q2 - f2), ctx.g2[j]);
-    }
+    if (kMode != kSelfOnly) column_prep(T, ctx, lane, kG, R);
     __syncwarp(gm);
 
     // ---- pair sweeps (GOSMA_PREP_ONLY: times the per-node prep alone)
@@ -797,7 +920,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
 }  // namespace
 
 size_t eval_smem_per_warp(const DevCtx& ctx) {
-  const size_t f4 = static_cast<size_t>(kRowF4 * ctx.n1_total + kColF4 * ctx.n2_total);
+  const size_t f4 = static_cast<size_t>((kRowF4 + 1) * ctx.n1_total + kColF4 * ctx.n2_total);
   return f4 * sizeof(float4);
 }
 
@@ -878,6 +1001,11 @@ cudaError_t launch_eval_cross_cached(const DevCtx& ctx, const EvalArgs& a, int s
   return launch_mode<kCrossCached>(ctx, a, sm_count, stream);
 }
 
+cudaError_t launch_eval_siblings(const DevCtx& ctx, const EvalArgs& a, int sm_count,
+                                 cudaStream_t stream) {
+  return launch_mode<kSiblings>(ctx, a, sm_count, stream);
+}
+
 
 unsigned long long bound_kernel_launch_count() { return g_launches.load(); }
 
@@ -896,6 +1024,58 @@ __global__ void boxes_to_nodes(const double* boxes, size_t n, gosma_node* out) {
   out[i] = b;
 }
 }  // namespace
+
+namespace {
+// subdivide_adaptive children (se3.cpp:107-147) of n parents with the given
+// split flags (1 rotation, 0 translation, -1 none: children = copies), and the
+// work lists of the siblings / full kernels (order irrelevant).
+__global__ void children_of(const gosma_node* parents, const int8_t* split, size_t n,
+                            gosma_node* kids, int* rot, int* trans_kids, int* counts) {
+  const size_t t = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+  if (t >= 8 * n) return;
+  const size_t p = t / 8;
+  const int c = static_cast<int>(t % 8);
+  const int sx = (c & 4) ? 1 : -1, sy = (c & 2) ? 1 : -1, sz = (c & 1) ? 1 : -1;
+  gosma_node k = parents[p];
+  if (split[p] == 1) {
+    const double h = 0.5 * k.rhw;
+    k.rc[0] += h * sx;
+    k.rc[1] += h * sy;
+    k.rc[2] += h * sz;
+    k.rhw = h;
+    if (c == 0) rot[atomicAdd(&counts[0], 1)] = static_cast<int>(p);
+  } else {
+    if (split[p] == 0) {
+      const double h0 = 0.5 * k.thw[0], h1 = 0.5 * k.thw[1], h2 = 0.5 * k.thw[2];
+      k.tc[0] += h0 * sx;
+      k.tc[1] += h1 * sy;
+      k.tc[2] += h2 * sz;
+      k.thw[0] = h0;
+      k.thw[1] = h1;
+      k.thw[2] = h2;
+    }
+    trans_kids[atomicAdd(&counts[1], 1)] = static_cast<int>(t);
+  }
+  kids[t] = k;
+}
+
+__global__ void identity_sel(unsigned int* sel, size_t n) {
+  const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+  if (i < n) sel[i] = static_cast<unsigned int>(i);
+}
+}  // namespace
+
+cudaError_t make_children(const gosma_node* d_parents, const int8_t* d_split, size_t n,
+                          gosma_node* d_kids, int* d_rot, int* d_trans, int* d_counts,
+                          unsigned int* d_sel, cudaStream_t stream) {
+  if (n == 0) return cudaSuccess;
+  cudaError_t e = cudaMemsetAsync(d_counts, 0, 2 * sizeof(int), stream);
+  if (e != cudaSuccess) return e;
+  children_of<<<static_cast<unsigned>((8 * n + 255) / 256), 256, 0, stream>>>(
+      d_parents, d_split, n, d_kids, d_rot, d_trans, d_counts);
+  identity_sel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(d_sel, n);
+  return cudaGetLastError();
+}
 
 cudaError_t boxes_as_nodes(const double* d_boxes, size_t n, gosma_node* d_out,
                            cudaStream_t stream) {

@@ -137,6 +137,13 @@ void ctx_free_device(gosma_ctx* ctx) {
   ctx->d_cache_nodes = nullptr;
   ctx->d_cache_self = nullptr;
   ctx->cache_cap = 0;
+  cudaFree(ctx->d_child_kids);
+  cudaFree(ctx->d_child_lists);
+  cudaFree(ctx->d_child_sel);
+  ctx->d_child_kids = nullptr;
+  ctx->d_child_lists = nullptr;
+  ctx->d_child_sel = nullptr;
+  ctx->child_cap = 0;
   ctx->scratch.release();
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   if (ctx->h2d_stream) cudaStreamDestroy(ctx->h2d_stream);
@@ -365,6 +372,64 @@ int gosma_eval_bounds_device(gosma_ctx* ctx, const gosma_node* d_nodes, size_t n
   a.work = static_cast<unsigned int*>(ctx->d_work);
   const cudaError_t e = launch_eval_bounds(ctx->dev, a, ctx->sm_count, s);
   if (e != cudaSuccess) return cuda_error(e, "eval_bounds launch");
+  return GOSMA_OK;
+}
+
+int gosma_eval_children_device(gosma_ctx* ctx, const gosma_node* d_parents, const int8_t* d_split,
+                               size_t n, double skip, double* d_lower, double* d_upper,
+                               int8_t* d_child_split, void* stream) {
+  if (!ctx) return set_error(GOSMA_EINVAL, "null context");
+  if (n == 0) return GOSMA_OK;
+  if (!d_parents || !d_split || !d_lower || !d_upper) return set_error(GOSMA_EINVAL, "null buffer");
+  DeviceGuard g(ctx->device);
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+  cudaError_t e;
+  if (n > ctx->child_cap) {
+    cudaFree(ctx->d_child_kids);
+    cudaFree(ctx->d_child_lists);
+    cudaFree(ctx->d_child_sel);
+    ctx->d_child_kids = nullptr;
+    ctx->d_child_lists = nullptr;
+    ctx->d_child_sel = nullptr;
+    if ((e = cudaMalloc(&ctx->d_child_kids, 8 * n * sizeof(gosma_node))) != cudaSuccess ||
+        (e = cudaMalloc(&ctx->d_child_lists, (9 * n + 2) * sizeof(int))) != cudaSuccess ||
+        (e = cudaMalloc(&ctx->d_child_sel, n * sizeof(unsigned int))) != cudaSuccess)
+      return cuda_error(e, "children alloc");
+    ctx->child_cap = n;
+  }
+  int* rot = ctx->d_child_lists;
+  int* trans = rot + n;
+  int* counts = trans + 8 * n;
+  if ((e = make_children(d_parents, d_split, n, ctx->d_child_kids, rot, trans, counts,
+                         ctx->d_child_sel, s)) != cudaSuccess)
+    return cuda_error(e, "children");
+  int h[2] = {0, 0};
+  if ((e = cudaMemcpyAsync(h, counts, sizeof(h), cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
+      (e = cudaStreamSynchronize(s)) != cudaSuccess)
+    return cuda_error(e, "children counts");
+  EvalArgs a;
+  a.skip_upper_at = skip;
+  a.lower = d_lower;
+  a.upper = d_upper;
+  a.split_rot = d_child_split;
+  a.work = static_cast<unsigned int*>(ctx->d_work);
+  if (h[0]) {
+    EvalArgs b = a;
+    b.nodes = reinterpret_cast<const double*>(d_parents);
+    b.n = h[0];
+    b.item_index = rot;
+    b.sel = ctx->d_child_sel;
+    if ((e = launch_eval_siblings(ctx->dev, b, ctx->sm_count, s)) != cudaSuccess)
+      return cuda_error(e, "siblings kernel");
+  }
+  if (h[1]) {
+    EvalArgs c = a;
+    c.nodes = reinterpret_cast<const double*>(ctx->d_child_kids);
+    c.n = h[1];
+    c.item_index = trans;
+    if ((e = launch_eval_bounds(ctx->dev, c, ctx->sm_count, s)) != cudaSuccess)
+      return cuda_error(e, "children kernel");
+  }
   return GOSMA_OK;
 }
 

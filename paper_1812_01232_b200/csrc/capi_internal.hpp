@@ -54,6 +54,10 @@ struct gosma_ctx {
   gosma_node* d_cache_nodes = nullptr;  // translation-cached mode scratch
   double* d_cache_self = nullptr;
   size_t cache_cap = 0;
+  gosma_node* d_child_kids = nullptr;  // gosma_eval_children_device scratch
+  int* d_child_lists = nullptr;
+  unsigned int* d_child_sel = nullptr;
+  size_t child_cap = 0;
   cudaStream_t stream = nullptr;
   // host-buffer pipeline (gosma_eval_bounds): copy-in / copy-out streams and
   // per-slot events (H2D done, kernel done, D2H done) x 2 slots

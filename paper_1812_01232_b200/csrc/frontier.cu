@@ -185,6 +185,21 @@ __global__ void expand(const gosma_node* front, const int8_t* split, const doubl
   }
 }
 
+// Work lists of a wave: rotation-split parents (siblings kernel) and the
+// children of translation-split parents (full kernel). Order is irrelevant:
+// every item writes its own output slots.
+__global__ void split_lists(const int8_t* split, const unsigned int* sel, size_t n_sel,
+                            int* rot, int* trans_kids, int* counts) {
+  const size_t k = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+  if (k >= n_sel) return;
+  if (split[sel[k]] == 1) {
+    rot[atomicAdd(&counts[0], 1)] = static_cast<int>(k);
+  } else {
+    const int b = atomicAdd(&counts[1], 8);
+    for (int c = 0; c < 8; ++c) trans_kids[b + c] = static_cast<int>(8 * k + c);
+  }
+}
+
 __global__ void cuboid_counts(const int8_t* split, const unsigned int* sel, size_t n_sel,
                               unsigned int* cnt) {
   const size_t k = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
@@ -406,6 +421,10 @@ cudaError_t Frontier::reserve(size_t cap_nodes, size_t wave) {
     dfree(sel);
     dfree(tcnt);
     dfree(toff);
+    dfree(rot_list);
+    dfree(trans_list);
+    if ((e = dmalloc(&rot_list, wave * 4)) != cudaSuccess) return e;
+    if ((e = dmalloc(&trans_list, wave * 8 * 4)) != cudaSuccess) return e;
     if ((e = dmalloc(&sel, wave * 4)) != cudaSuccess) return e;
     if ((e = dmalloc(&tcnt, (wave + 1) * 4)) != cudaSuccess) return e;
     if ((e = dmalloc(&toff, (wave + 1) * 4)) != cudaSuccess) return e;
@@ -440,6 +459,7 @@ cudaError_t Frontier::reserve(size_t cap_nodes, size_t wave) {
     if ((e = dmalloc(&amin, sizeof(ArgMin))) != cudaSuccess) return e;
     if ((e = dmalloc(&counter, 2 * sizeof(unsigned long long))) != cudaSuccess) return e;
     if ((e = dmalloc(&hist, kBins * sizeof(unsigned int))) != cudaSuccess) return e;
+    if ((e = dmalloc(&list_counts, 2 * sizeof(int))) != cudaSuccess) return e;
     if ((e = cudaMallocHost(&h_stats, sizeof(RouteStats))) != cudaSuccess) return e;
     if ((e = cudaMallocHost(&h_amin, sizeof(ArgMin))) != cudaSuccess) return e;
     if ((e = cudaMallocHost(&h_counter, 2 * sizeof(unsigned long long))) != cudaSuccess) return e;
@@ -473,6 +493,10 @@ void Frontier::release() {
   tself = nullptr;
   dfree(bsel);
   bsel = nullptr;
+  dfree(rot_list);
+  dfree(trans_list);
+  dfree(list_counts);
+  rot_list = trans_list = list_counts = nullptr;
   bsel_cap = 0;
   dfree(cidx);
   cidx = nullptr;
@@ -808,6 +832,23 @@ cudaError_t Frontier::expand_selected(size_t n_sel, cudaStream_t s) {
   if (n_sel == 0) return cudaSuccess;
   expand<<<grid_for(n_sel * 8, 256), 256, 0, s>>>(nodes, split, vol, sel, n_sel, kids, kid_vol,
                                                    nullptr, nullptr, nullptr);
+  return cudaGetLastError();
+}
+
+cudaError_t Frontier::wave_lists(size_t n_sel, cudaStream_t s, size_t* n_rot, size_t* n_trans) {
+  *n_rot = *n_trans = 0;
+  if (n_sel == 0) return cudaSuccess;
+  cudaError_t e = cudaMemsetAsync(list_counts, 0, 2 * sizeof(int), s);
+  if (e != cudaSuccess) return e;
+  split_lists<<<grid_for(n_sel, 256), 256, 0, s>>>(split, sel, n_sel, rot_list, trans_list,
+                                                    list_counts);
+  if ((e = cudaMemcpyAsync(h_counter, list_counts, 2 * sizeof(int), cudaMemcpyDeviceToHost, s)) !=
+      cudaSuccess)
+    return e;
+  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+  const int* c = reinterpret_cast<const int*>(h_counter);
+  *n_rot = static_cast<size_t>(c[0]);
+  *n_trans = static_cast<size_t>(c[1]);
   return cudaGetLastError();
 }
 

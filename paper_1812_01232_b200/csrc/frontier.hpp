@@ -78,6 +78,9 @@ struct Frontier {
   int* tidx = nullptr;           // child -> cuboid slot
   gosma_node* tnodes = nullptr;  // cuboid slots (translation part used)
   double* tself = nullptr;       // 4 doubles per cuboid: self LB, self UB, err, flag
+  int* rot_list = nullptr;       // selection indices with a rotation split
+  int* trans_list = nullptr;     // children 8k+c of translation-split selections
+  int* list_counts = nullptr;
   // reductions / scratch
   RouteStats* stats = nullptr;
   ArgMin* amin = nullptr;
@@ -106,6 +109,8 @@ struct Frontier {
   cudaError_t select_smallest(size_t want, unsigned long long limit, cudaStream_t s, size_t* n);
   cudaError_t expand_selected(size_t n_sel, cudaStream_t s);
   cudaError_t expand_selected_cached(size_t n_sel, cudaStream_t s, size_t* n_cuboids);
+  // rotation-split selections (rot_list) and translation-split children (trans_list)
+  cudaError_t wave_lists(size_t n_sel, cudaStream_t s, size_t* n_rot, size_t* n_trans);
   cudaError_t best_child(size_t n_kids, cudaStream_t s, int* index, double* value);
   // route children against d*, append survivors
   cudaError_t route_append(size_t n_kids, double dstar, cudaStream_t s, RouteStats* out);

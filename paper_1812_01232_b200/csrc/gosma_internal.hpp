@@ -74,6 +74,8 @@ struct EvalArgs {
   // translation-cached modes: per-cuboid {lb_self, ub_self, lb_err, flag}
   double* self_out = nullptr;
   const int32_t* tindex = nullptr;  // node -> cuboid (cross-cached mode)
+  const int* item_index = nullptr;  // optional work list: item -> node slot (or selection k)
+  const unsigned int* sel = nullptr;  // siblings mode: selection k -> pool slot
 };
 
 cudaError_t launch_eval_bounds(const DevCtx& ctx, const EvalArgs& a, int sm_count,
@@ -81,11 +83,18 @@ cudaError_t launch_eval_bounds(const DevCtx& ctx, const EvalArgs& a, int sm_coun
 // Translation-cached evaluation: self sums once per cuboid (a.nodes are the
 // cuboids as nodes, a.self_out receives 4 doubles each), then cross terms per
 // node with a.tindex mapping nodes to cuboids.
+// Rotation-split parents (item_index = selection indices k, sel = pool slots):
+// writes the bounds and split flags of children 8k .. 8k+7.
+cudaError_t launch_eval_siblings(const DevCtx& ctx, const EvalArgs& a, int sm_count,
+                                 cudaStream_t stream);
 cudaError_t launch_eval_self(const DevCtx& ctx, const EvalArgs& a, int sm_count,
                              cudaStream_t stream);
 cudaError_t launch_eval_cross_cached(const DevCtx& ctx, const EvalArgs& a, int sm_count,
                                      cudaStream_t stream);
 size_t eval_smem_per_warp(const DevCtx& ctx);
+cudaError_t make_children(const gosma_node* d_parents, const int8_t* d_split, size_t n,
+                          gosma_node* d_kids, int* d_rot, int* d_trans, int* d_counts,
+                          unsigned int* d_sel, cudaStream_t stream);
 cudaError_t boxes_as_nodes(const double* d_boxes, size_t n, gosma_node* d_out,
                            cudaStream_t stream);
 unsigned long long bound_kernel_launch_count();

@@ -366,9 +366,18 @@ struct gosma_solver {
   double floor_lower = kInf;
   unsigned long long evals = 0, expanded = 0, wave = 0;
   size_t wave_nodes = 0, qcap = 0, mem_cap = 0;
-  // translation-cached child bounds (GOSMA_FULL_KERNEL=1 selects the single
-  // full kernel, for A/B measurements)
-  bool cached = std::getenv("GOSMA_FULL_KERNEL") == nullptr;
+  // child bounds per wave: 2 = siblings (a rotation-split parent's cuboid
+  // prologue + self sums once, cross sums per child; translation-split
+  // children with the full kernel), 1 = translation-cached (self kernel per
+  // distinct cuboid + cross kernel per child), 0 = full kernel per child.
+  // GOSMA_WAVE_MODE=full|cached|siblings selects (A/B measurements).
+  int wave_mode = [] {
+    const char* e = std::getenv("GOSMA_WAVE_MODE");
+    if (!e) return 2;
+    const std::string m(e);
+    return m == "full" ? 0 : (m == "cached" ? 1 : 2);
+  }();
+  bool cached = wave_mode == 1;
   // GPU objective for incumbent refinements (large mixtures, see gpu_sma)
   std::unique_ptr<DeviceObjective> sma_dev;
   std::unique_ptr<BatchGate> sma_gate;
@@ -660,9 +669,29 @@ int gosma_solver_expand(gosma_solver* S, double limit, unsigned long long max_ev
   a.lower = S->F.kid_lower;
   a.upper = S->F.kid_upper;
   a.split_rot = S->F.kid_split;
-  if ((e = (S->cached ? launch_eval_cross_cached(ctx->dev, a, ctx->sm_count, s)
-                      : launch_eval_bounds(ctx->dev, a, ctx->sm_count, s))) != cudaSuccess)
+  if (S->wave_mode == 2) {
+    size_t n_rot = 0, n_trans = 0;
+    if ((e = S->F.wave_lists(n_sel, s, &n_rot, &n_trans)) != cudaSuccess)
+      return cuda_error(e, "wave lists");
+    S->lap(2, s);
+    EvalArgs b = a;
+    b.nodes = reinterpret_cast<const double*>(S->F.nodes);  // the parents, in the pool
+    b.n = static_cast<long long>(n_rot);
+    b.item_index = S->F.rot_list;
+    b.sel = S->F.sel;
+    if (n_rot && (e = launch_eval_siblings(ctx->dev, b, ctx->sm_count, s)) != cudaSuccess)
+      return cuda_error(e, "eval siblings");
+    EvalArgs c = a;
+    c.n = static_cast<long long>(n_trans);
+    c.item_index = S->F.trans_list;
+    if (n_trans && (e = launch_eval_bounds(ctx->dev, c, ctx->sm_count, s)) != cudaSuccess)
+      return cuda_error(e, "eval children");
+    S->cuboid_evals += n_rot + n_trans;
+  } else if ((e = (S->cached ? launch_eval_cross_cached(ctx->dev, a, ctx->sm_count, s)
+                             : launch_eval_bounds(ctx->dev, a, ctx->sm_count, s))) !=
+             cudaSuccess) {
     return cuda_error(e, "eval children");
+  }
   S->lap(3, s);
   S->evals += n_kids;
   S->expanded += n_sel;

@@ -417,3 +417,52 @@ def test_host_pipeline_matches_device_path(gosma):
     assert np.array_equal(lo, d_lo.cpu().numpy())
     assert np.array_equal(up, d_up.cpu().numpy())
     assert np.array_equal(sp, d_sp.cpu().numpy())
+
+
+@pytest.mark.parametrize("n1,n2,ncls", [(64, 32, 1), (12, 12, 1), (7, 5, 2), (40, 33, 1)])
+def test_children_branch_and_bound_equals_explicit_children(gosma, n1, n2, ncls):
+    """gosma_eval_children_device (siblings kernel for rotation splits, full
+    kernel for translation splits) equals subdivide_adaptive + the plain bound
+    kernel on the explicit children, with the parent's floor inherited."""
+    import torch
+    from paper_1812_01232_b200 import synth
+    classes = synth.mixture(n1, n2, "realistic", seed=n1 * 7 + n2, n_classes=ncls)
+    ctx = gosma.ObjectiveContext(classes, 0.5)
+    parents = synth.nodes(1500, seed=n2).view(np.float64).reshape(-1, 11).copy()
+    plo, _, psplit = gosma.evaluate_branch_batch(ctx, parents, return_split=True)
+    ok = np.isfinite(plo) & (psplit >= 0)
+    parents, psplit, plo = parents[ok], psplit[ok], plo[ok]
+    parents[:, 10] = plo  # children inherit the parent's bound as their floor
+    assert (psplit == 1).any() and (psplit == 0).any()
+    n = len(parents)
+    # explicit children with the kernel's split flags (se3.cpp:124-145 order)
+    kids = np.repeat(parents, 8, axis=0)
+    for c in range(8):
+        sgn = np.array([1 if c & 4 else -1, 1 if c & 2 else -1, 1 if c & 1 else -1], float)
+        rot = psplit == 1
+        h = 0.5 * parents[:, 3]
+        kids[c::8, 0:3] = np.where(rot[:, None], parents[:, 0:3] + h[:, None] * sgn,
+                                   parents[:, 0:3])
+        kids[c::8, 3] = np.where(rot, h, parents[:, 3])
+        ht = 0.5 * parents[:, 7:10]
+        kids[c::8, 4:7] = np.where(rot[:, None], parents[:, 4:7], parents[:, 4:7] + ht * sgn)
+        kids[c::8, 7:10] = np.where(rot[:, None], parents[:, 7:10], ht)
+    klo, kup, ksp = gosma.evaluate_branch_batch(ctx, kids, return_split=True)
+    d_par = torch.from_numpy(np.ascontiguousarray(parents).view(np.uint8).reshape(-1)).cuda()
+    d_sp = torch.from_numpy(psplit.astype(np.int8)).cuda()
+    d_lo = torch.empty(8 * n, dtype=torch.float64, device="cuda")
+    d_up = torch.empty_like(d_lo)
+    d_cs = torch.empty(8 * n, dtype=torch.int8, device="cuda")
+    s = torch.cuda.Stream()
+    gosma.evaluate_children_device(ctx, d_par.data_ptr(), d_sp.data_ptr(), n, d_lo.data_ptr(),
+                                   d_up.data_ptr(), d_cs.data_ptr(), float("inf"), s.cuda_stream)
+    s.synchronize()
+    lo, up, cs = d_lo.cpu().numpy(), d_up.cpu().numpy(), d_cs.cpu().numpy()
+    assert np.array_equal(np.isinf(lo), np.isinf(klo))
+    f = np.isfinite(klo)
+    scale = np.abs(klo[f]) + np.abs(kup[f]) + 1.0
+    assert np.all(np.abs(lo[f] - klo[f]) <= 1e-12 * scale)
+    fu = np.isfinite(kup)
+    assert np.array_equal(fu, np.isfinite(up))
+    assert np.all(np.abs(up[fu] - kup[fu]) <= 1e-12 * (np.abs(kup[fu]) + 1.0))
+    assert np.array_equal(cs, ksp)
