@@ -278,7 +278,7 @@ class ObjectiveContext:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and lib is not None:  # lib is None during interpreter shutdown
             lib.gosma_ctx_destroy(h)
             self._h = None
 
@@ -529,7 +529,7 @@ class ShardSolver:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and lib is not None:
             lib.gosma_solver_destroy(h)
             self._h = None
 
