@@ -18,7 +18,9 @@ __all__ = [
     "GosmaError", "InfeasiblePoseError", "ObjectiveContext", "NODE_DTYPE", "make_nodes",
     "evaluate_branch_batch", "evaluate_bounds", "objective_value", "objective_gradient",
     "SolverConfig", "SolverReport", "PoseDomain", "solve", "local_refine", "lib", "library_path",
-    "kernel_launches",
+    "kernel_launches", "evaluate_branch_batch_device", "evaluate_branch_batch_cached_device",
+    "evaluate_children_device", "objective_batch", "ShardSolver", "build_semantic_mixtures",
+    "dp_means", "dp_vmf_means", "release_cached_memory", "calibrate_pipes", "device_info",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
