@@ -372,7 +372,7 @@ __device__ __forceinline__ Row load_row(const WarpTables& T, int i) {
 }
 
 template <int kG, bool kSame, bool kCross, bool kSelf>
-__device__ __forceinline__ void class_pairs(const WarpTables& T, const ClassSpan cs, int lane,
+__device__ __forceinline__ void class_pairs_rows(const WarpTables& T, const ClassSpan cs, int lane,
                                             float w, double& lb_self, double& lb_cross,
                                             double& ub_self, double& ub_cross, double& lb_err) {
   const int n = cs.n1;
@@ -430,6 +430,91 @@ __device__ __forceinline__ void class_pairs(const WarpTables& T, const ClassSpan
       lb_err += static_cast<double>(2.0f * w * a1.y * fmaf(me, kErrExp, l * kErrTerm));
       ub_self += static_cast<double>(2.0f * w * a2.y * u);
     }
+  }
+}
+
+// Variant for classes whose last row chunk is partial: that chunk of r rows
+// gives each row k = kG / r lanes ("slots") sharing its partners round-robin
+// (the node sums are sums over pairs, so any pair -> lane assignment is
+// exact). Separate instantiation: the plain loops stay tighter for full chunks.
+template <int kG, bool kSame, bool kCross, bool kSelf>
+__device__ __forceinline__ void class_pairs_tail(const WarpTables& T, const ClassSpan cs,
+                                                 int lane, float w, double& lb_self,
+                                                 double& lb_cross, double& ub_self,
+                                                 double& ub_cross, double& lb_err) {
+  const int n = cs.n1;
+  // cross terms: columns broadcast (slot s takes columns s, s+k, ...)
+  for (int base = 0; kCross && base < n; base += kG) {
+    const int r = min(kG, n - base), k = kG / r;
+    const int il = base + lane % r, slot = lane / r;
+    if (lane < r * k) {
+      const Row rw = load_row(T, cs.o1 + il);
+      float l = 0.0f, u = 0.0f, ma = 0.0f, mb = 0.0f;
+      const float4* cp = T.col + (cs.o2 + slot) * kColF4;
+      const float4* const ce = T.col + (cs.o2 + cs.n2) * kColF4;
+      const int cstep = k * kColF4;
+#pragma unroll 2
+      for (; cp < ce; cp += cstep) cross_pair<kSame>(rw, cp[0], cp[1], l, u, ma, mb);
+      lb_cross += static_cast<double>(w * rw.Fhi * l);
+      lb_err += static_cast<double>(
+          2.0f * w * rw.Fhi * fmaf(ma, kErrAmp, fmaf(mb, kErrExp, l * kErrTerm)));
+      ub_cross += static_cast<double>(w * rw.Fst * u);
+    }
+  }
+  // self terms: circulant (i, i+d mod n); slot s takes d = 1+s, 1+s+k, ...,
+  // slot 0 the half-way pair of an even n
+  const int dfull = (n - 1) / 2;
+  const bool even = (n % 2) == 0;
+  for (int base = 0; kSelf && base < n; base += kG) {
+    const int r = min(kG, n - base), k = kG / r;
+    const int il = base + lane % r, slot = lane / r;
+    if (lane < r * k) {
+      const int i = cs.o1 + il;
+      const float4* pa = T.row + i * kRowF4;
+      const float4 a0 = pa[0], a1 = pa[1], a2 = pa[2], av3 = pa[3];
+      float3 a3 = make_float3(0.f, 0.f, 0.f);
+      if (!kSame) a3 = make_float3(pa[4].x, pa[4].y, pa[4].z);
+      const float3 al = make_float3(av3.x, av3.y, av3.z);
+      float l = 0.0f, u = 0.0f, me = 0.0f;
+      int jl = il + 1 + slot - k;  // partner row il + d (mod n) after each step
+#pragma unroll 2
+      for (int d = 1 + slot; d <= dfull; d += k) {
+        jl += k;
+        if (jl >= n) jl -= n;
+        const int j = cs.o1 + jl;
+        float3 b3 = make_float3(0.f, 0.f, 0.f);
+        const float4* pb = T.row + j * kRowF4;
+        if (!kSame) b3 = make_float3(pb[4].x, pb[4].y, pb[4].z);
+        const float4 bl = pb[3];
+        self_pair<kSame>(a0, a1, a2, a3, al, pb[0], pb[1], pb[2], b3,
+                         make_float3(bl.x, bl.y, bl.z), l, u, me);
+      }
+      if (even && slot == 0 && il < n / 2) {
+        const int j = i + n / 2;
+        float3 b3 = make_float3(0.f, 0.f, 0.f);
+        const float4* pb = T.row + j * kRowF4;
+        if (!kSame) b3 = make_float3(pb[4].x, pb[4].y, pb[4].z);
+        const float4 bl = pb[3];
+        self_pair<kSame>(a0, a1, a2, a3, al, pb[0], pb[1], pb[2], b3,
+                         make_float3(bl.x, bl.y, bl.z), l, u, me);
+      }
+      lb_self += static_cast<double>(2.0f * w * a1.y * l);
+      lb_err += static_cast<double>(2.0f * w * a1.y * fmaf(me, kErrExp, l * kErrTerm));
+      ub_self += static_cast<double>(2.0f * w * a2.y * u);
+    }
+  }
+}
+
+template <int kG, bool kSame, bool kCross, bool kSelf, bool kTail>
+__device__ __forceinline__ void class_pairs(const WarpTables& T, const ClassSpan cs, int lane,
+                                            float w, double& lb_self, double& lb_cross,
+                                            double& ub_self, double& ub_cross, double& lb_err) {
+  if constexpr (kTail) {
+    class_pairs_tail<kG, kSame, kCross, kSelf>(T, cs, lane, w, lb_self, lb_cross, ub_self,
+                                               ub_cross, lb_err);
+  } else {
+    class_pairs_rows<kG, kSame, kCross, kSelf>(T, cs, lane, w, lb_self, lb_cross, ub_self,
+                                               ub_cross, lb_err);
   }
 }
 
@@ -542,7 +627,7 @@ __device__ __forceinline__ void column_prep(const WarpTables& T, const DevCtx& c
 #ifndef GOSMA_MIN_BLOCKS
 #define GOSMA_MIN_BLOCKS 7
 #endif
-template <int kMode, int kG>
+template <int kMode, int kG, bool kTail>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
     eval_bounds_kernel(const DevCtx ctx, const EvalArgs args) {
   extern __shared__ float4 smem4[];
@@ -754,9 +839,9 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
           const float w = static_cast<float>(ctx.cls_w[c]);
           double dl = 0.0, du = 0.0;
           if (same) {
-            class_pairs<kG, true, false, true>(T, cs, lane, w, sl_self, dl, su_self, du, se_self);
+            class_pairs<kG, true, false, true, kTail>(T, cs, lane, w, sl_self, dl, su_self, du, se_self);
           } else {
-            class_pairs<kG, false, false, true>(T, cs, lane, w, sl_self, dl, su_self, du,
+            class_pairs<kG, false, false, true, kTail>(T, cs, lane, w, sl_self, dl, su_self, du,
                                                 se_self);
           }
         }
@@ -812,9 +897,9 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
           const ClassSpan cs = ctx.cls[c];
           const float w = static_cast<float>(ctx.cls_w[c]);
           if (same) {
-            class_pairs<kG, true, true, false>(T, cs, lane, w, dl, lcr, du, ucr, ecr);
+            class_pairs<kG, true, true, false, kTail>(T, cs, lane, w, dl, lcr, du, ucr, ecr);
           } else {
-            class_pairs<kG, false, true, false>(T, cs, lane, w, dl, lcr, du, ucr, ecr);
+            class_pairs<kG, false, true, false, kTail>(T, cs, lane, w, dl, lcr, du, ucr, ecr);
           }
         }
         lcr = group_sum_d<kG>(gm, lcr);
@@ -871,10 +956,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
       const float w = static_cast<float>(ctx.cls_w[c]);
       constexpr bool kC = kMode != kSelfOnly, kS = kMode != kCrossCached;
       if (same) {
-        class_pairs<kG, true, kC, kS>(T, cs, lane, w, lb_self, lb_cross, ub_self, ub_cross,
+        class_pairs<kG, true, kC, kS, kTail>(T, cs, lane, w, lb_self, lb_cross, ub_self, ub_cross,
                                       lb_err);
       } else {
-        class_pairs<kG, false, kC, kS>(T, cs, lane, w, lb_self, lb_cross, ub_self, ub_cross,
+        class_pairs<kG, false, kC, kS, kTail>(T, cs, lane, w, lb_self, lb_cross, ub_self, ub_cross,
                                        lb_err);
       }
     }
@@ -941,14 +1026,14 @@ int group_lanes(const DevCtx& ctx) {
   return 32;
 }
 
-template <int kMode, int kG>
+template <int kMode, int kG, bool kTail>
 cudaError_t launch_group(const DevCtx& ctx, const EvalArgs& a, int sm_count,
                          cudaStream_t stream) {
   constexpr int kGroupsPerCta = kWarpsPerCta * (32 / kG);
   const size_t smem = eval_smem_per_warp(ctx) * kGroupsPerCta;
   static size_t configured = 0;
   if (smem > 48 * 1024 && smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(eval_bounds_kernel<kMode, kG>,
+    cudaError_t e = cudaFuncSetAttribute(eval_bounds_kernel<kMode, kG, kTail>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
@@ -956,7 +1041,7 @@ cudaError_t launch_group(const DevCtx& ctx, const EvalArgs& a, int sm_count,
   }
   int per_sm = 0;
   cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-      &per_sm, eval_bounds_kernel<kMode, kG>, kWarpsPerCta * 32, smem);
+      &per_sm, eval_bounds_kernel<kMode, kG, kTail>, kWarpsPerCta * 32, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   long long grid = static_cast<long long>(per_sm) * sm_count;
@@ -964,7 +1049,7 @@ cudaError_t launch_group(const DevCtx& ctx, const EvalArgs& a, int sm_count,
   if (grid > need) grid = need;
   e = cudaMemsetAsync(a.work, 0, sizeof(unsigned int), stream);
   if (e != cudaSuccess) return e;
-  eval_bounds_kernel<kMode, kG>
+  eval_bounds_kernel<kMode, kG, kTail>
       <<<static_cast<unsigned>(grid), kWarpsPerCta * 32, smem, stream>>>(ctx, a);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
@@ -976,11 +1061,12 @@ cudaError_t launch_mode(const DevCtx& ctx, const EvalArgs& a, int sm_count,
   if (a.n <= 0) return cudaSuccess;
   switch (group_lanes(ctx)) {
     case 8:
-      return launch_group<kMode, 8>(ctx, a, sm_count, stream);
+      return launch_group<kMode, 8, false>(ctx, a, sm_count, stream);
     case 16:
-      return launch_group<kMode, 16>(ctx, a, sm_count, stream);
+      return launch_group<kMode, 16, false>(ctx, a, sm_count, stream);
     default:
-      return launch_group<kMode, 32>(ctx, a, sm_count, stream);
+      return ctx.tail_chunks ? launch_group<kMode, 32, true>(ctx, a, sm_count, stream)
+                             : launch_group<kMode, 32, false>(ctx, a, sm_count, stream);
   }
 }
 

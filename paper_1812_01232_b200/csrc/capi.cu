@@ -93,6 +93,9 @@ int ctx_upload(gosma_ctx* ctx) {
   d.zeta = hm.zeta;
   d.lb_margin = ctx->lb_margin;
   d.lb_err_scale = 1.0;
+  d.tail_chunks = 0;
+  for (const ClassSpan& cs : spans)
+    if (cs.n1 % 32 != 0 && cs.n1 % 32 <= 16) d.tail_chunks = 1;
   ClassSpan* dspans;
   if ((e = upload(spans, &dspans)) != cudaSuccess) return cuda_error(e, "ctx upload");
   d.cls = dspans;

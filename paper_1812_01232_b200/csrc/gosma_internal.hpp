@@ -45,6 +45,7 @@ struct DevCtx {
   double zeta;
   double lb_margin;      // relative soundness floor (x |term| mass)
   double lb_err_scale;   // 1: subtract the FP32 error estimate; 0: raw core (diagnostics)
+  int tail_chunks;       // some class has a last row chunk of <= 16 of 32 rows
 };
 
 // Host-side master copy of one class (ClassData, objective.hpp:19-31).

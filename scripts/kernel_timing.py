@@ -5,7 +5,8 @@ import numpy as np, torch
 import paper_1812_01232_b200 as g
 from paper_1812_01232_b200 import synth
 n = int(os.environ.get("NODES", "1000000"))
-W = [("realistic", 64, 32), ("moderate", 64, 32), ("realistic", 256, 128), ("realistic", 12, 12)]
+W = [("realistic", 64, 32), ("moderate", 64, 32), ("realistic", 256, 128), ("realistic", 12, 12),
+     ("realistic", 41, 36), ("realistic", 45, 40)]
 only = os.environ.get("ONLY")
 for regime, n1, n2 in ([W[int(k)] for k in only.split(",")] if only else W):
     cls = synth.mixture(n1, n2, regime, seed=2026)
