@@ -249,9 +249,9 @@ const char* gosma_last_error(void);
 /* Build / device introspection for benches and tests. */
 int gosma_device_info(int device, int* sm_count, int* sm_clock_khz, int* cc_major,
                       int* cc_minor);
-/* Frontier memory comes from the device's stream-ordered pool and is kept
- * (up to a third of the device memory) for the next solve; this returns the
- * cached, unused part to the driver. */
+/* A finished solver's frontier pool (when >= 16M nodes) is kept per device for
+ * the next solve instead of being freed (unmapping tens of GB is slow); this
+ * frees the kept pool of `device`. */
 int gosma_release_cached_memory(int device);
 
 /* Batched objective_value + objective_gradient (objective.cpp:175-334) on the

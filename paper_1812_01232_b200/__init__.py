@@ -349,7 +349,7 @@ def objective_value(ctx: ObjectiveContext, r, t) -> float:
 
 
 def release_cached_memory(device: int = 0):
-    """Returns the solver's cached frontier memory (stream-ordered pool) to the driver."""
+    """Frees the frontier pool a finished solver left parked on `device`."""
     _check(lib.gosma_release_cached_memory(device), "release_cached_memory")
 
 

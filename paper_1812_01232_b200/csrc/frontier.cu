@@ -29,39 +29,67 @@ namespace {
 
 constexpr int kBins = 4096;
 
-// Frontier buffers come from the device's stream-ordered pool (cudaMallocAsync)
-// with a release threshold, so a solver's multi-GB pool is recycled by the
-// next solve instead of being unmapped and remapped (cudaFree of tens of GB
-// costs tenths of a second). Allocation is synchronised before first use and
-// a free waits for the device, as cudaFree would.
-void ensure_pool_retention() {
-  static std::once_flag once;
-  std::call_once(once, [] {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) return;
-    size_t free_b = 0, total_b = 0;
-    cudaMemGetInfo(&free_b, &total_b);
-    unsigned long long keep = total_b / 3;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-  });
-}
-
 template <typename T>
 cudaError_t dmalloc(T** p, size_t bytes) {
-  ensure_pool_retention();
-  void* v = nullptr;
-  cudaError_t e = cudaMallocAsync(&v, bytes, 0);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(0);
-  *p = static_cast<T*>(v);
-  return e;
+  return cudaMalloc(reinterpret_cast<void**>(p), bytes);
 }
 
-void dfree(void* p) {
-  if (!p) return;
-  cudaDeviceSynchronize();  // like cudaFree: no kernel on any stream still uses p
-  cudaFreeAsync(p, 0);
+void dfree(void* p) { cudaFree(p); }
+
+// The four pool arrays of a released frontier are parked (one set per device)
+// instead of freed: unmapping tens of GB costs tenths of a second, and the
+// next solve on the device reuses them. gosma_release_cached_memory frees.
+struct ParkedPool {
+  int device = -1;
+  size_t cap = 0;
+  gosma_node* nodes = nullptr;
+  int8_t* split = nullptr;
+  double* vol = nullptr;
+  unsigned long long* key = nullptr;
+};
+std::mutex g_park_mu;
+std::vector<ParkedPool> g_parked;
+
+void free_parked(ParkedPool& p) {
+  cudaFree(p.nodes);
+  cudaFree(p.split);
+  cudaFree(p.vol);
+  cudaFree(p.key);
+  p = ParkedPool{};
+}
+
+// A parked set of at least `need` nodes on the current device, if any.
+bool take_parked(size_t need, ParkedPool* out) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_park_mu);
+  for (size_t k = 0; k < g_parked.size(); ++k) {
+    if (g_parked[k].device == dev && g_parked[k].cap >= need) {
+      *out = g_parked[k];
+      g_parked.erase(g_parked.begin() + static_cast<long>(k));
+      return true;
+    }
+  }
+  return false;
+}
+
+void park(ParkedPool p) {
+  if (!p.nodes) return;
+  cudaGetDevice(&p.device);
+  cudaDeviceSynchronize();
+  std::lock_guard<std::mutex> lk(g_park_mu);
+  for (ParkedPool& q : g_parked) {
+    if (q.device == p.device) {  // keep the larger set per device
+      if (q.cap >= p.cap) {
+        free_parked(p);
+      } else {
+        free_parked(q);
+        q = p;
+      }
+      return;
+    }
+  }
+  g_parked.push_back(p);
 }
 
 __host__ __device__ __forceinline__ unsigned long long order_key_bits(unsigned long long b) {
@@ -469,10 +497,20 @@ cudaError_t Frontier::reserve(size_t cap_nodes, size_t wave) {
 }
 
 void Frontier::release() {
-  dfree(nodes);
-  dfree(split);
-  dfree(vol);
-  dfree(key);
+  if (cap >= (size_t(1) << 24)) {  // >= 16M nodes (1.7 GB): keep for the next solve
+    ParkedPool p;
+    p.cap = cap;
+    p.nodes = nodes;
+    p.split = split;
+    p.vol = vol;
+    p.key = key;
+    park(p);
+  } else {
+    dfree(nodes);
+    dfree(split);
+    dfree(vol);
+    dfree(key);
+  }
   dfree(sel);
   dfree(hist);
   dfree(kids);
@@ -556,10 +594,19 @@ cudaError_t Frontier::grow(size_t need, cudaStream_t s) {
   double* v2 = nullptr;
   unsigned long long* k2 = nullptr;
   cudaError_t e;
-  if ((e = dmalloc(&n2, c * sizeof(gosma_node))) != cudaSuccess) return e;
-  if ((e = dmalloc(&s2, c)) != cudaSuccess) return e;
-  if ((e = dmalloc(&v2, c * sizeof(double))) != cudaSuccess) return e;
-  if ((e = dmalloc(&k2, c * 8)) != cudaSuccess) return e;
+  ParkedPool pk;
+  if (take_parked(need, &pk)) {
+    n2 = pk.nodes;
+    s2 = pk.split;
+    v2 = pk.vol;
+    k2 = pk.key;
+    c = pk.cap;
+  } else {
+    if ((e = dmalloc(&n2, c * sizeof(gosma_node))) != cudaSuccess) return e;
+    if ((e = dmalloc(&s2, c)) != cudaSuccess) return e;
+    if ((e = dmalloc(&v2, c * sizeof(double))) != cudaSuccess) return e;
+    if ((e = dmalloc(&k2, c * 8)) != cudaSuccess) return e;
+  }
   if (size) {
     cudaMemcpyAsync(n2, nodes, size * sizeof(gosma_node), cudaMemcpyDeviceToDevice, s);
     cudaMemcpyAsync(s2, split, size, cudaMemcpyDeviceToDevice, s);
@@ -1045,13 +1092,21 @@ cudaError_t Frontier::fold_to(size_t keep_n, cudaStream_t s, double* folded_volu
 }  // namespace gosma
 
 extern "C" int gosma_release_cached_memory(int device) {
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, device) != cudaSuccess) return GOSMA_ECUDA;
   int cur = 0;
   cudaGetDevice(&cur);
   cudaSetDevice(device);
-  cudaDeviceSynchronize();
-  const cudaError_t e = cudaMemPoolTrimTo(pool, 0);
+  {
+    std::lock_guard<std::mutex> lk(gosma::g_park_mu);
+    for (size_t k = 0; k < gosma::g_parked.size();) {
+      if (gosma::g_parked[k].device == device) {
+        gosma::free_parked(gosma::g_parked[k]);
+        gosma::g_parked.erase(gosma::g_parked.begin() + static_cast<long>(k));
+      } else {
+        ++k;
+      }
+    }
+  }
+  const cudaError_t e = cudaDeviceSynchronize();
   cudaSetDevice(cur);
   return e == cudaSuccess ? GOSMA_OK : GOSMA_ECUDA;
 }
