@@ -989,6 +989,8 @@ cudaError_t Frontier::route_append(size_t n_kids, double dstar, cudaStream_t s,
   *out = *h_stats;
   if (n_kids) {
     size += static_cast<size_t>(*reinterpret_cast<int*>(h_counter));
+    kids_total += n_kids;
+    kids_kept += static_cast<size_t>(*reinterpret_cast<int*>(h_counter));
     if (tau != 0) cand_n += static_cast<size_t>(*reinterpret_cast<int*>(h_counter + 1));
   }
   return cudaGetLastError();

@@ -62,6 +62,7 @@ struct Frontier {
   bool prof = false;                // synchronising sub-phase timers
   double t_sub[6] = {0, 0, 0, 0, 0, 0};  // rebuild, descend, pick, list; grow, route
   size_t max_bin = 0, max_cand = 0;
+  unsigned long long kids_total = 0, kids_kept = 0;  // routed / appended children
   std::vector<unsigned int> h_hist;
   // children of one wave
   gosma_node* kids = nullptr;

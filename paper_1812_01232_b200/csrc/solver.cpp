@@ -563,9 +563,10 @@ void gosma_solver_destroy(gosma_solver* S) {
     for (int k = 0; k < 8; ++k) std::fprintf(stderr, " %s %.3fs", kName[k], S->phase[k]);
     std::fprintf(stderr,
                  " | select: rebuild %.3fs descend %.3fs pick %.3fs list %.3fs (max bin %zu, "
-                 "max list %zu) | route: grow %.3fs rest %.3fs\n",
+                 "max list %zu) | route: grow %.3fs rest %.3fs | kept %.3f of children\n",
                  S->F.t_sub[0], S->F.t_sub[1], S->F.t_sub[2], S->F.t_sub[3], S->F.max_bin,
-                 S->F.max_cand, S->F.t_sub[4], S->F.t_sub[5]);
+                 S->F.max_cand, S->F.t_sub[4], S->F.t_sub[5],
+                 S->F.kids_total ? double(S->F.kids_kept) / double(S->F.kids_total) : 0.0);
   }
   DeviceGuard g(S->ctx->device);
   S->F.release();
