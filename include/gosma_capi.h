@@ -237,6 +237,12 @@ int gosma_solver_export(gosma_solver* solver, size_t max_nodes, gosma_node* node
                         double* volume, size_t* n_out);
 int gosma_solver_import(gosma_solver* solver, const gosma_node* nodes, const int8_t* split,
                         const double* volume, size_t n);
+/* Device-buffer variants (rebalancing over NCCL without host staging): the
+ * same records in device memory; export's buffers hold at least max_nodes. */
+int gosma_solver_export_device(gosma_solver* solver, size_t max_nodes, gosma_node* d_nodes,
+                               int8_t* d_split, double* d_vol, size_t* n_out);
+int gosma_solver_import_device(gosma_solver* solver, const gosma_node* d_nodes,
+                               const int8_t* d_split, const double* d_vol, size_t n);
 /* Local incumbent pose / value and counters (global_lower, gap, status are
  * the driver's). */
 int gosma_solver_result(gosma_solver* solver, gosma_report* report);

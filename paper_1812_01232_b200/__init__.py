@@ -117,6 +117,9 @@ def _load():
     lib.gosma_solver_export.argtypes = [vp, C.c_size_t, vp, vp, vp, C.POINTER(C.c_size_t)]
     lib.gosma_solver_import.argtypes = [vp, vp, vp, vp, C.c_size_t]
     lib.gosma_solver_result.argtypes = [vp, C.POINTER(_Report)]
+    lib.gosma_solver_export_device.argtypes = [vp, C.c_size_t, vp, vp, vp,
+                                               C.POINTER(C.c_size_t)]
+    lib.gosma_solver_import_device.argtypes = [vp, vp, vp, vp, C.c_size_t]
     lib.gosma_solver_live_volume.argtypes = [vp, _dp]
     lib.gosma_objective_batch.argtypes = [vp, _dp, C.c_size_t, _dp, _dp]
     lib.gosma_eval_children_device.argtypes = [vp, vp, vp, C.c_size_t, C.c_double, vp, vp, vp,
@@ -520,6 +523,26 @@ class ShardSolver:
         vol = np.ascontiguousarray(vol, dtype=np.float64)
         _check(lib.gosma_solver_import(self._h, nodes.ctypes.data, split.ctypes.data,
                                        vol.ctypes.data, len(nodes)), "solver_import")
+
+    def export_device(self, max_nodes: int, device):
+        """Best live nodes into torch CUDA tensors (node bytes uint8[n*88],
+        split int8[n], volume float64[n]) for device-to-device rebalancing."""
+        import torch
+        nodes = torch.empty(max_nodes * NODE_DTYPE.itemsize, dtype=torch.uint8, device=device)
+        split = torch.empty(max_nodes, dtype=torch.int8, device=device)
+        vol = torch.empty(max_nodes, dtype=torch.float64, device=device)
+        n = C.c_size_t(0)
+        _check(lib.gosma_solver_export_device(self._h, max_nodes, nodes.data_ptr(),
+                                              split.data_ptr(), vol.data_ptr(), C.byref(n)),
+               "solver_export_device")
+        k = n.value
+        return nodes[:k * NODE_DTYPE.itemsize], split[:k], vol[:k]
+
+    def import_device(self, nodes, split, vol):
+        """Import node records held in torch CUDA tensors (see export_device)."""
+        n = split.numel()
+        _check(lib.gosma_solver_import_device(self._h, nodes.data_ptr(), split.data_ptr(),
+                                              vol.data_ptr(), n), "solver_import_device")
 
     def result(self) -> dict:
         rep = _Report()

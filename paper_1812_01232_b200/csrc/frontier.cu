@@ -228,6 +228,22 @@ __global__ void split_lists(const int8_t* split, const unsigned int* sel, size_t
   }
 }
 
+__global__ void keys_of(const gosma_node* nodes, size_t n, unsigned long long* key) {
+  const size_t k = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+  if (k < n) key[k] = order_key(nodes[k].lower);
+}
+
+__global__ void gather_sel(const gosma_node* nodes, const int8_t* split, const double* vol,
+                           const unsigned int* sel, size_t n, gosma_node* on, int8_t* os,
+                           double* ov) {
+  const size_t k = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+  if (k >= n) return;
+  const unsigned int i = sel[k];
+  on[k] = nodes[i];
+  os[k] = split[i];
+  ov[k] = vol[i];
+}
+
 __global__ void cuboid_counts(const int8_t* split, const unsigned int* sel, size_t n_sel,
                               unsigned int* cnt) {
   const size_t k = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
@@ -880,6 +896,28 @@ cudaError_t Frontier::expand_selected(size_t n_sel, cudaStream_t s) {
   expand<<<grid_for(n_sel * 8, 256), 256, 0, s>>>(nodes, split, vol, sel, n_sel, kids, kid_vol,
                                                    nullptr, nullptr, nullptr);
   return cudaGetLastError();
+}
+
+cudaError_t Frontier::gather_selected(size_t n, cudaStream_t s, gosma_node* out_nodes,
+                                      int8_t* out_split, double* out_vol) {
+  if (n == 0) return cudaSuccess;
+  gather_sel<<<grid_for(n, 256), 256, 0, s>>>(nodes, split, vol, sel, n, out_nodes, out_split,
+                                              out_vol);
+  return cudaGetLastError();
+}
+
+cudaError_t Frontier::upload_device(const gosma_node* d_nodes, const int8_t* d_split,
+                                    const double* d_vol, size_t n, cudaStream_t s) {
+  cudaError_t e;
+  if ((e = grow(size + n, s)) != cudaSuccess) return e;
+  cudaMemcpyAsync(nodes + size, d_nodes, n * sizeof(gosma_node), cudaMemcpyDeviceToDevice, s);
+  cudaMemcpyAsync(split + size, d_split, n, cudaMemcpyDeviceToDevice, s);
+  cudaMemcpyAsync(vol + size, d_vol, n * sizeof(double), cudaMemcpyDeviceToDevice, s);
+  keys_of<<<grid_for(n, 256), 256, 0, s>>>(nodes + size, n, key + size);
+  size += n;
+  known_min = 0;  // imported keys may lie below the cached minimum
+  tau = 0;
+  return cudaStreamSynchronize(s);
 }
 
 cudaError_t Frontier::wave_lists(size_t n_sel, cudaStream_t s, size_t* n_rot, size_t* n_trans) {

@@ -112,6 +112,12 @@ struct Frontier {
   cudaError_t expand_selected_cached(size_t n_sel, cudaStream_t s, size_t* n_cuboids);
   // rotation-split selections (rot_list) and translation-split children (trans_list)
   cudaError_t wave_lists(size_t n_sel, cudaStream_t s, size_t* n_rot, size_t* n_trans);
+  // the selected records (sel[0..n)) into contiguous device buffers
+  cudaError_t gather_selected(size_t n, cudaStream_t s, gosma_node* out_nodes, int8_t* out_split,
+                              double* out_vol);
+  // device-side import of n records
+  cudaError_t upload_device(const gosma_node* d_nodes, const int8_t* d_split, const double* d_vol,
+                            size_t n, cudaStream_t s);
   cudaError_t best_child(size_t n_kids, cudaStream_t s, int* index, double* value);
   // route children against d*, append survivors
   cudaError_t route_append(size_t n_kids, double dstar, cudaStream_t s, RouteStats* out);

@@ -725,6 +725,22 @@ int gosma_solver_expand(gosma_solver* S, double limit, unsigned long long max_ev
   return GOSMA_OK;
 }
 
+namespace {
+// Selects the best live nodes (they are the next to expand) and gathers them
+// into the wave's child buffers; returns the count.
+int export_select(gosma_solver* S, size_t max_nodes, size_t* n) {
+  cudaStream_t s = S->ctx->stream;
+  cudaError_t e;
+  *n = 0;
+  max_nodes = std::min(max_nodes, S->F.sel_cap);
+  if ((e = S->F.select_smallest(max_nodes, host_order_key(S->dstar()), s, n)) != cudaSuccess)
+    return cuda_error(e, "export select");
+  if ((e = S->F.gather_selected(*n, s, S->F.kids, S->F.kid_split, S->F.kid_vol)) != cudaSuccess)
+    return cuda_error(e, "export gather");
+  return GOSMA_OK;
+}
+}  // namespace
+
 int gosma_solver_export(gosma_solver* S, size_t max_nodes, gosma_node* nodes, int8_t* split,
                         double* vol, size_t* n_out) {
   if (!S || !n_out) return set_error(GOSMA_EINVAL, "null argument");
@@ -732,22 +748,50 @@ int gosma_solver_export(gosma_solver* S, size_t max_nodes, gosma_node* nodes, in
   if (max_nodes == 0) return GOSMA_OK;
   DeviceGuard g(S->ctx->device);
   cudaStream_t s = S->ctx->stream;
-  cudaError_t e;
   size_t n = 0;
-  max_nodes = std::min(max_nodes, S->F.sel_cap);
-  // hand off the best live nodes (they are the next to expand)
-  if ((e = S->F.select_smallest(max_nodes, host_order_key(S->dstar()), s, &n)) != cudaSuccess)
-    return cuda_error(e, "export select");
+  int rc = export_select(S, max_nodes, &n);
+  if (rc != GOSMA_OK) return rc;
+  cudaError_t e = cudaSuccess;
   if (n) {
-    std::vector<unsigned int> idx(n);
-    cudaMemcpy(idx.data(), S->F.sel, n * 4, cudaMemcpyDeviceToHost);
-    for (size_t k = 0; k < n; ++k) {
-      cudaMemcpy(nodes + k, S->F.nodes + idx[k], sizeof(gosma_node), cudaMemcpyDeviceToHost);
-      cudaMemcpy(split + k, S->F.split + idx[k], 1, cudaMemcpyDeviceToHost);
-      cudaMemcpy(vol + k, S->F.vol + idx[k], 8, cudaMemcpyDeviceToHost);
-    }
+    cudaMemcpyAsync(nodes, S->F.kids, n * sizeof(gosma_node), cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(split, S->F.kid_split, n, cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(vol, S->F.kid_vol, n * sizeof(double), cudaMemcpyDeviceToHost, s);
+    e = cudaStreamSynchronize(s);
   }
+  if (e != cudaSuccess) return cuda_error(e, "export copy");
   *n_out = n;
+  return GOSMA_OK;
+}
+
+int gosma_solver_export_device(gosma_solver* S, size_t max_nodes, gosma_node* d_nodes,
+                               int8_t* d_split, double* d_vol, size_t* n_out) {
+  if (!S || !n_out) return set_error(GOSMA_EINVAL, "null argument");
+  *n_out = 0;
+  if (max_nodes == 0) return GOSMA_OK;
+  DeviceGuard g(S->ctx->device);
+  cudaStream_t s = S->ctx->stream;
+  size_t n = 0;
+  int rc = export_select(S, max_nodes, &n);
+  if (rc != GOSMA_OK) return rc;
+  cudaError_t e = cudaSuccess;
+  if (n) {
+    cudaMemcpyAsync(d_nodes, S->F.kids, n * sizeof(gosma_node), cudaMemcpyDeviceToDevice, s);
+    cudaMemcpyAsync(d_split, S->F.kid_split, n, cudaMemcpyDeviceToDevice, s);
+    cudaMemcpyAsync(d_vol, S->F.kid_vol, n * sizeof(double), cudaMemcpyDeviceToDevice, s);
+    e = cudaStreamSynchronize(s);
+  }
+  if (e != cudaSuccess) return cuda_error(e, "export copy");
+  *n_out = n;
+  return GOSMA_OK;
+}
+
+int gosma_solver_import_device(gosma_solver* S, const gosma_node* d_nodes, const int8_t* d_split,
+                               const double* d_vol, size_t n) {
+  if (!S) return set_error(GOSMA_EINVAL, "null argument");
+  if (n == 0) return GOSMA_OK;
+  DeviceGuard g(S->ctx->device);
+  const cudaError_t e = S->F.upload_device(d_nodes, d_split, d_vol, n, S->ctx->stream);
+  if (e != cudaSuccess) return cuda_error(e, "import");
   return GOSMA_OK;
 }
 

@@ -84,6 +84,27 @@ class Comm:
         if t.shape[0]:
             dist.send(t.reshape(-1), dst, group=self.group)
 
+    # node records as device tensors (uint8 node bytes, int8 split, f64 volume)
+    def send_tensors(self, tensors, dst: int):
+        nodes, split, vol = tensors
+        n = self._t([split.numel()], torch.int64)
+        dist.send(n, dst, group=self.group)
+        if split.numel():
+            for t in (nodes, split, vol):
+                dist.send(t.contiguous(), dst, group=self.group)
+
+    def recv_tensors(self, src: int):
+        n = self._t([0], torch.int64)
+        dist.recv(n, src, group=self.group)
+        k = int(n.item())
+        nodes = torch.empty(k * NODE_BYTES, dtype=torch.uint8, device=self.device)
+        split = torch.empty(k, dtype=torch.int8, device=self.device)
+        vol = torch.empty(k, dtype=torch.float64, device=self.device)
+        if k:
+            for t in (nodes, split, vol):
+                dist.recv(t, src, group=self.group)
+        return nodes, split, vol
+
     def recv_array(self, src: int, width: int) -> np.ndarray:
         n = self._t([0], torch.int64)
         dist.recv(n, src, group=self.group)
@@ -125,6 +146,7 @@ def plan_rebalance(counts, imbalance: float = 1.5, min_move: int = 1):
 
 
 NODE_WIDTH = 13  # 11 node doubles + volume + split flag
+NODE_BYTES = 88  # gosma_node
 
 
 def _pack(nodes, split, vol):
@@ -183,9 +205,16 @@ def solve_sharded(shard, epsilon: float, comm: Comm, time_limit: Optional[float]
         wave += 1
         if comm.world > 1 and rebalance_every > 0 and wave % rebalance_every == 0:
             counts = comm.allgather(float(shard.status()["live_nodes"]))
+            device_path = comm.device.type == "cuda" and hasattr(shard, "export_device")
             for src, dst, n in plan_rebalance(counts, imbalance):
                 n = min(n, max_migrate)
-                if comm.rank == src:
+                if device_path:
+                    # node records move GPU -> GPU over NCCL, no host staging
+                    if comm.rank == src:
+                        comm.send_tensors(shard.export_device(n, comm.device), dst)
+                    elif comm.rank == dst:
+                        shard.import_device(*comm.recv_tensors(src))
+                elif comm.rank == src:
                     comm.send_array(_pack(*shard.export(n)), dst)
                 elif comm.rank == dst:
                     nodes, split, vol = _unpack(comm.recv_array(src, NODE_WIDTH))

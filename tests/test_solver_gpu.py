@@ -270,3 +270,32 @@ print(json.dumps({"v": r.best_value, "r": list(r.r), "t": list(r.t), "sma": r.sm
         out[mode] = json.loads(p.stdout.strip().splitlines()[-1])
     assert out["gpu"]["sma"] == out["host"]["sma"] > 0
     assert abs(out["gpu"]["v"] - out["host"]["v"]) <= 1e-7 * (1.0 + abs(out["host"]["v"]))
+
+
+def test_export_import_host_and_device_paths(gosma):
+    """Rebalancing primitives: exported nodes leave the donor (its live volume
+    drops by their volume) and join the receiver; the device-buffer path moves
+    the same records as the host path."""
+    import torch
+    ctx = toy_ctx(gosma, var=4.0, k2=2.0)
+    dom = box_domain(gosma, 0.4, 0.4, (0.05, -0.03, 0.02))
+    cfg = gosma.SolverConfig(epsilon=1e-6, zeta=0.5, wave_nodes=256)
+    a = gosma.ShardSolver(ctx, dom, cfg, 0, 2)
+    b = gosma.ShardSolver(ctx, dom, cfg, 1, 2)
+    for _ in range(3):
+        st = a.status()
+        a.expand(st["best_value"] - 1e-6)
+    va, vb = a.live_volume(), b.live_volume()
+    nodes, split, vol = a.export(100)
+    assert len(nodes) == 100
+    assert abs(a.live_volume() - (va - vol.sum())) <= 1e-9 * va
+    b.import_(nodes, split, vol)
+    assert abs(b.live_volume() - (vb + vol.sum())) <= 1e-9 * max(va, 1.0)
+    # device path: the next best records, moved GPU to GPU
+    dn, ds, dv = a.export_device(50, torch.device("cuda", 0))
+    assert ds.numel() == 50
+    v_before = b.live_volume()
+    b.import_device(dn, ds, dv)
+    assert abs(b.live_volume() - (v_before + float(dv.sum()))) <= 1e-9 * max(va, 1.0)
+    rec = dn.cpu().numpy().view(gosma.NODE_DTYPE)
+    assert np.all(rec["lower"] >= nodes.view(gosma.NODE_DTYPE)["lower"].max() - 1e-12)
