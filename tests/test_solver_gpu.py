@@ -92,6 +92,10 @@ def test_matches_grid_oracle_on_toy_pair(gosma, golden_solver):
     assert r.best_value <= best + 0.05
     # the reference reaches the same incumbent within eps under the same budget
     assert abs(r.best_value - s["best_value"]) <= 0.05
+    # ... at the same pose (stated tolerances: 0.01 rad, 0.01 translation units)
+    from paper_1812_01232_b200.host import angular_distance
+    assert angular_distance(r.r, s["r"]) < 0.01
+    assert np.linalg.norm(r.t - np.array(s["t"])) < 0.01
     check_invariants(r, 0.05)
 
 
