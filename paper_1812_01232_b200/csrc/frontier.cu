@@ -29,6 +29,9 @@ namespace {
 
 constexpr int kBins = 4096;
 
+// First error of a chain of asynchronous calls.
+inline cudaError_t chain(cudaError_t e, cudaError_t next) { return e != cudaSuccess ? e : next; }
+
 template <typename T>
 cudaError_t dmalloc(T** p, size_t bytes) {
   return cudaMalloc(reinterpret_cast<void**>(p), bytes);
@@ -623,13 +626,15 @@ cudaError_t Frontier::grow(size_t need, cudaStream_t s) {
     if ((e = dmalloc(&v2, c * sizeof(double))) != cudaSuccess) return e;
     if ((e = dmalloc(&k2, c * 8)) != cudaSuccess) return e;
   }
+  e = cudaSuccess;
   if (size) {
-    cudaMemcpyAsync(n2, nodes, size * sizeof(gosma_node), cudaMemcpyDeviceToDevice, s);
-    cudaMemcpyAsync(s2, split, size, cudaMemcpyDeviceToDevice, s);
-    cudaMemcpyAsync(v2, vol, size * sizeof(double), cudaMemcpyDeviceToDevice, s);
-    cudaMemcpyAsync(k2, key, size * 8, cudaMemcpyDeviceToDevice, s);
+    e = chain(e, cudaMemcpyAsync(n2, nodes, size * sizeof(gosma_node), cudaMemcpyDeviceToDevice,
+                                 s));
+    e = chain(e, cudaMemcpyAsync(s2, split, size, cudaMemcpyDeviceToDevice, s));
+    e = chain(e, cudaMemcpyAsync(v2, vol, size * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    e = chain(e, cudaMemcpyAsync(k2, key, size * 8, cudaMemcpyDeviceToDevice, s));
   }
-  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+  if ((e = chain(e, cudaStreamSynchronize(s))) != cudaSuccess) return e;
   dfree(nodes);
   dfree(split);
   dfree(vol);
@@ -650,12 +655,13 @@ cudaError_t Frontier::upload(const gosma_node* h_nodes, const int8_t* h_split,
   for (size_t i = 0; i < n; ++i) k[i] = host_order_key(h_nodes[i].lower);
   known_min = 0;  // imported keys may lie below the cached minimum
   tau = 0;
-  cudaMemcpyAsync(nodes + size, h_nodes, n * sizeof(gosma_node), cudaMemcpyHostToDevice, s);
-  cudaMemcpyAsync(split + size, h_split, n, cudaMemcpyHostToDevice, s);
-  cudaMemcpyAsync(vol + size, h_vol, n * sizeof(double), cudaMemcpyHostToDevice, s);
-  cudaMemcpyAsync(key + size, k.data(), n * 8, cudaMemcpyHostToDevice, s);
-  size += n;
-  return cudaStreamSynchronize(s);
+  e = cudaMemcpyAsync(nodes + size, h_nodes, n * sizeof(gosma_node), cudaMemcpyHostToDevice, s);
+  e = chain(e, cudaMemcpyAsync(split + size, h_split, n, cudaMemcpyHostToDevice, s));
+  e = chain(e, cudaMemcpyAsync(vol + size, h_vol, n * sizeof(double), cudaMemcpyHostToDevice, s));
+  e = chain(e, cudaMemcpyAsync(key + size, k.data(), n * 8, cudaMemcpyHostToDevice, s));
+  e = chain(e, cudaStreamSynchronize(s));
+  if (e == cudaSuccess) size += n;
+  return e;
 }
 
 cudaError_t Frontier::min_key(cudaStream_t s, unsigned long long* out) {
@@ -910,14 +916,17 @@ cudaError_t Frontier::upload_device(const gosma_node* d_nodes, const int8_t* d_s
                                     const double* d_vol, size_t n, cudaStream_t s) {
   cudaError_t e;
   if ((e = grow(size + n, s)) != cudaSuccess) return e;
-  cudaMemcpyAsync(nodes + size, d_nodes, n * sizeof(gosma_node), cudaMemcpyDeviceToDevice, s);
-  cudaMemcpyAsync(split + size, d_split, n, cudaMemcpyDeviceToDevice, s);
-  cudaMemcpyAsync(vol + size, d_vol, n * sizeof(double), cudaMemcpyDeviceToDevice, s);
+  e = cudaMemcpyAsync(nodes + size, d_nodes, n * sizeof(gosma_node), cudaMemcpyDeviceToDevice, s);
+  e = chain(e, cudaMemcpyAsync(split + size, d_split, n, cudaMemcpyDeviceToDevice, s));
+  e = chain(e, cudaMemcpyAsync(vol + size, d_vol, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  if (e != cudaSuccess) return e;
   keys_of<<<grid_for(n, 256), 256, 0, s>>>(nodes + size, n, key + size);
+  e = chain(cudaGetLastError(), cudaStreamSynchronize(s));
+  if (e != cudaSuccess) return e;
   size += n;
   known_min = 0;  // imported keys may lie below the cached minimum
   tau = 0;
-  return cudaStreamSynchronize(s);
+  return cudaSuccess;
 }
 
 cudaError_t Frontier::wave_lists(size_t n_sel, cudaStream_t s, size_t* n_rot, size_t* n_trans) {

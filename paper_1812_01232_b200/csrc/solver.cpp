@@ -753,10 +753,11 @@ int gosma_solver_export(gosma_solver* S, size_t max_nodes, gosma_node* nodes, in
   if (rc != GOSMA_OK) return rc;
   cudaError_t e = cudaSuccess;
   if (n) {
-    cudaMemcpyAsync(nodes, S->F.kids, n * sizeof(gosma_node), cudaMemcpyDeviceToHost, s);
-    cudaMemcpyAsync(split, S->F.kid_split, n, cudaMemcpyDeviceToHost, s);
-    cudaMemcpyAsync(vol, S->F.kid_vol, n * sizeof(double), cudaMemcpyDeviceToHost, s);
-    e = cudaStreamSynchronize(s);
+    e = cudaMemcpyAsync(nodes, S->F.kids, n * sizeof(gosma_node), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(split, S->F.kid_split, n, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(vol, S->F.kid_vol, n * sizeof(double), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   }
   if (e != cudaSuccess) return cuda_error(e, "export copy");
   *n_out = n;
@@ -775,10 +776,12 @@ int gosma_solver_export_device(gosma_solver* S, size_t max_nodes, gosma_node* d_
   if (rc != GOSMA_OK) return rc;
   cudaError_t e = cudaSuccess;
   if (n) {
-    cudaMemcpyAsync(d_nodes, S->F.kids, n * sizeof(gosma_node), cudaMemcpyDeviceToDevice, s);
-    cudaMemcpyAsync(d_split, S->F.kid_split, n, cudaMemcpyDeviceToDevice, s);
-    cudaMemcpyAsync(d_vol, S->F.kid_vol, n * sizeof(double), cudaMemcpyDeviceToDevice, s);
-    e = cudaStreamSynchronize(s);
+    e = cudaMemcpyAsync(d_nodes, S->F.kids, n * sizeof(gosma_node), cudaMemcpyDeviceToDevice, s);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(d_split, S->F.kid_split, n, cudaMemcpyDeviceToDevice, s);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(d_vol, S->F.kid_vol, n * sizeof(double), cudaMemcpyDeviceToDevice, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   }
   if (e != cudaSuccess) return cuda_error(e, "export copy");
   *n_out = n;
