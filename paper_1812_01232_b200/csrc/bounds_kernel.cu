@@ -40,6 +40,11 @@
 
 #include "gosma_internal.hpp"
 
+// Unroll factor of the pair loops (A/B builds: -DGOSMA_UNROLL=n).
+#ifndef GOSMA_UNROLL
+#define GOSMA_UNROLL 1
+#endif
+
 namespace gosma {
 
 namespace {
@@ -47,6 +52,7 @@ namespace {
 std::atomic<unsigned long long> g_launches{0};
 
 constexpr int kWarpsPerCta = 4;
+constexpr int kUnrollPairs = GOSMA_UNROLL;
 constexpr unsigned kFull = 0xffffffffu;
 // Pair exponents (log2) below this leave the term under 2^-45 of its F_i G_j
 // prefactor (<= ~2^34): the exact W paths are skipped for them.
@@ -382,7 +388,7 @@ __device__ __forceinline__ void class_pairs_rows(const WarpTables& T, const Clas
     if (il < n) {
       const Row r = load_row(T, cs.o1 + il);
       float l = 0.0f, u = 0.0f, ma = 0.0f, mb = 0.0f;
-#pragma unroll 2
+#pragma unroll kUnrollPairs
       for (int j = cs.o2; j < cs.o2 + cs.n2; ++j)
         cross_pair<kSame>(r, T.col[j * kColF4], T.col[j * kColF4 + 1], l, u, ma, mb);
       lb_cross += static_cast<double>(w * r.Fhi * l);
@@ -406,7 +412,7 @@ __device__ __forceinline__ void class_pairs_rows(const WarpTables& T, const Clas
       const float3 al = make_float3(av3.x, av3.y, av3.z);
       float l = 0.0f, u = 0.0f, me = 0.0f;
       int jl = il;
-#pragma unroll 2
+#pragma unroll kUnrollPairs
       for (int d = 1; d <= dfull; ++d) {
         jl = (jl + 1 == n) ? 0 : jl + 1;
         const int j = cs.o1 + jl;
@@ -453,7 +459,7 @@ __device__ __forceinline__ void class_pairs_tail(const WarpTables& T, const Clas
       const float4* cp = T.col + (cs.o2 + slot) * kColF4;
       const float4* const ce = T.col + (cs.o2 + cs.n2) * kColF4;
       const int cstep = k * kColF4;
-#pragma unroll 2
+#pragma unroll kUnrollPairs
       for (; cp < ce; cp += cstep) cross_pair<kSame>(rw, cp[0], cp[1], l, u, ma, mb);
       lb_cross += static_cast<double>(w * rw.Fhi * l);
       lb_err += static_cast<double>(
@@ -477,7 +483,7 @@ __device__ __forceinline__ void class_pairs_tail(const WarpTables& T, const Clas
       const float3 al = make_float3(av3.x, av3.y, av3.z);
       float l = 0.0f, u = 0.0f, me = 0.0f;
       int jl = il + 1 + slot - k;  // partner row il + d (mod n) after each step
-#pragma unroll 2
+#pragma unroll kUnrollPairs
       for (int d = 1 + slot; d <= dfull; d += k) {
         jl += k;
         if (jl >= n) jl -= n;
