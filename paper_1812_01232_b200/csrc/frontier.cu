@@ -53,6 +53,20 @@ struct ParkedPool {
 std::mutex g_park_mu;
 std::vector<ParkedPool> g_parked;
 
+// Child buffers of a wave, parked the same way.
+struct ParkedWave {
+  int device = -1;
+  size_t cap = 0;
+  void* buf[10] = {nullptr, nullptr, nullptr, nullptr, nullptr,
+                   nullptr, nullptr, nullptr, nullptr, nullptr};
+};
+std::vector<ParkedWave> g_parked_wave;
+
+void free_parked_wave(ParkedWave& w) {
+  for (void* b : w.buf) cudaFree(b);
+  w = ParkedWave{};
+}
+
 void free_parked(ParkedPool& p) {
   cudaFree(p.nodes);
   cudaFree(p.split);
@@ -455,6 +469,50 @@ double key_to_double(unsigned long long k) {
   return d;
 }
 
+// Child buffers for n_sel selected parents (8 children each), grown
+// geometrically on demand so small solves do not map a full wave's worth.
+// Child buffers for n_sel selected parents (8 children each): a small set
+// first, then a full wave's worth (at most two allocations per solver; a
+// finished solver parks them for the next solve on the device).
+cudaError_t Frontier::ensure_kids(size_t n_sel) {
+  const size_t need = 8 * n_sel;
+  if (need <= kid_cap) return cudaSuccess;
+  const size_t full = 8 * std::max(sel_cap, n_sel);
+  const size_t nk = need <= (size_t(1) << 16) && full > (size_t(1) << 16) ? (size_t(1) << 16)
+                                                                            : full;
+  void** slots[10] = {reinterpret_cast<void**>(&tidx),      reinterpret_cast<void**>(&tnodes),
+                      reinterpret_cast<void**>(&tself),     reinterpret_cast<void**>(&kids),
+                      reinterpret_cast<void**>(&kid_lower), reinterpret_cast<void**>(&kid_upper),
+                      reinterpret_cast<void**>(&kid_split), reinterpret_cast<void**>(&kid_vol),
+                      reinterpret_cast<void**>(&keep),      reinterpret_cast<void**>(&kept_idx)};
+  const size_t elem[10] = {4, sizeof(gosma_node), 4 * sizeof(double), sizeof(gosma_node), 8, 8,
+                           1, 8, 4, 4};
+  for (void** p : slots) {
+    dfree(*p);
+    *p = nullptr;
+  }
+  kid_cap = 0;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(g_park_mu);
+    for (size_t k = 0; k < g_parked_wave.size(); ++k) {
+      ParkedWave& w = g_parked_wave[k];
+      if (w.device == dev && w.cap >= nk) {
+        for (int i = 0; i < 10; ++i) *slots[i] = w.buf[i];
+        kid_cap = w.cap;
+        g_parked_wave.erase(g_parked_wave.begin() + static_cast<long>(k));
+        return cudaSuccess;
+      }
+    }
+  }
+  cudaError_t e;
+  for (int i = 0; i < 10; ++i)
+    if ((e = cudaMalloc(slots[i], nk * elem[i])) != cudaSuccess) return e;
+  kid_cap = nk;
+  return cudaSuccess;
+}
+
 cudaError_t Frontier::reserve(size_t cap_nodes, size_t wave) {
   cudaError_t e = cudaSuccess;
   if (cap_nodes > cap) {
@@ -476,30 +534,6 @@ cudaError_t Frontier::reserve(size_t cap_nodes, size_t wave) {
     if ((e = dmalloc(&tcnt, (wave + 1) * 4)) != cudaSuccess) return e;
     if ((e = dmalloc(&toff, (wave + 1) * 4)) != cudaSuccess) return e;
     sel_cap = wave;
-  }
-  const size_t nk = wave * 8;
-  if (nk > kid_cap) {
-    dfree(kids);
-    dfree(kid_lower);
-    dfree(kid_upper);
-    dfree(kid_split);
-    dfree(kid_vol);
-    dfree(keep);
-    dfree(kept_idx);
-    dfree(tidx);
-    dfree(tnodes);
-    dfree(tself);
-    if ((e = dmalloc(&tidx, nk * 4)) != cudaSuccess) return e;
-    if ((e = dmalloc(&tnodes, nk * sizeof(gosma_node))) != cudaSuccess) return e;
-    if ((e = dmalloc(&tself, nk * 4 * sizeof(double))) != cudaSuccess) return e;
-    if ((e = dmalloc(&kids, nk * sizeof(gosma_node))) != cudaSuccess) return e;
-    if ((e = dmalloc(&kid_lower, nk * 8)) != cudaSuccess) return e;
-    if ((e = dmalloc(&kid_upper, nk * 8)) != cudaSuccess) return e;
-    if ((e = dmalloc(&kid_split, nk)) != cudaSuccess) return e;
-    if ((e = dmalloc(&kid_vol, nk * 8)) != cudaSuccess) return e;
-    if ((e = dmalloc(&keep, nk * 4)) != cudaSuccess) return e;
-    if ((e = dmalloc(&kept_idx, nk * 4)) != cudaSuccess) return e;
-    kid_cap = nk;
   }
   if (!stats) {
     if ((e = dmalloc(&stats, sizeof(RouteStats))) != cudaSuccess) return e;
@@ -532,18 +566,43 @@ void Frontier::release() {
   }
   dfree(sel);
   dfree(hist);
-  dfree(kids);
-  dfree(kid_lower);
-  dfree(kid_upper);
-  dfree(kid_split);
-  dfree(kid_vol);
-  dfree(keep);
-  dfree(kept_idx);
+  if (kid_cap >= (size_t(1) << 20)) {  // keep a full wave's child buffers for the next solve
+    ParkedWave w;
+    cudaGetDevice(&w.device);
+    w.cap = kid_cap;
+    void* bufs[10] = {tidx, tnodes, tself, kids, kid_lower, kid_upper, kid_split, kid_vol, keep,
+                      kept_idx};
+    for (int i = 0; i < 10; ++i) w.buf[i] = bufs[i];
+    cudaDeviceSynchronize();
+    std::lock_guard<std::mutex> lk(g_park_mu);
+    bool placed = false;
+    for (ParkedWave& q : g_parked_wave) {
+      if (q.device == w.device) {
+        if (q.cap >= w.cap) {
+          free_parked_wave(w);
+        } else {
+          free_parked_wave(q);
+          q = w;
+        }
+        placed = true;
+        break;
+      }
+    }
+    if (!placed) g_parked_wave.push_back(w);
+  } else {
+    dfree(kids);
+    dfree(kid_lower);
+    dfree(kid_upper);
+    dfree(kid_split);
+    dfree(kid_vol);
+    dfree(keep);
+    dfree(kept_idx);
+    dfree(tidx);
+    dfree(tnodes);
+    dfree(tself);
+  }
   dfree(tcnt);
   dfree(toff);
-  dfree(tidx);
-  dfree(tnodes);
-  dfree(tself);
   tcnt = toff = nullptr;
   tidx = nullptr;
   tnodes = nullptr;
@@ -1150,6 +1209,14 @@ extern "C" int gosma_release_cached_memory(int device) {
       if (gosma::g_parked[k].device == device) {
         gosma::free_parked(gosma::g_parked[k]);
         gosma::g_parked.erase(gosma::g_parked.begin() + static_cast<long>(k));
+      } else {
+        ++k;
+      }
+    }
+    for (size_t k = 0; k < gosma::g_parked_wave.size();) {
+      if (gosma::g_parked_wave[k].device == device) {
+        gosma::free_parked_wave(gosma::g_parked_wave[k]);
+        gosma::g_parked_wave.erase(gosma::g_parked_wave.begin() + static_cast<long>(k));
       } else {
         ++k;
       }

@@ -93,6 +93,7 @@ struct Frontier {
   size_t temp_bytes = 0;
 
   cudaError_t reserve(size_t cap_nodes, size_t wave);
+  cudaError_t ensure_kids(size_t n_sel);
   void release();
   cudaError_t ensure_temp(size_t bytes);
   cudaError_t grow(size_t need, cudaStream_t s);

@@ -463,7 +463,7 @@ int solver_init(gosma_solver* S) {
           ? static_cast<size_t>(cfg.wave_nodes)
           : std::min<size_t>(std::max<size_t>(300000000 / std::max<size_t>(pairs, 1), 1024),
                              1u << 19);
-  cudaError_t e = S->F.reserve(std::max<size_t>(8 * S->wave_nodes, roots.size() * 2 + 16),
+  cudaError_t e = S->F.reserve(std::max<size_t>(size_t(1) << 20, roots.size() * 2 + 16),
                                S->wave_nodes);
   if (e != cudaSuccess) return cuda_error(e, "frontier reserve");
   // Device memory budget for the pool: beyond it the worst nodes fold into the
@@ -644,6 +644,7 @@ int gosma_solver_expand(gosma_solver* S, double limit, unsigned long long max_ev
     }
   }
   const size_t n_kids = n_sel * 8;
+  if ((e = S->F.ensure_kids(n_sel)) != cudaSuccess) return cuda_error(e, "child buffers");
   S->lap(1, s);
   EvalArgs a;
   a.work = static_cast<unsigned int*>(ctx->d_work);
@@ -735,6 +736,7 @@ int export_select(gosma_solver* S, size_t max_nodes, size_t* n) {
   max_nodes = std::min(max_nodes, S->F.sel_cap);
   if ((e = S->F.select_smallest(max_nodes, host_order_key(S->dstar()), s, n)) != cudaSuccess)
     return cuda_error(e, "export select");
+  if ((e = S->F.ensure_kids((*n + 7) / 8)) != cudaSuccess) return cuda_error(e, "export buffers");
   if ((e = S->F.gather_selected(*n, s, S->F.kids, S->F.kid_split, S->F.kid_vol)) != cudaSuccess)
     return cuda_error(e, "export gather");
   return GOSMA_OK;

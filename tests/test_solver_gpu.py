@@ -303,3 +303,26 @@ def test_export_import_host_and_device_paths(gosma):
     assert abs(b.live_volume() - (v_before + float(dv.sum()))) <= 1e-9 * max(va, 1.0)
     rec = dn.cpu().numpy().view(gosma.NODE_DTYPE)
     assert np.all(rec["lower"] >= nodes.view(gosma.NODE_DTYPE)["lower"].max() - 1e-12)
+
+
+def test_certified_optimum_matches_reference_on_random_instances(gosma):
+    """Instances the unmodified reference certifies (tests/golden/
+    certify_golden.json): the GPU solver certifies them too, its optimum is
+    within epsilon of the reference's, and each side's certified lower bound
+    lies below the other's incumbent."""
+    import json
+    G = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "certify_golden.json")))
+    assert len(G["instances"]) >= 5
+    for inst in G["instances"]:
+        mix = Mixture.from_dict(inst["mixture"])
+        ctx = gosma.ObjectiveContext([{"mu": mix.mu, "sigma2": mix.sigma2, "phi1": mix.phi1,
+                                       "dir": mix.dir, "kappa2": mix.kappa2, "phi2": mix.phi2}],
+                                     mix.zeta, single_mixture=True)
+        dom = gosma.PoseDomain(np.array(inst["rot_c"]), inst["rot_hw"], np.array(inst["boxes"]))
+        eps = inst["epsilon"]
+        r = gosma.solve(ctx, dom, gosma.SolverConfig(epsilon=eps, zeta=mix.zeta, time_limit=60))
+        assert r.status == "epsilon_optimal"
+        assert abs(r.best_value - inst["best_value"]) <= eps + 1e-9
+        assert r.global_lower <= inst["best_value"] + 1e-9
+        assert inst["global_lower"] <= r.best_value + 1e-9
+        check_invariants(r, eps)
