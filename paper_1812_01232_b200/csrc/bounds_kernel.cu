@@ -1035,28 +1035,41 @@ int group_lanes(const DevCtx& ctx) {
 template <int kMode, int kG, bool kTail>
 cudaError_t launch_group(const DevCtx& ctx, const EvalArgs& a, int sm_count,
                          cudaStream_t stream) {
-  constexpr int kGroupsPerCta = kWarpsPerCta * (32 / kG);
-  const size_t smem = eval_smem_per_warp(ctx) * kGroupsPerCta;
-  static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(eval_bounds_kernel<kMode, kG, kTail>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-    configured = smem;
+  // Warps per CTA: 4, or fewer when large mixtures' per-group tables would
+  // leave few CTAs resident (e.g. 256x128: 1 CTA of 4 warps vs 7 of 1 warp).
+  static int configured = 0;  // largest dynamic smem set on this kernel
+  int best_warps = kWarpsPerCta, best_resident = -1, best_per_sm = 0;
+  size_t best_smem = 0;
+  for (int warps = kWarpsPerCta; warps >= 1; warps /= 2) {
+    const int groups = warps * (32 / kG);
+    const size_t smem = eval_smem_per_warp(ctx) * groups;
+    if (smem > 48 * 1024 && static_cast<int>(smem) > configured) {
+      const cudaError_t e = cudaFuncSetAttribute(eval_bounds_kernel<kMode, kG, kTail>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 static_cast<int>(smem));
+      if (e != cudaSuccess) continue;
+      configured = static_cast<int>(smem);
+    }
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &per_sm, eval_bounds_kernel<kMode, kG, kTail>, warps * 32, smem) != cudaSuccess)
+      continue;
+    if (per_sm * warps > best_resident) {
+      best_resident = per_sm * warps;
+      best_warps = warps;
+      best_per_sm = per_sm;
+      best_smem = smem;
+    }
   }
-  int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-      &per_sm, eval_bounds_kernel<kMode, kG, kTail>, kWarpsPerCta * 32, smem);
-  if (e != cudaSuccess) return e;
-  if (per_sm < 1) return cudaErrorInvalidConfiguration;
-  long long grid = static_cast<long long>(per_sm) * sm_count;
-  const long long need = (a.n + kGroupsPerCta - 1) / kGroupsPerCta;
+  if (best_per_sm < 1) return cudaErrorInvalidConfiguration;
+  const int groups_per_cta = best_warps * (32 / kG);
+  long long grid = static_cast<long long>(best_per_sm) * sm_count;
+  const long long need = (a.n + groups_per_cta - 1) / groups_per_cta;
   if (grid > need) grid = need;
-  e = cudaMemsetAsync(a.work, 0, sizeof(unsigned int), stream);
+  cudaError_t e = cudaMemsetAsync(a.work, 0, sizeof(unsigned int), stream);
   if (e != cudaSuccess) return e;
   eval_bounds_kernel<kMode, kG, kTail>
-      <<<static_cast<unsigned>(grid), kWarpsPerCta * 32, smem, stream>>>(ctx, a);
+      <<<static_cast<unsigned>(grid), best_warps * 32, best_smem, stream>>>(ctx, a);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }
