@@ -123,20 +123,94 @@ __device__ __forceinline__ float diag_term(float phi, float k) {
   return phi * phi * 0.5f * k * (1.0f + e) * rcpf(1.0f - e);
 }
 
-// Lane groups: a group of kG lanes (32, 16 or 8) evaluates one node; small
-// mixtures (max class n1 <= 16 / 8) run 2 or 4 nodes per warp so the row
-// lanes stay busy. `gm` is the group's lane mask.
-template <int kG>
-__device__ __forceinline__ double shfl_d(unsigned gm, double v, int src) {
-  return __shfl_sync(gm, v, src, kG);
-}
+// Lane groups: a group of kG lanes evaluates one node. kG = 32 is a warp;
+// small mixtures (max class n1 <= 16 / 8) run 2 or 4 nodes per warp (kG =
+// 16 / 8) so the row lanes stay busy; large mixtures (kG = 128) give one node
+// to a whole CTA, so 4 warps share one set of tables and residency is not
+// capped by shared memory. Group collectives below cover all three shapes.
+constexpr int kCtaGroup = 128;
+
+struct GroupScratch {  // static shared memory of a CTA-wide group
+  double d[4];
+  long long ll;
+  int i[4];
+  double node[11];
+};
 
 template <int kG>
-__device__ __forceinline__ double group_sum_d(unsigned gm, double v) {
+struct Group {
+  unsigned gm;   // lane mask (warp groups)
+  int gbase;     // first lane of the group in its warp
+  GroupScratch* sh;
+  __device__ __forceinline__ void sync() const {
+    if constexpr (kG <= 32) {
+      __syncwarp(gm);
+    } else {
+      __syncthreads();
+    }
+  }
+  __device__ __forceinline__ bool any(bool b) const {
+    if constexpr (kG <= 32) {
+      return __any_sync(gm, b);
+    } else {
+      return __syncthreads_or(b) != 0;
+    }
+  }
+  __device__ __forceinline__ double sum(double v) const {
+    if constexpr (kG <= 32) {
 #pragma unroll
-  for (int o = kG / 2; o > 0; o >>= 1) v += __shfl_xor_sync(gm, v, o, kG);
-  return v;
-}
+      for (int o = kG / 2; o > 0; o >>= 1) v += __shfl_xor_sync(gm, v, o, kG);
+      return v;
+    } else {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+      __syncthreads();
+      if ((threadIdx.x & 31) == 0) sh->d[threadIdx.x >> 5] = v;
+      __syncthreads();
+      return (sh->d[0] + sh->d[1]) + (sh->d[2] + sh->d[3]);
+    }
+  }
+  __device__ __forceinline__ double max(double v) const {
+    if constexpr (kG <= 32) {
+#pragma unroll
+      for (int o = kG / 2; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(gm, v, o, kG));
+      return v;
+    } else {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(kFull, v, o));
+      __syncthreads();
+      if ((threadIdx.x & 31) == 0) sh->d[threadIdx.x >> 5] = v;
+      __syncthreads();
+      return fmax(fmax(sh->d[0], sh->d[1]), fmax(sh->d[2], sh->d[3]));
+    }
+  }
+  // value of group lane 0
+  __device__ __forceinline__ long long bcast0(long long v) const {
+    if constexpr (kG <= 32) {
+      return __shfl_sync(gm, v, 0, kG);
+    } else {
+      __syncthreads();
+      if (threadIdx.x == 0) sh->ll = v;
+      __syncthreads();
+      return sh->ll;
+    }
+  }
+  // first group lane with b set (-1: none)
+  __device__ __forceinline__ int first(bool b) const {
+    if constexpr (kG <= 32) {
+      const unsigned bal = __ballot_sync(gm, b) >> gbase;
+      return bal ? __ffs(bal) - 1 : -1;
+    } else {
+      const unsigned bal = __ballot_sync(kFull, b);
+      __syncthreads();
+      if ((threadIdx.x & 31) == 0) sh->i[threadIdx.x >> 5] = bal ? __ffs(bal) - 1 : -1;
+      __syncthreads();
+      for (int w = 0; w < 4; ++w)
+        if (sh->i[w] >= 0) return 32 * w + sh->i[w];
+      return -1;
+    }
+  }
+};
 
 // sqrt(s) < z with the reference's rounding (Eigen norm() = sqrt of the
 // squared norm): the squared comparison decides unless s is within a relative
@@ -637,11 +711,13 @@ template <int kMode, int kG, bool kTail>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
     eval_bounds_kernel(const DevCtx ctx, const EvalArgs args) {
   extern __shared__ float4 smem4[];
+  __shared__ GroupScratch gscratch;
   const int wl = threadIdx.x & 31;
-  const int lane = wl & (kG - 1);  // lane within the group
-  const int gbase = wl & ~(kG - 1);
-  const unsigned gm = kG == 32 ? kFull : (((1u << kG) - 1u) << gbase);
+  const int lane = kG <= 32 ? (wl & (kG - 1)) : static_cast<int>(threadIdx.x);  // in the group
+  const int gbase = kG <= 32 ? (wl & ~(kG - 1)) : 0;
+  const unsigned gm = kG >= 32 ? kFull : (((1u << kG) - 1u) << gbase);
   const int group = static_cast<int>(threadIdx.x) / kG;
+  const Group<kG> G{gm, gbase, &gscratch};
   const int N1 = ctx.n1_total, N2 = ctx.n2_total;
   const size_t per_warp_f4 = static_cast<size_t>((kRowF4 + 1) * N1 + kColF4 * N2);
   float4* base = smem4 + group * per_warp_f4;
@@ -655,7 +731,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
   for (;;) {
     long long node = 0;
     if (lane == 0) node = static_cast<long long>(atomicAdd(args.work, 1u));
-    node = __shfl_sync(gm, node, 0, kG);
+    node = G.bcast0(node);
     if (node >= args.n) break;
     // item lists: full mode over a subset (node = slot); siblings: the item
     // is a selection index k, the parent the pool slot sel[k], the outputs
@@ -671,9 +747,17 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
     double v = 0.0, v2 = 0.0;
     if (lane < 11) v = args.nodes[node * 11 + lane];
     if (kG < 11 && lane < 11 - kG) v2 = args.nodes[node * 11 + kG + lane];
-    auto fetch = [&](int k) {
-      if (kG < 11 && k >= kG) return shfl_d<kG>(gm, v2, k - kG);
-      return shfl_d<kG>(gm, v, k);
+    if constexpr (kG > 32) {
+      if (lane < 11) gscratch.node[lane] = v;
+      __syncthreads();
+    }
+    auto fetch = [&](int k) -> double {
+      if constexpr (kG > 32) {
+        return gscratch.node[k];
+      } else {
+        if (kG < 11 && k >= kG) return __shfl_sync(gm, v2, k - kG, kG);
+        return __shfl_sync(gm, v, k, kG);
+      }
     };
     const double rc0 = fetch(0), rc1 = fetch(1), rc2 = fetch(2);
     const double rhw = fetch(3);
@@ -695,7 +779,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
                                    __dmul_rn(f2, f2)),
                          zeta, zeta2);
       }
-      if (__any_sync(gm, hit)) {
+      if (G.any(hit)) {
         infeasible = true;
         break;
       }
@@ -727,9 +811,9 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
                 __dadd_rn(__dadd_rn(__dmul_rn(d0, d0), __dmul_rn(d1, d1)), __dmul_rn(d2, d2)),
                 zeta, zeta2);
           }
-          const unsigned bal = __ballot_sync(gm, hit) >> gbase;
-          if (bal) {
-            off = mb + __ffs(bal) - 1;
+          const int f = G.first(hit);
+          if (f >= 0) {
+            off = mb + f;
             break;
           }
         }
@@ -830,16 +914,14 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
       }
     }
     // split decision (subdivide_adaptive, se3.cpp:107-121)
-#pragma unroll
-    for (int o = kG / 2; o > 0; o >>= 1)
-      st_max = fmax(st_max, __shfl_xor_sync(gm, st_max, o, kG));
+    st_max = G.max(st_max);
     if constexpr (kMode == kSiblings) {
       // one cuboid, 8 rotation children: self sums once, then per child
       const double hr = 0.5 * rhw;
       const bool trans_ok = fmax(fmax(h0, h1), h2) > 1e-9;
       double sl_self = lb_self, su_self = ub_self, se_self = lb_err;
       if (!infeasible) {
-        __syncwarp(gm);
+        G.sync();
         for (int c = 0; c < ctx.n_classes; ++c) {
           const ClassSpan cs = ctx.cls[c];
           const float w = static_cast<float>(ctx.cls_w[c]);
@@ -851,9 +933,9 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
                                                 se_self);
           }
         }
-        sl_self = group_sum_d<kG>(gm, sl_self);
-        su_self = group_sum_d<kG>(gm, su_self);
-        se_self = group_sum_d<kG>(gm, se_self);
+        sl_self = G.sum(sl_self);
+        su_self = G.sum(su_self);
+        se_self = G.sum(se_self);
       }
       for (int ch = 0; ch < 8; ++ch) {
         const long long slot = 8 * item + ch;
@@ -882,7 +964,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
         }
         double Rc[9];
         rodrigues(crc0, crc1, crc2, Rc);
-        __syncwarp(gm);
+        G.sync();
         for (int c = 0; c < ctx.n_classes; ++c) {
           const ClassSpan cs = ctx.cls[c];
           for (int il = lane; il < cs.n1; il += kG) {
@@ -897,7 +979,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
           }
         }
         column_prep(T, ctx, lane, kG, Rc);
-        __syncwarp(gm);
+        G.sync();
         double lcr = 0.0, ucr = 0.0, ecr = 0.0, dl = 0.0, du = 0.0;
         for (int c = 0; c < ctx.n_classes; ++c) {
           const ClassSpan cs = ctx.cls[c];
@@ -908,9 +990,9 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
             class_pairs<kG, false, true, false, kTail>(T, cs, lane, w, dl, lcr, du, ucr, ecr);
           }
         }
-        lcr = group_sum_d<kG>(gm, lcr);
-        ucr = group_sum_d<kG>(gm, ucr);
-        ecr = group_sum_d<kG>(gm, ecr);
+        lcr = G.sum(lcr);
+        ucr = G.sum(ucr);
+        ecr = G.sum(ecr);
         if (lane == 0) {
           const double mass = sl_self + 2.0 * lcr;
           const double core = (sl_self - 2.0 * lcr) - ctx.lb_err_scale * (se_self + ecr) -
@@ -921,9 +1003,9 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
           args.lower[slot] = lo;
           args.upper[slot] = up;
         }
-        __syncwarp(gm);
+        G.sync();
       }
-      __syncwarp(gm);
+      G.sync();
       continue;
     }
     if (kMode != kSelfOnly && lane == 0 && args.split_rot) {
@@ -948,12 +1030,12 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
           args.upper[node] = INFINITY;
         }
       }
-      __syncwarp(gm);
+      G.sync();
       continue;
     }
     // ---- per-column prep: q_j = R0^T m_j (bounds.cpp:97-102), double-float
     if (kMode != kSelfOnly) column_prep(T, ctx, lane, kG, R);
-    __syncwarp(gm);
+    G.sync();
 
     // ---- pair sweeps (GOSMA_PREP_ONLY: times the per-node prep alone)
 #ifndef GOSMA_PREP_ONLY
@@ -970,11 +1052,11 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
       }
     }
 #endif
-    lb_self = group_sum_d<kG>(gm, lb_self);
-    lb_cross = group_sum_d<kG>(gm, lb_cross);
-    ub_self = group_sum_d<kG>(gm, ub_self);
-    ub_cross = group_sum_d<kG>(gm, ub_cross);
-    lb_err = group_sum_d<kG>(gm, lb_err);
+    lb_self = G.sum(lb_self);
+    lb_cross = G.sum(lb_cross);
+    ub_self = G.sum(ub_self);
+    ub_cross = G.sum(ub_cross);
+    lb_err = G.sum(lb_err);
     if (kMode == kSelfOnly) {
       if (lane == 0) {
         double* o = args.self_out + 4 * node;
@@ -983,7 +1065,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
         o[2] = lb_err;
         o[3] = have_center ? 0.0 : 2.0;  // 2: no feasible centre (upper = +inf)
       }
-      __syncwarp(gm);
+      G.sync();
       continue;
     }
     if (kMode == kCrossCached) {  // the cuboid's translation-only sums
@@ -1004,7 +1086,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
       args.lower[node] = lo;
       args.upper[node] = up;
     }
-    __syncwarp(gm);
+    G.sync();
   }
 }
 
@@ -1025,10 +1107,13 @@ int group_lanes(const DevCtx& ctx) {
     return e ? std::atoi(e) : 0;
   }();
   if (forced == 8 || forced == 16 || forced == 32) return forced;
+  if (forced == 128) return kCtaGroup;
   const size_t table = eval_smem_per_warp(ctx);
   for (int g : {8, 16}) {
     if (ctx.max_n1 <= g && table * kWarpsPerCta * (32 / g) <= 64 * 1024) return g;
   }
+  // large tables: one node per CTA (4 warps share the tables)
+  if (forced == kCtaGroup || (ctx.max_n1 >= 64 && table > 10 * 1024)) return kCtaGroup;
   return 32;
 }
 
@@ -1040,8 +1125,8 @@ cudaError_t launch_group(const DevCtx& ctx, const EvalArgs& a, int sm_count,
   static int configured = 0;  // largest dynamic smem set on this kernel
   int best_warps = kWarpsPerCta, best_resident = -1, best_per_sm = 0;
   size_t best_smem = 0;
-  for (int warps = kWarpsPerCta; warps >= 1; warps /= 2) {
-    const int groups = warps * (32 / kG);
+  for (int warps = kWarpsPerCta; warps >= (kG > 32 ? kWarpsPerCta : 1); warps /= 2) {
+    const int groups = kG > 32 ? 1 : warps * (32 / kG);
     const size_t smem = eval_smem_per_warp(ctx) * groups;
     if (smem > 48 * 1024 && static_cast<int>(smem) > configured) {
       const cudaError_t e = cudaFuncSetAttribute(eval_bounds_kernel<kMode, kG, kTail>,
@@ -1062,7 +1147,7 @@ cudaError_t launch_group(const DevCtx& ctx, const EvalArgs& a, int sm_count,
     }
   }
   if (best_per_sm < 1) return cudaErrorInvalidConfiguration;
-  const int groups_per_cta = best_warps * (32 / kG);
+  const int groups_per_cta = kG > 32 ? 1 : best_warps * (32 / kG);
   long long grid = static_cast<long long>(best_per_sm) * sm_count;
   const long long need = (a.n + groups_per_cta - 1) / groups_per_cta;
   if (grid > need) grid = need;
@@ -1079,6 +1164,8 @@ cudaError_t launch_mode(const DevCtx& ctx, const EvalArgs& a, int sm_count,
                         cudaStream_t stream) {
   if (a.n <= 0) return cudaSuccess;
   switch (group_lanes(ctx)) {
+    case kCtaGroup:
+      return launch_group<kMode, kCtaGroup, false>(ctx, a, sm_count, stream);
     case 8:
       return launch_group<kMode, 8, false>(ctx, a, sm_count, stream);
     case 16:
