@@ -117,12 +117,14 @@ int ctx_upload(gosma_ctx* ctx) {
   ctx->owned = {dspans, dw, dmu, dis2, dphi, dm, dlp, dk2, de2};
   if ((e = cudaMalloc(&ctx->d_work, sizeof(unsigned int))) != cudaSuccess)
     return cuda_error(e, "ctx upload");
-  size_t smem = eval_smem_per_warp(d) * 4;
+  // one node's tables must fit a CTA (launches shrink the CTA, down to one
+  // table per CTA, as tables grow)
+  const size_t smem = eval_smem_per_warp(d) + 256;
   int max_optin = 0;
   cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
   if (smem > static_cast<size_t>(max_optin)) {
-    return set_error(GOSMA_EINVAL, "mixtures too large for the per-warp shared-memory tables (" +
-                                       std::to_string(smem) + " B per CTA)");
+    return set_error(GOSMA_EINVAL, "mixtures too large for the shared-memory tables (" +
+                                       std::to_string(smem) + " B per node)");
   }
   return GOSMA_OK;
 }

@@ -469,3 +469,12 @@ def test_children_branch_and_bound_equals_explicit_children(gosma, n1, n2, ncls)
     assert np.array_equal(fu, np.isfinite(up))
     assert np.all(np.abs(up[fu] - kup[fu]) <= 1e-12 * (np.abs(kup[fu]) + 1.0))
     assert np.array_equal(cs, ksp)
+
+
+def test_very_large_mixture_parity(gosma):
+    """600 GMM x 300 vMF (one node's tables ~67 KB: one node per CTA)."""
+    from paper_1812_01232_b200 import synth
+    classes = synth.mixture(600, 300, "realistic", seed=11)
+    mix = Mixture(**synth.to_mixture_arrays(classes, 0.5))
+    nodes = synth.nodes(12, seed=12).view(np.float64).reshape(-1, 11)
+    check_parity(gosma, mix, nodes)
