@@ -22,8 +22,11 @@ from tests.golden.make_golden import random_context  # noqa: E402
 def main():
     rng = np.random.default_rng(5)
     out = []
-    for trial in range(10):
-        mix = random_context(rng, int(rng.integers(1, 3)), int(rng.integers(1, 3)), 20.0, 0.3)
+    for trial in range(14):
+        # trials 10-13: two semantic classes (block-diagonal pair terms)
+        ncls = 2 if trial >= 10 else 1
+        mix = random_context(rng, int(rng.integers(1, 3)), int(rng.integers(1, 3)), 20.0, 0.3,
+                             n_classes=ncls)
         c = rng.uniform(-0.2, 0.2, 3)
         box = np.array([[*rng.uniform(-0.3, 0.3, 3), 0.3, 0.3, 0.3]])
         eps = 0.05
@@ -40,6 +43,7 @@ def main():
                     "bound_evaluations": int(rep["bound_evaluations"]),
                     "seconds_8_threads": dt})
         print(trial, mix.n1, mix.n2, f"{dt:.2f}s", rep["bound_evaluations"])
+        out[-1]["classes"] = ncls
     with open(os.path.join(HERE, "certify_golden.json"), "w") as f:
         json.dump({"instances": out}, f)
 

@@ -313,11 +313,16 @@ def test_certified_optimum_matches_reference_on_random_instances(gosma):
     import json
     G = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "certify_golden.json")))
     assert len(G["instances"]) >= 5
+    from tests.test_bounds_gpu import mix_classes
+    assert any(inst.get("classes", 1) > 1 for inst in G["instances"])
     for inst in G["instances"]:
         mix = Mixture.from_dict(inst["mixture"])
-        ctx = gosma.ObjectiveContext([{"mu": mix.mu, "sigma2": mix.sigma2, "phi1": mix.phi1,
-                                       "dir": mix.dir, "kappa2": mix.kappa2, "phi2": mix.phi2}],
-                                     mix.zeta, single_mixture=True)
+        if len(mix.n1) == 1:
+            ctx = gosma.ObjectiveContext([{"mu": mix.mu, "sigma2": mix.sigma2, "phi1": mix.phi1,
+                                           "dir": mix.dir, "kappa2": mix.kappa2,
+                                           "phi2": mix.phi2}], mix.zeta, single_mixture=True)
+        else:  # semantic classes
+            ctx = gosma.ObjectiveContext(mix_classes(mix), mix.zeta)
         dom = gosma.PoseDomain(np.array(inst["rot_c"]), inst["rot_hw"], np.array(inst["boxes"]))
         eps = inst["epsilon"]
         r = gosma.solve(ctx, dom, gosma.SolverConfig(epsilon=eps, zeta=mix.zeta, time_limit=60))
