@@ -225,11 +225,12 @@ __device__ __forceinline__ bool norm_below(double s, double z, double z2) {
 // (80 B: conflict-free when lanes read consecutive rows) and kColF4 float4 per
 // image column (broadcast), so a row or column costs one address.
 struct WarpTables {
-  float4* row;  // [0] (uhx, uhy, uhz, klo)   uhat at the cuboid centre (FP32 high part), kappa_lo
+  float4* row;  // [0] (uhx, uhy, uhz, Fst)   uhat at the cuboid centre (FP32 high part), phi/W(kst)
                 // [1] (khi, Flo, st, ct)     Flo = phi / W(klo); psi_t half-angle
-                // [2] (kst, Fst, sp, cp)     kappa at t*, phi / W(kst), half-angle of psi_t + psi_r
-                // [3] (ulx, uly, ulz, Fhi)   uhat low part (double-float), phi / W(khi)
-                // [4] (usx, usy, usz, s4)    uhat at t*, s4 = 4 sin^2((psi_t + psi_r)/2)
+                // [2] (ulx, uly, ulz, kst)   uhat low part (double-float), kappa at t*
+                // [3] (usx, usy, usz, s4)    uhat at t*, s4 = 4 sin^2((psi_t + psi_r)/2)
+                // [4] (klo, sp, cp, Fhi)     kappa_lo, half-angle of psi_t + psi_r, phi/W(khi)
+                // (a self pair reads [0..2] of its partner row: whole 128-bit loads)
   float4* col;  // [0] (qhx, qhy, qhz, k2)    q_j = R0^T m_j, FP32 high part
                 // [1] (qlx, qly, qlz, G)     q_j low part, G = phi2 / W(k2)
 };
@@ -360,15 +361,18 @@ __device__ __noinline__ float self_lb_exact(float alo, float ahi, float blo, flo
 
 template <bool kSame>
 __device__ __forceinline__ void self_pair(const float4& a0, const float4& a1, const float4& a2,
-                                          const float3& a3, const float3& al, const float4& b0,
-                                          const float4& b1, const float4& b2, const float3& b3,
-                                          const float3& bl, float& l, float& u, float& me) {
+                                          const float4& a3, const float4* pa, const float4* pb,
+                                          float& l, float& u, float& me) {
+  // records (kRowF4 float4 per row): [0] (uh, Fst) [1] (khi, Flo, st, ct)
+  // [2] (ul, kst) [3] (us, s4) [4] (klo, sp, cp, Fhi); a self pair reads
+  // [0..2] of row j as three conflict-free 128-bit loads ([3] only off-centre).
+  const float4 b0 = pb[0], b1 = pb[1], b2 = pb[2];
   // spread angle A = min(pi, theta + psi_i + psi_j) (bounds.cpp:108-124);
-  // directions are double-float (high part in a0/b0, low part in al/bl)
-  const float dx = (a0.x - b0.x) + (al.x - bl.x), dy = (a0.y - b0.y) + (al.y - bl.y),
-              dz = (a0.z - b0.z) + (al.z - bl.z);
-  const float px = (a0.x + b0.x) + (al.x + bl.x), py = (a0.y + b0.y) + (al.y + bl.y),
-              pz = (a0.z + b0.z) + (al.z + bl.z);
+  // directions are double-float (high part in [0], low part in [2])
+  const float dx = (a0.x - b0.x) + (a2.x - b2.x), dy = (a0.y - b0.y) + (a2.y - b2.y),
+              dz = (a0.z - b0.z) + (a2.z - b2.z);
+  const float px = (a0.x + b0.x) + (a2.x + b2.x), py = (a0.y + b0.y) + (a2.y + b2.y),
+              pz = (a0.z + b0.z) + (a2.z + b2.z);
   const float x = fmaf(dx, dx, fmaf(dy, dy, dz * dz));  // |u_i - u_j|^2
   const float y = fmaf(px, px, fmaf(py, py, pz * pz));  // |u_i + u_j|^2
   const float sij = fmaf(a1.z, b1.w, a1.w * b1.z);   // sin((psi_i+psi_j)/2)
@@ -397,12 +401,13 @@ __device__ __forceinline__ void self_pair(const float4& a0, const float4& a1, co
     xs = x;
     ys = y;
   } else {
+    const float4 b3 = pb[3];
     const float ex = a3.x - b3.x, ey = a3.y - b3.y, ez = a3.z - b3.z;
     const float fx = a3.x + b3.x, fy = a3.y + b3.y, fz = a3.z + b3.z;
     xs = fmaf(ex, ex, fmaf(ey, ey, ez * ez));
     ys = fmaf(fx, fx, fmaf(fy, fy, fz * fz));
   }
-  const float ka = a2.x, kb = b2.x;
+  const float ka = a2.w, kb = b2.w;
   const float ab2 = ka * kb;
   const float d2 = ka - kb;
   const float K2u = fmaf(d2, d2, ab2 * ys);
@@ -416,12 +421,12 @@ __device__ __forceinline__ void self_pair(const float4& a0, const float4& a1, co
   float t1 = ex2f(e1) * rKhh;
   float t2 = ex2f(e2) * rK2;
   if (e1 > kNegligibleLog2 && (c2 < 2.0f || !(Khh > 15.0f)))
-    t1 = self_lb_exact(a0.w, ahi, b0.w, bhi, c2, K2hh, e1);
+    t1 = self_lb_exact(pa[4].x, ahi, pb[4].x, bhi, c2, K2hh, e1);
   if (e2 > kNegligibleLog2 && !(K2 > 15.0f)) t2 = ex2f(e2 + log2w(K2));
   const float ft1 = b1.y * t1;  // F_j (Flo); 2 F_i is applied to the row sum
   l += ft1;
   me = fmaf(ft1, fabsf(e1), me);
-  u = fmaf(b2.y, t2, u);  // F_j (Fst)
+  u = fmaf(b0.w, t2, u);  // F_j (Fst)
 }
 
 __device__ __forceinline__ Row load_row(const WarpTables& T, int i) {
@@ -431,23 +436,23 @@ __device__ __forceinline__ Row load_row(const WarpTables& T, int i) {
   r.uhx = a0.x;
   r.uhy = a0.y;
   r.uhz = a0.z;
-  r.klo = a0.w;
-  r.klo2 = 2.0f * a0.w;
+  r.Fst = a0.w;
   r.khi = a1.x;
-  r.kst = a2.x;
-  r.Fst = a2.y;
-  r.sp2 = a2.z * a2.z;
-  r.cp2 = a2.w * a2.w;
-  r.csp2 = 2.0f * a2.z * a2.w;
+  r.ulx = a2.x;
+  r.uly = a2.y;
+  r.ulz = a2.z;
+  r.kst = a2.w;
+  r.usx = a3.x;
+  r.usy = a3.y;
+  r.usz = a3.z;
+  r.s4 = a3.w;
+  r.klo = a4.x;
+  r.klo2 = 2.0f * a4.x;
+  r.sp2 = a4.y * a4.y;
+  r.cp2 = a4.z * a4.z;
+  r.csp2 = 2.0f * a4.y * a4.z;
   r.c4 = 4.0f * r.cp2;
-  r.ulx = a3.x;
-  r.uly = a3.y;
-  r.ulz = a3.z;
-  r.Fhi = a3.w;
-  r.usx = a4.x;
-  r.usy = a4.y;
-  r.usz = a4.z;
-  r.s4 = a4.w;
+  r.Fhi = a4.w;
   return r;
 }
 
@@ -480,35 +485,23 @@ __device__ __forceinline__ void class_pairs_rows(const WarpTables& T, const Clas
     if (il < n) {
       const int i = cs.o1 + il;
       const float4* pa = T.row + i * kRowF4;
-      const float4 a0 = pa[0], a1 = pa[1], a2 = pa[2], av3 = pa[3];
-      float3 a3 = make_float3(0.f, 0.f, 0.f);
-      if (!kSame) a3 = make_float3(pa[4].x, pa[4].y, pa[4].z);
-      const float3 al = make_float3(av3.x, av3.y, av3.z);
+      const float4 a0 = pa[0], a1 = pa[1], a2 = pa[2];
+      const float4 a3 = kSame ? make_float4(0.f, 0.f, 0.f, 0.f) : pa[3];
       float l = 0.0f, u = 0.0f, me = 0.0f;
       int jl = il;
 #pragma unroll kUnrollPairs
       for (int d = 1; d <= dfull; ++d) {
         jl = (jl + 1 == n) ? 0 : jl + 1;
         const int j = cs.o1 + jl;
-        float3 b3 = make_float3(0.f, 0.f, 0.f);
-        const float4* pb = T.row + j * kRowF4;
-        if (!kSame) b3 = make_float3(pb[4].x, pb[4].y, pb[4].z);
-        const float4 bl = pb[3];
-        self_pair<kSame>(a0, a1, a2, a3, al, pb[0], pb[1], pb[2], b3,
-                         make_float3(bl.x, bl.y, bl.z), l, u, me);
+        self_pair<kSame>(a0, a1, a2, a3, pa, T.row + j * kRowF4, l, u, me);
       }
       if (even && il < n / 2) {
         const int j = i + n / 2;
-        float3 b3 = make_float3(0.f, 0.f, 0.f);
-        const float4* pb = T.row + j * kRowF4;
-        if (!kSame) b3 = make_float3(pb[4].x, pb[4].y, pb[4].z);
-        const float4 bl = pb[3];
-        self_pair<kSame>(a0, a1, a2, a3, al, pb[0], pb[1], pb[2], b3,
-                         make_float3(bl.x, bl.y, bl.z), l, u, me);
+        self_pair<kSame>(a0, a1, a2, a3, pa, T.row + j * kRowF4, l, u, me);
       }
       lb_self += static_cast<double>(2.0f * w * a1.y * l);
       lb_err += static_cast<double>(2.0f * w * a1.y * fmaf(me, kErrExp, l * kErrTerm));
-      ub_self += static_cast<double>(2.0f * w * a2.y * u);
+      ub_self += static_cast<double>(2.0f * w * a0.w * u);
     }
   }
 }
@@ -551,10 +544,8 @@ __device__ __forceinline__ void class_pairs_tail(const WarpTables& T, const Clas
     if (lane < r * k) {
       const int i = cs.o1 + il;
       const float4* pa = T.row + i * kRowF4;
-      const float4 a0 = pa[0], a1 = pa[1], a2 = pa[2], av3 = pa[3];
-      float3 a3 = make_float3(0.f, 0.f, 0.f);
-      if (!kSame) a3 = make_float3(pa[4].x, pa[4].y, pa[4].z);
-      const float3 al = make_float3(av3.x, av3.y, av3.z);
+      const float4 a0 = pa[0], a1 = pa[1], a2 = pa[2];
+      const float4 a3 = kSame ? make_float4(0.f, 0.f, 0.f, 0.f) : pa[3];
       float l = 0.0f, u = 0.0f, me = 0.0f;
       int jl = il + 1 + slot - k;  // partner row il + d (mod n) after each step
 #pragma unroll kUnrollPairs
@@ -562,25 +553,15 @@ __device__ __forceinline__ void class_pairs_tail(const WarpTables& T, const Clas
         jl += k;
         if (jl >= n) jl -= n;
         const int j = cs.o1 + jl;
-        float3 b3 = make_float3(0.f, 0.f, 0.f);
-        const float4* pb = T.row + j * kRowF4;
-        if (!kSame) b3 = make_float3(pb[4].x, pb[4].y, pb[4].z);
-        const float4 bl = pb[3];
-        self_pair<kSame>(a0, a1, a2, a3, al, pb[0], pb[1], pb[2], b3,
-                         make_float3(bl.x, bl.y, bl.z), l, u, me);
+        self_pair<kSame>(a0, a1, a2, a3, pa, T.row + j * kRowF4, l, u, me);
       }
       if (even && slot == 0 && il < n / 2) {
         const int j = i + n / 2;
-        float3 b3 = make_float3(0.f, 0.f, 0.f);
-        const float4* pb = T.row + j * kRowF4;
-        if (!kSame) b3 = make_float3(pb[4].x, pb[4].y, pb[4].z);
-        const float4 bl = pb[3];
-        self_pair<kSame>(a0, a1, a2, a3, al, pb[0], pb[1], pb[2], b3,
-                         make_float3(bl.x, bl.y, bl.z), l, u, me);
+        self_pair<kSame>(a0, a1, a2, a3, pa, T.row + j * kRowF4, l, u, me);
       }
       lb_self += static_cast<double>(2.0f * w * a1.y * l);
       lb_err += static_cast<double>(2.0f * w * a1.y * fmaf(me, kErrExp, l * kErrTerm));
-      ub_self += static_cast<double>(2.0f * w * a2.y * u);
+      ub_self += static_cast<double>(2.0f * w * a0.w * u);
     }
   }
 }
@@ -899,13 +880,13 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
         const float uhx = static_cast<float>(c0), uhy = static_cast<float>(c1),
                     uhz = static_cast<float>(c2);
         float4* pr = T.row + i * kRowF4;
-        pr[0] = make_float4(uhx, uhy, uhz, klo);
+        pr[0] = make_float4(uhx, uhy, uhz, Fst);
         pr[1] = make_float4(khi, Flo, static_cast<float>(st), static_cast<float>(ct));
-        pr[2] = make_float4(kst, Fst, static_cast<float>(sp), static_cast<float>(cp));
-        pr[3] = make_float4(static_cast<float>(c0 - uhx), static_cast<float>(c1 - uhy),
-                            static_cast<float>(c2 - uhz), Fhi);
-        pr[4] = make_float4(static_cast<float>(v0 * iv), static_cast<float>(v1 * iv),
+        pr[2] = make_float4(static_cast<float>(c0 - uhx), static_cast<float>(c1 - uhy),
+                            static_cast<float>(c2 - uhz), kst);
+        pr[3] = make_float4(static_cast<float>(v0 * iv), static_cast<float>(v1 * iv),
                             static_cast<float>(v2 * iv), static_cast<float>(4.0 * sp * sp));
+        pr[4] = make_float4(klo, static_cast<float>(sp), static_cast<float>(cp), Fhi);
       }
       if (!infeasible && kMode != kCrossCached) {
         lb_self += static_cast<double>(w * dsl);
@@ -973,9 +954,9 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
             double sp, cp;
             half_angles(sc.x, sc.y, cs_r, cc_r, sp, cp);
             float4* pr = T.row + i * kRowF4;
-            pr[2].z = static_cast<float>(sp);
-            pr[2].w = static_cast<float>(cp);
-            pr[4].w = static_cast<float>(4.0 * sp * sp);
+            pr[4].y = static_cast<float>(sp);
+            pr[4].z = static_cast<float>(cp);
+            pr[3].w = static_cast<float>(4.0 * sp * sp);
           }
         }
         column_prep(T, ctx, lane, kG, Rc);
