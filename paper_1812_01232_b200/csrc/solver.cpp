@@ -102,7 +102,7 @@ bool gpu_sma(const HostModel& m) {
     return std::string(e) == "gpu" ? 1 : (std::string(e) == "host" ? 0 : -1);
   }();
   if (forced >= 0) return forced == 1;
-  return model_pairs(m) >= 512;
+  return model_pairs(m) >= 3000;  // measured: host faster at 41x36, GPU at 64x32
 }
 
 // process_wave's incumbent update (solver.cpp:409-431) for one improving
@@ -255,6 +255,7 @@ int discovery_dive(gosma_ctx* ctx, const Domain& dom, const std::vector<gosma_no
     beam.resize(out);
   }
   *evals += used;
+  const auto t_beam = std::chrono::steady_clock::now();
   // annealing ladder per sector: coarse -> 0.03 -> 0.01 -> exact
   const HostModel hc = blurred_model(m, kCoarse, dbar);
   const HostModel h3 = blurred_model(m, 0.03, dbar);
@@ -316,6 +317,10 @@ int discovery_dive(gosma_ctx* ctx, const Domain& dom, const std::vector<gosma_no
     work();
     for (auto& th : pool) th.join();
   }
+  if (std::getenv("GOSMA_PROFILE"))
+    std::fprintf(stderr, "[gosma profile] dive: ladder %.3fs (%s SMA), %zu starts\n",
+                 std::chrono::duration<double>(std::chrono::steady_clock::now() - t_beam).count(),
+                 dobj ? "GPU" : "host", best.size());
   for (size_t s = 0; s < best.size(); ++s) {
     if (!ok[s]) continue;
     inc->sma += 4;
