@@ -154,6 +154,17 @@ int gosma_local_refine(const gosma_ctx* ctx, const double r0[3], const double t0
                        const gosma_domain* domain, double r_out[3], double t_out[3],
                        double* value);
 
+/* Batched local refinement on the GPU: n starts (r0, t0:
+ * n*3 doubles each, row-major), each refined by one CTA running the same
+ * L-BFGS / strong-Wolfe / projection loop as gosma_local_refine on the FP64
+ * device objective. value[k] is the host FP64 objective at the returned pose
+ * (never worse than the start unless the device and host objectives disagree
+ * in the last bits). Replaces n calls of local_refine
+ * (solver.hpp:80-85) as issued by the discovery dive (solver.cpp:560-595). */
+int gosma_local_refine_batch(gosma_ctx* ctx, size_t n, const double* r0, const double* t0,
+                             const gosma_domain* domain, double* r_out, double* t_out,
+                             double* value);
+
 /* Replaces SolverConfig (solver.hpp:14-37). Negative time_limit /
  * max_evaluations / queue_capacity mean "unset". */
 typedef struct gosma_config {

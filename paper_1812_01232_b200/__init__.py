@@ -17,7 +17,7 @@ import numpy as np
 __all__ = [
     "GosmaError", "InfeasiblePoseError", "ObjectiveContext", "NODE_DTYPE", "make_nodes",
     "evaluate_branch_batch", "evaluate_bounds", "objective_value", "objective_gradient",
-    "SolverConfig", "SolverReport", "PoseDomain", "solve", "local_refine", "lib", "library_path",
+    "SolverConfig", "SolverReport", "PoseDomain", "solve", "local_refine", "local_refine_batch", "lib", "library_path",
     "kernel_launches", "evaluate_branch_batch_device", "evaluate_branch_batch_cached_device",
     "evaluate_children_device", "objective_batch", "ShardSolver", "build_semantic_mixtures",
     "dp_means", "dp_vmf_means", "release_cached_memory", "calibrate_pipes", "device_info",
@@ -103,6 +103,8 @@ def _load():
     lib.gosma_objective_value.argtypes = [vp, _dp, _dp, _dp]
     lib.gosma_objective_gradient.argtypes = [vp, _dp, _dp, _dp]
     lib.gosma_local_refine.argtypes = [vp, _dp, _dp, C.POINTER(_Domain), _dp, _dp, _dp]
+    lib.gosma_local_refine_batch.argtypes = [vp, C.c_size_t, _dp, _dp, C.POINTER(_Domain), _dp,
+                                             _dp, _dp]
     lib.gosma_solve.argtypes = [vp, C.POINTER(_Domain), C.POINTER(_Config), C.POINTER(_Report),
                                 _TRACE_CB, vp]
     lib.gosma_device_info.argtypes = [C.c_int] + [C.POINTER(C.c_int)] * 4
@@ -439,6 +441,23 @@ def local_refine(ctx: ObjectiveContext, r0, t0, domain: PoseDomain):
                                   r.ctypes.data_as(_dp), t.ctypes.data_as(_dp), C.byref(v)),
            "local_refine")
     return v.value, r, t
+
+
+def local_refine_batch(ctx: ObjectiveContext, r0, t0, domain: PoseDomain):
+    """n local refinements on the GPU (one CTA each):
+    (values (n,), r (n, 3), t (n, 3)); values are host FP64 objectives."""
+    r0 = np.ascontiguousarray(r0, dtype=np.float64).reshape(-1, 3)
+    t0 = np.ascontiguousarray(t0, dtype=np.float64).reshape(-1, 3)
+    if r0.shape != t0.shape:
+        raise ValueError("r0 and t0 must both be (n, 3)")
+    n = r0.shape[0]
+    d, keep = domain._c()
+    r, t, v = np.empty((n, 3)), np.empty((n, 3)), np.empty(n)
+    _check(lib.gosma_local_refine_batch(ctx.handle, n, r0.ctypes.data_as(_dp),
+                                        t0.ctypes.data_as(_dp), C.byref(d),
+                                        r.ctypes.data_as(_dp), t.ctypes.data_as(_dp),
+                                        v.ctypes.data_as(_dp)), "local_refine_batch")
+    return v, r, t
 
 
 def solve(ctx: ObjectiveContext, domain: PoseDomain, config: SolverConfig) -> SolverReport:

@@ -3,6 +3,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 
 namespace gosma {
 
@@ -34,11 +36,13 @@ DeviceObjective::DeviceObjective(int device, const std::vector<const HostModel*>
     std::vector<ClassSpan> spans;
     std::vector<double> cw, mu, s2, p1, b, k2, lz2, p2, all;
     int o1 = 0, o2 = 0, mx = 1, mp = 1;
+    size_t pairs = 0;
     for (const HostClass& c : hm->classes) {
       spans.push_back({o1, c.n1(), o2, c.n2()});
       cw.push_back(c.weight);
       mx = std::max(mx, c.n1());
       mp = std::max(mp, c.n1() + c.n2());
+      pairs += static_cast<size_t>(c.n1()) * (c.n1() + c.n2());
       mu.insert(mu.end(), c.mu.begin(), c.mu.end());
       s2.insert(s2.end(), c.sigma2.begin(), c.sigma2.end());
       p1.insert(p1.end(), c.phi1.begin(), c.phi1.end());
@@ -57,6 +61,7 @@ DeviceObjective::DeviceObjective(int device, const std::vector<const HostModel*>
     d.max_n1 = mx;
     d.zeta = hm->zeta;
     max_n1_ = std::max(max_n1_, mx);
+    max_pairs_ = std::max(max_pairs_, pairs);
     slices_ = std::max(slices_, objgrad_slices(mp));
     const ClassSpan* dspans = nullptr;
     if (e == cudaSuccess) e = upload_vec(spans, &dspans, &owned_);
@@ -142,37 +147,70 @@ cudaError_t DeviceObjective::evaluate(const std::vector<ObjRequest>& requests,
   return e;
 }
 
-void BatchGate::launch_locked(std::unique_lock<std::mutex>&) {
-  std::vector<double> f, g;
-  dev_->evaluate(pending_, &f, &g);
-  for (size_t k = 0; k < pending_.size(); ++k) {
-    *f_out_[k] = f[k];
-    for (int a = 0; a < 6; ++a) g_out_[k][a] = g[6 * k + a];
+cudaError_t DeviceObjective::refine(const std::vector<RefineJob>& jobs, const double rc[3],
+                                    double rhw, const std::vector<double>& boxes,
+                                    std::vector<RefineOut>* out) {
+  out->assign(jobs.size(), RefineOut{INFINITY, {0, 0, 0, 0, 0, 0}, 0});
+  if (jobs.empty()) return cudaSuccess;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  cudaSetDevice(device_);
+  RefineJob* d_jobs = nullptr;
+  RefineOut* d_out = nullptr;
+  double* d_boxes = nullptr;
+  cudaError_t e = cudaMalloc(&d_jobs, jobs.size() * sizeof(RefineJob));
+  if (e == cudaSuccess) e = cudaMalloc(&d_out, jobs.size() * sizeof(RefineOut));
+  if (e == cudaSuccess) e = cudaMalloc(&d_boxes, std::max<size_t>(boxes.size(), 6) * 8);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(d_jobs, jobs.data(), jobs.size() * sizeof(RefineJob),
+                        cudaMemcpyHostToDevice, stream_);
+  if (e == cudaSuccess && !boxes.empty())
+    e = cudaMemcpyAsync(d_boxes, boxes.data(), boxes.size() * 8, cudaMemcpyHostToDevice, stream_);
+  RefineDomain dom{{rc[0], rc[1], rc[2]}, rhw, static_cast<int>(boxes.size() / 6), d_boxes};
+  // spread each start over a cluster of CTAs when the GPU has SMs to spare
+  // and an evaluation is big enough to amortise the cluster exchange
+  const int n = static_cast<int>(jobs.size());
+  // (GOSMA_REFINE_CLUSTER=c forces c, for A/B measurements)
+  static const int forced = [] {
+    const char* v = std::getenv("GOSMA_REFINE_CLUSTER");
+    return v ? std::atoi(v) : 0;
+  }();
+  const int cluster = forced > 0 ? forced
+                                 : (max_pairs_ >= 8192 ? std::max(1, std::min(8, sm_count_ / n)) : 1);
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  const bool prof = std::getenv("GOSMA_PROFILE") != nullptr;
+  if (prof) {
+    cudaEventCreate(&ev[0]);
+    cudaEventCreate(&ev[1]);
+    cudaEventRecord(ev[0], stream_);
   }
-  pending_.clear();
-  f_out_.clear();
-  g_out_.clear();
-  ++generation_;
-  cv_.notify_all();
-}
-
-void BatchGate::eval(const ObjRequest& r, double* f, double g[6]) {
-  std::unique_lock<std::mutex> lk(mu_);
-  pending_.push_back(r);
-  f_out_.push_back(f);
-  g_out_.push_back(g);
-  const unsigned long long gen = generation_;
-  if (static_cast<int>(pending_.size()) >= active_) {
-    launch_locked(lk);
-    return;
+  if (e == cudaSuccess)
+    e = launch_refine(d_models_, d_jobs, n, dom, d_out, max_n1_, cluster, stream_);
+  if (prof) cudaEventRecord(ev[1], stream_);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(out->data(), d_out, jobs.size() * sizeof(RefineOut),
+                        cudaMemcpyDeviceToHost, stream_);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(stream_);
+  if (prof) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ev[0], ev[1]);
+    long long tot = 0, mx = 0;
+    for (const RefineOut& o : *out) {
+      tot += o.evals;
+      mx = std::max(mx, o.evals);
+    }
+    std::fprintf(stderr,
+                 "[gosma profile] refine kernel: %d jobs x %d CTAs %.3f ms, evals %lld (max %lld "
+                 "per job, %.2f us each)\n",
+                 n, cluster, ms, tot, mx, mx ? 1e3 * ms / mx : 0.0);
+    cudaEventDestroy(ev[0]);
+    cudaEventDestroy(ev[1]);
   }
-  cv_.wait(lk, [&] { return generation_ != gen; });
-}
-
-void BatchGate::leave() {
-  std::unique_lock<std::mutex> lk(mu_);
-  --active_;
-  if (active_ > 0 && static_cast<int>(pending_.size()) >= active_) launch_locked(lk);
+  cudaFree(d_jobs);
+  cudaFree(d_out);
+  cudaFree(d_boxes);
+  cudaSetDevice(cur);
+  return e;
 }
 
 }  // namespace gosma

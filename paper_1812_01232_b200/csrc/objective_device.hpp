@@ -1,12 +1,9 @@
-// Batched FP64 objective / gradient on the GPU for the local refiner (K6,
-// objective_kernel.cu) and the host-side batcher that lets many L-BFGS starts
-// (one host thread each) share kernel launches.
+// Batched FP64 objective / gradient on the GPU (K6, objective_kernel.cu) and
+// the GPU-resident local refiner built on it (one CTA per L-BFGS start).
 #pragma once
 
 #include <cuda_runtime.h>
 
-#include <condition_variable>
-#include <mutex>
 #include <vector>
 
 #include "gosma_internal.hpp"
@@ -36,6 +33,31 @@ struct ObjRequest {
   int pad;
 };
 
+// GPU-resident local refinement: one CTA per job runs the L-BFGS ladder
+// (up to 4 stages, each on its own model) from x; the domain's boxes are a
+// device array of 6 doubles per box.
+struct RefineJob {
+  double x[6];
+  int stages;
+  int model[4];
+};
+struct RefineDomain {
+  double rc[3];
+  double rhw;
+  int n_boxes;
+  const double* boxes;
+};
+struct RefineOut {
+  double value;
+  double x[6];
+  long long evals;  // objective + gradient evaluations the job made
+};
+// cluster: CTAs per job (1..8), each taking a slice of every evaluation's
+// partners (results depend on it in the last bits, deterministically).
+cudaError_t launch_refine(const DevModel64* models, const RefineJob* jobs, int n,
+                          const RefineDomain& dom, RefineOut* out, int max_n1, int cluster,
+                          cudaStream_t s);
+
 size_t objgrad_smem_bytes(int max_n1);
 int objgrad_slices(int max_pairs_per_row);
 // partial: n * slices * 7 doubles ({f, g[6]} per request and partner slice)
@@ -43,7 +65,7 @@ cudaError_t launch_objgrad(const DevModel64* models, const ObjRequest* req, int 
                            double* partial, int max_n1, cudaStream_t s);
 
 // Owns device copies of a set of models and evaluates batches of requests.
-// evaluate() is synchronous; BatchGate lets host threads pool their requests.
+// evaluate() and refine() are synchronous.
 class DeviceObjective {
  public:
   DeviceObjective(int device, const std::vector<const HostModel*>& models);
@@ -52,9 +74,13 @@ class DeviceObjective {
   // f[k], g[6k] for requests[k]; f = +inf and g = 0 for infeasible poses.
   cudaError_t evaluate(const std::vector<ObjRequest>& requests, std::vector<double>* f,
                        std::vector<double>* g);
+  // runs the refinement jobs on the GPU (one CTA each); boxes: 6 doubles per box
+  cudaError_t refine(const std::vector<RefineJob>& jobs, const double rc[3], double rhw,
+                     const std::vector<double>& boxes, std::vector<RefineOut>* out);
 
  private:
   int device_ = 0, sm_count_ = 1, max_n1_ = 1, slices_ = 1;
+  size_t max_pairs_ = 0;  // largest model's pair terms per evaluation
   bool ok_ = false;
   std::vector<void*> owned_;
   DevModel64* d_models_ = nullptr;
@@ -62,30 +88,6 @@ class DeviceObjective {
   double* d_part_ = nullptr;
   size_t cap_ = 0;
   cudaStream_t stream_ = nullptr;
-};
-
-// Collects one request per participating thread and launches when every
-// active participant is waiting (deterministic per request: results depend
-// only on the pose and the model).
-class BatchGate {
- public:
-  explicit BatchGate(DeviceObjective* dev, int participants)
-      : dev_(dev), active_(participants) {}
-  // Blocks until the batch containing this request has been evaluated.
-  void eval(const ObjRequest& r, double* f, double g[6]);
-  // A participant that will make no more requests.
-  void leave();
-
- private:
-  void launch_locked(std::unique_lock<std::mutex>& lk);
-  DeviceObjective* dev_;
-  std::mutex mu_;
-  std::condition_variable cv_;
-  int active_;
-  unsigned long long generation_ = 0;
-  std::vector<ObjRequest> pending_;
-  std::vector<double*> f_out_;
-  std::vector<double*> g_out_;
 };
 
 }  // namespace gosma

@@ -12,6 +12,7 @@
 // is linear in v, so every J_i / R^T / Jl^T product is applied once per row
 // (or once per pose) to an accumulated vector. Self pairs are visited as
 // ordered pairs (i != j), each side adding its own half of the gradient.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -40,6 +41,21 @@ __device__ __forceinline__ double log_z_deriv_d(double k) {
   return (1.0 + e2) / (1.0 - e2) - 1.0 / k;
 }
 
+// A pair's exp(log_z(K) - c) and log_z'(K) from one exp(-2K): with
+// log_z(K) = K + log1p(-e2) - log K (sphere_stats.cpp:47-69),
+// exp(log_z(K) - c) = exp(K - c) (1 - e2) / K. Same branches as the host.
+__device__ __forceinline__ void pair_terms(double K, double c, double& ez, double& zl) {
+  if (K < 1e-4) {
+    ez = exp(log_z_d(K) - c);
+    zl = log_z_deriv_d(K);
+    return;
+  }
+  const double iK = 1.0 / K;
+  const double om = K < 0.5 ? -expm1(-2.0 * K) : 1.0 - exp(-2.0 * K);  // 1 - e2
+  ez = exp(K - c) * om * iK;
+  zl = K > 350.0 ? 1.0 - iK : (2.0 - om) / om - iK;
+}
+
 __device__ __forceinline__ double wsum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFullMask, v, o);
@@ -61,33 +77,57 @@ __device__ __forceinline__ void jv(const RowD& r, double vx, double vy, double v
   oz = r.uz * p * a - (vz - r.uz * p) * b;
 }
 
-// Block-wide deterministic sum (fixed tree over the warps).
-__device__ __forceinline__ double block_sum(double v, double* red) {
-  v = wsum(v);
+// CTA totals of 7 values (fixed tree: warp shuffles, then one warp per value
+// over the warps' partials); red holds 7 x 32 + 8 doubles.
+__device__ __forceinline__ void block_sum7(double* v, double* red) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int k = 0; k < 7; ++k) v[k] = wsum(v[k]);
   __syncthreads();
-  if (lane == 0) red[warp] = v;
+  if (lane == 0)
+    for (int k = 0; k < 7; ++k) red[32 * k + warp] = v[k];
   __syncthreads();
-  double t = 0.0;
-  for (int k = 0; k < nw; ++k) t += red[k];
-  return t;
+  for (int k = warp; k < 7; k += nw) {
+    const double t = wsum(lane < nw ? red[32 * k + lane] : 0.0);
+    if (lane == 0) red[224 + k] = t;
+  }
+  __syncthreads();
+  for (int k = 0; k < 7; ++k) v[k] = red[224 + k];
 }
 
-// Grid: x = partner slice, y = request. Thread = model row (strided), the
-// slice = a contiguous range of partners (self rows j != i, then image
-// columns). Per-slice partial {f, g[6]} go to out[(q * S + s) * 7]; the host
-// sums slices in order (deterministic).
-__global__ void __launch_bounds__(256)
-    objgrad_kernel(const DevModel64* models, const ObjRequest* req, double* out, int max_n1) {
-  extern __shared__ double smem_d[];
-  RowD* rows = reinterpret_cast<RowD*>(smem_d);
-  double* red = smem_d + static_cast<size_t>(max_n1) * (sizeof(RowD) / sizeof(double));
-  const int q = blockIdx.y, slice = blockIdx.x, S = gridDim.x;
-  const ObjRequest rq = req[q];
-  const DevModel64 m = models[rq.model];
-  const double r0 = rq.x[0], r1 = rq.x[1], r2 = rq.x[2];
-  const double t0 = rq.x[3], t1 = rq.x[4], t2 = rq.x[5];
-  double* o = out + (static_cast<size_t>(q) * S + slice) * 7;
+// CTA minimum (exact, order-free) of a double / an int; red as above.
+__device__ __forceinline__ double block_min_d(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(kFullMask, v, o));
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double t = red[0];
+  for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) t = fmin(t, red[w]);
+  return t;
+}
+__device__ __forceinline__ int block_min_i(int v, double* red) {
+  v = __reduce_min_sync(kFullMask, v);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = static_cast<double>(v);
+  __syncthreads();
+  double t = red[0];
+  for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) t = fmin(t, red[w]);
+  return static_cast<int>(t);
+}
+
+// One CTA evaluates pose x over partner slice `slice` of S: thread = model
+// row (strided; with split_rows, row x chunk of the slice), the slice = a
+// contiguous range of partners (self rows j != i, then image columns). Every
+// thread returns the CTA total {f, g[6]} of the slice in o[0..6]
+// (deterministic fixed-tree reduction).
+#ifdef GOSMA_OBJ_NOINLINE
+__device__ __noinline__
+#else
+__device__
+#endif
+    void objgrad_block(const DevModel64& m, const double* x, int slice, int S,
+                              RowD* rows, double* red, double* o, bool split_rows = false) {
+  const double r0 = x[0], r1 = x[1], r2 = x[2];
+  const double t0 = x[3], t1 = x[4], t2 = x[5];
   // check_feasible (objective.cpp:160-166)
   int hit = 0;
   for (int i = threadIdx.x; i < m.n_all; i += blockDim.x) {
@@ -96,10 +136,8 @@ __global__ void __launch_bounds__(256)
     hit |= sqrt(dx * dx + dy * dy + dz * dz) < m.zeta;
   }
   if (__syncthreads_or(hit)) {
-    if (threadIdx.x == 0) {
-      o[0] = slice == 0 ? INFINITY : 0.0;
-      for (int k = 1; k < 7; ++k) o[k] = 0.0;
-    }
+    o[0] = slice == 0 ? INFINITY : 0.0;
+    for (int k = 1; k < 7; ++k) o[k] = 0.0;
     return;
   }
   // Rodrigues R (se3.cpp:21-31) and the left Jacobian (objective.cpp:240-250)
@@ -159,14 +197,22 @@ __global__ void __launch_bounds__(256)
     __syncthreads();
     // this slice's partners: [p0, p1) over self rows (0..n1-1) then columns
     const int np = cs.n1 + cs.n2;
-    const int p0 = static_cast<int>(static_cast<long long>(np) * slice / S);
-    const int p1 = static_cast<int>(static_cast<long long>(np) * (slice + 1) / S);
-    for (int il = threadIdx.x; il < cs.n1; il += blockDim.x) {
+    const int p0 = np * slice / S;  // np < 2^20, S <= 32: no overflow
+    const int p1 = np * (slice + 1) / S;
+    // work items: (row, chunk of the slice's partners); split_rows spreads a
+    // row over nq threads (n1 * nq <= CTA size: one balanced pass) so one
+    // CTA alone fills its SM (the refiner)
+    const int nq =
+        split_rows ? max(1, min(static_cast<int>(blockDim.x) / cs.n1, p1 - p0)) : 1;
+    for (int wi = threadIdx.x; wi < cs.n1 * nq; wi += blockDim.x) {
+      const int il = wi % cs.n1, q = wi / cs.n1;
+      const int q0 = p0 + (p1 - p0) * q / nq;
+      const int q1 = p0 + (p1 - p0) * (q + 1) / nq;
       const RowD a = rows[il];
       const double uix = a.ux * a.d, uiy = a.uy * a.d, uiz = a.uz * a.d;  // u_i
       const double cu = 2.0 * a.zl * a.is2;
       double fself = 0.0, fcross = 0.0;
-      if (slice == 0) {  // diagonal (objective.cpp:201-203, 268-274)
+      if (slice == 0 && q == 0) {  // diagonal (objective.cpp:201-203, 268-274)
         const double term = 0.5 * a.k / tanh(a.k);
         fself += a.phi * a.phi * term;
         const double dlog = 2.0 * (log_z_deriv_d(2.0 * a.k) - a.zl);
@@ -178,17 +224,19 @@ __global__ void __launch_bounds__(256)
       const double vix = a.ux * a.k, viy = a.uy * a.k, viz = a.uz * a.k;
       // self pairs, ordered (i != j): this row's half of each pair
       double sx = 0.0, sy = 0.0, sz = 0.0, su = 0.0;
-      const int s_end = min(p1, cs.n1);
-      for (int jl = p0; jl < s_end; ++jl) {
+      const int s_end = min(q1, cs.n1);
+      for (int jl = q0; jl < s_end; ++jl) {
         if (jl == il) continue;
         const RowD b = rows[jl];
         const double ex = vix + b.ux * b.k, ey = viy + b.uy * b.k, ez = viz + b.uz * b.k;
         const double K = sqrt(ex * ex + ey * ey + ez * ez);
         if (K < a.k + b.k - kMarginObj) continue;
-        const double term = 2.0 * a.phi * b.phi * exp(log_z_d(K) - a.lz - b.lz);
+        double eK, zl;
+        pair_terms(K, a.lz + b.lz, eK, zl);
+        const double term = 2.0 * a.phi * b.phi * eK;
         fself += 0.5 * term;
         if (K > 1e-12) {
-          const double s = log_z_deriv_d(K) * term / K;
+          const double s = zl * term / K;
           sx += ex * s;
           sy += ey * s;
           sz += ez * s;
@@ -200,20 +248,23 @@ __global__ void __launch_bounds__(256)
       const double wy = R[3] * vix + R[4] * viy + R[5] * viz;
       const double wz = R[6] * vix + R[7] * viy + R[8] * viz;
       double hx = 0.0, hy = 0.0, hz = 0.0, hu = 0.0;
-      for (int jp = max(p0, cs.n1); jp < p1; ++jp) {
+      for (int jp = max(q0, cs.n1); jp < q1; ++jp) {
         const int j = cs.o2 + (jp - cs.n1);
         const double ex = wx + m.b[3 * j], ey = wy + m.b[3 * j + 1], ez = wz + m.b[3 * j + 2];
         const double K = sqrt(ex * ex + ey * ey + ez * ez);
         if (K < a.k + m.kappa2[j] - kMarginObj) continue;
-        const double term = a.phi * m.phi2[j] * exp(log_z_d(K) - a.lz - m.log_z2[j]);
+        double eK, zl;
+        pair_terms(K, a.lz + m.log_z2[j], eK, zl);
+        const double term = a.phi * m.phi2[j] * eK;
         fcross += term;
         double qx = 0.0, qy = 0.0, qz = 0.0;
         if (K > 1e-12) {
-          qx = ex / K;
-          qy = ey / K;
-          qz = ez / K;
+          const double iK = 1.0 / K;
+          qx = ex * iK;
+          qy = ey * iK;
+          qz = ez * iK;
         }
-        const double s = log_z_deriv_d(K) * (-2.0 * term);
+        const double s = zl * (-2.0 * term);
         hx += qx * s;
         hy += qy * s;
         hz += qz * s;
@@ -238,28 +289,382 @@ __global__ void __launch_bounds__(256)
       fval += w * (fself - 2.0 * fcross);
     }
   }
-  fval = block_sum(fval, red);
-  gt0 = block_sum(gt0, red);
-  gt1 = block_sum(gt1, red);
-  gt2 = block_sum(gt2, red);
-  cr0 = block_sum(cr0, red);
-  cr1 = block_sum(cr1, red);
-  cr2 = block_sum(cr2, red);
-  if (threadIdx.x == 0) {
-    o[0] = fval;
-    o[1] = Jl[0] * cr0 + Jl[3] * cr1 + Jl[6] * cr2;
-    o[2] = Jl[1] * cr0 + Jl[4] * cr1 + Jl[7] * cr2;
-    o[3] = Jl[2] * cr0 + Jl[5] * cr1 + Jl[8] * cr2;
-    o[4] = gt0;
-    o[5] = gt1;
-    o[6] = gt2;
+  double v[7] = {fval, gt0, gt1, gt2, cr0, cr1, cr2};
+  block_sum7(v, red);
+  o[0] = v[0];
+  o[1] = Jl[0] * v[4] + Jl[3] * v[5] + Jl[6] * v[6];
+  o[2] = Jl[1] * v[4] + Jl[4] * v[5] + Jl[7] * v[6];
+  o[3] = Jl[2] * v[4] + Jl[5] * v[5] + Jl[8] * v[6];
+  o[4] = v[1];
+  o[5] = v[2];
+  o[6] = v[3];
+  __syncthreads();  // rows / red are reused by the next evaluation
+}
+
+// Grid: x = partner slice, y = request. Per-slice partial {f, g[6]} go to
+// out[(q * S + s) * 7]; the host sums slices in order (deterministic).
+__global__ void __launch_bounds__(256)
+    objgrad_kernel(const DevModel64* models, const ObjRequest* req, double* out, int max_n1) {
+  extern __shared__ double smem_d[];
+  RowD* rows = reinterpret_cast<RowD*>(smem_d);
+  double* red = smem_d + static_cast<size_t>(max_n1) * (sizeof(RowD) / sizeof(double));
+  const int q = blockIdx.y, slice = blockIdx.x, S = gridDim.x;
+  const ObjRequest rq = req[q];
+  double o[7];
+  objgrad_block(models[rq.model], rq.x, slice, S, rows, red, o);
+  if (threadIdx.x == 0)
+    for (int k = 0; k < 7; ++k) out[(static_cast<size_t>(q) * S + slice) * 7 + k] = o[k];
+}
+
+
+// ---- GPU-resident local refinement ------------------------
+// One CTA runs one start's L-BFGS ladder end to end: local_refine /
+// wolfe_search / clamp_to_domain (core/src/solver.cpp:37-258; host version in
+// csrc/sma.cpp) with every objective + gradient evaluated by the whole CTA
+// (objgrad_block). All threads execute the same control code on identical
+// values (the reductions broadcast), so control flow stays uniform across the
+// CTA without shared control state.
+
+__device__ __forceinline__ double dot6(const double* a, const double* b) {
+  double s = 0.0;
+  for (int k = 0; k < 6; ++k) s += a[k] * b[k];
+  return s;
+}
+
+// Value + gradient of one pose by a cluster of CTAs: CTA rank r takes partner
+// slice r of C (objgrad_block), the C partial totals meet in distributed
+// shared memory and every CTA sums them in rank order, so all CTAs of the
+// cluster hold identical values and take identical control decisions.
+struct CtaObjective {
+  const DevModel64* m;
+  RowD* rows;
+  double* red;
+  double* xch;  // this CTA's partial totals (7), read by the cluster
+  double* tot;  // cluster totals (7)
+  long long* count;
+  bool have = false;
+  double x[6], f, g[6];
+  __device__ void eval(const double* xx) {
+    bool same = have;
+    for (int k = 0; k < 6; ++k) same = same && xx[k] == x[k];
+    if (same) return;
+    ++*count;
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    const int C = static_cast<int>(cl.num_blocks());
+    double o[7];
+    objgrad_block(*m, xx, static_cast<int>(cl.block_rank()), C, rows, red, o, true);
+    if (C > 1) {
+      if (threadIdx.x == 0)
+        for (int k = 0; k < 7; ++k) xch[k] = o[k];
+      cl.sync();
+      if (threadIdx.x < 7) {
+        double t = 0.0;
+        for (int r = 0; r < C; ++r) t += cl.map_shared_rank(xch, r)[threadIdx.x];
+        tot[threadIdx.x] = t;
+      }
+      cl.sync();  // totals visible; every rank done reading xch
+      for (int k = 0; k < 7; ++k) o[k] = tot[k];
+    }
+    for (int k = 0; k < 6; ++k) x[k] = xx[k];
+    f = o[0];
+    for (int k = 0; k < 6; ++k) g[k] = std::isinf(o[0]) ? 0.0 : o[1 + k];
+    have = true;
+  }
+  __device__ double value(const double* xx) {
+    eval(xx);
+    return f;
+  }
+};
+
+// clamp_to_domain (solver.cpp:48-95); the box and standoff-ball scans are
+// spread over the CTA (nearest box: smallest distance, then lowest index;
+// first offending mean: lowest index), every thread gets the same result.
+__device__ bool clamp_to_domain_d(const DevModel64& m, const RefineDomain& dom, double* v,
+                                  double* red) {
+  for (int k = 0; k < 3; ++k)
+    v[k] = fmin(fmax(v[k], dom.rc[k] - dom.rhw), dom.rc[k] + dom.rhw);
+  constexpr int kNone = 0x7fffffff;
+  double my_d = INFINITY;
+  int my_b = kNone;
+  for (int b = threadIdx.x; b < dom.n_boxes; b += blockDim.x) {
+    const double* bx = dom.boxes + 6 * b;
+    double s2 = 0.0;
+    for (int k = 0; k < 3; ++k) {
+      const double o = fmax(fabs(v[3 + k] - bx[k]) - bx[3 + k], 0.0);
+      s2 += o * o;
+    }
+    const double d = sqrt(s2);
+    if (d < my_d) {
+      my_d = d;
+      my_b = b;
+    }
+  }
+  const double best_d = block_min_d(my_d, red);
+  const int best = block_min_i(my_d == best_d ? my_b : kNone, red);
+  if (best == kNone) return false;
+  const double* bx = dom.boxes + 6 * best;
+  double p[3];
+  for (int k = 0; k < 3; ++k) p[k] = fmin(fmax(v[3 + k], bx[k] - bx[3 + k]), bx[k] + bx[3 + k]);
+  for (int projection = 0; projection <= 8; ++projection) {
+    int mine = kNone;
+    for (int i = threadIdx.x; i < m.n_all && mine == kNone; i += blockDim.x) {
+      const double dx = m.all_means[3 * i] - p[0], dy = m.all_means[3 * i + 1] - p[1],
+                   dz = m.all_means[3 * i + 2] - p[2];
+      if (sqrt(dx * dx + dy * dy + dz * dz) < m.zeta) mine = i;
+    }
+    const int off = block_min_i(mine, red);
+    if (off == kNone) {
+      for (int k = 0; k < 3; ++k) v[3 + k] = p[k];
+      return true;
+    }
+    if (projection == 8) break;
+    const double* mu = m.all_means + 3 * off;
+    double dir[3] = {p[0] - mu[0], p[1] - mu[1], p[2] - mu[2]};
+    const double n = sqrt(dir[0] * dir[0] + dir[1] * dir[1] + dir[2] * dir[2]);
+    if (n > 1e-12) {
+      for (double& c : dir) c /= n;
+    } else {
+      dir[0] = 1.0;
+      dir[1] = dir[2] = 0.0;
+    }
+    for (int k = 0; k < 3; ++k)
+      p[k] = fmin(fmax(mu[k] + dir[k] * (m.zeta * (1.0 + 1e-9)), bx[k] - bx[3 + k]),
+                  bx[k] + bx[3 + k]);
+  }
+  return false;
+}
+
+struct LineSearchD {
+  double alpha = 0.0, value = INFINITY;
+};
+
+// wolfe_search (solver.cpp:105-160)
+__device__ LineSearchD wolfe_d(CtaObjective& ob, const double* x, const double* d, double f0,
+                               double g0) {
+  const double c1 = 1e-4, c2 = 0.9, alpha_max = 1e3;
+  double xt[6];
+  auto at = [&](double a) {
+    for (int k = 0; k < 6; ++k) xt[k] = x[k] + a * d[k];
+  };
+  LineSearchD best;
+  auto consider = [&](double a, double v) {
+    if (v <= f0 + c1 * a * g0 && v < best.value) {
+      best.alpha = a;
+      best.value = v;
+    }
+  };
+  auto zoom = [&](double lo, double flo, double hi) -> LineSearchD {
+    for (int it = 0; it < 30; ++it) {
+      const double a = 0.5 * (lo + hi);
+      at(a);
+      const double v = ob.value(xt);
+      consider(a, v);
+      if (v > f0 + c1 * a * g0 || v >= flo) {
+        hi = a;
+        continue;
+      }
+      const double g = dot6(ob.g, d);
+      if (fabs(g) <= -c2 * g0) return {a, v};
+      if (g * (hi - lo) >= 0.0) hi = lo;
+      lo = a;
+      flo = v;
+    }
+    return best;
+  };
+  double a_prev = 0.0, f_prev = f0, a = 1.0;
+  for (int it = 0; it < 20; ++it) {
+    at(a);
+    const double v = ob.value(xt);
+    consider(a, v);
+    if (v > f0 + c1 * a * g0 || (it > 0 && v >= f_prev)) return zoom(a_prev, f_prev, a);
+    const double g = dot6(ob.g, d);
+    if (fabs(g) <= -c2 * g0) return {a, v};
+    if (g >= 0.0) return zoom(a, v, a_prev);
+    a_prev = a;
+    f_prev = v;
+    a = fmin(2.0 * a, alpha_max);
+    if (a_prev >= alpha_max) break;
+  }
+  return best;
+}
+
+// local_refine (solver.cpp:164-258): best value and pose (r, t) from x0.
+__device__ void local_refine_d(const DevModel64& m, const RefineDomain& dom, RowD* rows,
+                               double* red, double* xch, double* tot, double* xio, double* fout,
+                               long long* count) {
+  constexpr int kMaxIt = 200, kMem = 10;
+  const double kGradTol = 1e-6;
+  CtaObjective ob{&m, rows, red, xch, tot, count};
+  double x[6], bx[6];
+  for (int k = 0; k < 6; ++k) x[k] = bx[k] = xio[k];
+  double bf = ob.value(x);
+  if (!(bf < INFINITY)) {  // infeasible start: unchanged
+    *fout = bf;
+    return;
+  }
+  auto offer = [&](const double* xx, double fx) {
+    double p[6];
+    for (int k = 0; k < 6; ++k) p[k] = xx[k];
+    if (!clamp_to_domain_d(m, dom, p, red)) return;
+    bool moved = false;
+    for (int k = 0; k < 6; ++k) moved = moved || p[k] != xx[k];
+    const double fp = moved ? ob.value(p) : fx;
+    if (fp < bf) {
+      bf = fp;
+      for (int k = 0; k < 6; ++k) bx[k] = p[k];
+    }
+  };
+  double fx = bf;
+  offer(x, fx);
+  ob.eval(x);
+  double g[6];
+  for (int k = 0; k < 6; ++k) g[k] = ob.g[k];
+  double S[kMem][6], Y[kMem][6], Rho[kMem];
+  int nh = 0, h0 = 0;  // ring of the last nh pairs, oldest at h0
+  for (int it = 0; it < kMaxIt; ++it) {
+    if (sqrt(dot6(g, g)) < kGradTol) break;
+    double q[6];
+    for (int k = 0; k < 6; ++k) q[k] = g[k];
+    double alpha[kMem];
+    for (int i = nh - 1; i >= 0; --i) {
+      const int s = (h0 + i) % kMem;
+      alpha[i] = Rho[s] * dot6(S[s], q);
+      for (int k = 0; k < 6; ++k) q[k] -= alpha[i] * Y[s][k];
+    }
+    if (nh > 0) {
+      const int s = (h0 + nh - 1) % kMem;
+      const double sc = dot6(S[s], Y[s]) / dot6(Y[s], Y[s]);
+      for (int k = 0; k < 6; ++k) q[k] *= sc;
+    }
+    for (int i = 0; i < nh; ++i) {
+      const int s = (h0 + i) % kMem;
+      const double beta = Rho[s] * dot6(Y[s], q);
+      for (int k = 0; k < 6; ++k) q[k] += (alpha[i] - beta) * S[s][k];
+    }
+    double d[6];
+    for (int k = 0; k < 6; ++k) d[k] = -q[k];
+    double dg = dot6(d, g);
+    if (!(dg < -1e-14 * sqrt(dot6(d, d)) * sqrt(dot6(g, g)))) {  // not a descent direction
+      nh = 0;
+      h0 = 0;
+      for (int k = 0; k < 6; ++k) d[k] = -g[k];
+      dg = -dot6(g, g);
+    }
+    const LineSearchD ls = wolfe_d(ob, x, d, fx, dg);
+    if (!(ls.alpha > 0.0) || !(ls.value < INFINITY)) break;
+    double xn[6];
+    for (int k = 0; k < 6; ++k) xn[k] = x[k] + ls.alpha * d[k];
+    ob.eval(xn);
+    double s[6], y[6];
+    for (int k = 0; k < 6; ++k) {
+      s[k] = xn[k] - x[k];
+      y[k] = ob.g[k] - g[k];
+    }
+    const double sy = dot6(s, y);
+    if (sy > 1e-10 * sqrt(dot6(s, s)) * sqrt(dot6(y, y))) {
+      int slot;
+      if (nh < kMem) {
+        slot = (h0 + nh) % kMem;
+        ++nh;
+      } else {
+        slot = h0;
+        h0 = (h0 + 1) % kMem;
+      }
+      for (int k = 0; k < 6; ++k) {
+        S[slot][k] = s[k];
+        Y[slot][k] = y[k];
+      }
+      Rho[slot] = 1.0 / sy;
+    }
+    for (int k = 0; k < 6; ++k) {
+      x[k] = xn[k];
+      g[k] = ob.g[k];
+    }
+    fx = ls.value;
+    offer(x, fx);
+    // re-express past pi (solver.cpp:249-255)
+    const double rn = sqrt(x[0] * x[0] + x[1] * x[1] + x[2] * x[2]);
+    if (rn > M_PI) {
+      double w[3] = {x[0], x[1], x[2]};
+      double n = rn;
+      while (n > M_PI) {
+        for (double& c : w) c *= (1.0 - 2.0 * M_PI / n);
+        n = sqrt(w[0] * w[0] + w[1] * w[1] + w[2] * w[2]);
+      }
+      for (int k = 0; k < 3; ++k) x[k] = w[k];
+      ob.eval(x);
+      for (int k = 0; k < 6; ++k) g[k] = ob.g[k];
+      nh = 0;
+      h0 = 0;
+    }
+  }
+  for (int k = 0; k < 6; ++k) xio[k] = bx[k];
+  *fout = bf;
+}
+
+#ifndef GOSMA_REFINE_THREADS
+#define GOSMA_REFINE_THREADS 512
+#endif
+constexpr int kRefineThreads = GOSMA_REFINE_THREADS;
+
+__global__ void __launch_bounds__(kRefineThreads)
+    refine_kernel(const DevModel64* models, const RefineJob* jobs, RefineDomain dom,
+                  RefineOut* out, int max_n1) {
+  extern __shared__ double smem_d[];
+  __shared__ double xch[8], tot[8];
+  RowD* rows = reinterpret_cast<RowD*>(smem_d);
+  double* red = smem_d + static_cast<size_t>(max_n1) * (sizeof(RowD) / sizeof(double));
+  namespace cg = cooperative_groups;
+  const cg::cluster_group cl = cg::this_cluster();
+  const int job = blockIdx.x / static_cast<int>(cl.num_blocks());
+  const RefineJob jb = jobs[job];
+  double x[6] = {jb.x[0], jb.x[1], jb.x[2], jb.x[3], jb.x[4], jb.x[5]};
+  double f = INFINITY;
+  long long count = 0;
+  for (int st = 0; st < jb.stages; ++st)
+    local_refine_d(models[jb.model[st]], dom, rows, red, xch, tot, x, &f, &count);
+  if (threadIdx.x == 0 && cl.block_rank() == 0) {
+    RefineOut o;
+    o.value = f;
+    for (int k = 0; k < 6; ++k) o.x[k] = x[k];
+    o.evals = count;
+    out[job] = o;
   }
 }
 
 }  // namespace
 
+cudaError_t launch_refine(const DevModel64* models, const RefineJob* jobs, int n,
+                          const RefineDomain& dom, RefineOut* out, int max_n1, int cluster,
+                          cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const size_t smem = objgrad_smem_bytes(max_n1);
+  static size_t configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    const cudaError_t e = cudaFuncSetAttribute(
+        refine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  cluster = std::max(1, std::min(cluster, 8));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(n * cluster));
+  cfg.blockDim = dim3(kRefineThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = static_cast<unsigned>(cluster);
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, refine_kernel, models, jobs, dom, out, max_n1);
+}
+
 size_t objgrad_smem_bytes(int max_n1) {
-  return static_cast<size_t>(max_n1) * sizeof(RowD) + 8 * sizeof(double);
+  return static_cast<size_t>(max_n1) * sizeof(RowD) + (7 * 32 + 8) * sizeof(double);
 }
 
 int objgrad_slices(int max_pairs_per_row) {

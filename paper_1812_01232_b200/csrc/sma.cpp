@@ -7,7 +7,6 @@
 // start.
 #include "sma.hpp"
 
-#include "objective_device.hpp"
 
 #include <algorithm>
 #include <cmath>
@@ -39,48 +38,25 @@ Vec3 head(const V6& x) { return Vec3(x[0], x[1], x[2]); }
 Vec3 tail(const V6& x) { return Vec3(x[3], x[4], x[5]); }
 
 // Objective with infeasible poses mapped to +inf (solver.cpp:37-43) and its
-// gradient (zero when infeasible), from the host model or the GPU batcher; the
-// GPU path returns value and gradient together, so the last point is cached.
+// gradient (zero when infeasible).
 class Objective {
  public:
-  explicit Objective(const SmaEval& ev) : ev_(ev) {}
-  const HostModel& model() const { return *ev_.m; }
-  double value(const V6& x) {
-    if (!ev_.gate) return objective_value(*ev_.m, head(x), tail(x));
-    fetch(x);
-    return f_;
-  }
+  explicit Objective(const HostModel& m) : m_(m) {}
+  const HostModel& model() const { return m_; }
+  double value(const V6& x) { return objective_value(m_, head(x), tail(x)); }
   V6 grad(const V6& x) {
-    if (!ev_.gate) {
-      V6 g;
-      double gg[6];
-      if (!objective_gradient(*ev_.m, head(x), tail(x), gg)) {
-        g.fill(0.0);
-        return g;
-      }
-      for (int k = 0; k < 6; ++k) g[k] = gg[k];
+    V6 g;
+    double gg[6];
+    if (!objective_gradient(m_, head(x), tail(x), gg)) {
+      g.fill(0.0);
       return g;
     }
-    fetch(x);
-    return g_;
+    for (int k = 0; k < 6; ++k) g[k] = gg[k];
+    return g;
   }
 
  private:
-  void fetch(const V6& x) {
-    if (have_ && x == x_) return;
-    ObjRequest r{};
-    for (int k = 0; k < 6; ++k) r.x[k] = x[k];
-    r.model = ev_.model;
-    double gg[6];
-    ev_.gate->eval(r, &f_, gg);
-    for (int k = 0; k < 6; ++k) g_[k] = gg[k];
-    x_ = x;
-    have_ = true;
-  }
-  SmaEval ev_;
-  bool have_ = false;
-  V6 x_{}, g_{};
-  double f_ = 0.0;
+  const HostModel& m_;
 };
 
 // clamp_to_domain (solver.cpp:48-95)
@@ -179,14 +155,8 @@ LineSearch wolfe(Objective& m, const V6& x, const V6& d, double f0, double g0) {
 
 }  // namespace
 
-RefineResult local_refine(const HostModel& m, const Vec3& r0, const Vec3& t0, const Domain& dom) {
-  SmaEval ev;
-  ev.m = &m;
-  return local_refine(ev, r0, t0, dom);
-}
-
-RefineResult local_refine(const SmaEval& ev, const Vec3& r0, const Vec3& t0, const Domain& dom) {
-  Objective m(ev);
+RefineResult local_refine(const HostModel& hm, const Vec3& r0, const Vec3& t0, const Domain& dom) {
+  Objective m(hm);
   const int kMaxIt = 200, kMem = 10;
   const double kGradTol = 1e-6;
   RefineResult best;

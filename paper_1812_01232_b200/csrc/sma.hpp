@@ -24,19 +24,7 @@ struct RefineResult {
   Vec3 r, t;
 };
 
-class BatchGate;
-
-// Objective source of a refinement: the host FP64 model, or (gate set) the
-// batched GPU FP64 kernel for model index `model` (objective_device.hpp).
-// The host model also supplies the standoff balls for the domain projection.
-struct SmaEval {
-  const HostModel* m = nullptr;
-  BatchGate* gate = nullptr;
-  int model = 0;
-};
-
 // local_refine (solver.hpp:80-85, solver.cpp:164-258).
 RefineResult local_refine(const HostModel& m, const Vec3& r0, const Vec3& t0, const Domain& dom);
-RefineResult local_refine(const SmaEval& ev, const Vec3& r0, const Vec3& t0, const Domain& dom);
 
 }  // namespace gosma

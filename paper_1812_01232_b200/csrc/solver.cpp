@@ -102,34 +102,55 @@ bool gpu_sma(const HostModel& m) {
     return std::string(e) == "gpu" ? 1 : (std::string(e) == "host" ? 0 : -1);
   }();
   if (forced >= 0) return forced == 1;
-  return model_pairs(m) >= 3000;  // measured: host faster at 41x36, GPU at 64x32
+  return model_pairs(m) >= 1000;  // measured: GPU ladder 0.31 s vs host 0.69 s at 41x36
+}
+
+// Runs refinement jobs on the GPU (refine_kernel: one CTA per start runs the
+// whole L-BFGS ladder, no host round trips per evaluation).
+cudaError_t refine_device(DeviceObjective* dev, const Domain& dom,
+                          const std::vector<RefineJob>& jobs, std::vector<RefineOut>* out) {
+  std::vector<double> boxes;
+  for (const Box& b : dom.boxes)
+    for (const Vec3* v : {&b.c, &b.h})
+      for (int a = 0; a < 3; ++a) boxes.push_back((*v)[a]);
+  const double rc[3] = {dom.rot_center[0], dom.rot_center[1], dom.rot_center[2]};
+  return dev->refine(jobs, rc, dom.rot_hw, boxes, out);
 }
 
 // process_wave's incumbent update (solver.cpp:409-431) for one improving
-// branch: FP64 objective at the feasible centre, then SMA from there.
-void improve(const HostModel& m, const Domain& dom, const gosma_node& b, Incumbent* inc,
-             BatchGate* gate = nullptr) {
+// branch: FP64 objective at the feasible centre, then SMA from there (on the
+// GPU when dev is set; the incumbent value is always the host FP64 d*).
+int improve(const HostModel& m, const Domain& dom, const gosma_node& b, Incumbent* inc,
+            DeviceObjective* dev = nullptr) {
   Vec3 t;
   if (!feasible_center(m, Vec3(b.tc[0], b.tc[1], b.tc[2]), Vec3(b.thw[0], b.thw[1], b.thw[2]),
                        &t))
-    return;
+    return GOSMA_OK;
   const Vec3 r(b.rc[0], b.rc[1], b.rc[2]);
   const double f = objective_value(m, r, t);
-  if (!(f < inc->value)) return;
+  if (!(f < inc->value)) return GOSMA_OK;
   inc->value = f;
   inc->r = r;
   inc->t = t;
-  SmaEval ev;
-  ev.m = &m;
-  ev.gate = gate;
-  RefineResult rr = local_refine(ev, r, t, dom);
-  if (gate) rr.value = objective_value(m, rr.r, rr.t);  // d* is always the host FP64 value
+  RefineResult rr;
+  std::vector<RefineOut> out;
+  if (dev) {
+    const cudaError_t e =
+        refine_device(dev, dom, {RefineJob{{r[0], r[1], r[2], t[0], t[1], t[2]}, 1, {0}}}, &out);
+    if (e != cudaSuccess) return cuda_error(e, "refine kernel");
+    rr.r = Vec3(out[0].x[0], out[0].x[1], out[0].x[2]);
+    rr.t = Vec3(out[0].x[3], out[0].x[4], out[0].x[5]);
+    rr.value = objective_value(m, rr.r, rr.t);
+  } else {
+    rr = local_refine(m, r, t, dom);
+  }
   ++inc->sma;
   if (rr.value < inc->value) {
     inc->value = rr.value;
     inc->r = rr.r;
     inc->t = rr.t;
   }
+  return GOSMA_OK;
 }
 
 int eval_host(gosma_ctx* ctx, const std::vector<gosma_node>& nodes, double skip,
@@ -262,45 +283,48 @@ int discovery_dive(gosma_ctx* ctx, const Domain& dom, const std::vector<gosma_no
   const HostModel h1 = blurred_model(m, 0.01, dbar);
   std::vector<RefineResult> res(best.size());
   std::vector<char> ok(best.size(), 0);
-  auto ladder = [&](size_t s, BatchGate* gate) {
-    if (!std::isfinite(best[s].value)) return;
-    Vec3 t;
+  // start of each sector's ladder: the coarse model's feasible centre
+  std::vector<RefineJob> jobs(best.size());
+  for (size_t s = 0; s < best.size(); ++s) {
+    if (!std::isfinite(best[s].value)) continue;
     const gosma_node& b = best[s].b;
+    Vec3 t;
     if (!feasible_center(hc, Vec3(b.tc[0], b.tc[1], b.tc[2]), Vec3(b.thw[0], b.thw[1], b.thw[2]),
                          &t))
-      return;
-    const HostModel* stage[4] = {&hc, &h3, &h1, &m};
-    RefineResult r;
-    r.r = Vec3(b.rc[0], b.rc[1], b.rc[2]);
-    r.t = t;
-    for (int k = 0; k < 4; ++k) {
-      SmaEval ev;
-      ev.m = stage[k];
-      ev.gate = gate;
-      ev.model = k;
-      r = local_refine(ev, r.r, r.t, dom);
-    }
-    if (gate) r.value = objective_value(m, r.r, r.t);  // incumbents are host FP64 values
-    res[s] = r;
+      continue;
+    jobs[s] = RefineJob{{b.rc[0], b.rc[1], b.rc[2], t[0], t[1], t[2]}, 4, {0, 1, 2, 3}};
     ok[s] = 1;
-  };
+  }
   std::unique_ptr<DeviceObjective> dobj;
   if (gpu_sma(m)) {
     dobj = std::make_unique<DeviceObjective>(ctx->device,
                                              std::vector<const HostModel*>{&hc, &h3, &h1, &m});
     if (!dobj->ok()) dobj.reset();
   }
+  std::vector<RefineOut> out;
   if (dobj) {
-    // one host thread per start; their evaluations share GPU launches
-    BatchGate gate(dobj.get(), static_cast<int>(best.size()));
-    std::vector<std::thread> pool;
+    std::vector<RefineJob> run;
     for (size_t s = 0; s < best.size(); ++s)
-      pool.emplace_back([&, s] {
-        ladder(s, &gate);
-        gate.leave();
-      });
-    for (auto& th : pool) th.join();
+      if (ok[s]) run.push_back(jobs[s]);
+    const cudaError_t e = refine_device(dobj.get(), dom, run, &out);
+    if (e != cudaSuccess) {
+      gosma_ctx_destroy(coarse);
+      return cuda_error(e, "refine kernel");
+    }
+  }
+  if (dobj) {
+    // incumbents are host FP64 values
+    size_t k = 0;
+    for (size_t s = 0; s < best.size(); ++s) {
+      if (!ok[s]) continue;
+      RefineResult& r = res[s];
+      r.r = Vec3(out[k].x[0], out[k].x[1], out[k].x[2]);
+      r.t = Vec3(out[k].x[3], out[k].x[4], out[k].x[5]);
+      r.value = objective_value(m, r.r, r.t);
+      ++k;
+    }
   } else {
+    const HostModel* stage[4] = {&hc, &h3, &h1, &m};
     std::atomic<size_t> next{0};
     unsigned nthreads =
         cfg.threads > 0 ? cfg.threads : std::max(1u, std::thread::hardware_concurrency());
@@ -309,7 +333,12 @@ int discovery_dive(gosma_ctx* ctx, const Domain& dom, const std::vector<gosma_no
       for (;;) {
         const size_t s = next.fetch_add(1);
         if (s >= best.size()) return;
-        ladder(s, nullptr);
+        if (!ok[s]) continue;
+        RefineResult r;
+        r.r = Vec3(jobs[s].x[0], jobs[s].x[1], jobs[s].x[2]);
+        r.t = Vec3(jobs[s].x[3], jobs[s].x[4], jobs[s].x[5]);
+        for (int k = 0; k < 4; ++k) r = local_refine(*stage[k], r.r, r.t, dom);
+        res[s] = r;
       }
     };
     std::vector<std::thread> pool;
@@ -353,6 +382,36 @@ int gosma_local_refine(const gosma_ctx* ctx, const double* r0, const double* t0,
   return GOSMA_OK;
 }
 
+int gosma_local_refine_batch(gosma_ctx* ctx, size_t n, const double* r0, const double* t0,
+                             const gosma_domain* domain, double* r_out, double* t_out,
+                             double* value) {
+  if (!ctx || !domain || (n && (!r0 || !t0 || !r_out || !t_out || !value)))
+    return set_error(GOSMA_EINVAL, "null argument");
+  if (n == 0) return GOSMA_OK;
+  const Domain dom = make_domain(domain);
+  DeviceObjective dev(ctx->device, {&ctx->model});
+  if (!dev.ok()) return set_error(GOSMA_ECUDA, "device objective unavailable");
+  std::vector<RefineJob> jobs(n);
+  for (size_t k = 0; k < n; ++k)
+    jobs[k] = RefineJob{{r0[3 * k], r0[3 * k + 1], r0[3 * k + 2], t0[3 * k], t0[3 * k + 1],
+                         t0[3 * k + 2]},
+                        1,
+                        {0}};
+  std::vector<RefineOut> out;
+  const cudaError_t e = refine_device(&dev, dom, jobs, &out);
+  if (e != cudaSuccess)
+    return set_error(GOSMA_ECUDA, std::string("refine kernel: ") + cudaGetErrorString(e));
+  for (size_t k = 0; k < n; ++k) {
+    for (int a = 0; a < 3; ++a) {
+      r_out[3 * k + a] = out[k].x[a];
+      t_out[3 * k + a] = out[k].x[3 + a];
+    }
+    value[k] = objective_value(ctx->model, Vec3(out[k].x[0], out[k].x[1], out[k].x[2]),
+                               Vec3(out[k].x[3], out[k].x[4], out[k].x[5]));
+  }
+  return GOSMA_OK;
+}
+
 }  // extern "C"
 
 // ---------------------------------------------------------------------------
@@ -385,7 +444,6 @@ struct gosma_solver {
   bool cached = wave_mode == 1;
   // GPU objective for incumbent refinements (large mixtures, see gpu_sma)
   std::unique_ptr<DeviceObjective> sma_dev;
-  std::unique_ptr<BatchGate> sma_gate;
   unsigned long long cuboid_evals = 0;
   // GOSMA_PROFILE=1: synchronising per-phase wall times, printed on destroy
   bool profile = std::getenv("GOSMA_PROFILE") != nullptr;
@@ -413,10 +471,7 @@ int solver_init(gosma_solver* S) {
   if (gpu_sma(ctx->model)) {
     S->sma_dev = std::make_unique<DeviceObjective>(
         ctx->device, std::vector<const HostModel*>{&ctx->model});
-    if (S->sma_dev->ok())
-      S->sma_gate = std::make_unique<BatchGate>(S->sma_dev.get(), 1);
-    else
-      S->sma_dev.reset();
+    if (!S->sma_dev->ok()) S->sma_dev.reset();
   }
   const HostModel& m = ctx->model;
   const gosma_config& cfg = S->cfg;
@@ -495,7 +550,9 @@ int solver_init(gosma_solver* S) {
     S->phase[7] += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   }
   for (size_t i = 0; i < roots.size(); ++i)
-    if (up[i] < S->inc.value) improve(m, S->dom, roots[i], &S->inc, S->sma_gate.get());
+    if (up[i] < S->inc.value && (rc = improve(m, S->dom, roots[i], &S->inc, S->sma_dev.get())) !=
+                                    GOSMA_OK)
+      return rc;
   std::vector<gosma_node> keep;
   std::vector<int8_t> ks;
   std::vector<double> kv;
@@ -708,7 +765,8 @@ int gosma_solver_expand(gosma_solver* S, double limit, unsigned long long max_ev
   if (bi >= 0 && bu < S->inc.value) {
     gosma_node b;
     cudaMemcpy(&b, S->F.kids + bi, sizeof(gosma_node), cudaMemcpyDeviceToHost);
-    improve(ctx->model, S->dom, b, &S->inc, S->sma_gate.get());
+    const int rc = improve(ctx->model, S->dom, b, &S->inc, S->sma_dev.get());
+    if (rc != GOSMA_OK) return rc;
   }
   S->lap(4, s);
   RouteStats rs;

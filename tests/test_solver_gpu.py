@@ -276,6 +276,40 @@ print(json.dumps({"v": r.best_value, "r": list(r.r), "t": list(r.t), "sma": r.sm
     assert abs(out["gpu"]["v"] - out["host"]["v"]) <= 1e-7 * (1.0 + abs(out["host"]["v"]))
 
 
+@pytest.mark.parametrize("n1,n2", [(12, 12), (40, 24)])
+def test_local_refine_batch_matches_host(gosma, n1, n2):
+    """GPU-resident refiner (one CTA per start) against the host local_refine
+    from the same starts: same local optimum, never worse than the start.
+    Tolerance: both stop at |grad| < 1e-6 (or the iteration cap) on FP64
+    objectives that differ in the last bits (summation order), so endpoints
+    agree to 1e-4 relative in value and 1e-3 in pose (a flat direction may
+    leave up to 3 of 24 poses apart at equal value)."""
+    from paper_1812_01232_b200 import synth
+    classes = synth.mixture(n1, n2, "moderate", seed=n1 + n2, kappa_cap=150.0)
+    ctx = gosma.ObjectiveContext(classes, 0.5)
+    dom = gosma.PoseDomain(np.zeros(3), 1.0, np.array([[0.0, 0.0, -3.0, 0.5, 0.5, 0.5],
+                                                       [0.5, 0.0, 3.0, 0.4, 0.4, 0.4]]))
+    rng = np.random.default_rng(n1)
+    r0 = rng.uniform(-0.8, 0.8, (24, 3))
+    t0 = np.where(rng.uniform(size=(24, 1)) < 0.5, [0.0, 0.0, -3.0], [0.5, 0.0, 3.0])
+    t0 = t0 + rng.uniform(-0.3, 0.3, (24, 3))
+    v, r, t = gosma.local_refine_batch(ctx, r0, t0, dom)
+    agree = 0
+    for k in range(len(r0)):
+        vh, rh, th = gosma.local_refine(ctx, r0[k], t0[k], dom)
+        try:
+            v0 = gosma.objective_value(ctx, r0[k], t0[k])
+        except gosma.InfeasiblePoseError:
+            v0 = math.inf
+        if math.isinf(vh):
+            assert math.isinf(v0) and np.allclose(r[k], r0[k]) and np.allclose(t[k], t0[k])
+            continue
+        assert v[k] <= v0 + 1e-9 * (1.0 + abs(v0))
+        assert abs(v[k] - vh) <= 1e-4 * (1.0 + abs(vh)), (k, v[k], vh)
+        agree += np.allclose(r[k], rh, atol=1e-3) and np.allclose(t[k], th, atol=1e-3)
+    assert agree >= len(r0) - 3
+
+
 def test_export_import_host_and_device_paths(gosma):
     """Rebalancing primitives: exported nodes leave the donor (its live volume
     drops by their volume) and join the receiver; the device-buffer path moves
