@@ -266,9 +266,11 @@ const char* gosma_last_error(void);
 /* Build / device introspection for benches and tests. */
 int gosma_device_info(int device, int* sm_count, int* sm_clock_khz, int* cc_major,
                       int* cc_minor);
-/* A finished solver's frontier pool (when >= 16M nodes) is kept per device for
- * the next solve instead of being freed (unmapping tens of GB is slow); this
- * frees the kept pool of `device`. */
+/* A finished solver's device buffers are kept per device for the next solve
+ * instead of being freed (the frontier pool when >= 16M nodes; every other
+ * frontier block, up to 8 GB, in an exact-size cache): cudaMalloc / cudaFree
+ * of large blocks cost milliseconds to tenths of a second. This frees what is
+ * kept for `device`. */
 int gosma_release_cached_memory(int device);
 
 /* Batched objective_value + objective_gradient (objective.cpp:175-334) on the
