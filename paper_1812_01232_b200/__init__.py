@@ -354,7 +354,8 @@ def objective_value(ctx: ObjectiveContext, r, t) -> float:
 
 
 def release_cached_memory(device: int = 0):
-    """Frees the frontier pool a finished solver left parked on `device`."""
+    """Frees the device buffers finished solvers left cached on `device`
+    (the parked frontier pool and the exact-size block cache)."""
     _check(lib.gosma_release_cached_memory(device), "release_cached_memory")
 
 

@@ -365,3 +365,30 @@ def test_certified_optimum_matches_reference_on_random_instances(gosma):
         assert r.global_lower <= inst["best_value"] + 1e-9
         assert inst["global_lower"] <= r.best_value + 1e-9
         check_invariants(r, eps)
+
+
+def test_cached_blocks_are_reused_and_released(gosma):
+    """Solves reuse the frontier blocks an earlier solve left cached (same
+    result, same evaluations); release_cached_memory hands them back to the
+    driver and the next solve allocates afresh."""
+    import json
+    import torch
+    G = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "certify_golden.json")))
+    inst = max(G["instances"], key=lambda x: x["bound_evaluations"])
+    mix = Mixture.from_dict(inst["mixture"])
+    ctx = gosma.ObjectiveContext([{"mu": mix.mu, "sigma2": mix.sigma2, "phi1": mix.phi1,
+                                   "dir": mix.dir, "kappa2": mix.kappa2, "phi2": mix.phi2}],
+                                 mix.zeta, single_mixture=True)
+    dom = gosma.PoseDomain(np.array(inst["rot_c"]), inst["rot_hw"], np.array(inst["boxes"]))
+    cfg = gosma.SolverConfig(epsilon=inst["epsilon"], zeta=mix.zeta, time_limit=120)
+    ref = gosma.solve(ctx, dom, cfg)
+    assert ref.status == "epsilon_optimal"
+    again = gosma.solve(ctx, dom, cfg)
+    assert (again.best_value, again.global_lower, again.bound_evaluations) == \
+        (ref.best_value, ref.global_lower, ref.bound_evaluations)
+    free_cached = torch.cuda.mem_get_info(0)[0]
+    gosma.release_cached_memory(0)
+    assert torch.cuda.mem_get_info(0)[0] > free_cached  # the cache held device memory
+    fresh = gosma.solve(ctx, dom, cfg)
+    assert (fresh.best_value, fresh.global_lower, fresh.bound_evaluations) == \
+        (ref.best_value, ref.global_lower, ref.bound_evaluations)
