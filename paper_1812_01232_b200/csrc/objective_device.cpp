@@ -94,6 +94,9 @@ DeviceObjective::~DeviceObjective() {
   for (void* p : owned_) cudaFree(p);
   cudaFree(d_req_);
   cudaFree(d_part_);
+  cudaFree(d_jobs_);
+  cudaFree(d_out_);
+  cudaFree(d_boxes_);
   if (stream_) cudaStreamDestroy(stream_);
   cudaSetDevice(cur);
 }
@@ -155,18 +158,34 @@ cudaError_t DeviceObjective::refine(const std::vector<RefineJob>& jobs, const do
   int cur = 0;
   cudaGetDevice(&cur);
   cudaSetDevice(device_);
-  RefineJob* d_jobs = nullptr;
-  RefineOut* d_out = nullptr;
-  double* d_boxes = nullptr;
-  cudaError_t e = cudaMalloc(&d_jobs, jobs.size() * sizeof(RefineJob));
-  if (e == cudaSuccess) e = cudaMalloc(&d_out, jobs.size() * sizeof(RefineOut));
-  if (e == cudaSuccess) e = cudaMalloc(&d_boxes, std::max<size_t>(boxes.size(), 6) * 8);
+  // persistent buffers (grown on demand): refinements run once per improving
+  // wave, so per-call cudaMalloc / cudaFree (a device sync each) would show
+  cudaError_t e = cudaSuccess;
+  if (jobs.size() > job_cap_) {
+    cudaFree(d_jobs_);
+    cudaFree(d_out_);
+    d_jobs_ = nullptr;
+    d_out_ = nullptr;
+    const size_t c = std::max<size_t>(jobs.size(), 64);
+    if ((e = cudaMalloc(&d_jobs_, c * sizeof(RefineJob))) == cudaSuccess)
+      e = cudaMalloc(&d_out_, c * sizeof(RefineOut));
+    job_cap_ = e == cudaSuccess ? c : 0;
+  }
+  if (e == cudaSuccess && boxes.size() > box_cap_) {
+    cudaFree(d_boxes_);
+    d_boxes_ = nullptr;
+    if ((e = cudaMalloc(&d_boxes_, boxes.size() * sizeof(double))) == cudaSuccess)
+      box_cap_ = boxes.size();
+    else
+      box_cap_ = 0;
+  }
   if (e == cudaSuccess)
-    e = cudaMemcpyAsync(d_jobs, jobs.data(), jobs.size() * sizeof(RefineJob),
+    e = cudaMemcpyAsync(d_jobs_, jobs.data(), jobs.size() * sizeof(RefineJob),
                         cudaMemcpyHostToDevice, stream_);
   if (e == cudaSuccess && !boxes.empty())
-    e = cudaMemcpyAsync(d_boxes, boxes.data(), boxes.size() * 8, cudaMemcpyHostToDevice, stream_);
-  RefineDomain dom{{rc[0], rc[1], rc[2]}, rhw, static_cast<int>(boxes.size() / 6), d_boxes};
+    e = cudaMemcpyAsync(d_boxes_, boxes.data(), boxes.size() * 8, cudaMemcpyHostToDevice,
+                        stream_);
+  RefineDomain dom{{rc[0], rc[1], rc[2]}, rhw, static_cast<int>(boxes.size() / 6), d_boxes_};
   // spread each start over a cluster of CTAs when the GPU has SMs to spare
   // and an evaluation is big enough to amortise the cluster exchange
   const int n = static_cast<int>(jobs.size());
@@ -178,17 +197,17 @@ cudaError_t DeviceObjective::refine(const std::vector<RefineJob>& jobs, const do
   const int cluster = forced > 0 ? forced
                                  : (max_pairs_ >= 8192 ? std::max(1, std::min(8, sm_count_ / n)) : 1);
   cudaEvent_t ev[2] = {nullptr, nullptr};
-  const bool prof = std::getenv("GOSMA_PROFILE") != nullptr;
+  const bool prof = n > 1 && std::getenv("GOSMA_PROFILE") != nullptr;  // batches only
   if (prof) {
     cudaEventCreate(&ev[0]);
     cudaEventCreate(&ev[1]);
     cudaEventRecord(ev[0], stream_);
   }
   if (e == cudaSuccess)
-    e = launch_refine(d_models_, d_jobs, n, dom, d_out, max_n1_, cluster, stream_);
+    e = launch_refine(d_models_, d_jobs_, n, dom, d_out_, max_n1_, cluster, stream_);
   if (prof) cudaEventRecord(ev[1], stream_);
   if (e == cudaSuccess)
-    e = cudaMemcpyAsync(out->data(), d_out, jobs.size() * sizeof(RefineOut),
+    e = cudaMemcpyAsync(out->data(), d_out_, jobs.size() * sizeof(RefineOut),
                         cudaMemcpyDeviceToHost, stream_);
   if (e == cudaSuccess) e = cudaStreamSynchronize(stream_);
   if (prof) {
@@ -206,9 +225,6 @@ cudaError_t DeviceObjective::refine(const std::vector<RefineJob>& jobs, const do
     cudaEventDestroy(ev[0]);
     cudaEventDestroy(ev[1]);
   }
-  cudaFree(d_jobs);
-  cudaFree(d_out);
-  cudaFree(d_boxes);
   cudaSetDevice(cur);
   return e;
 }

@@ -87,6 +87,10 @@ class DeviceObjective {
   ObjRequest* d_req_ = nullptr;
   double* d_part_ = nullptr;
   size_t cap_ = 0;
+  RefineJob* d_jobs_ = nullptr;
+  RefineOut* d_out_ = nullptr;
+  double* d_boxes_ = nullptr;
+  size_t job_cap_ = 0, box_cap_ = 0;
   cudaStream_t stream_ = nullptr;
 };
 

@@ -204,6 +204,9 @@ int discovery_dive(gosma_ctx* ctx, const Domain& dom, const std::vector<gosma_no
   double dbar = 0.0;
   for (const Box& b : dom.boxes) dbar += (b.c - centroid).norm();
   dbar /= static_cast<double>(dom.boxes.size());
+  const auto t_dive = std::chrono::steady_clock::now();
+  double t_eval = 0.0;
+  int beam_its = 0;
   gosma_ctx* coarse = nullptr;
   int rc = gosma_ctx_blurred(ctx, kCoarse, dbar, &coarse);
   if (rc != GOSMA_OK) return rc;
@@ -252,7 +255,10 @@ int discovery_dive(gosma_ctx* ctx, const Domain& dom, const std::vector<gosma_no
     }
     double skip = -kInf;  // worst sector candidate (kInf until all seeded)
     for (const Cand& c : best) skip = std::max(skip, c.value);
+    const auto te = std::chrono::steady_clock::now();
     rc = eval_host(coarse, kids, skip, &lo, &up, &sp);
+    t_eval += std::chrono::duration<double>(std::chrono::steady_clock::now() - te).count();
+    ++beam_its;
     if (rc != GOSMA_OK) break;
     used += kids.size();
     beam.clear();
@@ -277,6 +283,9 @@ int discovery_dive(gosma_ctx* ctx, const Domain& dom, const std::vector<gosma_no
   }
   *evals += used;
   const auto t_beam = std::chrono::steady_clock::now();
+  if (std::getenv("GOSMA_PROFILE"))
+    std::fprintf(stderr, "[gosma profile] dive: beam %.3fs (%d iterations, bounds %.3fs, %llu evals)\n",
+                 std::chrono::duration<double>(t_beam - t_dive).count(), beam_its, t_eval, used);
   // annealing ladder per sector: coarse -> 0.03 -> 0.01 -> exact
   const HostModel hc = blurred_model(m, kCoarse, dbar);
   const HostModel h3 = blurred_model(m, 0.03, dbar);
