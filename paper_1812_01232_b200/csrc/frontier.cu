@@ -551,28 +551,22 @@ __global__ void min_key_at_least(const unsigned long long* key, size_t n,
   if (threadIdx.x == 0 && r != kHoleKey) atomicMin(out, r);
 }
 
-__global__ void min_upper_key(const double* upper, size_t n, ArgMin* out) {
-  typedef cub::BlockReduce<unsigned long long, 256> BR;
-  __shared__ typename BR::TempStorage tmp;
-  unsigned long long best = ~0ull;
+// Children whose upper bound is below the exclusive prefix minimum (records).
+__global__ void flag_records(const double* upper, const double* pmin, size_t n,
+                             ImprovingChild* out, unsigned long long* count, unsigned cap) {
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<size_t>(gridDim.x) * blockDim.x) {
     const double u = upper[i];
-    if (u < INFINITY) best = min(best, order_key(u));
+    if (u < pmin[i]) {
+      const unsigned long long k = atomicAdd(count, 1ull);
+      if (k < cap) out[k] = ImprovingChild{u, i};
+    }
   }
-  const unsigned long long r = BR(tmp).Reduce(best, cub::Min());
-  if (threadIdx.x == 0 && r != ~0ull) atomicMin(&out->key, r);
 }
 
-// First index attaining the minimal key (deterministic argmin).
-__global__ void first_index_of_key(const double* upper, size_t n, ArgMin* out) {
-  const unsigned long long k = out->key;
-  if (k == ~0ull) return;
-  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
-    if (order_key(upper[i]) == k) atomicMin(&out->index, static_cast<unsigned long long>(i));
-  }
-}
+struct MinOp {
+  __device__ __forceinline__ double operator()(double a, double b) const { return fmin(a, b); }
+};
 
 }  // namespace
 
@@ -657,12 +651,10 @@ cudaError_t Frontier::reserve(size_t cap_nodes, size_t wave) {
   }
   if (!stats) {
     if ((e = dmalloc(&stats, sizeof(RouteStats))) != cudaSuccess) return e;
-    if ((e = dmalloc(&amin, sizeof(ArgMin))) != cudaSuccess) return e;
     if ((e = dmalloc(&counter, 2 * sizeof(unsigned long long))) != cudaSuccess) return e;
     if ((e = dmalloc(&hist, kBins * sizeof(unsigned int))) != cudaSuccess) return e;
     if ((e = dmalloc(&list_counts, 2 * sizeof(int))) != cudaSuccess) return e;
     if ((e = hmalloc(&h_stats, sizeof(RouteStats))) != cudaSuccess) return e;
-    if ((e = hmalloc(&h_amin, sizeof(ArgMin))) != cudaSuccess) return e;
     if ((e = hmalloc(&h_counter, 2 * sizeof(unsigned long long))) != cudaSuccess) return e;
     h_hist.resize(kBins);
   }
@@ -737,6 +729,11 @@ void Frontier::release() {
   dfree(cidx);
   cidx = nullptr;
   cidx_cap = 0;
+  dfree(kid_pmin);
+  kid_pmin = nullptr;
+  pmin_cap = 0;
+  dfree(rec);
+  rec = nullptr;
   dfree(cand);
   dfree(cand_tmp);
   cand = cand_tmp = nullptr;
@@ -744,11 +741,9 @@ void Frontier::release() {
   tau = 0;
   known_min = 0;
   dfree(stats);
-  dfree(amin);
   dfree(counter);
   dfree(temp);
   dfree(h_stats);
-  dfree(h_amin);
   dfree(h_counter);
   nodes = nullptr;
   split = nullptr;
@@ -763,11 +758,9 @@ void Frontier::release() {
   keep = nullptr;
   kept_idx = nullptr;
   stats = nullptr;
-  amin = nullptr;
   counter = nullptr;
   temp = nullptr;
   h_stats = nullptr;
-  h_amin = nullptr;
   h_counter = nullptr;
   size = holes = cap = sel_cap = kid_cap = temp_bytes = 0;
 }
@@ -1146,24 +1139,42 @@ cudaError_t Frontier::expand_selected_cached(size_t n_sel, cudaStream_t s, size_
   return cudaGetLastError();
 }
 
-cudaError_t Frontier::best_child(size_t n_kids, cudaStream_t s, int* index, double* value) {
-  ArgMin init;
-  cudaError_t e = cudaMemcpyAsync(amin, &init, sizeof(ArgMin), cudaMemcpyHostToDevice, s);
-  if (e != cudaSuccess) return e;
-  const unsigned g = grid_cap(n_kids, 256);
-  min_upper_key<<<g, 256, 0, s>>>(kid_upper, n_kids, amin);
-  first_index_of_key<<<g, 256, 0, s>>>(kid_upper, n_kids, amin);
-  if ((e = cudaMemcpyAsync(h_amin, amin, sizeof(ArgMin), cudaMemcpyDeviceToHost, s)) !=
-      cudaSuccess)
+cudaError_t Frontier::improving_children(size_t n_kids, double bound, cudaStream_t s,
+                                         std::vector<ImprovingChild>* out) {
+  constexpr unsigned kRecCap = 4096;
+  out->clear();
+  if (n_kids == 0) return cudaSuccess;
+  cudaError_t e = cudaSuccess;
+  if (n_kids > pmin_cap) {
+    dfree(kid_pmin);
+    kid_pmin = nullptr;
+    pmin_cap = 0;
+    if ((e = dmalloc(&kid_pmin, kid_cap * sizeof(double))) != cudaSuccess) return e;
+    pmin_cap = kid_cap;
+  }
+  if (!rec && (e = dmalloc(&rec, kRecCap * sizeof(ImprovingChild))) != cudaSuccess) return e;
+  size_t bytes = 0;
+  cub::DeviceScan::ExclusiveScan(nullptr, bytes, kid_upper, kid_pmin, MinOp(), bound,
+                                 static_cast<int>(n_kids), s);
+  if ((e = ensure_temp(bytes)) != cudaSuccess) return e;
+  bytes = temp_bytes;
+  if ((e = cub::DeviceScan::ExclusiveScan(temp, bytes, kid_upper, kid_pmin, MinOp(), bound,
+                                          static_cast<int>(n_kids), s)) != cudaSuccess)
+    return e;
+  if ((e = cudaMemsetAsync(counter, 0, sizeof(unsigned long long), s)) != cudaSuccess) return e;
+  flag_records<<<grid_cap(n_kids, 256), 256, 0, s>>>(kid_upper, kid_pmin, n_kids, rec, counter,
+                                                     kRecCap);
+  if ((e = cudaMemcpyAsync(h_counter, counter, sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost, s)) != cudaSuccess)
     return e;
   if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
-  if (h_amin->key == ~0ull || h_amin->index == ~0ull) {
-    *index = -1;
-    *value = INFINITY;
-    return cudaSuccess;
-  }
-  *index = static_cast<int>(h_amin->index);
-  *value = key_to_double(h_amin->key);
+  const size_t m = std::min<size_t>(*h_counter, kRecCap);
+  out->resize(m);
+  if (m && (e = cudaMemcpy(out->data(), rec, m * sizeof(ImprovingChild),
+                           cudaMemcpyDeviceToHost)) != cudaSuccess)
+    return e;
+  std::sort(out->begin(), out->end(),
+            [](const ImprovingChild& a, const ImprovingChild& b) { return a.index < b.index; });
   return cudaSuccess;
 }
 

@@ -24,12 +24,14 @@ struct RouteStats {
   double scratch = 0.0;
 };
 
-struct ArgMin {
-  unsigned long long key = ~0ull;    // order key of the min upper bound
-  unsigned long long index = ~0ull;  // first child attaining it
-};
-
 unsigned long long host_order_key(double v);
+
+// A child whose upper bound beats every earlier child of its wave and the
+// incumbent (process_wave's refinement candidates, solver.cpp:409-431).
+struct ImprovingChild {
+  double upper;
+  unsigned long long index;
+};
 double key_to_double(unsigned long long k);
 
 struct Frontier {
@@ -84,10 +86,8 @@ struct Frontier {
   int* list_counts = nullptr;
   // reductions / scratch
   RouteStats* stats = nullptr;
-  ArgMin* amin = nullptr;
   unsigned long long* counter = nullptr;
   RouteStats* h_stats = nullptr;
-  ArgMin* h_amin = nullptr;
   unsigned long long* h_counter = nullptr;
   void* temp = nullptr;
   size_t temp_bytes = 0;
@@ -119,7 +119,14 @@ struct Frontier {
   // device-side import of n records
   cudaError_t upload_device(const gosma_node* d_nodes, const int8_t* d_split, const double* d_vol,
                             size_t n, cudaStream_t s);
-  cudaError_t best_child(size_t n_kids, cudaStream_t s, int* index, double* value);
+  // children i with upper[i] < min(bound, upper[0..i-1]) in index order: the
+  // branches the reference's in-order wave loop would refine (before its
+  // refinements lower the incumbent further)
+  cudaError_t improving_children(size_t n_kids, double bound, cudaStream_t s,
+                                 std::vector<ImprovingChild>* out);
+  double* kid_pmin = nullptr;  // exclusive prefix minimum of kid_upper
+  size_t pmin_cap = 0;
+  ImprovingChild* rec = nullptr;  // device record list (kRecCap)
   // route children against d*, append survivors
   cudaError_t route_append(size_t n_kids, double dstar, cudaStream_t s, RouteStats* out);
   // drop holes and nodes with key >= limit; returns the dropped (non-hole) volume

@@ -453,6 +453,7 @@ struct gosma_solver {
   bool cached = wave_mode == 1;
   // GPU objective for incumbent refinements (large mixtures, see gpu_sma)
   std::unique_ptr<DeviceObjective> sma_dev;
+  std::vector<ImprovingChild> improving;
   unsigned long long cuboid_evals = 0;
   // GOSMA_PROFILE=1: synchronising per-phase wall times, printed on destroy
   bool profile = std::getenv("GOSMA_PROFILE") != nullptr;
@@ -768,12 +769,18 @@ int gosma_solver_expand(gosma_solver* S, double limit, unsigned long long max_ev
   S->lap(3, s);
   S->evals += n_kids;
   S->expanded += n_sel;
-  int bi = -1;
-  double bu = kInf;
-  if ((e = S->F.best_child(n_kids, s, &bi, &bu)) != cudaSuccess) return cuda_error(e, "argmin");
-  if (bi >= 0 && bu < S->inc.value) {
+  // process_wave (solver.cpp:409-431): in child order, every branch whose
+  // upper bound beats the incumbent at that moment is refined; the device
+  // hands over the prefix-minimum records below the incumbent, the host
+  // replays them against the incumbent as the refinements lower it
+  if ((e = S->F.improving_children(n_kids, S->inc.value, s, &S->improving)) != cudaSuccess)
+    return cuda_error(e, "improving children");
+  for (const ImprovingChild& c : S->improving) {
+    if (!(c.upper < S->inc.value)) continue;
     gosma_node b;
-    cudaMemcpy(&b, S->F.kids + bi, sizeof(gosma_node), cudaMemcpyDeviceToHost);
+    if ((e = cudaMemcpy(&b, S->F.kids + c.index, sizeof(gosma_node), cudaMemcpyDeviceToHost)) !=
+        cudaSuccess)
+      return cuda_error(e, "improving child");
     const int rc = improve(ctx->model, S->dom, b, &S->inc, S->sma_dev.get());
     if (rc != GOSMA_OK) return rc;
   }
