@@ -440,9 +440,13 @@ __device__ __forceinline__ void self_pair(const float4& a0, const float4& a1, co
   const float e2 = n2 * D1 * inv;
   float t1 = ex2f(e1) * rKhh;
   float t2 = ex2f(e2) * rK2;
-  if (e1 > kNegligibleLog2 && (c2 < 2.0f || !(Khh > 15.0f)))
-    t1 = self_lb_exact(pa[4].x, ahi, pb[4].x, bhi, c2, K2hh, e1);
-  if (e2 > kNegligibleLog2 && !(K2 > 15.0f)) t2 = ex2f(e2 + log2w(K2));
+  // exact paths (one rarely-taken branch, as in cross_pair)
+  const bool x1 = e1 > kNegligibleLog2 && (c2 < 2.0f || !(Khh > 15.0f));
+  const bool x2 = e2 > kNegligibleLog2 && !(K2 > 15.0f);
+  if (x1 | x2) {
+    if (x1) t1 = self_lb_exact(pa[4].x, ahi, pb[4].x, bhi, c2, K2hh, e1);
+    if (x2) t2 = ex2f(e2 + log2w(K2));
+  }
   const float ft1 = b1.y * t1;  // F_j (Flo); 2 F_i is applied to the row sum
   l += ft1;
   me = fmaf(ft1, fabsf(e1), me);
@@ -1123,7 +1127,10 @@ cudaError_t launch_group(const DevCtx& ctx, const EvalArgs& a, int sm_count,
                          cudaStream_t stream) {
   // Warps per CTA: 4, or fewer when large mixtures' per-group tables would
   // leave few CTAs resident (e.g. 256x128: 1 CTA of 4 warps vs 7 of 1 warp).
-  static int configured = 0;  // largest dynamic smem set on this kernel
+  static int configured_on[64] = {};  // largest dynamic smem set on this kernel, per device
+  int device = 0;
+  cudaGetDevice(&device);
+  int& configured = configured_on[device & 63];
   int best_warps = kWarpsPerCta, best_resident = -1, best_per_sm = 0;
   size_t best_smem = 0;
   for (int warps = kWarpsPerCta; warps >= (kG > 32 ? kWarpsPerCta : 1); warps /= 2) {

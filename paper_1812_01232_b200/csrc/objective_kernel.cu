@@ -640,12 +640,10 @@ cudaError_t launch_refine(const DevModel64* models, const RefineJob* jobs, int n
                           cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
   const size_t smem = objgrad_smem_bytes(max_n1);
-  static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
+  if (smem > 48 * 1024) {  // per call: the attribute is per device, the call is cheap
     const cudaError_t e = cudaFuncSetAttribute(
         refine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    configured = smem;
   }
   cluster = std::max(1, std::min(cluster, 8));
   cudaLaunchConfig_t cfg{};
@@ -676,12 +674,10 @@ cudaError_t launch_objgrad(const DevModel64* models, const ObjRequest* req, int 
                            double* partial, int max_n1, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
   const size_t smem = objgrad_smem_bytes(max_n1);
-  static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
+  if (smem > 48 * 1024) {  // per call: the attribute is per device, the call is cheap
     const cudaError_t e = cudaFuncSetAttribute(
         objgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    configured = smem;
   }
   const int threads = std::min(256, std::max(32, (max_n1 + 31) / 32 * 32));
   objgrad_kernel<<<dim3(slices, n), threads, smem, s>>>(models, req, partial, max_n1);
