@@ -491,9 +491,10 @@ __device__ __forceinline__ void class_pairs_rows(const WarpTables& T, const Clas
     if (il < n) {
       const Row r = load_row(T, cs.o1 + il);
       float l = 0.0f, u = 0.0f, ma = 0.0f, mb = 0.0f;
+      const float4* cp = T.col + cs.o2 * kColF4;  // pointer walk: no index math per pair
+      const float4* const ce = cp + cs.n2 * kColF4;
 #pragma unroll kUnrollPairs
-      for (int j = cs.o2; j < cs.o2 + cs.n2; ++j)
-        cross_pair<kSame>(r, T.col[j * kColF4], T.col[j * kColF4 + 1], l, u, ma, mb);
+      for (; cp < ce; cp += kColF4) cross_pair<kSame>(r, cp[0], cp[1], l, u, ma, mb);
       lb_cross += static_cast<double>(w * r.Fhi * l);
       lb_err += static_cast<double>(
           2.0f * w * r.Fhi * fmaf(ma, kErrAmp, fmaf(mb, kErrExp, l * kErrTerm)));
@@ -512,12 +513,14 @@ __device__ __forceinline__ void class_pairs_rows(const WarpTables& T, const Clas
       const float4 a0 = pa[0], a1 = pa[1], a2 = pa[2];
       const float4 a3 = kSame ? make_float4(0.f, 0.f, 0.f, 0.f) : pa[3];
       float l = 0.0f, u = 0.0f, me = 0.0f;
-      int jl = il;
+      const float4* const rbeg = T.row + cs.o1 * kRowF4;
+      const float4* const rend = rbeg + n * kRowF4;
+      const float4* pb = pa;  // partner row i + d (mod n)
 #pragma unroll kUnrollPairs
-      for (int d = 1; d <= dfull; ++d) {
-        jl = (jl + 1 == n) ? 0 : jl + 1;
-        const int j = cs.o1 + jl;
-        self_pair<kSame>(a0, a1, a2, a3, pa, T.row + j * kRowF4, l, u, me);
+      for (int d = dfull; d > 0; --d) {
+        pb += kRowF4;
+        pb = pb == rend ? rbeg : pb;
+        self_pair<kSame>(a0, a1, a2, a3, pa, pb, l, u, me);
       }
       if (even && il < n / 2) {
         const int j = i + n / 2;
