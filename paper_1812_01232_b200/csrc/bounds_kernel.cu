@@ -574,13 +574,16 @@ __device__ __forceinline__ void class_pairs_tail(const WarpTables& T, const Clas
       const float4 a0 = pa[0], a1 = pa[1], a2 = pa[2];
       const float4 a3 = kSame ? make_float4(0.f, 0.f, 0.f, 0.f) : pa[3];
       float l = 0.0f, u = 0.0f, me = 0.0f;
-      int jl = il + 1 + slot - k;  // partner row il + d (mod n) after each step
+      // partner row il + d (mod n), walked as a pointer
+      const float4* const rbeg = T.row + cs.o1 * kRowF4;
+      const float4* const rend = rbeg + n * kRowF4;
+      const int step = k * kRowF4;
+      const float4* pb = pa + (1 + slot - k) * kRowF4;
 #pragma unroll kUnrollPairs
       for (int d = 1 + slot; d <= dfull; d += k) {
-        jl += k;
-        if (jl >= n) jl -= n;
-        const int j = cs.o1 + jl;
-        self_pair<kSame>(a0, a1, a2, a3, pa, T.row + j * kRowF4, l, u, me);
+        pb += step;
+        pb = pb >= rend ? pb - n * kRowF4 : pb;
+        self_pair<kSame>(a0, a1, a2, a3, pa, pb, l, u, me);
       }
       if (even && slot == 0 && il < n / 2) {
         const int j = i + n / 2;
