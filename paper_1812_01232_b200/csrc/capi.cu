@@ -336,6 +336,7 @@ int gosma_ctx_blurred(const gosma_ctx* src, double w, double reference_distance,
 
 void gosma_ctx_destroy(gosma_ctx* ctx) {
   if (!ctx) return;
+  gosma_ctx_destroy(ctx->dive_ctx);
   ctx_free_device(ctx);
   delete ctx;
 }
@@ -497,6 +498,27 @@ int gosma_eval_bounds(gosma_ctx* ctx, const gosma_node* nodes, size_t n, double 
   // still work (the copies then serialise).
   const size_t chunk = std::min<size_t>(n, static_cast<size_t>(1) << 17);
   if ((e = ctx->scratch.reserve(2 * chunk)) != cudaSuccess) return cuda_error(e, "scratch");
+  if (n <= chunk && n <= 8192) {
+    // a small batch (the discovery dive's beam): one stream, no cross-stream
+    // events (their latency would dominate)
+    cudaStream_t ks = ctx->stream;
+    if ((e = cudaMemcpyAsync(ctx->scratch.d_nodes, nodes, n * sizeof(gosma_node),
+                             cudaMemcpyHostToDevice, ks)) != cudaSuccess)
+      return cuda_error(e, "H2D nodes");
+    int8_t* dsp = split_rot ? ctx->scratch.d_split : nullptr;
+    const int rc = gosma_eval_bounds_device(ctx, ctx->scratch.d_nodes, n, skip,
+                                            ctx->scratch.d_lower, ctx->scratch.d_upper, dsp, ks);
+    if (rc != GOSMA_OK) return rc;
+    if ((e = cudaMemcpyAsync(lower, ctx->scratch.d_lower, n * sizeof(double),
+                             cudaMemcpyDeviceToHost, ks)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(upper, ctx->scratch.d_upper, n * sizeof(double),
+                             cudaMemcpyDeviceToHost, ks)) != cudaSuccess ||
+        (split_rot && (e = cudaMemcpyAsync(split_rot, dsp, n * sizeof(int8_t),
+                                           cudaMemcpyDeviceToHost, ks)) != cudaSuccess))
+      return cuda_error(e, "D2H bounds");
+    if ((e = cudaStreamSynchronize(ks)) != cudaSuccess) return cuda_error(e, "eval_bounds");
+    return GOSMA_OK;
+  }
   if (!ctx->h2d_stream) {
     if ((e = cudaStreamCreateWithFlags(&ctx->h2d_stream, cudaStreamNonBlocking)) != cudaSuccess ||
         (e = cudaStreamCreateWithFlags(&ctx->d2h_stream, cudaStreamNonBlocking)) != cudaSuccess)

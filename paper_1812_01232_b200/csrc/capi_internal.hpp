@@ -65,6 +65,11 @@ struct gosma_ctx {
   cudaEvent_t pipe_ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   gosma::Scratch scratch;
   std::mutex mu;
+  // the discovery dive's blurred copy (solver.cpp:449-457), kept for the
+  // next solve on this context (creating one costs device allocations)
+  gosma_ctx* dive_ctx = nullptr;
+  double dive_w = -1.0, dive_dist = -1.0;
+  std::mutex dive_mu;
 };
 
 namespace gosma {

@@ -207,9 +207,20 @@ int discovery_dive(gosma_ctx* ctx, const Domain& dom, const std::vector<gosma_no
   const auto t_dive = std::chrono::steady_clock::now();
   double t_eval = 0.0;
   int beam_its = 0;
-  gosma_ctx* coarse = nullptr;
-  int rc = gosma_ctx_blurred(ctx, kCoarse, dbar, &coarse);
-  if (rc != GOSMA_OK) return rc;
+  // the blurred context is cached on ctx (same width and reference distance
+  // on the next solve of this problem); the dive holds its lock throughout
+  std::lock_guard<std::mutex> dive_lock(ctx->dive_mu);
+  int rc = GOSMA_OK;
+  if (!ctx->dive_ctx || ctx->dive_w != kCoarse || ctx->dive_dist != dbar ||
+      ctx->dive_ctx->lb_margin != ctx->lb_margin ||
+      ctx->dive_ctx->dev.lb_err_scale != ctx->dev.lb_err_scale) {
+    gosma_ctx_destroy(ctx->dive_ctx);
+    ctx->dive_ctx = nullptr;
+    if ((rc = gosma_ctx_blurred(ctx, kCoarse, dbar, &ctx->dive_ctx)) != GOSMA_OK) return rc;
+    ctx->dive_w = kCoarse;
+    ctx->dive_dist = dbar;
+  }
+  gosma_ctx* const coarse = ctx->dive_ctx;
   struct Cand {
     double value = kInf;
     gosma_node b{};
@@ -228,10 +239,7 @@ int discovery_dive(gosma_ctx* ctx, const Domain& dom, const std::vector<gosma_no
   std::vector<int8_t> sp;
   unsigned long long used = 0;
   rc = eval_host(coarse, roots, kInf, &lo, &up, &sp);
-  if (rc != GOSMA_OK) {
-    gosma_ctx_destroy(coarse);
-    return rc;
-  }
+  if (rc != GOSMA_OK) return rc;
   used += roots.size();
   for (size_t i = 0; i < roots.size(); ++i) {
     offer(up[i], roots[i], i);
@@ -316,10 +324,7 @@ int discovery_dive(gosma_ctx* ctx, const Domain& dom, const std::vector<gosma_no
     for (size_t s = 0; s < best.size(); ++s)
       if (ok[s]) run.push_back(jobs[s]);
     const cudaError_t e = refine_device(dobj.get(), dom, run, &out);
-    if (e != cudaSuccess) {
-      gosma_ctx_destroy(coarse);
-      return cuda_error(e, "refine kernel");
-    }
+    if (e != cudaSuccess) return cuda_error(e, "refine kernel");
   }
   if (dobj) {
     // incumbents are host FP64 values
@@ -368,7 +373,6 @@ int discovery_dive(gosma_ctx* ctx, const Domain& dom, const std::vector<gosma_no
       inc->t = res[s].t;
     }
   }
-  gosma_ctx_destroy(coarse);
   return GOSMA_OK;
 }
 
@@ -475,9 +479,38 @@ struct gosma_solver {
 
 namespace {
 
+// Free device memory, re-read at most every 0.5 s per device: cudaMemGetInfo
+// costs ~1 ms, a tenth of a short solve. The pool budget derived from it only
+// decides when to fold (sound either way).
+void free_device_memory(int device, size_t* free_b) {
+  static std::mutex mu;
+  static std::vector<std::pair<std::chrono::steady_clock::time_point, size_t>> seen(64);
+  const auto now = std::chrono::steady_clock::now();
+  std::lock_guard<std::mutex> lk(mu);
+  auto& slot = seen[device & 63];
+  if (slot.second == 0 || now - slot.first > std::chrono::milliseconds(500)) {
+    size_t total = 0;
+    cudaMemGetInfo(&slot.second, &total);
+    slot.first = now;
+  }
+  *free_b = slot.second;
+}
+
 int solver_init(gosma_solver* S) {
   gosma_ctx* ctx = S->ctx;
   S->F.prof = S->profile;
+  // GOSMA_PROFILE: wall time of the init steps
+  auto t_last = std::chrono::steady_clock::now();
+  std::string init_prof;
+  auto mark = [&](const char* what) {
+    if (!S->profile) return;
+    const auto now = std::chrono::steady_clock::now();
+    char buf[64];
+    std::snprintf(buf, sizeof buf, " %s %.2fms", what,
+                  1e3 * std::chrono::duration<double>(now - t_last).count());
+    init_prof += buf;
+    t_last = now;
+  };
   if (gpu_sma(ctx->model)) {
     S->sma_dev = std::make_unique<DeviceObjective>(
         ctx->device, std::vector<const HostModel*>{&ctx->model});
@@ -536,22 +569,25 @@ int solver_init(gosma_solver* S) {
   cudaError_t e = S->F.reserve(std::max<size_t>(size_t(1) << 20, roots.size() * 2 + 16),
                                S->wave_nodes);
   if (e != cudaSuccess) return cuda_error(e, "frontier reserve");
+  mark("reserve");
   // Device memory budget for the pool: beyond it the worst nodes fold into the
   // resolved set (sound; the reference's queue_capacity mechanism).
-  size_t free_b = 0, total_b = 0;
-  cudaMemGetInfo(&free_b, &total_b);
+  size_t free_b = 0;
+  free_device_memory(ctx->device, &free_b);
   const size_t per_node = sizeof(gosma_node) + 1 + 8 + 8;
   S->mem_cap = std::max<size_t>(free_b / 4 / per_node, 16 * S->wave_nodes);
   S->F.cap_limit = S->mem_cap;
   S->qcap = cfg.queue_capacity >= 0
                 ? std::min<size_t>(static_cast<size_t>(cfg.queue_capacity), S->mem_cap)
                 : S->mem_cap;
+  mark("meminfo");
   if (roots.empty()) return GOSMA_OK;
   // Wave 0: the roots (solver.cpp:611-621) + discovery dive.
   std::vector<double> lo, up;
   std::vector<int8_t> sp;
   int rc = eval_host(ctx, roots, kInf, &lo, &up, &sp);
   if (rc != GOSMA_OK) return rc;
+  mark("roots");
   S->evals += roots.size();
   if (cfg.discovery_dive) {
     const auto t0 = std::chrono::steady_clock::now();
@@ -559,10 +595,12 @@ int solver_init(gosma_solver* S) {
     if (rc != GOSMA_OK) return rc;
     S->phase[7] += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   }
+  mark("dive");
   for (size_t i = 0; i < roots.size(); ++i)
     if (up[i] < S->inc.value && (rc = improve(m, S->dom, roots[i], &S->inc, S->sma_dev.get())) !=
                                     GOSMA_OK)
       return rc;
+  mark("improve");
   std::vector<gosma_node> keep;
   std::vector<int8_t> ks;
   std::vector<double> kv;
@@ -587,6 +625,8 @@ int solver_init(gosma_solver* S) {
   if (!keep.empty() &&
       (e = S->F.upload(keep.data(), ks.data(), kv.data(), keep.size(), s)) != cudaSuccess)
     return cuda_error(e, "frontier upload");
+  mark("upload");
+  if (S->profile) std::fprintf(stderr, "[gosma profile] init:%s\n", init_prof.c_str());
   return GOSMA_OK;
 }
 
