@@ -37,6 +37,8 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
+#include <mutex>
+#include <vector>
 
 #include "gosma_internal.hpp"
 
@@ -1133,22 +1135,43 @@ cudaError_t launch_group(const DevCtx& ctx, const EvalArgs& a, int sm_count,
                          cudaStream_t stream) {
   // Warps per CTA: 4, or fewer when large mixtures' per-group tables would
   // leave few CTAs resident (e.g. 256x128: 1 CTA of 4 warps vs 7 of 1 warp).
-  static int configured_on[64] = {};  // largest dynamic smem set on this kernel, per device
+  // The choice depends only on the device and the table size: cached, since
+  // the occupancy queries cost microseconds per launch (short solves launch
+  // thousands of small batches).
+  struct Choice {
+    int device;
+    size_t per_warp;
+    int warps, per_sm;
+    size_t smem;
+  };
+  static std::mutex mu;
+  static std::vector<Choice> cache;
   int device = 0;
   cudaGetDevice(&device);
-  int& configured = configured_on[device & 63];
-  int best_warps = kWarpsPerCta, best_resident = -1, best_per_sm = 0;
+  const size_t per_warp = eval_smem_per_warp(ctx);
+  int best_warps = kWarpsPerCta, best_per_sm = 0;
   size_t best_smem = 0;
-  for (int warps = kWarpsPerCta; warps >= (kG > 32 ? kWarpsPerCta : 1); warps /= 2) {
+  bool hit = false;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    for (const Choice& c : cache)
+      if (c.device == device && c.per_warp == per_warp) {
+        best_warps = c.warps;
+        best_per_sm = c.per_sm;
+        best_smem = c.smem;
+        hit = true;
+        break;
+      }
+  }
+  for (int warps = kWarpsPerCta, best_resident = -1;
+       !hit && warps >= (kG > 32 ? kWarpsPerCta : 1); warps /= 2) {
     const int groups = kG > 32 ? 1 : warps * (32 / kG);
-    const size_t smem = eval_smem_per_warp(ctx) * groups;
-    if (smem > 48 * 1024 && static_cast<int>(smem) > configured) {
-      const cudaError_t e = cudaFuncSetAttribute(eval_bounds_kernel<kMode, kG, kTail>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 static_cast<int>(smem));
-      if (e != cudaSuccess) continue;
-      configured = static_cast<int>(smem);
-    }
+    const size_t smem = per_warp * groups;
+    if (smem > 48 * 1024 &&
+        cudaFuncSetAttribute(eval_bounds_kernel<kMode, kG, kTail>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem)) != cudaSuccess)
+      continue;
     int per_sm = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(
             &per_sm, eval_bounds_kernel<kMode, kG, kTail>, warps * 32, smem) != cudaSuccess)
@@ -1159,6 +1182,16 @@ cudaError_t launch_group(const DevCtx& ctx, const EvalArgs& a, int sm_count,
       best_per_sm = per_sm;
       best_smem = smem;
     }
+  }
+  if (!hit && best_per_sm >= 1) {
+    // the attribute must cover the chosen size (the loop may have set a larger
+    // one last); set it once more for the choice
+    if (best_smem > 48 * 1024)
+      cudaFuncSetAttribute(eval_bounds_kernel<kMode, kG, kTail>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(best_smem));
+    std::lock_guard<std::mutex> lk(mu);
+    cache.push_back(Choice{device, per_warp, best_warps, best_per_sm, best_smem});
   }
   if (best_per_sm < 1) return cudaErrorInvalidConfiguration;
   const int groups_per_cta = kG > 32 ? 1 : best_warps * (32 / kG);
