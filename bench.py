@@ -435,7 +435,7 @@ def main():
                                      None)
         if rc:
             raise RuntimeError(g.lib.gosma_last_error().decode())
-        return float(h_up.numpy().min())
+        return float(h_up[n - 1])  # the bounds are in host memory once the call returns
 
     for _ in range(2):
         e2e_step()

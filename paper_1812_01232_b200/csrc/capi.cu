@@ -536,9 +536,15 @@ int gosma_eval_bounds(gosma_ctx* ctx, const gosma_node* nodes, size_t n, double 
   cudaEventRecord(k_done[1], ks);
   cudaEventRecord(d2h_done[0], ks);
   cudaEventRecord(d2h_done[1], ks);
-  const size_t nchunks = (n + chunk - 1) / chunk;
+  // chunk k covers [off[k], off[k+1]); the first chunks ramp up (chunk/8,
+  // chunk/4, chunk/2) so the kernel starts after a short copy instead of a
+  // full 11 MB one, then full chunks
+  std::vector<size_t> offs{0};
+  for (size_t c = std::max<size_t>(chunk / 8, 1); offs.back() < n; c = std::min(2 * c, chunk))
+    offs.push_back(std::min(n, offs.back() + c));
+  const size_t nchunks = offs.size() - 1;
   auto h2d = [&](size_t k) -> cudaError_t {
-    const size_t off = k * chunk, m = std::min(chunk, n - off), slot = k & 1;
+    const size_t off = offs[k], m = offs[k + 1] - offs[k], slot = k & 1;
     cudaStreamWaitEvent(hs, k_done[slot], 0);  // the kernel of chunk k-2 has read the slot
     cudaError_t err = cudaMemcpyAsync(ctx->scratch.d_nodes + slot * chunk, nodes + off,
                                       m * sizeof(gosma_node), cudaMemcpyHostToDevice, hs);
@@ -547,7 +553,7 @@ int gosma_eval_bounds(gosma_ctx* ctx, const gosma_node* nodes, size_t n, double 
   };
   if ((e = h2d(0)) != cudaSuccess) return cuda_error(e, "H2D nodes");
   for (size_t k = 0; k < nchunks; ++k) {
-    const size_t off = k * chunk, m = std::min(chunk, n - off), slot = k & 1;
+    const size_t off = offs[k], m = offs[k + 1] - offs[k], slot = k & 1;
     if (k + 1 < nchunks && (e = h2d(k + 1)) != cudaSuccess) return cuda_error(e, "H2D nodes");
     cudaStreamWaitEvent(ks, h2d_done[slot], 0);
     cudaStreamWaitEvent(ks, d2h_done[slot], 0);  // chunk k-2's bounds have left the slot
