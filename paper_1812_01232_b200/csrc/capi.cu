@@ -498,25 +498,39 @@ int gosma_eval_bounds(gosma_ctx* ctx, const gosma_node* nodes, size_t n, double 
   // still work (the copies then serialise).
   const size_t chunk = std::min<size_t>(n, static_cast<size_t>(1) << 17);
   if ((e = ctx->scratch.reserve(2 * chunk)) != cudaSuccess) return cuda_error(e, "scratch");
-  if (n <= chunk && n <= 8192) {
+  constexpr size_t kSmall = 8192;
+  if (n <= kSmall) {
     // a small batch (the discovery dive's beam): one stream, no cross-stream
-    // events (their latency would dominate)
+    // events (their latency would dominate), staged through pinned memory
+    // (pageable copies go through the driver's own staging, ~10 us each)
+    constexpr size_t kRec = sizeof(gosma_node) + 2 * sizeof(double) + 1;
+    if (!ctx->scratch.h_pinned &&
+        (e = cudaMallocHost(&ctx->scratch.h_pinned, kSmall * kRec)) != cudaSuccess)
+      return cuda_error(e, "pinned staging");
+    auto* hn = static_cast<gosma_node*>(ctx->scratch.h_pinned);
+    auto* hl = reinterpret_cast<double*>(hn + kSmall);
+    double* hu = hl + kSmall;
+    auto* hs = reinterpret_cast<int8_t*>(hu + kSmall);
+    std::memcpy(hn, nodes, n * sizeof(gosma_node));
     cudaStream_t ks = ctx->stream;
-    if ((e = cudaMemcpyAsync(ctx->scratch.d_nodes, nodes, n * sizeof(gosma_node),
+    if ((e = cudaMemcpyAsync(ctx->scratch.d_nodes, hn, n * sizeof(gosma_node),
                              cudaMemcpyHostToDevice, ks)) != cudaSuccess)
       return cuda_error(e, "H2D nodes");
     int8_t* dsp = split_rot ? ctx->scratch.d_split : nullptr;
     const int rc = gosma_eval_bounds_device(ctx, ctx->scratch.d_nodes, n, skip,
                                             ctx->scratch.d_lower, ctx->scratch.d_upper, dsp, ks);
     if (rc != GOSMA_OK) return rc;
-    if ((e = cudaMemcpyAsync(lower, ctx->scratch.d_lower, n * sizeof(double),
+    if ((e = cudaMemcpyAsync(hl, ctx->scratch.d_lower, n * sizeof(double),
                              cudaMemcpyDeviceToHost, ks)) != cudaSuccess ||
-        (e = cudaMemcpyAsync(upper, ctx->scratch.d_upper, n * sizeof(double),
+        (e = cudaMemcpyAsync(hu, ctx->scratch.d_upper, n * sizeof(double),
                              cudaMemcpyDeviceToHost, ks)) != cudaSuccess ||
-        (split_rot && (e = cudaMemcpyAsync(split_rot, dsp, n * sizeof(int8_t),
-                                           cudaMemcpyDeviceToHost, ks)) != cudaSuccess))
+        (split_rot && (e = cudaMemcpyAsync(hs, dsp, n * sizeof(int8_t), cudaMemcpyDeviceToHost,
+                                           ks)) != cudaSuccess))
       return cuda_error(e, "D2H bounds");
     if ((e = cudaStreamSynchronize(ks)) != cudaSuccess) return cuda_error(e, "eval_bounds");
+    std::memcpy(lower, hl, n * sizeof(double));
+    std::memcpy(upper, hu, n * sizeof(double));
+    if (split_rot) std::memcpy(split_rot, hs, n * sizeof(int8_t));
     return GOSMA_OK;
   }
   if (!ctx->h2d_stream) {
