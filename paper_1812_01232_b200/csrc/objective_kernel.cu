@@ -1,11 +1,18 @@
-// K6 — batched FP64 objective value + gradient for the local refiner (SMA):
-// objective_value / objective_gradient (core/src/objective.cpp:175-334) for
-// many poses at once, so the L-BFGS starts of the discovery dive and the
-// incumbent refinements evaluate on the GPU. A request is
-// spread over a grid row of CTAs (threads = model rows, CTAs = slices of the
-// pair partners) so a batch of a few dozen starts still fills the GPU; model
-// rows live in shared memory; FP64 throughout (the refiner tests |g| < 1e-6). Pair terms below the reference's margin
-// (K < a + b - 64, objective.cpp:17) are skipped exactly as on the host.
+// FP64 objective value + gradient on the GPU:
+// objective_value / objective_gradient (core/src/objective.cpp:175-334).
+//
+// * objgrad_block: one CTA evaluates one pose (model rows in shared memory,
+//   FP64 throughout: the refiner tests |g| < 1e-6; pair terms below the
+//   reference's margin, K < a + b - 64, objective.cpp:17, are skipped exactly
+//   as on the host).
+// * K6 (objgrad_kernel): a batch of poses, each spread over a grid row of CTAs
+//   (CTAs = slices of the pair partners, partial sums added on the host in a
+//   fixed order) - gosma_objective_batch.
+// * refine_kernel: the GPU-resident local refiner. One CTA (or a cluster of
+//   CTAs, each taking a partner slice, totals exchanged through distributed
+//   shared memory) runs one start's whole L-BFGS ladder (local_refine /
+//   wolfe_search / clamp_to_domain, solver.cpp:37-258) - the discovery dive's
+//   SMA ladder and the wave refinements for large mixtures.
 //
 // Gradient algebra (objective.cpp:254-334), rearranged so no 3x3 matrix is
 // stored: J_i v = u_i (u_i.v)(-2 d_i / s2_i) - (v - u_i (u_i.v)) (k_i / d_i)
