@@ -741,11 +741,12 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
 
   const double zeta = ctx.zeta;
   const double zeta2 = zeta * zeta;
+  const long long n_items = args.n_dev ? *args.n_dev : args.n;
   for (;;) {
     long long node = 0;
     if (lane == 0) node = static_cast<long long>(atomicAdd(args.work, 1u));
     node = G.bcast0(node);
-    if (node >= args.n) break;
+    if (node >= n_items) break;
     // item lists: full mode over a subset (node = slot); siblings: the item
     // is a selection index k, the parent the pool slot sel[k], the outputs
     // are children 8k .. 8k+7

@@ -150,6 +150,11 @@ void ctx_free_device(gosma_ctx* ctx) {
   ctx->d_child_sel = nullptr;
   ctx->child_cap = 0;
   ctx->scratch.release();
+  if (ctx->dive_graph) cudaGraphExecDestroy(ctx->dive_graph);
+  ctx->dive_graph = nullptr;
+  cudaFree(ctx->dive_buf);
+  ctx->dive_buf = nullptr;
+  ctx->dive_bytes = 0;
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   if (ctx->h2d_stream) cudaStreamDestroy(ctx->h2d_stream);
   if (ctx->d2h_stream) cudaStreamDestroy(ctx->d2h_stream);

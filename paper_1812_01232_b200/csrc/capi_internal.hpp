@@ -70,6 +70,12 @@ struct gosma_ctx {
   gosma_ctx* dive_ctx = nullptr;
   double dive_w = -1.0, dive_dist = -1.0;
   std::mutex dive_mu;
+  // device beam of the dive run on this (blurred) context: one device block
+  // and the captured two-iteration graph, reused while the sizes match
+  void* dive_buf = nullptr;
+  size_t dive_bytes = 0;
+  int dive_sectors = 0, dive_quota = 0;
+  cudaGraphExec_t dive_graph = nullptr;
 };
 
 namespace gosma {

@@ -77,6 +77,7 @@ struct EvalArgs {
   const int32_t* tindex = nullptr;  // node -> cuboid (cross-cached mode)
   const int* item_index = nullptr;  // optional work list: item -> node slot (or selection k)
   const unsigned int* sel = nullptr;  // siblings mode: selection k -> pool slot
+  const long long* n_dev = nullptr;   // item count in device memory (<= n, which sizes the grid)
 };
 
 cudaError_t launch_eval_bounds(const DevCtx& ctx, const EvalArgs& a, int sm_count,

@@ -26,6 +26,7 @@
 #include "capi_internal.hpp"
 #include "frontier.hpp"
 #include "objective_device.hpp"
+#include "dive.hpp"
 #include "sma.hpp"
 
 using namespace gosma;
@@ -249,6 +250,26 @@ int discovery_dive(gosma_ctx* ctx, const Domain& dom, const std::vector<gosma_no
       beam.push_back(e);
     }
   }
+  // the beam loop runs on the device (dive.cu: no host round trip per
+  // iteration); GOSMA_DIVE=host runs the same loop here (A/B, tests)
+  static const bool device_beam = [] {
+    const char* e = std::getenv("GOSMA_DIVE");
+    return !(e && std::string(e) == "host");
+  }();
+  if (device_beam) {
+    std::vector<DiveEntry> db;
+    db.reserve(beam.size());
+    for (const Beam& e : beam) db.push_back(DiveEntry{e.b, e.split, e.sector});
+    std::vector<DiveBest> b0(best.size());
+    for (size_t k = 0; k < best.size(); ++k) b0[k] = DiveBest{best[k].value, best[k].b};
+    DiveBeamResult res;
+    rc = dive_beam_device(coarse, db, b0, used, budget, kMaxIt, static_cast<int>(kQuota), kFloor,
+                          &res);
+    if (rc != GOSMA_OK) return rc;
+    for (size_t k = 0; k < best.size(); ++k) best[k] = Cand{res.best[k].value, res.best[k].node};
+    used = res.used;
+    beam.clear();
+  }
   std::vector<gosma_node> kids;
   std::vector<unsigned> ksec;
   for (int it = 0; it < kMaxIt && !beam.empty() && used + beam.size() * 8 <= budget; ++it) {
@@ -292,8 +313,11 @@ int discovery_dive(gosma_ctx* ctx, const Domain& dom, const std::vector<gosma_no
   *evals += used;
   const auto t_beam = std::chrono::steady_clock::now();
   if (std::getenv("GOSMA_PROFILE"))
-    std::fprintf(stderr, "[gosma profile] dive: beam %.3fs (%d iterations, bounds %.3fs, %llu evals)\n",
-                 std::chrono::duration<double>(t_beam - t_dive).count(), beam_its, t_eval, used);
+    std::fprintf(stderr,
+                 "[gosma profile] dive: beam %.3fs (%s: %d host iterations, bounds %.3fs, %llu "
+                 "evals)\n",
+                 std::chrono::duration<double>(t_beam - t_dive).count(),
+                 device_beam ? "device" : "host", beam_its, t_eval, used);
   // annealing ladder per sector: coarse -> 0.03 -> 0.01 -> exact
   const HostModel hc = blurred_model(m, kCoarse, dbar);
   const HostModel h3 = blurred_model(m, 0.03, dbar);

@@ -314,6 +314,46 @@ def test_local_refine_batch_matches_host(gosma, n1, n2):
     assert agree >= len(r0) - 3
 
 
+def test_device_dive_beam_matches_host_beam(gosma):
+    """The discovery dive's beam on the device (dive.cu, default) takes the
+    same decisions as the host loop (GOSMA_DIVE=host, run in a subprocess: the
+    switch is read once per process): identical incumbent, bound and
+    evaluation counts on budget-limited solves of a 44-sector scene-like
+    problem and of the certify instance."""
+    import json
+    import subprocess
+    import sys
+    code = r"""
+import json, numpy as np, paper_1812_01232_b200 as g
+from paper_1812_01232_b200 import synth
+from oracle.bind import Mixture
+out = []
+for n1, n2 in [(12, 12), (40, 24)]:
+    ctx = g.ObjectiveContext(synth.mixture(n1, n2, "realistic", seed=5), 0.5)
+    dom = g.PoseDomain(np.zeros(3), np.pi, synth.torus_cover(3.5, 0.5))
+    r = g.solve(ctx, dom, g.SolverConfig(epsilon=0.1, zeta=0.5, max_evaluations=3000000))
+    out.append([r.best_value, r.global_lower, r.bound_evaluations, r.sma_invocations])
+G = json.load(open("tests/golden/certify_golden.json"))
+inst = max(G["instances"], key=lambda x: x["bound_evaluations"])
+mix = Mixture.from_dict(inst["mixture"])
+ctx = g.ObjectiveContext([{"mu": mix.mu, "sigma2": mix.sigma2, "phi1": mix.phi1, "dir": mix.dir,
+                           "kappa2": mix.kappa2, "phi2": mix.phi2}], mix.zeta, single_mixture=True)
+dom = g.PoseDomain(np.array(inst["rot_c"]), inst["rot_hw"], np.array(inst["boxes"]))
+r = g.solve(ctx, dom, g.SolverConfig(epsilon=inst["epsilon"], zeta=mix.zeta, time_limit=120))
+out.append([r.best_value, r.global_lower, r.bound_evaluations, r.sma_invocations])
+print(json.dumps(out))
+"""
+    res = {}
+    for mode in ("device", "host"):
+        env = dict(os.environ, GOSMA_DIVE=mode)
+        p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                           cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                           timeout=600)
+        assert p.returncode == 0, p.stderr[-2000:]
+        res[mode] = json.loads(p.stdout.strip().splitlines()[-1])
+    assert res["device"] == res["host"]
+
+
 def test_export_import_host_and_device_paths(gosma):
     """Rebalancing primitives: exported nodes leave the donor (its live volume
     drops by their volume) and join the receiver; the device-buffer path moves
