@@ -6,17 +6,18 @@ import paper_1812_01232_b200 as g
 from paper_1812_01232_b200 import synth
 n = int(os.environ.get("NODES", "1000000"))
 W = [("realistic", 64, 32), ("moderate", 64, 32), ("realistic", 256, 128), ("realistic", 12, 12),
-     ("realistic", 41, 36), ("realistic", 45, 40)]
+     ("realistic", 41, 36), ("realistic", 45, 40), ("realistic", 8, 4, 8), ("realistic", 32, 16, 8)]
 only = os.environ.get("ONLY")
-for regime, n1, n2 in ([W[int(k)] for k in only.split(",")] if only else W):
-    cls = synth.mixture(n1, n2, regime, seed=2026)
+for regime, n1, n2, *rest in ([W[int(k)] for k in only.split(",")] if only else W):
+    nc = rest[0] if rest else 1  # semantic classes (block-sparse pair terms, BASELINE configs[3])
+    cls = synth.mixture(n1, n2, regime, seed=2026, n_classes=nc)
     ctx = g.ObjectiveContext(cls, 0.5)
     nn = n if n1 < 256 else n // 16
     nodes = synth.nodes(nn, seed=2027)
     st = torch.cuda.Stream()
     dn = torch.from_numpy(nodes.view(np.uint8)).cuda()
     lo = torch.empty(nn, dtype=torch.float64, device="cuda"); up = torch.empty_like(lo)
-    P = n1 * n2 + n1 * (n1 - 1) // 2
+    P = nc * (n1 * n2 + n1 * (n1 - 1) // 2)
     for rep in range(1):
         with torch.cuda.stream(st):
             for _ in range(2):
@@ -28,4 +29,4 @@ for regime, n1, n2 in ([W[int(k)] for k in only.split(",")] if only else W):
             e1.record(st)
         st.synchronize()
         ms = e0.elapsed_time(e1) / 3
-        print(f"{regime:9s} {n1}x{n2} nodes {nn} {ms:8.3f} ms  {nn/ms*1e3:.3e} bounds/s  {nn*P/ms*1e3:.3e} pairs/s", flush=True)
+        print(f"{regime:9s} {nc}x({n1}x{n2}) nodes {nn} {ms:8.3f} ms  {nn/ms*1e3:.3e} bounds/s  {nn*P/ms*1e3:.3e} pairs/s", flush=True)
