@@ -663,7 +663,9 @@ __device__ __forceinline__ void psi_trans_half(double u0, double u1, double u2, 
 // the cross terms plus the cached self sums of the node's cuboid; kSiblings =
 // per rotation-split parent: the cuboid prologue and self sums once, then the
 // cross sums of its 8 children (subdivide_adaptive, se3.cpp:124-131).
-enum { kModeFull = 0, kSelfOnly = 1, kCrossCached = 2, kSiblings = 3 };
+// kModeStream = the full mode for multi-class contexts, one class's table at
+// a time (a separate instantiation: the single-class kernel is unchanged).
+enum { kModeFull = 0, kSelfOnly = 1, kCrossCached = 2, kSiblings = 3, kModeStream = 4 };
 
 // Rodrigues R0 = rotation_matrix(rc) (se3.cpp:21-31), FP64.
 __device__ __forceinline__ void rodrigues(double rc0, double rc1, double rc2, double R[9]) {
@@ -717,6 +719,23 @@ __device__ __forceinline__ void column_prep(const WarpTables& T, const DevCtx& c
   }
 }
 
+// Columns [o2, o2 + n2) of the context into table slots 0..n2-1.
+__device__ __forceinline__ void column_prep_span(const WarpTables& T, const DevCtx& ctx, int lane,
+                                                 int step, const double R[9], int o2, int n2) {
+  for (int jl = lane; jl < n2; jl += step) {
+    const int j = o2 + jl;
+    const double x0 = ctx.m[3 * j], x1 = ctx.m[3 * j + 1], x2 = ctx.m[3 * j + 2];
+    const double q0 = R[0] * x0 + R[3] * x1 + R[6] * x2;
+    const double q1 = R[1] * x0 + R[4] * x1 + R[7] * x2;
+    const double q2 = R[2] * x0 + R[5] * x1 + R[8] * x2;
+    const float f0 = static_cast<float>(q0), f1 = static_cast<float>(q1),
+                f2 = static_cast<float>(q2);
+    T.col[jl * kColF4] = make_float4(f0, f1, f2, ctx.kappa2[j]);
+    T.col[jl * kColF4 + 1] = make_float4(static_cast<float>(q0 - f0), static_cast<float>(q1 - f1),
+                                         static_cast<float>(q2 - f2), ctx.g2[j]);
+  }
+}
+
 #ifndef GOSMA_MIN_BLOCKS
 #define GOSMA_MIN_BLOCKS 7
 #endif
@@ -731,13 +750,17 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
   const unsigned gm = kG >= 32 ? kFull : (((1u << kG) - 1u) << gbase);
   const int group = static_cast<int>(threadIdx.x) / kG;
   const Group<kG> G{gm, gbase, &gscratch};
-  const int N1 = ctx.n1_total, N2 = ctx.n2_total;
-  const size_t per_warp_f4 = static_cast<size_t>((kRowF4 + 1) * N1 + kColF4 * N2);
+  // class-streamed full mode (multi-class contexts): the table holds one
+  // class's rows and columns at a time, so it is sized by the largest class
+  constexpr bool streamed = kMode == kModeStream;
+  const int N1 = ctx.n1_total;  // every model mean (feasibility scans)
+  const int TN1 = streamed ? ctx.max_n1 : N1, TN2 = streamed ? ctx.max_n2 : ctx.n2_total;
+  const size_t per_warp_f4 = static_cast<size_t>((kRowF4 + 1) * TN1 + kColF4 * TN2);
   float4* base = smem4 + group * per_warp_f4;
   WarpTables T;
   T.row = base;
-  T.col = base + kRowF4 * N1;
-  double2* stct = reinterpret_cast<double2*>(T.col + kColF4 * N2);  // FP64 psi_t half-angles
+  T.col = base + kRowF4 * TN1;
+  double2* stct = reinterpret_cast<double2*>(T.col + kColF4 * TN2);  // FP64 psi_t half-angles
 
   const double zeta = ctx.zeta;
   const double zeta2 = zeta * zeta;
@@ -860,71 +883,99 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
     }
     const bool same = (ts0 == tc0) && (ts1 == tc1) && (ts2 == tc2);
 
-    // ---- per-row prep (all classes): kappa interval, psi_t, projections
+    // ---- per-row prep: kappa interval, psi_t, projections; row i of the
+    // context into table slot `slot`
     double lb_self = 0.0, lb_cross = 0.0, ub_self = 0.0, ub_cross = 0.0, lb_err = 0.0;
     double st_max = 0.0;
-    for (int c = 0; c < ctx.n_classes; ++c) {
-      const ClassSpan cs = ctx.cls[c];
-      const float w = static_cast<float>(ctx.cls_w[c]);
-      float dsl = 0.0f, dsu = 0.0f;
-      for (int il = lane; il < cs.n1; il += kG) {
-        const int i = cs.o1 + il;
-        const double m0 = ctx.mu[3 * i], m1 = ctx.mu[3 * i + 1], m2 = ctx.mu[3 * i + 2];
-        const double is2 = ctx.inv_s2[i];
-        const double u0 = m0 - tc0, u1 = m1 - tc1, u2 = m2 - tc2;
-        const double a0 = fabs(u0), a1 = fabs(u1), a2 = fabs(u2);
-        // point_cuboid_distance (se3.cpp:60-66); dlo floored at zeta
-        const double o0 = fmax(a0 - h0, 0.0), o1 = fmax(a1 - h1, 0.0), o2 = fmax(a2 - h2, 0.0);
-        const double dlo2 = fmax(o0 * o0 + o1 * o1 + o2 * o2, zeta2);
-        const double dhi2 = (a0 + h0) * (a0 + h0) + (a1 + h1) * (a1 + h1) + (a2 + h2) * (a2 + h2);
-        const float klo = static_cast<float>(dlo2 * is2 + 1.0);
-        const float khi = static_cast<float>(dhi2 * is2 + 1.0);
-        const double un2 = u0 * u0 + u1 * u1 + u2 * u2;
-        double c0 = 1.0, c1 = 0.0, c2 = 0.0;  // UnitX when the mean is at the centre
-        if (un2 > 1e-24) {
-          const double inv = rsqrt(un2);
-          c0 = u0 * inv;
-          c1 = u1 * inv;
-          c2 = u2 * inv;
-        }
-        double st, ct;
-        if (a0 <= h0 && a1 <= h1 && a2 <= h2) {
-          st = 1.0;  // psi_t = pi
-          ct = 0.0;
-        } else {
-          psi_trans_half(u0, u1, u2, h0, h1, h2, c0, c1, c2, st, ct);
-        }
-        st_max = fmax(st_max, st);
-        stct[i] = make_double2(st, ct);
-        double sp, cp;
-        half_angles(st, ct, s_r, c_r, sp, cp);
-        // UB projection at t* (project_model, objective.cpp:175-192)
-        const double v0 = m0 - ts0, v1 = m1 - ts1, v2 = m2 - ts2;
-        const double vn2 = v0 * v0 + v1 * v1 + v2 * v2;
-        const float kst = static_cast<float>(vn2 * is2 + 1.0);
-        const double iv = rsqrt(vn2);
-        const float phi = static_cast<float>(ctx.phi1[i]);
-        dsl += diag_term(phi, klo);
-        dsu += diag_term(phi, kst);
-        // phi / W(k) = phi * k / (1 - e^{-2k}) (k >= 1)
-        const float Flo = phi * klo * rcpf(1.0f - ex2f(-2.0f * kL2E * klo));
-        const float Fhi = phi * khi * rcpf(1.0f - ex2f(-2.0f * kL2E * khi));
-        const float Fst = phi * kst * rcpf(1.0f - ex2f(-2.0f * kL2E * kst));
-        const float uhx = static_cast<float>(c0), uhy = static_cast<float>(c1),
-                    uhz = static_cast<float>(c2);
-        float4* pr = T.row + i * kRowF4;
-        pr[0] = make_float4(uhx, uhy, uhz, Fst);
-        pr[1] = make_float4(khi, Flo, static_cast<float>(st), static_cast<float>(ct));
-        pr[2] = make_float4(static_cast<float>(c0 - uhx), static_cast<float>(c1 - uhy),
-                            static_cast<float>(c2 - uhz), kst);
-        pr[3] = make_float4(static_cast<float>(v0 * iv), static_cast<float>(v1 * iv),
-                            static_cast<float>(v2 * iv), static_cast<float>(4.0 * sp * sp));
-        pr[4] = make_float4(klo, static_cast<float>(sp), static_cast<float>(cp), Fhi);
+    auto prep_row = [&](int i, int slot, float& dsl, float& dsu) {
+      const double m0 = ctx.mu[3 * i], m1 = ctx.mu[3 * i + 1], m2 = ctx.mu[3 * i + 2];
+      const double is2 = ctx.inv_s2[i];
+      const double u0 = m0 - tc0, u1 = m1 - tc1, u2 = m2 - tc2;
+      const double a0 = fabs(u0), a1 = fabs(u1), a2 = fabs(u2);
+      // point_cuboid_distance (se3.cpp:60-66); dlo floored at zeta
+      const double o0 = fmax(a0 - h0, 0.0), o1 = fmax(a1 - h1, 0.0), o2 = fmax(a2 - h2, 0.0);
+      const double dlo2 = fmax(o0 * o0 + o1 * o1 + o2 * o2, zeta2);
+      const double dhi2 = (a0 + h0) * (a0 + h0) + (a1 + h1) * (a1 + h1) + (a2 + h2) * (a2 + h2);
+      const float klo = static_cast<float>(dlo2 * is2 + 1.0);
+      const float khi = static_cast<float>(dhi2 * is2 + 1.0);
+      const double un2 = u0 * u0 + u1 * u1 + u2 * u2;
+      double c0 = 1.0, c1 = 0.0, c2 = 0.0;  // UnitX when the mean is at the centre
+      if (un2 > 1e-24) {
+        const double inv = rsqrt(un2);
+        c0 = u0 * inv;
+        c1 = u1 * inv;
+        c2 = u2 * inv;
       }
-      if (!infeasible && kMode != kCrossCached) {
+      double st, ct;
+      if (a0 <= h0 && a1 <= h1 && a2 <= h2) {
+        st = 1.0;  // psi_t = pi
+        ct = 0.0;
+      } else {
+        psi_trans_half(u0, u1, u2, h0, h1, h2, c0, c1, c2, st, ct);
+      }
+      st_max = fmax(st_max, st);
+      if (kMode == kSiblings) stct[i] = make_double2(st, ct);
+      double sp, cp;
+      half_angles(st, ct, s_r, c_r, sp, cp);
+      // UB projection at t* (project_model, objective.cpp:175-192)
+      const double v0 = m0 - ts0, v1 = m1 - ts1, v2 = m2 - ts2;
+      const double vn2 = v0 * v0 + v1 * v1 + v2 * v2;
+      const float kst = static_cast<float>(vn2 * is2 + 1.0);
+      const double iv = rsqrt(vn2);
+      const float phi = static_cast<float>(ctx.phi1[i]);
+      dsl += diag_term(phi, klo);
+      dsu += diag_term(phi, kst);
+      // phi / W(k) = phi * k / (1 - e^{-2k}) (k >= 1)
+      const float Flo = phi * klo * rcpf(1.0f - ex2f(-2.0f * kL2E * klo));
+      const float Fhi = phi * khi * rcpf(1.0f - ex2f(-2.0f * kL2E * khi));
+      const float Fst = phi * kst * rcpf(1.0f - ex2f(-2.0f * kL2E * kst));
+      const float uhx = static_cast<float>(c0), uhy = static_cast<float>(c1),
+                  uhz = static_cast<float>(c2);
+      float4* pr = T.row + slot * kRowF4;
+      pr[0] = make_float4(uhx, uhy, uhz, Fst);
+      pr[1] = make_float4(khi, Flo, static_cast<float>(st), static_cast<float>(ct));
+      pr[2] = make_float4(static_cast<float>(c0 - uhx), static_cast<float>(c1 - uhy),
+                          static_cast<float>(c2 - uhz), kst);
+      pr[3] = make_float4(static_cast<float>(v0 * iv), static_cast<float>(v1 * iv),
+                          static_cast<float>(v2 * iv), static_cast<float>(4.0 * sp * sp));
+      pr[4] = make_float4(klo, static_cast<float>(sp), static_cast<float>(cp), Fhi);
+    };
+    if (!streamed) {
+      for (int c = 0; c < ctx.n_classes; ++c) {
+        const ClassSpan cs = ctx.cls[c];
+        const float w = static_cast<float>(ctx.cls_w[c]);
+        float dsl = 0.0f, dsu = 0.0f;
+        for (int il = lane; il < cs.n1; il += kG) prep_row(cs.o1 + il, cs.o1 + il, dsl, dsu);
+        if (!infeasible && kMode != kCrossCached) {
+          lb_self += static_cast<double>(w * dsl);
+          lb_err += static_cast<double>(w * dsl * kErrTerm);
+          ub_self += static_cast<double>(w * dsu);
+        }
+      }
+    } else {
+      // one class at a time: rows, columns, then its pairs
+      for (int c = 0; c < ctx.n_classes; ++c) {
+        const ClassSpan cs = ctx.cls[c];
+        const float w = static_cast<float>(ctx.cls_w[c]);
+        float dsl = 0.0f, dsu = 0.0f;
+        G.sync();  // the previous class's pairs are done with the table
+        for (int il = lane; il < cs.n1; il += kG) prep_row(cs.o1 + il, il, dsl, dsu);
+        if (infeasible) continue;  // (rows still feed the split decision)
         lb_self += static_cast<double>(w * dsl);
         lb_err += static_cast<double>(w * dsl * kErrTerm);
         ub_self += static_cast<double>(w * dsu);
+        column_prep_span(T, ctx, lane, kG, R, cs.o2, cs.n2);
+        G.sync();
+#ifndef GOSMA_PREP_ONLY
+        const ClassSpan loc{0, cs.n1, 0, cs.n2};
+        if (same) {
+          class_pairs<kG, true, true, true, kTail>(T, loc, lane, w, lb_self, lb_cross, ub_self,
+                                                   ub_cross, lb_err);
+        } else {
+          class_pairs<kG, false, true, true, kTail>(T, loc, lane, w, lb_self, lb_cross, ub_self,
+                                                    ub_cross, lb_err);
+        }
+#endif
       }
     }
     // split decision (subdivide_adaptive, se3.cpp:107-121)
@@ -1048,12 +1099,12 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
       continue;
     }
     // ---- per-column prep: q_j = R0^T m_j (bounds.cpp:97-102), double-float
-    if (kMode != kSelfOnly) column_prep(T, ctx, lane, kG, R);
+    if (kMode != kSelfOnly && !streamed) column_prep(T, ctx, lane, kG, R);
     G.sync();
 
     // ---- pair sweeps (GOSMA_PREP_ONLY: times the per-node prep alone)
 #ifndef GOSMA_PREP_ONLY
-    for (int c = 0; c < ctx.n_classes; ++c) {
+    for (int c = 0; !streamed && c < ctx.n_classes; ++c) {
       const ClassSpan cs = ctx.cls[c];
       const float w = static_cast<float>(ctx.cls_w[c]);
       constexpr bool kC = kMode != kSelfOnly, kS = kMode != kCrossCached;
@@ -1106,8 +1157,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
 
 }  // namespace
 
-size_t eval_smem_per_warp(const DevCtx& ctx) {
-  const size_t f4 = static_cast<size_t>((kRowF4 + 1) * ctx.n1_total + kColF4 * ctx.n2_total);
+size_t eval_smem_per_warp(const DevCtx& ctx, int mode) {
+  const bool streamed = mode == kModeStream;
+  const int n1 = streamed ? ctx.max_n1 : ctx.n1_total, n2 = streamed ? ctx.max_n2 : ctx.n2_total;
+  const size_t f4 = static_cast<size_t>((kRowF4 + 1) * n1 + kColF4 * n2);
   return f4 * sizeof(float4);
 }
 
@@ -1115,14 +1168,14 @@ namespace {
 
 // Lanes per node: 8 / 16 when every class has at most that many model rows
 // and the per-group tables stay small (GOSMA_GROUP=32 forces whole warps).
-int group_lanes(const DevCtx& ctx) {
+int group_lanes(const DevCtx& ctx, int mode) {
   static const int forced = [] {
     const char* e = std::getenv("GOSMA_GROUP");
     return e ? std::atoi(e) : 0;
   }();
   if (forced == 8 || forced == 16 || forced == 32) return forced;
   if (forced == 128) return kCtaGroup;
-  const size_t table = eval_smem_per_warp(ctx);
+  const size_t table = eval_smem_per_warp(ctx, mode);
   for (int g : {8, 16}) {
     if (ctx.max_n1 <= g && table * kWarpsPerCta * (32 / g) <= 64 * 1024) return g;
   }
@@ -1149,7 +1202,7 @@ cudaError_t launch_group(const DevCtx& ctx, const EvalArgs& a, int sm_count,
   static std::vector<Choice> cache;
   int device = 0;
   cudaGetDevice(&device);
-  const size_t per_warp = eval_smem_per_warp(ctx);
+  const size_t per_warp = eval_smem_per_warp(ctx, kMode);
   int best_warps = kWarpsPerCta, best_per_sm = 0;
   size_t best_smem = 0;
   bool hit = false;
@@ -1211,7 +1264,7 @@ template <int kMode>
 cudaError_t launch_mode(const DevCtx& ctx, const EvalArgs& a, int sm_count,
                         cudaStream_t stream) {
   if (a.n <= 0) return cudaSuccess;
-  switch (group_lanes(ctx)) {
+  switch (group_lanes(ctx, kMode)) {
     case kCtaGroup:
       return launch_group<kMode, kCtaGroup, false>(ctx, a, sm_count, stream);
     case 8:
@@ -1228,7 +1281,8 @@ cudaError_t launch_mode(const DevCtx& ctx, const EvalArgs& a, int sm_count,
 
 cudaError_t launch_eval_bounds(const DevCtx& ctx, const EvalArgs& a, int sm_count,
                                cudaStream_t stream) {
-  return launch_mode<kModeFull>(ctx, a, sm_count, stream);
+  return ctx.stream_classes ? launch_mode<kModeStream>(ctx, a, sm_count, stream)
+                            : launch_mode<kModeFull>(ctx, a, sm_count, stream);
 }
 
 cudaError_t launch_eval_self(const DevCtx& ctx, const EvalArgs& a, int sm_count,

@@ -90,6 +90,14 @@ int ctx_upload(gosma_ctx* ctx) {
   d.n1_total = o1;
   d.n2_total = o2;
   d.max_n1 = max_n1;
+  d.max_n2 = 0;
+  for (const HostClass& c : hm.classes) d.max_n2 = std::max(d.max_n2, c.n2());
+  // GOSMA_STREAM_CLASSES=0: keep every class's table (A/B measurements)
+  static const bool no_stream = [] {
+    const char* e = std::getenv("GOSMA_STREAM_CLASSES");
+    return e && std::string(e) == "0";
+  }();
+  d.stream_classes = hm.classes.size() > 1 && !no_stream ? 1 : 0;
   d.zeta = hm.zeta;
   d.lb_margin = ctx->lb_margin;
   d.lb_err_scale = 1.0;

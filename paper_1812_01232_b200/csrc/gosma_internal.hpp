@@ -46,6 +46,8 @@ struct DevCtx {
   double lb_margin;      // relative soundness floor (x |term| mass)
   double lb_err_scale;   // 1: subtract the FP32 error estimate; 0: raw core (diagnostics)
   int tail_chunks;       // some class has a last row chunk of <= 16 of 32 rows
+  int max_n2;            // largest class n2
+  int stream_classes;    // full mode keeps one class's table at a time (n_classes > 1)
 };
 
 // Host-side master copy of one class (ClassData, objective.hpp:19-31).
@@ -93,7 +95,10 @@ cudaError_t launch_eval_self(const DevCtx& ctx, const EvalArgs& a, int sm_count,
                              cudaStream_t stream);
 cudaError_t launch_eval_cross_cached(const DevCtx& ctx, const EvalArgs& a, int sm_count,
                                      cudaStream_t stream);
-size_t eval_smem_per_warp(const DevCtx& ctx);
+// Shared-memory table bytes per lane group: every class's rows and columns
+// (mode < 0: the largest over the modes), or one class's at a time for the
+// class-streamed full mode of a multi-class context (mode 4).
+size_t eval_smem_per_warp(const DevCtx& ctx, int mode = -1);
 cudaError_t make_children(const gosma_node* d_parents, const int8_t* d_split, size_t n,
                           gosma_node* d_kids, int* d_rot, int* d_trans, int* d_counts,
                           unsigned int* d_sel, cudaStream_t stream);
