@@ -108,7 +108,10 @@ def rand_nodes(rng, n):
     (12, 10, 150.0, 0.2, 1), (16, 16, 150.0, 0.2, 1), (9, 3, 150.0, 0.2, 2), (8, 40, 150.0, 0.2, 1),
     # partial last row chunks (lanes share a row's partners): 41, 70, and a
     # small class next to a 35-row class
-    (41, 36, 150.0, 0.2, 1), (70, 20, 150.0, 0.2, 1), (35, 9, 150.0, 0.2, 2)])
+    (41, 36, 150.0, 0.2, 1), (70, 20, 150.0, 0.2, 1), (35, 9, 150.0, 0.2, 2),
+    # multi-class contexts run the class-streamed full mode (one class's table
+    # at a time): whole-warp groups with and without partial chunks, CTA groups
+    (33, 17, 150.0, 0.2, 3), (32, 16, 150.0, 0.2, 4), (96, 24, 150.0, 0.2, 2)])
 def test_moderate_regimes(gosma, n1, n2, kcap, zeta, ncls):
     rng = np.random.default_rng(1000 + n1 * 7 + n2)
     check_parity(gosma, rand_mix(rng, n1, n2, kcap, zeta, ncls), rand_nodes(rng, 1500))
