@@ -755,12 +755,11 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
   constexpr bool streamed = kMode == kModeStream;
   const int N1 = ctx.n1_total;  // every model mean (feasibility scans)
   const int TN1 = streamed ? ctx.max_n1 : N1, TN2 = streamed ? ctx.max_n2 : ctx.n2_total;
-  const size_t per_warp_f4 = static_cast<size_t>((kRowF4 + 1) * TN1 + kColF4 * TN2);
+  const size_t per_warp_f4 = static_cast<size_t>(kRowF4 * TN1 + kColF4 * TN2);
   float4* base = smem4 + group * per_warp_f4;
   WarpTables T;
   T.row = base;
   T.col = base + kRowF4 * TN1;
-  double2* stct = reinterpret_cast<double2*>(T.col + kColF4 * TN2);  // FP64 psi_t half-angles
 
   const double zeta = ctx.zeta;
   const double zeta2 = zeta * zeta;
@@ -829,6 +828,11 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
       rodrigues(rc0, rc1, rc2, R);
       const double psi_r = fmin(sqrt(3.0) * rhw, M_PI);
       sincos(0.5 * psi_r, &s_r, &c_r);
+    } else {
+      // the 8 rotation children share psi_r (their half-width 0.5 rhw): the
+      // rows are prepared once with it (psi_t + psi_r half-angles)
+      const double psi_c = fmin(sqrt(3.0) * (0.5 * rhw), M_PI);
+      sincos(0.5 * psi_c, &s_r, &c_r);
     }
 
     // ---- feasible_center (bounds.cpp:187-214): t*, warp-cooperative scan
@@ -914,7 +918,6 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
         psi_trans_half(u0, u1, u2, h0, h1, h2, c0, c1, c2, st, ct);
       }
       st_max = fmax(st_max, st);
-      if (kMode == kSiblings) stct[i] = make_double2(st, ct);
       double sp, cp;
       half_angles(st, ct, s_r, c_r, sp, cp);
       // UB projection at t* (project_model, objective.cpp:175-192)
@@ -1007,9 +1010,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
         const int sx = (ch & 4) ? 1 : -1, sy = (ch & 2) ? 1 : -1, sz = (ch & 1) ? 1 : -1;
         // the child exactly as the expand kernel builds it (k.rc[a] += h * s)
         const double crc0 = rc0 + hr * sx, crc1 = rc1 + hr * sy, crc2 = rc2 + hr * sz;
-        const double psi_c = fmin(sqrt(3.0) * hr, M_PI);
-        double cs_r, cc_r;
-        sincos(0.5 * psi_c, &cs_r, &cc_r);
+        const double cs_r = s_r;  // sin(psi_c / 2), shared by the children
         if (lane == 0 && args.split_rot) {
           const bool rot_ok = hr > 1e-9;
           int8_t sr;
@@ -1030,19 +1031,6 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
         double Rc[9];
         rodrigues(crc0, crc1, crc2, Rc);
         G.sync();
-        for (int c = 0; c < ctx.n_classes; ++c) {
-          const ClassSpan cs = ctx.cls[c];
-          for (int il = lane; il < cs.n1; il += kG) {
-            const int i = cs.o1 + il;
-            const double2 sc = stct[i];
-            double sp, cp;
-            half_angles(sc.x, sc.y, cs_r, cc_r, sp, cp);
-            float4* pr = T.row + i * kRowF4;
-            pr[4].y = static_cast<float>(sp);
-            pr[4].z = static_cast<float>(cp);
-            pr[3].w = static_cast<float>(4.0 * sp * sp);
-          }
-        }
         column_prep(T, ctx, lane, kG, Rc);
         G.sync();
         double lcr = 0.0, ucr = 0.0, ecr = 0.0, dl = 0.0, du = 0.0;
@@ -1160,7 +1148,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
 size_t eval_smem_per_warp(const DevCtx& ctx, int mode) {
   const bool streamed = mode == kModeStream;
   const int n1 = streamed ? ctx.max_n1 : ctx.n1_total, n2 = streamed ? ctx.max_n2 : ctx.n2_total;
-  const size_t f4 = static_cast<size_t>((kRowF4 + 1) * n1 + kColF4 * n2);
+  const size_t f4 = static_cast<size_t>(kRowF4 * n1 + kColF4 * n2);
   return f4 * sizeof(float4);
 }
 
