@@ -665,7 +665,17 @@ __device__ __forceinline__ void psi_trans_half(double u0, double u1, double u2, 
 // cross sums of its 8 children (subdivide_adaptive, se3.cpp:124-131).
 // kModeStream = the full mode for multi-class contexts, one class's table at
 // a time (a separate instantiation: the single-class kernel is unchanged).
-enum { kModeFull = 0, kSelfOnly = 1, kCrossCached = 2, kSiblings = 3, kModeStream = 4 };
+enum {
+  kModeFull = 0,
+  kSelfOnly = 1,
+  kCrossCached = 2,
+  kSiblings = 3,
+  kModeStream = 4,
+  kSiblingsStream = 5  // siblings mode of a multi-class context, one class's table at a time
+};
+// per-group extra shared memory of kSiblingsStream: the 8 children's R (72
+// doubles) and their {lb, ub, err} cross sums (24 doubles)
+constexpr int kSibStreamExtraF4 = (72 + 24) * 8 / 16;
 
 // Rodrigues R0 = rotation_matrix(rc) (se3.cpp:21-31), FP64.
 __device__ __forceinline__ void rodrigues(double rc0, double rc1, double rc2, double R[9]) {
@@ -752,10 +762,12 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
   const Group<kG> G{gm, gbase, &gscratch};
   // class-streamed full mode (multi-class contexts): the table holds one
   // class's rows and columns at a time, so it is sized by the largest class
-  constexpr bool streamed = kMode == kModeStream;
+  constexpr bool streamed = kMode == kModeStream || kMode == kSiblingsStream;
+  constexpr bool kSib = kMode == kSiblings || kMode == kSiblingsStream;
   const int N1 = ctx.n1_total;  // every model mean (feasibility scans)
   const int TN1 = streamed ? ctx.max_n1 : N1, TN2 = streamed ? ctx.max_n2 : ctx.n2_total;
-  const size_t per_warp_f4 = static_cast<size_t>(kRowF4 * TN1 + kColF4 * TN2);
+  const size_t table_f4 = static_cast<size_t>(kRowF4 * TN1 + kColF4 * TN2);
+  const size_t per_warp_f4 = table_f4 + (kMode == kSiblingsStream ? kSibStreamExtraF4 : 0);
   float4* base = smem4 + group * per_warp_f4;
   WarpTables T;
   T.row = base;
@@ -774,7 +786,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
     // are children 8k .. 8k+7
     long long item = node;
     if (args.item_index) node = args.item_index[node];
-    if (kMode == kSiblings) {
+    if (kSib) {
       item = node;
       node = args.sel[node];
     }
@@ -824,7 +836,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
     // ---- rotation: R0 = rotation_matrix(rc) (se3.cpp:21-31), psi_r (se3.cpp:68-70)
     double R[9];
     double s_r = 0.0, c_r = 1.0;
-    if (kMode != kSiblings) {
+    if (!kSib) {
       rodrigues(rc0, rc1, rc2, R);
       const double psi_r = fmin(sqrt(3.0) * rhw, M_PI);
       sincos(0.5 * psi_r, &s_r, &c_r);
@@ -943,7 +955,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
                           static_cast<float>(v2 * iv), static_cast<float>(4.0 * sp * sp));
       pr[4] = make_float4(klo, static_cast<float>(sp), static_cast<float>(cp), Fhi);
     };
-    if (!streamed) {
+    if constexpr (!streamed) {
       for (int c = 0; c < ctx.n_classes; ++c) {
         const ClassSpan cs = ctx.cls[c];
         const float w = static_cast<float>(ctx.cls_w[c]);
@@ -955,7 +967,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
           ub_self += static_cast<double>(w * dsu);
         }
       }
-    } else {
+    } else if constexpr (kMode == kModeStream) {
       // one class at a time: rows, columns, then its pairs
       for (int c = 0; c < ctx.n_classes; ++c) {
         const ClassSpan cs = ctx.cls[c];
@@ -980,6 +992,100 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
         }
 #endif
       }
+    }
+    if constexpr (kMode == kSiblingsStream) {
+      // one cuboid, 8 rotation children, one class at a time: the class's
+      // rows (with the children's shared psi_r) and self sums, then per child
+      // its columns and cross sums, accumulated per child in shared memory
+      double* const Rcs = reinterpret_cast<double*>(base + table_f4);  // [8][9]
+      double* const acc = Rcs + 72;                                      // [8][3]
+      const double hr = 0.5 * rhw;
+      for (int ch = lane; ch < 8; ch += kG) {
+        const int sx = (ch & 4) ? 1 : -1, sy = (ch & 2) ? 1 : -1, sz = (ch & 1) ? 1 : -1;
+        rodrigues(rc0 + hr * sx, rc1 + hr * sy, rc2 + hr * sz, Rcs + 9 * ch);
+      }
+      for (int k = lane; k < 24; k += kG) acc[k] = 0.0;
+      double sl_self = 0.0, su_self = 0.0, se_self = 0.0;
+      for (int c = 0; c < ctx.n_classes; ++c) {
+        const ClassSpan cs = ctx.cls[c];
+        const float w = static_cast<float>(ctx.cls_w[c]);
+        float dsl = 0.0f, dsu = 0.0f;
+        G.sync();  // the previous class's pairs are done with the table
+        for (int il = lane; il < cs.n1; il += kG) prep_row(cs.o1 + il, il, dsl, dsu);
+        if (infeasible) continue;  // (rows still feed the split decision)
+        sl_self += static_cast<double>(w * dsl);
+        se_self += static_cast<double>(w * dsl * kErrTerm);
+        su_self += static_cast<double>(w * dsu);
+        G.sync();
+        const ClassSpan loc{0, cs.n1, 0, cs.n2};
+        double dl = 0.0, du = 0.0;
+#ifndef GOSMA_PREP_ONLY
+        if (same) {
+          class_pairs<kG, true, false, true, kTail>(T, loc, lane, w, sl_self, dl, su_self, du,
+                                                    se_self);
+        } else {
+          class_pairs<kG, false, false, true, kTail>(T, loc, lane, w, sl_self, dl, su_self, du,
+                                                     se_self);
+        }
+#endif
+        for (int ch = 0; ch < 8; ++ch) {
+          G.sync();  // the previous child's pairs are done with the columns
+          column_prep_span(T, ctx, lane, kG, Rcs + 9 * ch, cs.o2, cs.n2);
+          G.sync();
+          double lcr = 0.0, ucr = 0.0, ecr = 0.0;
+#ifndef GOSMA_PREP_ONLY
+          if (same) {
+            class_pairs<kG, true, true, false, kTail>(T, loc, lane, w, dl, lcr, du, ucr, ecr);
+          } else {
+            class_pairs<kG, false, true, false, kTail>(T, loc, lane, w, dl, lcr, du, ucr, ecr);
+          }
+#endif
+          lcr = G.sum(lcr);
+          ucr = G.sum(ucr);
+          ecr = G.sum(ecr);
+          if (lane == 0) {
+            acc[3 * ch] += lcr;
+            acc[3 * ch + 1] += ucr;
+            acc[3 * ch + 2] += ecr;
+          }
+        }
+      }
+      st_max = G.max(st_max);
+      sl_self = G.sum(sl_self);
+      su_self = G.sum(su_self);
+      se_self = G.sum(se_self);
+      G.sync();
+      const bool trans_ok = fmax(fmax(h0, h1), h2) > 1e-9;
+      if (lane < 8) {
+        const int ch = lane;
+        const long long slot = 8 * item + ch;
+        if (args.split_rot) {
+          const bool rot_ok = hr > 1e-9;
+          int8_t sr;
+          if (!rot_ok && !trans_ok) {
+            sr = -1;
+          } else {
+            sr = (rot_ok && (!trans_ok || s_r >= st_max)) ? 1 : 0;
+          }
+          args.split_rot[slot] = sr;
+        }
+        if (infeasible) {
+          args.lower[slot] = INFINITY;
+          args.upper[slot] = INFINITY;
+        } else {
+          const double lcr = acc[3 * ch], ucr = acc[3 * ch + 1], ecr = acc[3 * ch + 2];
+          const double mass = sl_self + 2.0 * lcr;
+          const double core = (sl_self - 2.0 * lcr) - ctx.lb_err_scale * (se_self + ecr) -
+                              ctx.lb_margin * mass;
+          const double lo = core < parent_lower ? parent_lower : core;
+          double up = INFINITY;
+          if (!(lo >= args.skip_upper_at) && have_center) up = su_self - 2.0 * ucr;
+          args.lower[slot] = lo;
+          args.upper[slot] = up;
+        }
+      }
+      G.sync();
+      continue;
     }
     // split decision (subdivide_adaptive, se3.cpp:107-121)
     st_max = G.max(st_max);
@@ -1146,9 +1252,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
 }  // namespace
 
 size_t eval_smem_per_warp(const DevCtx& ctx, int mode) {
-  const bool streamed = mode == kModeStream;
+  const bool streamed = mode == kModeStream || mode == kSiblingsStream;
   const int n1 = streamed ? ctx.max_n1 : ctx.n1_total, n2 = streamed ? ctx.max_n2 : ctx.n2_total;
-  const size_t f4 = static_cast<size_t>(kRowF4 * n1 + kColF4 * n2);
+  size_t f4 = static_cast<size_t>(kRowF4 * n1 + kColF4 * n2);
+  if (mode == kSiblingsStream) f4 += kSibStreamExtraF4;
   return f4 * sizeof(float4);
 }
 
@@ -1285,7 +1392,8 @@ cudaError_t launch_eval_cross_cached(const DevCtx& ctx, const EvalArgs& a, int s
 
 cudaError_t launch_eval_siblings(const DevCtx& ctx, const EvalArgs& a, int sm_count,
                                  cudaStream_t stream) {
-  return launch_mode<kSiblings>(ctx, a, sm_count, stream);
+  return ctx.stream_classes ? launch_mode<kSiblingsStream>(ctx, a, sm_count, stream)
+                            : launch_mode<kSiblings>(ctx, a, sm_count, stream);
 }
 
 
