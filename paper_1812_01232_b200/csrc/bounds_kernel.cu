@@ -673,8 +673,9 @@ enum {
   kModeStream = 4,
   kSiblingsStream = 5  // siblings mode of a multi-class context, one class's table at a time
 };
-// per-group extra shared memory of kSiblingsStream: the 8 children's R (72
-// doubles) and their {lb, ub, err} cross sums (24 doubles)
+// per-group extra shared memory of the siblings modes: the 8 children's R
+// (72 doubles, computed by 8 lanes at once) and (streamed) their {lb, ub,
+// err} cross sums (24 doubles)
 constexpr int kSibStreamExtraF4 = (72 + 24) * 8 / 16;
 
 // Rodrigues R0 = rotation_matrix(rc) (se3.cpp:21-31), FP64.
@@ -767,7 +768,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
   const int N1 = ctx.n1_total;  // every model mean (feasibility scans)
   const int TN1 = streamed ? ctx.max_n1 : N1, TN2 = streamed ? ctx.max_n2 : ctx.n2_total;
   const size_t table_f4 = static_cast<size_t>(kRowF4 * TN1 + kColF4 * TN2);
-  const size_t per_warp_f4 = table_f4 + (kMode == kSiblingsStream ? kSibStreamExtraF4 : 0);
+  const size_t per_warp_f4 = table_f4 + (kSib ? kSibStreamExtraF4 : 0);
   float4* base = smem4 + group * per_warp_f4;
   WarpTables T;
   T.row = base;
@@ -1094,6 +1095,13 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
       const double hr = 0.5 * rhw;
       const bool trans_ok = fmax(fmax(h0, h1), h2) > 1e-9;
       double sl_self = lb_self, su_self = ub_self, se_self = lb_err;
+      // the children's rotations, 8 lanes at once (each child exactly as the
+      // expand kernel builds it: k.rc[a] += h * s)
+      double* const Rcs = reinterpret_cast<double*>(base + table_f4);  // [8][9]
+      for (int ch = lane; ch < 8; ch += kG) {
+        const int sx = (ch & 4) ? 1 : -1, sy = (ch & 2) ? 1 : -1, sz = (ch & 1) ? 1 : -1;
+        rodrigues(rc0 + hr * sx, rc1 + hr * sy, rc2 + hr * sz, Rcs + 9 * ch);
+      }
       if (!infeasible) {
         G.sync();
         for (int c = 0; c < ctx.n_classes; ++c) {
@@ -1113,9 +1121,6 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
       }
       for (int ch = 0; ch < 8; ++ch) {
         const long long slot = 8 * item + ch;
-        const int sx = (ch & 4) ? 1 : -1, sy = (ch & 2) ? 1 : -1, sz = (ch & 1) ? 1 : -1;
-        // the child exactly as the expand kernel builds it (k.rc[a] += h * s)
-        const double crc0 = rc0 + hr * sx, crc1 = rc1 + hr * sy, crc2 = rc2 + hr * sz;
         const double cs_r = s_r;  // sin(psi_c / 2), shared by the children
         if (lane == 0 && args.split_rot) {
           const bool rot_ok = hr > 1e-9;
@@ -1134,10 +1139,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
           }
           continue;
         }
-        double Rc[9];
-        rodrigues(crc0, crc1, crc2, Rc);
         G.sync();
-        column_prep(T, ctx, lane, kG, Rc);
+        column_prep(T, ctx, lane, kG, Rcs + 9 * ch);
         G.sync();
         double lcr = 0.0, ucr = 0.0, ecr = 0.0, dl = 0.0, du = 0.0;
         for (int c = 0; c < ctx.n_classes; ++c) {
@@ -1255,7 +1258,7 @@ size_t eval_smem_per_warp(const DevCtx& ctx, int mode) {
   const bool streamed = mode == kModeStream || mode == kSiblingsStream;
   const int n1 = streamed ? ctx.max_n1 : ctx.n1_total, n2 = streamed ? ctx.max_n2 : ctx.n2_total;
   size_t f4 = static_cast<size_t>(kRowF4 * n1 + kColF4 * n2);
-  if (mode == kSiblingsStream) f4 += kSibStreamExtraF4;
+  if (mode == kSiblings || mode == kSiblingsStream) f4 += kSibStreamExtraF4;
   return f4 * sizeof(float4);
 }
 
