@@ -145,14 +145,18 @@ struct Group {
   int gbase;     // first lane of the group in its warp
   GroupScratch* sh;
   __device__ __forceinline__ void sync() const {
-    if constexpr (kG <= 32) {
+    if constexpr (kG == 1) {
+      // a one-lane group needs no synchronisation
+    } else if constexpr (kG <= 32) {
       __syncwarp(gm);
     } else {
       __syncthreads();
     }
   }
   __device__ __forceinline__ bool any(bool b) const {
-    if constexpr (kG <= 32) {
+    if constexpr (kG == 1) {
+      return b;
+    } else if constexpr (kG <= 32) {
       return __any_sync(gm, b);
     } else {
       return __syncthreads_or(b) != 0;
@@ -188,7 +192,9 @@ struct Group {
   }
   // value of group lane 0
   __device__ __forceinline__ long long bcast0(long long v) const {
-    if constexpr (kG <= 32) {
+    if constexpr (kG == 1) {
+      return v;
+    } else if constexpr (kG <= 32) {
       return __shfl_sync(gm, v, 0, kG);
     } else {
       __syncthreads();
@@ -199,7 +205,9 @@ struct Group {
   }
   // first group lane with b set (-1: none)
   __device__ __forceinline__ int first(bool b) const {
-    if constexpr (kG <= 32) {
+    if constexpr (kG == 1) {
+      return b ? 0 : -1;
+    } else if constexpr (kG <= 32) {
       const unsigned bal = __ballot_sync(gm, b) >> gbase;
       return bal ? __ffs(bal) - 1 : -1;
     } else {
@@ -794,14 +802,21 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
 
     // ---- node fetch (gosma_node: rc[3], rhw, tc[3], thw[3], lower)
     double v = 0.0, v2 = 0.0;
-    if (lane < 11) v = args.nodes[node * 11 + lane];
-    if (kG < 11 && lane < 11 - kG) v2 = args.nodes[node * 11 + kG + lane];
+    double nv[kG == 1 ? 11 : 1];  // one-lane groups: the lane reads its node itself
+    if constexpr (kG == 1) {
+      for (int k = 0; k < 11; ++k) nv[k] = args.nodes[node * 11 + k];
+    } else {
+      if (lane < 11) v = args.nodes[node * 11 + lane];
+      if (kG < 11 && lane < 11 - kG) v2 = args.nodes[node * 11 + kG + lane];
+    }
     if constexpr (kG > 32) {
       if (lane < 11) gscratch.node[lane] = v;
       __syncthreads();
     }
     auto fetch = [&](int k) -> double {
-      if constexpr (kG > 32) {
+      if constexpr (kG == 1) {
+        return nv[k];
+      } else if constexpr (kG > 32) {
         return gscratch.node[k];
       } else {
         if (kG < 11 && k >= kG) return __shfl_sync(gm, v2, k - kG, kG);
@@ -1057,8 +1072,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
       se_self = G.sum(se_self);
       G.sync();
       const bool trans_ok = fmax(fmax(h0, h1), h2) > 1e-9;
-      if (lane < 8) {
-        const int ch = lane;
+      for (int ch = lane; ch < 8; ch += kG) {
         const long long slot = 8 * item + ch;
         if (args.split_rot) {
           const bool rot_ok = hr > 1e-9;
@@ -1264,21 +1278,31 @@ size_t eval_smem_per_warp(const DevCtx& ctx, int mode) {
 
 namespace {
 
-// Lanes per node: 8 / 16 when every class has at most that many model rows
-// and the per-group tables stay small (GOSMA_GROUP=32 forces whole warps).
+// Lanes per node, from measured sweeps (scripts/kernel_timing.py, B200):
+//  1  tiny mixtures (5 n1 + 2 n2 <= 48 table float4, e.g. up to 6x6): one lane
+//     runs a whole node - 4.8x at 2x2, 2x at 4x4 over 8-lane groups;
+//  8  up to 24 rows per class (8x8 .. 24x20: 1.2-2x over 16 / 32 lanes);
+//  16 up to 32 rows; 32 beyond; a whole CTA (4 warps sharing one node's
+//     tables) for large mixtures whose tables would cap residency.
+// Each choice also keeps the CTA's tables within a shared-memory budget.
+// GOSMA_GROUP forces a size (A/B runs).
 int group_lanes(const DevCtx& ctx, int mode) {
   static const int forced = [] {
     const char* e = std::getenv("GOSMA_GROUP");
     return e ? std::atoi(e) : 0;
   }();
-  if (forced == 8 || forced == 16 || forced == 32) return forced;
+  if (forced == 1 || forced == 8 || forced == 16 || forced == 32) return forced;
   if (forced == 128) return kCtaGroup;
-  const size_t table = eval_smem_per_warp(ctx, mode);
-  for (int g : {8, 16}) {
-    if (ctx.max_n1 <= g && table * kWarpsPerCta * (32 / g) <= 64 * 1024) return g;
-  }
-  // large tables: one node per CTA (4 warps share the tables)
-  if (forced == kCtaGroup || (ctx.max_n1 >= 64 && table > 10 * 1024)) return kCtaGroup;
+  const size_t table = eval_smem_per_warp(ctx, mode);  // per group, incl. the siblings' extras
+  const size_t core =
+      table - ((mode == kSiblings || mode == kSiblingsStream) ? kSibStreamExtraF4 * 16 : 0);
+  const int groups_per_cta = kWarpsPerCta * 32;
+  const long long n1 = ctx.n1_total, n2 = ctx.n2_total;
+  const long long pairs_bound = n1 * (n1 - 1) / 2 + n1 * n2;  // exact for one class
+  if (core <= 48 * 16 && pairs_bound <= 64 && table * groups_per_cta <= 160 * 1024) return 1;
+  if (ctx.max_n1 <= 24 && table * kWarpsPerCta * 4 <= 64 * 1024) return 8;
+  if (ctx.max_n1 <= 32 && table * kWarpsPerCta * 2 <= 64 * 1024) return 16;
+  if (ctx.max_n1 >= 64 && table > 10 * 1024) return kCtaGroup;
   return 32;
 }
 
@@ -1298,6 +1322,8 @@ cudaError_t launch_group(const DevCtx& ctx, const EvalArgs& a, int sm_count,
   };
   static std::mutex mu;
   static std::vector<Choice> cache;
+  static int limit_on[64] = {};  // dynamic smem limit set on this kernel, per device
+  auto limit_of = [](int dev) -> int& { return limit_on[dev & 63]; };
   int device = 0;
   cudaGetDevice(&device);
   const size_t per_warp = eval_smem_per_warp(ctx, kMode);
@@ -1319,11 +1345,18 @@ cudaError_t launch_group(const DevCtx& ctx, const EvalArgs& a, int sm_count,
        !hit && warps >= (kG > 32 ? kWarpsPerCta : 1); warps /= 2) {
     const int groups = kG > 32 ? 1 : warps * (32 / kG);
     const size_t smem = per_warp * groups;
-    if (smem > 48 * 1024 &&
-        cudaFuncSetAttribute(eval_bounds_kernel<kMode, kG, kTail>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem)) != cudaSuccess)
-      continue;
+    if (smem > 48 * 1024) {
+      // the occupancy query needs the limit to cover smem; never lower it
+      std::lock_guard<std::mutex> lk(mu);
+      int& lim = limit_of(device);
+      if (static_cast<int>(smem) > lim) {
+        if (cudaFuncSetAttribute(eval_bounds_kernel<kMode, kG, kTail>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)) != cudaSuccess)
+          continue;
+        lim = static_cast<int>(smem);
+      }
+    }
     int per_sm = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(
             &per_sm, eval_bounds_kernel<kMode, kG, kTail>, warps * 32, smem) != cudaSuccess)
@@ -1336,14 +1369,21 @@ cudaError_t launch_group(const DevCtx& ctx, const EvalArgs& a, int sm_count,
     }
   }
   if (!hit && best_per_sm >= 1) {
-    // the attribute must cover the chosen size (the loop may have set a larger
-    // one last); set it once more for the choice
-    if (best_smem > 48 * 1024)
-      cudaFuncSetAttribute(eval_bounds_kernel<kMode, kG, kTail>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(best_smem));
     std::lock_guard<std::mutex> lk(mu);
     cache.push_back(Choice{device, per_warp, best_warps, best_per_sm, best_smem});
+  }
+  // the kernel's dynamic shared-memory limit on this device only ever grows
+  // (another context may have chosen a larger table): raise it when needed
+  if (best_smem > 48 * 1024) {
+    std::lock_guard<std::mutex> lk(mu);
+    int& lim = limit_of(device);
+    if (static_cast<int>(best_smem) > lim) {
+      const cudaError_t e = cudaFuncSetAttribute(eval_bounds_kernel<kMode, kG, kTail>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 static_cast<int>(best_smem));
+      if (e != cudaSuccess) return e;
+      lim = static_cast<int>(best_smem);
+    }
   }
   if (best_per_sm < 1) return cudaErrorInvalidConfiguration;
   const int groups_per_cta = kG > 32 ? 1 : best_warps * (32 / kG);
@@ -1365,6 +1405,8 @@ cudaError_t launch_mode(const DevCtx& ctx, const EvalArgs& a, int sm_count,
   switch (group_lanes(ctx, kMode)) {
     case kCtaGroup:
       return launch_group<kMode, kCtaGroup, false>(ctx, a, sm_count, stream);
+    case 1:
+      return launch_group<kMode, 1, false>(ctx, a, sm_count, stream);
     case 8:
       return launch_group<kMode, 8, false>(ctx, a, sm_count, stream);
     case 16:

@@ -6,7 +6,9 @@ import paper_1812_01232_b200 as g
 from paper_1812_01232_b200 import synth
 n = int(os.environ.get("NODES", "1000000"))
 W = [("realistic", 64, 32), ("moderate", 64, 32), ("realistic", 256, 128), ("realistic", 12, 12),
-     ("realistic", 41, 36), ("realistic", 45, 40), ("realistic", 8, 4, 8), ("realistic", 32, 16, 8)]
+     ("realistic", 41, 36), ("realistic", 45, 40), ("realistic", 8, 4, 8), ("realistic", 32, 16, 8),
+     ("realistic", 2, 2), ("realistic", 4, 4), ("realistic", 6, 6), ("realistic", 8, 8),
+     ("realistic", 16, 16), ("realistic", 24, 20), ("realistic", 32, 32)]
 only = os.environ.get("ONLY")
 for regime, n1, n2, *rest in ([W[int(k)] for k in only.split(",")] if only else W):
     nc = rest[0] if rest else 1  # semantic classes (block-sparse pair terms, BASELINE configs[3])
