@@ -57,8 +57,9 @@ struct DiveDev {
   DiveBest* best;
   unsigned long long* key;
   unsigned long long* idx;
-  unsigned* cnt;
-  unsigned* off;
+  unsigned* cnt;   // beam entries per sector (this beam)
+  unsigned* off;   // their offsets
+  unsigned* ncnt;  // entries per sector of the next beam
   unsigned* sel;
   int R, quota;
   unsigned cap_beam, cap_kids;
@@ -147,27 +148,31 @@ __global__ void __launch_bounds__(1024) offer_commit_select(DiveDev d, int to) {
   for (int s = warp; s < d.R; s += nw) {
     unsigned c = 0;
     if (n > 0) {
-      // [a, b): children of sector s (binary searches over ksec, sorted)
-      long long lo_i = 0, hi_i = n;
-      while (lo_i < hi_i) {
-        const long long m = (lo_i + hi_i) >> 1;
-        if (d.ksec[m] < static_cast<unsigned>(s)) lo_i = m + 1; else hi_i = m;
+      // [a, b): children of sector s - 8 per beam entry of the sector, whose
+      // offset and count the previous selection left in off / cnt
+      const long long a = 8ll * d.off[s];
+      const long long b = a + 8ll * d.cnt[s];
+      // this lane's candidates (a sector has at most quota * 8 <= 128
+      // children: <= 4 per lane), read once
+      constexpr int kPer = 4;
+      double cl[kPer];
+      long long ci[kPer];
+      for (int k = 0; k < kPer; ++k) {
+        const long long i = a + lane + 32ll * k;
+        const bool ok = i < b && splittable_d(d.kids[i], v.floor);
+        cl[k] = ok ? d.lo[i] : INFINITY;
+        ci[k] = ok ? i : -1;
       }
-      const long long a = lo_i;
-      hi_i = n;
-      while (lo_i < hi_i) {
-        const long long m = (lo_i + hi_i) >> 1;
-        if (d.ksec[m] <= static_cast<unsigned>(s)) lo_i = m + 1; else hi_i = m;
-      }
-      const long long b = lo_i;
       double pl = -INFINITY;
       long long pi = -1;
       for (; c < static_cast<unsigned>(d.quota); ++c) {
         double bl = INFINITY;
         long long bi = -1;
-        for (long long i = a + lane; i < b; i += 32) {
-          if (!splittable_d(d.kids[i], v.floor)) continue;
-          const double l = d.lo[i];
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+          const long long i = ci[k];
+          if (i < 0) continue;
+          const double l = cl[k];
           const bool after = l > pl || (l == pl && i > pi);
           const bool better = bi < 0 || l < bl || (l == bl && i < bi);
           if (after && better) {
@@ -190,14 +195,15 @@ __global__ void __launch_bounds__(1024) offer_commit_select(DiveDev d, int to) {
         pi = bi;
       }
     }
-    if (lane == 0) d.cnt[s] = c;
+    if (lane == 0) d.ncnt[s] = c;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
     unsigned total = 0;
     for (int s = 0; s < d.R; ++s) {
       d.off[s] = total;
-      total += d.cnt[s];
+      d.cnt[s] = d.ncnt[s];
+      total += d.ncnt[s];
     }
     v.count[to] = total;
     v.used += static_cast<unsigned long long>(n);
@@ -245,6 +251,7 @@ size_t carve(char* p, int R, int quota, DiveDev* d) {
   d->idx = reinterpret_cast<unsigned long long*>(take(R * 8));
   d->cnt = reinterpret_cast<unsigned*>(take(R * 4));
   d->off = reinterpret_cast<unsigned*>(take(R * 4));
+  d->ncnt = reinterpret_cast<unsigned*>(take(R * 4));
   d->sel = reinterpret_cast<unsigned*>(take(cb * 4));
   d->R = R;
   d->quota = quota;
@@ -300,6 +307,7 @@ int dive_beam_device(gosma_ctx* ctx, const std::vector<DiveEntry>& beam,
   }
   carve(static_cast<char*>(ctx->dive_buf), R, quota, &d);
   if (beam.size() > d.cap_beam) return set_error(GOSMA_EINVAL, "dive beam larger than its quota");
+  if (quota > 16) return set_error(GOSMA_EINVAL, "dive quota above 16 (4 candidates per lane)");
   // state: vars, beam A, sector candidates, empty argmin slots
   DiveVars v{};
   v.used = used0;
@@ -317,6 +325,14 @@ int dive_beam_device(gosma_ctx* ctx, const std::vector<DiveEntry>& beam,
       (e = cudaMemcpyAsync(d.key, none.data(), R * 8, cudaMemcpyHostToDevice, s)) !=
           cudaSuccess ||
       (e = cudaMemcpyAsync(d.idx, none.data(), R * 8, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+    return cuda_error(e, "dive upload");
+  // the initial beam's per-sector counts and offsets (it is in sector order)
+  std::vector<unsigned> cnt(R, 0), off(R, 0);
+  for (const DiveEntry& en : beam) ++cnt[en.sector];
+  for (int k = 1; k < R; ++k) off[k] = off[k - 1] + cnt[k - 1];
+  if ((e = cudaMemcpyAsync(d.cnt, cnt.data(), R * 4, cudaMemcpyHostToDevice, s)) != cudaSuccess ||
+      (e = cudaMemcpyAsync(d.off, off.data(), R * 4, cudaMemcpyHostToDevice, s)) != cudaSuccess ||
+      (e = cudaStreamSynchronize(s)) != cudaSuccess)  // cnt / off are host locals
     return cuda_error(e, "dive upload");
   const bool prof = std::getenv("GOSMA_PROFILE") != nullptr;
   const auto t0 = std::chrono::steady_clock::now();
