@@ -103,7 +103,7 @@ bool gpu_sma(const HostModel& m) {
     return std::string(e) == "gpu" ? 1 : (std::string(e) == "host" ? 0 : -1);
   }();
   if (forced >= 0) return forced == 1;
-  return model_pairs(m) >= 1000;  // measured: GPU ladder 0.31 s vs host 0.69 s at 41x36
+  return model_pairs(m) >= 500;  // measured dive ladders: 20x16 GPU 0.15 s vs host 0.17 s, 12x12 0.70 vs 0.09
 }
 
 // Runs refinement jobs on the GPU (refine_kernel: one CTA per start runs the
