@@ -272,6 +272,15 @@ def test_config2_batch_properties(gosma):
     assert np.all(np.isfinite(up[f]))
     assert np.all(lo[f] <= up[f] + 1e-6 * np.abs(up[f]) + 1e-9)
     assert set(np.unique(sp)).issubset({-1, 0, 1})
+    # deterministic: a second launch (another work-counter interleaving of the
+    # persistent groups) gives bitwise the same bounds
+    with torch.cuda.stream(s):
+        gosma.evaluate_branch_batch_device(ctx, d_nodes.data_ptr(), n, d_lo.data_ptr(),
+                                           d_up.data_ptr(), d_sp.data_ptr(), float("inf"),
+                                           s.cuda_stream)
+    s.synchronize()
+    assert np.array_equal(d_lo.cpu().numpy(), lo) and np.array_equal(d_up.cpu().numpy(), up)
+    assert np.array_equal(d_sp.cpu().numpy(), sp)
     # sampled parity against the oracle
     rng = np.random.default_rng(0)
     idx = rng.choice(n, 600, replace=False)
