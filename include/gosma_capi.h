@@ -99,8 +99,11 @@ int gosma_ctx_set_lb_margin(gosma_ctx* ctx, double rel_margin);
  * d_upper / d_child_split. Rotation-split parents evaluate their cuboid's
  * prologue and self sums once for all 8 children. Children inherit the
  * parent's lower field as their floor. Device pointers, asynchronous on
- * `stream`; results equal gosma_eval_bounds_device on the explicit children
- * to 1e-12 of the |term| mass. */
+ * `stream` (no host synchronisation: the rotation / translation split counts
+ * stay on the device); the context's child scratch is reused, so calls on one
+ * context must be ordered (one stream per context). Results equal
+ * gosma_eval_bounds_device on the explicit children to 1e-12 of the |term|
+ * mass. */
 int gosma_eval_children_device(gosma_ctx* ctx, const gosma_node* d_parents, const int8_t* d_split,
                                size_t n, double skip_upper_at, double* d_lower, double* d_upper,
                                int8_t* d_child_split, void* stream);

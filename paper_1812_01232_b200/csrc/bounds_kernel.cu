@@ -1465,7 +1465,8 @@ namespace {
 // split flags (1 rotation, 0 translation, -1 none: children = copies), and the
 // work lists of the siblings / full kernels (order irrelevant).
 __global__ void children_of(const gosma_node* parents, const int8_t* split, size_t n,
-                            gosma_node* kids, int* rot, int* trans_kids, int* counts) {
+                            gosma_node* kids, int* rot, int* trans_kids,
+                            unsigned long long* counts) {
   const size_t t = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
   if (t >= 8 * n) return;
   const size_t p = t / 8;
@@ -1478,7 +1479,7 @@ __global__ void children_of(const gosma_node* parents, const int8_t* split, size
     k.rc[1] += h * sy;
     k.rc[2] += h * sz;
     k.rhw = h;
-    if (c == 0) rot[atomicAdd(&counts[0], 1)] = static_cast<int>(p);
+    if (c == 0) rot[atomicAdd(&counts[0], 1ull)] = static_cast<int>(p);
   } else {
     if (split[p] == 0) {
       const double h0 = 0.5 * k.thw[0], h1 = 0.5 * k.thw[1], h2 = 0.5 * k.thw[2];
@@ -1489,7 +1490,7 @@ __global__ void children_of(const gosma_node* parents, const int8_t* split, size
       k.thw[1] = h1;
       k.thw[2] = h2;
     }
-    trans_kids[atomicAdd(&counts[1], 1)] = static_cast<int>(t);
+    trans_kids[atomicAdd(&counts[1], 1ull)] = static_cast<int>(t);
   }
   kids[t] = k;
 }
@@ -1501,10 +1502,11 @@ __global__ void identity_sel(unsigned int* sel, size_t n) {
 }  // namespace
 
 cudaError_t make_children(const gosma_node* d_parents, const int8_t* d_split, size_t n,
-                          gosma_node* d_kids, int* d_rot, int* d_trans, int* d_counts,
-                          unsigned int* d_sel, cudaStream_t stream) {
+                          gosma_node* d_kids, int* d_rot, int* d_trans,
+                          unsigned long long* d_counts, unsigned int* d_sel,
+                          cudaStream_t stream) {
   if (n == 0) return cudaSuccess;
-  cudaError_t e = cudaMemsetAsync(d_counts, 0, 2 * sizeof(int), stream);
+  cudaError_t e = cudaMemsetAsync(d_counts, 0, 2 * sizeof(unsigned long long), stream);
   if (e != cudaSuccess) return e;
   children_of<<<static_cast<unsigned>((8 * n + 255) / 256), 256, 0, stream>>>(
       d_parents, d_split, n, d_kids, d_rot, d_trans, d_counts);

@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdint>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -411,44 +412,41 @@ int gosma_eval_children_device(gosma_ctx* ctx, const gosma_node* d_parents, cons
     ctx->d_child_lists = nullptr;
     ctx->d_child_sel = nullptr;
     if ((e = cudaMalloc(&ctx->d_child_kids, 8 * n * sizeof(gosma_node))) != cudaSuccess ||
-        (e = cudaMalloc(&ctx->d_child_lists, (9 * n + 2) * sizeof(int))) != cudaSuccess ||
+        (e = cudaMalloc(&ctx->d_child_lists, 9 * n * sizeof(int) + 32)) != cudaSuccess ||
         (e = cudaMalloc(&ctx->d_child_sel, n * sizeof(unsigned int))) != cudaSuccess)
       return cuda_error(e, "children alloc");
     ctx->child_cap = n;
   }
   int* rot = ctx->d_child_lists;
   int* trans = rot + n;
-  int* counts = trans + 8 * n;
+  // the two counts (8-byte aligned after the lists) stay on the device: the
+  // kernels read them (grids sized for the upper bounds), no host round trip
+  auto* counts = reinterpret_cast<unsigned long long*>(
+      (reinterpret_cast<uintptr_t>(trans + 8 * n) + 7) & ~uintptr_t(7));
   if ((e = make_children(d_parents, d_split, n, ctx->d_child_kids, rot, trans, counts,
                          ctx->d_child_sel, s)) != cudaSuccess)
     return cuda_error(e, "children");
-  int h[2] = {0, 0};
-  if ((e = cudaMemcpyAsync(h, counts, sizeof(h), cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
-      (e = cudaStreamSynchronize(s)) != cudaSuccess)
-    return cuda_error(e, "children counts");
   EvalArgs a;
   a.skip_upper_at = skip;
   a.lower = d_lower;
   a.upper = d_upper;
   a.split_rot = d_child_split;
   a.work = static_cast<unsigned int*>(ctx->d_work);
-  if (h[0]) {
-    EvalArgs b = a;
-    b.nodes = reinterpret_cast<const double*>(d_parents);
-    b.n = h[0];
-    b.item_index = rot;
-    b.sel = ctx->d_child_sel;
-    if ((e = launch_eval_siblings(ctx->dev, b, ctx->sm_count, s)) != cudaSuccess)
-      return cuda_error(e, "siblings kernel");
-  }
-  if (h[1]) {
-    EvalArgs c = a;
-    c.nodes = reinterpret_cast<const double*>(ctx->d_child_kids);
-    c.n = h[1];
-    c.item_index = trans;
-    if ((e = launch_eval_bounds(ctx->dev, c, ctx->sm_count, s)) != cudaSuccess)
-      return cuda_error(e, "children kernel");
-  }
+  EvalArgs b = a;
+  b.nodes = reinterpret_cast<const double*>(d_parents);
+  b.n = static_cast<long long>(n);
+  b.n_dev = reinterpret_cast<const long long*>(counts);
+  b.item_index = rot;
+  b.sel = ctx->d_child_sel;
+  if ((e = launch_eval_siblings(ctx->dev, b, ctx->sm_count, s)) != cudaSuccess)
+    return cuda_error(e, "siblings kernel");
+  EvalArgs c = a;
+  c.nodes = reinterpret_cast<const double*>(ctx->d_child_kids);
+  c.n = static_cast<long long>(8 * n);
+  c.n_dev = reinterpret_cast<const long long*>(counts + 1);
+  c.item_index = trans;
+  if ((e = launch_eval_bounds(ctx->dev, c, ctx->sm_count, s)) != cudaSuccess)
+    return cuda_error(e, "children kernel");
   return GOSMA_OK;
 }
 

@@ -354,13 +354,13 @@ __global__ void expand(const gosma_node* front, const int8_t* split, const doubl
 // children of translation-split parents (full kernel). Order is irrelevant:
 // every item writes its own output slots.
 __global__ void split_lists(const int8_t* split, const unsigned int* sel, size_t n_sel,
-                            int* rot, int* trans_kids, int* counts) {
+                            int* rot, int* trans_kids, unsigned long long* counts) {
   const size_t k = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
   if (k >= n_sel) return;
   if (split[sel[k]] == 1) {
-    rot[atomicAdd(&counts[0], 1)] = static_cast<int>(k);
+    rot[atomicAdd(&counts[0], 1ull)] = static_cast<int>(k);
   } else {
-    const int b = atomicAdd(&counts[1], 8);
+    const int b = static_cast<int>(atomicAdd(&counts[1], 8ull));
     for (int c = 0; c < 8; ++c) trans_kids[b + c] = static_cast<int>(8 * k + c);
   }
 }
@@ -653,7 +653,7 @@ cudaError_t Frontier::reserve(size_t cap_nodes, size_t wave) {
     if ((e = dmalloc(&stats, sizeof(RouteStats))) != cudaSuccess) return e;
     if ((e = dmalloc(&counter, 2 * sizeof(unsigned long long))) != cudaSuccess) return e;
     if ((e = dmalloc(&hist, kBins * sizeof(unsigned int))) != cudaSuccess) return e;
-    if ((e = dmalloc(&list_counts, 2 * sizeof(int))) != cudaSuccess) return e;
+    if ((e = dmalloc(&list_counts, 2 * sizeof(unsigned long long))) != cudaSuccess) return e;
     if ((e = hmalloc(&h_stats, sizeof(RouteStats))) != cudaSuccess) return e;
     if ((e = hmalloc(&h_counter, 2 * sizeof(unsigned long long))) != cudaSuccess) return e;
     h_hist.resize(kBins);
@@ -724,7 +724,8 @@ void Frontier::release() {
   dfree(rot_list);
   dfree(trans_list);
   dfree(list_counts);
-  rot_list = trans_list = list_counts = nullptr;
+  rot_list = trans_list = nullptr;
+  list_counts = nullptr;
   bsel_cap = 0;
   dfree(cidx);
   cidx = nullptr;
@@ -1101,20 +1102,12 @@ cudaError_t Frontier::upload_device(const gosma_node* d_nodes, const int8_t* d_s
   return cudaSuccess;
 }
 
-cudaError_t Frontier::wave_lists(size_t n_sel, cudaStream_t s, size_t* n_rot, size_t* n_trans) {
-  *n_rot = *n_trans = 0;
+cudaError_t Frontier::wave_lists(size_t n_sel, cudaStream_t s) {
   if (n_sel == 0) return cudaSuccess;
-  cudaError_t e = cudaMemsetAsync(list_counts, 0, 2 * sizeof(int), s);
+  cudaError_t e = cudaMemsetAsync(list_counts, 0, 2 * sizeof(unsigned long long), s);
   if (e != cudaSuccess) return e;
   split_lists<<<grid_for(n_sel, 256), 256, 0, s>>>(split, sel, n_sel, rot_list, trans_list,
                                                     list_counts);
-  if ((e = cudaMemcpyAsync(h_counter, list_counts, 2 * sizeof(int), cudaMemcpyDeviceToHost, s)) !=
-      cudaSuccess)
-    return e;
-  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
-  const int* c = reinterpret_cast<const int*>(h_counter);
-  *n_rot = static_cast<size_t>(c[0]);
-  *n_trans = static_cast<size_t>(c[1]);
   return cudaGetLastError();
 }
 

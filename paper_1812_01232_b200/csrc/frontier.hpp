@@ -83,7 +83,7 @@ struct Frontier {
   double* tself = nullptr;       // 4 doubles per cuboid: self LB, self UB, err, flag
   int* rot_list = nullptr;       // selection indices with a rotation split
   int* trans_list = nullptr;     // children 8k+c of translation-split selections
-  int* list_counts = nullptr;
+  unsigned long long* list_counts = nullptr;  // {rotation parents, translation children}
   // reductions / scratch
   RouteStats* stats = nullptr;
   unsigned long long* counter = nullptr;
@@ -112,7 +112,9 @@ struct Frontier {
   cudaError_t expand_selected(size_t n_sel, cudaStream_t s);
   cudaError_t expand_selected_cached(size_t n_sel, cudaStream_t s, size_t* n_cuboids);
   // rotation-split selections (rot_list) and translation-split children (trans_list)
-  cudaError_t wave_lists(size_t n_sel, cudaStream_t s, size_t* n_rot, size_t* n_trans);
+  // rotation-split selections / translation-split children lists; their
+  // counts stay on the device (list_counts, read by the bound kernels)
+  cudaError_t wave_lists(size_t n_sel, cudaStream_t s);
   // the selected records (sel[0..n)) into contiguous device buffers
   cudaError_t gather_selected(size_t n, cudaStream_t s, gosma_node* out_nodes, int8_t* out_split,
                               double* out_vol);

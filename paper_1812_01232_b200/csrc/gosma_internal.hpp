@@ -100,8 +100,9 @@ cudaError_t launch_eval_cross_cached(const DevCtx& ctx, const EvalArgs& a, int s
 // class-streamed full mode of a multi-class context (mode 4).
 size_t eval_smem_per_warp(const DevCtx& ctx, int mode = -1);
 cudaError_t make_children(const gosma_node* d_parents, const int8_t* d_split, size_t n,
-                          gosma_node* d_kids, int* d_rot, int* d_trans, int* d_counts,
-                          unsigned int* d_sel, cudaStream_t stream);
+                          gosma_node* d_kids, int* d_rot, int* d_trans,
+                          unsigned long long* d_counts, unsigned int* d_sel,
+                          cudaStream_t stream);
 cudaError_t boxes_as_nodes(const double* d_boxes, size_t n, gosma_node* d_out,
                            cudaStream_t stream);
 unsigned long long bound_kernel_launch_count();

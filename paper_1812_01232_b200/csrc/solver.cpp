@@ -808,23 +808,26 @@ int gosma_solver_expand(gosma_solver* S, double limit, unsigned long long max_ev
   a.upper = S->F.kid_upper;
   a.split_rot = S->F.kid_split;
   if (S->wave_mode == 2) {
-    size_t n_rot = 0, n_trans = 0;
-    if ((e = S->F.wave_lists(n_sel, s, &n_rot, &n_trans)) != cudaSuccess)
-      return cuda_error(e, "wave lists");
+    // the split of the selection into rotation parents / translation children
+    // stays on the device: the kernels read their item counts there (grids
+    // sized for the upper bounds), no host round trip
+    if ((e = S->F.wave_lists(n_sel, s)) != cudaSuccess) return cuda_error(e, "wave lists");
     S->lap(2, s);
     EvalArgs b = a;
     b.nodes = reinterpret_cast<const double*>(S->F.nodes);  // the parents, in the pool
-    b.n = static_cast<long long>(n_rot);
+    b.n = static_cast<long long>(n_sel);
+    b.n_dev = reinterpret_cast<const long long*>(S->F.list_counts);
     b.item_index = S->F.rot_list;
     b.sel = S->F.sel;
-    if (n_rot && (e = launch_eval_siblings(ctx->dev, b, ctx->sm_count, s)) != cudaSuccess)
+    if ((e = launch_eval_siblings(ctx->dev, b, ctx->sm_count, s)) != cudaSuccess)
       return cuda_error(e, "eval siblings");
     EvalArgs c = a;
-    c.n = static_cast<long long>(n_trans);
+    c.n = static_cast<long long>(n_kids);
+    c.n_dev = reinterpret_cast<const long long*>(S->F.list_counts + 1);
     c.item_index = S->F.trans_list;
-    if (n_trans && (e = launch_eval_bounds(ctx->dev, c, ctx->sm_count, s)) != cudaSuccess)
+    if ((e = launch_eval_bounds(ctx->dev, c, ctx->sm_count, s)) != cudaSuccess)
       return cuda_error(e, "eval children");
-    S->cuboid_evals += n_rot + n_trans;
+    S->cuboid_evals += n_sel;
   } else if ((e = (S->cached ? launch_eval_cross_cached(ctx->dev, a, ctx->sm_count, s)
                              : launch_eval_bounds(ctx->dev, a, ctx->sm_count, s))) !=
              cudaSuccess) {
