@@ -589,7 +589,7 @@ int solver_init(gosma_solver* S) {
       cfg.wave_nodes > 0
           ? static_cast<size_t>(cfg.wave_nodes)
           : std::min<size_t>(std::max<size_t>(300000000 / std::max<size_t>(pairs, 1), 1024),
-                             1u << 19);
+                             1u << 21);
   cudaError_t e = S->F.reserve(std::max<size_t>(size_t(1) << 20, roots.size() * 2 + 16),
                                S->wave_nodes);
   if (e != cudaSuccess) return cuda_error(e, "frontier reserve");
