@@ -49,6 +49,9 @@ def parse():
     p.add_argument("--solve-seconds", type=float, default=10.0,
                    help="reference CPU solve budget for the time-to-certified-gap line "
                         "(0 disables)")
+    p.add_argument("--scene-seconds", type=float, default=20.0,
+                   help="reference CPU solve budget for the configs[2]-style scene "
+                        "time-to-gap line (0 disables)")
     p.add_argument("--cpu-seconds", type=float, default=12.0,
                    help="target CPU work for the cpu_baseline sample")
     return p.parse_args()
@@ -296,6 +299,56 @@ def solve_vs_reference(g, ref_seconds):
     return out
 
 
+def scene_vs_reference(g, ref_seconds):
+    """Time-to-certified-gap on a BASELINE configs[2]-style scene: the
+    generate_scene instance seed 1 (N_I = 30, omega = 0.5 outliers/occlusion,
+    2 px noise; test_bench.cpp:241-250 recipe, tests/golden/solver_golden.json
+    "scenes"), full rotation ball, the 44-box torus_cover(3.5, 0.5) prior,
+    epsilon 0.1, zeta 0.5. The reference solve() runs `ref_seconds` on all host
+    cores; the GPU solver is timed to the reference's final certified gap."""
+    from oracle.bind import Mixture, Reference, reference_available
+    G = json.load(open(os.path.join(ROOT, "tests", "golden", "solver_golden.json")))
+    sc = next(s for s in G["scenes"] if s["seed"] == 1)
+    mix = Mixture.from_dict(sc["mixture"])
+    boxes = np.array(G["torus_cover_3.5_0.5"])
+    out = {"instance": f"generate_scene seed 1 (N_I=30, omega=0.5, 2 px): {mix.n1[0]} GMM x "
+                       f"{mix.n2[0]} vMF, rotation ball pi, torus_cover(3.5,0.5) "
+                       f"{boxes.shape[0]} boxes, epsilon 0.1"}
+    if not reference_available():
+        out["reference"] = "unavailable (oracle/_ref not built)"
+        return out
+    cores = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    rep = Reference(mix, single_ctor=True).solve(np.zeros(3), math.pi, boxes, 0.1, mix.zeta,
+                                                 batch_size=1024, time_limit=ref_seconds,
+                                                 threads=cores)
+    ref_s = time.perf_counter() - t0
+    ref_ok = int(rep["status"]) == 0
+    gap = float(rep["best_value"] - rep["global_lower"])
+    ctx = g.ObjectiveContext([{"mu": mix.mu, "sigma2": mix.sigma2, "phi1": mix.phi1,
+                               "dir": mix.dir, "kappa2": mix.kappa2, "phi2": mix.phi2}],
+                             mix.zeta, single_mixture=True)
+    dom = g.PoseDomain(np.zeros(3), math.pi, boxes)
+    cfg = g.SolverConfig(epsilon=max(gap, 0.1), zeta=mix.zeta,
+                         time_limit=max(60.0, 2 * ref_seconds))
+    g.solve(ctx, dom, cfg)  # warm-up (module loading, pool mapping)
+    t0 = time.perf_counter()
+    r = g.solve(ctx, dom, cfg)
+    ours_s = time.perf_counter() - t0
+    out.update({
+        "target_gap": max(gap, 0.1),
+        "reference": {"seconds": ref_s, "cores": cores, "certified": ref_ok,
+                      "best_value": float(rep["best_value"]),
+                      "global_lower": float(rep["global_lower"]),
+                      "bound_evaluations": int(rep["bound_evaluations"]),
+                      "kind": "oracle/_ref (unmodified reference solve(), threads = cores)"},
+        "gosma": {"seconds": ours_s, "status": r.status, "best_value": r.best_value,
+                  "global_lower": r.global_lower, "bound_evaluations": r.bound_evaluations},
+        "speedup_time_to_gap": ref_s / ours_s if r.gap <= max(gap, 0.1) + 1e-12 else None,
+    })
+    return out
+
+
 def certified_vs_reference(g):
     """Time-to-certified-optimum (status epsilon_optimal) of both solvers on
     the hardest instance of tests/golden/certify_golden.json that the
@@ -493,6 +546,8 @@ def main():
     if a.solve_seconds > 0 and world == 1:
         line["solve"] = solve_vs_reference(g, a.solve_seconds)
         line["solve_certified"] = certified_vs_reference(g)
+    if a.scene_seconds > 0 and world == 1:
+        line["solve_scene"] = scene_vs_reference(g, a.scene_seconds)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
