@@ -37,13 +37,15 @@ constexpr double kMarginObj = 64.0;  // objective.cpp:17
 __device__ __forceinline__ double log_z_d(double k) {
   // sphere_stats.cpp:47-56
   if (k < 1e-4) return 0.69314718055994531 + log1p(k * k / 6.0);
+  // above 19, exp(-2k) < 2^-54: k + log1p(-exp(-2k)) rounds to k (bit-identical)
+  if (k > 19.0) return k - log(k);
   return k + log1p(-exp(-2.0 * k)) - log(k);
 }
 
 __device__ __forceinline__ double log_z_deriv_d(double k) {
   // sphere_stats.cpp:58-69
   if (k < 1e-4) return k / 3.0 - k * k * k / 45.0;
-  if (k > 350.0) return 1.0 - 1.0 / k;
+  if (k > 19.0) return 1.0 - 1.0 / k;  // (1 + e2) / (1 - e2) == 1 exactly above 19
   const double e2 = exp(-2.0 * k);
   return (1.0 + e2) / (1.0 - e2) - 1.0 / k;
 }
@@ -58,7 +60,9 @@ __device__ __forceinline__ void pair_terms(double K, double c, double& ez, doubl
     return;
   }
   const double iK = 1.0 / K;
-  const double om = K < 0.5 ? -expm1(-2.0 * K) : 1.0 - exp(-2.0 * K);  // 1 - e2
+  // 1 - e2; above K = 19, e2 = exp(-2K) < 2^-54 and 1 - e2 rounds to 1.0 in
+  // FP64, so the exp is skipped with bit-identical results (realistic K ~ 1e2-1e5)
+  const double om = K < 0.5 ? -expm1(-2.0 * K) : (K > 19.0 ? 1.0 : 1.0 - exp(-2.0 * K));
   ez = exp(K - c) * om * iK;
   zl = K > 350.0 ? 1.0 - iK : (2.0 - om) / om - iK;
 }
@@ -157,21 +161,26 @@ __device__
       for (int c = 0; c < 3; ++c)
         K2[3 * a + c] = K[3 * a] * K[c] + K[3 * a + 1] * K[3 + c] + K[3 * a + 2] * K[6 + c];
     double ra, rc, ja, jb;
+    // sin / cos of theta once for both R and Jl (same values as separate calls)
+    double th = 0.0, sth = 0.0, cth = 1.0;
+    if (th2 >= 1e-16) {
+      th = sqrt(th2);
+      sth = sin(th);
+      cth = cos(th);
+    }
     if (th2 < 1e-16) {
       ra = 1.0;
       rc = 0.5;
     } else {
-      const double th = sqrt(th2);
-      ra = sin(th) / th;
-      rc = (1.0 - cos(th)) / th2;
+      ra = sth / th;
+      rc = (1.0 - cth) / th2;
     }
     if (th2 < 1e-12) {
       ja = 0.5;
       jb = 1.0 / 6.0;
     } else {
-      const double th = sqrt(th2);
-      ja = (1.0 - cos(th)) / th2;
-      jb = (th - sin(th)) / (th2 * th);
+      ja = (1.0 - cth) / th2;
+      jb = (th - sth) / (th2 * th);
     }
     for (int e = 0; e < 9; ++e) {
       const double id = (e % 4 == 0) ? 1.0 : 0.0;
