@@ -506,10 +506,23 @@ __device__ LineSearchD wolfe_d(CtaObjective& ob, const double* x, const double* 
 }
 
 // local_refine (solver.cpp:164-258): best value and pose (r, t) from x0.
+// L-BFGS memory (solver.cpp:197-199)
+constexpr int kLbfgsMem = 10;
+struct LbfgsHistory {
+  double S[kLbfgsMem][6], Y[kLbfgsMem][6], Rho[kLbfgsMem];
+};
+
+// H: the CTA's one copy of the L-BFGS history in shared memory. Every thread
+// computes the same pairs; thread 0 stores them and all threads read them
+// back (broadcast loads) - per-thread copies would be 1 KB of local memory per
+// thread (0.5 MB per CTA, spilled through L2 on every two-loop recursion).
 __device__ void local_refine_d(const DevModel64& m, const RefineDomain& dom, RowD* rows,
-                               double* red, double* xch, double* tot, double* xio, double* fout,
-                               long long* count) {
-  constexpr int kMaxIt = 200, kMem = 10;
+                               double* red, double* xch, double* tot, LbfgsHistory& H,
+                               double* xio, double* fout, long long* count) {
+  constexpr int kMaxIt = 200, kMem = kLbfgsMem;
+  double (&S)[kMem][6] = H.S;
+  double (&Y)[kMem][6] = H.Y;
+  double (&Rho)[kMem] = H.Rho;
   const double kGradTol = 1e-6;
   CtaObjective ob{&m, rows, red, xch, tot, count};
   double x[6], bx[6];
@@ -536,7 +549,6 @@ __device__ void local_refine_d(const DevModel64& m, const RefineDomain& dom, Row
   ob.eval(x);
   double g[6];
   for (int k = 0; k < 6; ++k) g[k] = ob.g[k];
-  double S[kMem][6], Y[kMem][6], Rho[kMem];
   int nh = 0, h0 = 0;  // ring of the last nh pairs, oldest at h0
   for (int it = 0; it < kMaxIt; ++it) {
     if (sqrt(dot6(g, g)) < kGradTol) break;
@@ -587,11 +599,15 @@ __device__ void local_refine_d(const DevModel64& m, const RefineDomain& dom, Row
         slot = h0;
         h0 = (h0 + 1) % kMem;
       }
-      for (int k = 0; k < 6; ++k) {
-        S[slot][k] = s[k];
-        Y[slot][k] = y[k];
+      __syncthreads();  // every thread is past its reads of the history
+      if (threadIdx.x == 0) {
+        for (int k = 0; k < 6; ++k) {
+          S[slot][k] = s[k];
+          Y[slot][k] = y[k];
+        }
+        Rho[slot] = 1.0 / sy;
       }
-      Rho[slot] = 1.0 / sy;
+      __syncthreads();
     }
     for (int k = 0; k < 6; ++k) {
       x[k] = xn[k];
@@ -629,6 +645,7 @@ __global__ void __launch_bounds__(kRefineThreads)
                   RefineOut* out, int max_n1) {
   extern __shared__ double smem_d[];
   __shared__ double xch[8], tot[8];
+  __shared__ LbfgsHistory hist;
   RowD* rows = reinterpret_cast<RowD*>(smem_d);
   double* red = smem_d + static_cast<size_t>(max_n1) * (sizeof(RowD) / sizeof(double));
   namespace cg = cooperative_groups;
@@ -639,7 +656,7 @@ __global__ void __launch_bounds__(kRefineThreads)
   double f = INFINITY;
   long long count = 0;
   for (int st = 0; st < jb.stages; ++st)
-    local_refine_d(models[jb.model[st]], dom, rows, red, xch, tot, x, &f, &count);
+    local_refine_d(models[jb.model[st]], dom, rows, red, xch, tot, hist, x, &f, &count);
   if (threadIdx.x == 0 && cl.block_rank() == 0) {
     RefineOut o;
     o.value = f;
