@@ -151,9 +151,14 @@ __device__
     for (int k = 1; k < 7; ++k) o[k] = 0.0;
     return;
   }
-  // Rodrigues R (se3.cpp:21-31) and the left Jacobian (objective.cpp:240-250)
-  double R[9], Jl[9];
-  {
+  // Rodrigues R (se3.cpp:21-31) and the left Jacobian (objective.cpp:240-250),
+  // computed by the CTA's last warp only (FP64 sin / cos / divisions would
+  // otherwise occupy the FP64 pipe once per thread) and published in shared
+  // memory; every reader comes after the first class's row barrier below, and
+  // the last reads precede the trailing barrier of this evaluation.
+  __shared__ double rjl[18];
+  if (threadIdx.x >= blockDim.x - 32) {
+    double R[9], Jl[9];
     const double th2 = r0 * r0 + r1 * r1 + r2 * r2;
     const double K[9] = {0.0, -r2, r1, r2, 0.0, -r0, -r1, r0, 0.0};
     double K2[9];
@@ -187,7 +192,14 @@ __device__
       R[e] = (id + ra * K[e]) + rc * K2[e];
       Jl[e] = id + K[e] * ja + K2[e] * jb;
     }
+    if (threadIdx.x == blockDim.x - 32)
+      for (int e = 0; e < 9; ++e) {
+        rjl[e] = R[e];
+        rjl[9 + e] = Jl[e];
+      }
   }
+  const double* const R = rjl;
+  const double* const Jl = rjl + 9;
   double fval = 0.0, gt0 = 0.0, gt1 = 0.0, gt2 = 0.0, cr0 = 0.0, cr1 = 0.0, cr2 = 0.0;
   for (int c = 0; c < m.n_classes; ++c) {
     const ClassSpan cs = m.cls[c];
