@@ -156,32 +156,76 @@ def cpu_reference_rate(classes, nodes_np, threads, target_s, max_nodes=None):
     return n / dt, kind, desc, threads, dt
 
 
+def host_cpu():
+    """nproc and the lscpu model name of this host."""
+    model = None
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count() or 1, "model": model}
+
+
+def mapped_native_libs():
+    """In-tree shared objects mapped into this process (the reference arm must
+    map only oracle/_ref, never the product's libgosma.so)."""
+    libs = set()
+    try:
+        for ln in open("/proc/self/maps"):
+            p = ln.split()[-1]
+            if p.endswith(".so") and p.startswith(ROOT):
+                libs.add(os.path.relpath(p, ROOT))
+    except OSError:
+        pass
+    return sorted(libs)
+
+
 def run_reference_arm(a):
+    """The reference's own CPU evaluate_branch_batch (oracle/_ref: the
+    unmodified sources compiled in place) on all host cores, over the SAME
+    seeded batch as our arm. Every timed step evaluates the whole batch (so
+    ms_per_step is measured, not extrapolated); the W warm-up steps run a
+    small prefix (they only page in the library and the inputs)."""
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return 0
-    from paper_1812_01232_b200 import synth  # noqa: F401 (import-only; no GPU work)
+    from paper_1812_01232_b200 import synth  # pure numpy: maps no native code
+    from oracle import bind
     classes, P, cfg = workload_config(a, world)
     nodes_np = synth.nodes(a.nodes, seed=a.seed + 1)
+    arr = nodes_np.view(np.float64).reshape(-1, 11)
     threads = os.cpu_count() or 1
-    per_step = max(2.0, min(20.0, 150.0 / max(1, a.steps + a.warmup)))
-    rates = []
-    kind = desc = None
-    for s in range(a.warmup + a.steps):
-        r, kind, desc, cores, dt = cpu_reference_rate(classes, nodes_np, threads, per_step)
-        if s >= a.warmup:
-            rates.append(r)
-    value = statistics.median(rates)
+    mix = bind.Mixture(**synth.to_mixture_arrays(classes, 0.5))
+    if bind.reference_available():
+        ev, kind = bind.Reference(mix), "reference"
+    else:
+        ev, kind = bind.Oracle(mix), "port"
+    for _ in range(a.warmup):
+        ev.eval_bounds(arr[: min(len(arr), 16 * threads)], threads=threads)
+    times = []
+    for _ in range(a.steps):
+        t0 = time.perf_counter()
+        ev.eval_bounds(arr, threads=threads)
+        times.append(time.perf_counter() - t0)
+    total = sum(times)
+    value = a.steps * a.nodes / total
+    desc = (f"the whole {a.nodes}-sub-cube batch per step, evaluate_branch_batch("
+            f"threads={threads}, skip=+inf) via "
+            f"{'oracle/_ref (unmodified reference, -O3)' if kind == 'reference' else 'oracle C port'}")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-        "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * a.nodes / value,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * total / a.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": cfg,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
-                         "sample": desc},
+                         "sample": desc, "host": host_cpu()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "pair_terms_per_s": value * P,
+        "mapped_native": mapped_native_libs(),
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -542,7 +586,7 @@ def main():
         r, kind, desc, cores, dt = cpu_reference_rate(classes, nodes_np, os.cpu_count() or 1,
                                                       a.cpu_seconds)
         line["cpu_baseline"] = {"value": r, "unit": UNIT, "cores": cores, "kind": kind,
-                                "sample": desc, "seconds": dt}
+                                "sample": desc, "seconds": dt, "host": host_cpu()}
     if a.solve_seconds > 0 and world == 1:
         line["solve"] = solve_vs_reference(g, a.solve_seconds)
         line["solve_certified"] = certified_vs_reference(g)

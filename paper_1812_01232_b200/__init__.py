@@ -2,8 +2,11 @@
 solver API (/root/reference/proj/core/include/smalign/*.hpp) over the C ABI
 in include/gosma_capi.h (libgosma.so, built in-tree by csrc/Makefile).
 
-There is no CPU fallback: importing this package without a built
-libgosma.so, or calling a compute entry point without a CUDA device, raises.
+There is no CPU fallback: the first call into the package without a built
+libgosma.so raises ImportError, and a compute entry point without a CUDA
+device raises GosmaError. The library is mapped on first use, so the pure
+data helpers (NODE_DTYPE, synth) load nothing native (bench.py's reference
+arm relies on that: it must not map libgosma.so).
 """
 from __future__ import annotations
 
@@ -144,7 +147,25 @@ def _load():
     return lib
 
 
-lib = _load()
+class _LazyLib:
+    """libgosma.so, mapped on first attribute access (then cached)."""
+
+    def __init__(self):
+        self._lib = None
+
+    def __getattr__(self, name):
+        if name == "_lib":
+            raise AttributeError(name)
+        if self._lib is None:
+            self._lib = _load()
+        return getattr(self._lib, name)
+
+    @property
+    def loaded(self) -> bool:
+        return self._lib is not None
+
+
+lib = _LazyLib()
 
 
 def kernel_launches() -> int:

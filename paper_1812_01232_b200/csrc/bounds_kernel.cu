@@ -1402,6 +1402,7 @@ template <int kMode>
 cudaError_t launch_mode(const DevCtx& ctx, const EvalArgs& a, int sm_count,
                         cudaStream_t stream) {
   if (a.n <= 0) return cudaSuccess;
+  if (!a.work) return cudaErrorMemoryAllocation;  // no node counter for this stream
   switch (group_lanes(ctx, kMode)) {
     case kCtaGroup:
       return launch_group<kMode, kCtaGroup, false>(ctx, a, sm_count, stream);

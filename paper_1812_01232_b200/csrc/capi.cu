@@ -26,6 +26,17 @@ int cuda_error(cudaError_t e, const char* where) {
   return set_error(GOSMA_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
 }
 
+unsigned int* work_counter(gosma_ctx* ctx, cudaStream_t s) {
+  if (s == ctx->stream || s == nullptr) return static_cast<unsigned int*>(ctx->d_work);
+  std::lock_guard<std::mutex> lk(ctx->work_mu);
+  for (const auto& ws : ctx->work_slots)
+    if (ws.first == s) return static_cast<unsigned int*>(ws.second);
+  void* p = nullptr;
+  if (cudaMalloc(&p, sizeof(unsigned int)) != cudaSuccess) return nullptr;
+  ctx->work_slots.emplace_back(s, p);
+  return static_cast<unsigned int*>(p);
+}
+
 namespace {
 
 bool weights_close(double sum) { return std::fabs(sum - 1.0) <= 1e-9; }
@@ -146,6 +157,11 @@ void ctx_free_device(gosma_ctx* ctx) {
   ctx->owned.clear();
   if (ctx->d_work) cudaFree(ctx->d_work);
   ctx->d_work = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(ctx->work_mu);
+    for (auto& ws : ctx->work_slots) cudaFree(ws.second);
+    ctx->work_slots.clear();
+  }
   cudaFree(ctx->d_cache_nodes);
   cudaFree(ctx->d_cache_self);
   ctx->d_cache_nodes = nullptr;
@@ -389,7 +405,7 @@ int gosma_eval_bounds_device(gosma_ctx* ctx, const gosma_node* d_nodes, size_t n
   a.lower = d_lower;
   a.upper = d_upper;
   a.split_rot = d_split;
-  a.work = static_cast<unsigned int*>(ctx->d_work);
+  a.work = work_counter(ctx, s);
   const cudaError_t e = launch_eval_bounds(ctx->dev, a, ctx->sm_count, s);
   if (e != cudaSuccess) return cuda_error(e, "eval_bounds launch");
   return GOSMA_OK;
@@ -411,6 +427,7 @@ int gosma_eval_children_device(gosma_ctx* ctx, const gosma_node* d_parents, cons
     ctx->d_child_kids = nullptr;
     ctx->d_child_lists = nullptr;
     ctx->d_child_sel = nullptr;
+    ctx->child_cap = 0;  // stays 0 unless every allocation below succeeds
     if ((e = cudaMalloc(&ctx->d_child_kids, 8 * n * sizeof(gosma_node))) != cudaSuccess ||
         (e = cudaMalloc(&ctx->d_child_lists, 9 * n * sizeof(int) + 32)) != cudaSuccess ||
         (e = cudaMalloc(&ctx->d_child_sel, n * sizeof(unsigned int))) != cudaSuccess)
@@ -431,7 +448,7 @@ int gosma_eval_children_device(gosma_ctx* ctx, const gosma_node* d_parents, cons
   a.lower = d_lower;
   a.upper = d_upper;
   a.split_rot = d_child_split;
-  a.work = static_cast<unsigned int*>(ctx->d_work);
+  a.work = work_counter(ctx, s);
   EvalArgs b = a;
   b.nodes = reinterpret_cast<const double*>(d_parents);
   b.n = static_cast<long long>(n);
@@ -466,6 +483,7 @@ int gosma_eval_bounds_cached_device(gosma_ctx* ctx, const gosma_node* d_nodes, s
     cudaFree(ctx->d_cache_self);
     ctx->d_cache_nodes = nullptr;
     ctx->d_cache_self = nullptr;
+    ctx->cache_cap = 0;  // stays 0 unless both allocations below succeed
     if ((e = cudaMalloc(&ctx->d_cache_nodes, n_tboxes * sizeof(gosma_node))) != cudaSuccess ||
         (e = cudaMalloc(&ctx->d_cache_self, n_tboxes * 4 * sizeof(double))) != cudaSuccess)
       return cuda_error(e, "cache alloc");
@@ -480,7 +498,7 @@ int gosma_eval_bounds_cached_device(gosma_ctx* ctx, const gosma_node* d_nodes, s
   a.lower = nullptr;
   a.upper = nullptr;
   a.split_rot = nullptr;
-  a.work = static_cast<unsigned int*>(ctx->d_work);
+  a.work = work_counter(ctx, s);
   a.self_out = ctx->d_cache_self;
   if ((e = launch_eval_self(ctx->dev, a, ctx->sm_count, s)) != cudaSuccess)
     return cuda_error(e, "self kernel");

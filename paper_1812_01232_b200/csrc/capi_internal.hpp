@@ -50,7 +50,12 @@ struct gosma_ctx {
   gosma::DevCtx dev{};
   double lb_margin = gosma::kDefaultLbMargin;
   std::vector<void*> owned;
-  void* d_work = nullptr;
+  void* d_work = nullptr;  // persistent-warp node counter of launches on `stream`
+  // one node counter per caller stream (the kernels' persistent warps claim
+  // nodes from it; two launches in flight on different streams must not share
+  // one): work_counter() hands them out, ctx_free_device releases them
+  std::vector<std::pair<cudaStream_t, void*>> work_slots;
+  std::mutex work_mu;
   gosma_node* d_cache_nodes = nullptr;  // translation-cached mode scratch
   double* d_cache_self = nullptr;
   size_t cache_cap = 0;
@@ -79,6 +84,9 @@ struct gosma_ctx {
 };
 
 namespace gosma {
+// The node counter of bound-kernel launches on stream s (launches on one
+// stream are ordered, so they may share it; other streams get their own).
+unsigned int* work_counter(gosma_ctx* ctx, cudaStream_t s);
 int set_error(int code, const std::string& msg);
 int cuda_error(cudaError_t e, const char* where);
 }  // namespace gosma

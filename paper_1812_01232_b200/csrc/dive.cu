@@ -271,7 +271,7 @@ cudaError_t launch_iteration(gosma_ctx* ctx, const DiveDev& d, int from, cudaStr
   a.lower = d.lo;
   a.upper = d.up;
   a.split_rot = d.sp;
-  a.work = static_cast<unsigned int*>(ctx->d_work);
+  a.work = work_counter(ctx, s);
   cudaError_t e = launch_eval_bounds(ctx->dev, a, ctx->sm_count, s);
   if (e != cudaSuccess) return e;
   const unsigned g = std::min<unsigned>((ck + 255) / 256, 4u * ctx->sm_count);

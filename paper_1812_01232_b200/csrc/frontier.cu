@@ -247,17 +247,21 @@ inline unsigned grid_cap(size_t n, unsigned block) {
 
 // Histogram of digit (key >> shift) & mask among keys < limit whose bits above
 // `prefix_shift` equal `prefix` (prefix_shift 64: no prefix).
+// With `inv` set the keys are ranked from the top: key' = limit - 1 - key
+// (the drain order, largest lower bounds first).
 __global__ void digit_hist(const unsigned long long* key, const unsigned int* idx, size_t n,
                            unsigned long long limit, int shift, int bits,
-                           unsigned long long prefix, int prefix_shift, unsigned int* hist) {
+                           unsigned long long prefix, int prefix_shift, unsigned int* hist,
+                           bool inv) {
   __shared__ unsigned int sh[kBins];
   const int nb = 1 << bits;
   for (int b = threadIdx.x; b < nb; b += blockDim.x) sh[b] = 0;
   __syncthreads();
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<size_t>(gridDim.x) * blockDim.x) {
-    const unsigned long long k = idx ? key[idx[i]] : key[i];
+    unsigned long long k = idx ? key[idx[i]] : key[i];
     if (k >= limit) continue;
+    if (inv) k = limit - 1 - k;
     if (prefix_shift < 64 && (k >> prefix_shift) != prefix) continue;
     atomicAdd(&sh[(k >> shift) & static_cast<unsigned long long>(nb - 1)], 1u);
   }
@@ -272,6 +276,18 @@ struct KeyBelow {
   __device__ __forceinline__ bool operator()(const unsigned int& i) const {
     const unsigned long long k = key[i];
     return k >= lo && k < hi;
+  }
+};
+
+// Drain order: key < limit with limit - 1 - key in [lo, hi).
+struct KeyTopRange {
+  const unsigned long long* key;
+  unsigned long long lo, hi, limit;
+  __device__ __forceinline__ bool operator()(const unsigned int& i) const {
+    const unsigned long long k = key[i];
+    if (k >= limit) return false;
+    const unsigned long long r = limit - 1 - k;
+    return r >= lo && r < hi;
   }
 };
 
@@ -876,13 +892,14 @@ cudaError_t Frontier::min_key(cudaStream_t s, unsigned long long* out) {
 // the digits run out), and hi = the end of the boundary bin (capped at limit).
 cudaError_t Frontier::descend(size_t want, unsigned long long limit, double fill, cudaStream_t s,
                               unsigned long long* lo, unsigned long long* hi, size_t* below_out,
-                              size_t* bin_out, const unsigned int* idx, size_t n_items) {
+                              size_t* bin_out, const unsigned int* idx, size_t n_items,
+                              bool inv) {
   // Digit schedule over the 64-bit key: 12,12,12,12,12,4 bits.
   // Every live key lies in [known_min, limit): the digits start below their
   // common high bits (one 12-bit level usually resolves a wave).
   int pshift = 64;  // bits >= pshift are fixed to `prefix` (64: none)
   unsigned long long prefix = 0;
-  if (known_min > 0 && known_min < limit) {
+  if (!inv && known_min > 0 && known_min < limit) {
     const unsigned long long x = known_min ^ (limit - 1);
     pshift = std::max(12, x ? 64 - __builtin_clzll(x) : 0);
     prefix = pshift >= 64 ? 0ull : (known_min >> pshift);
@@ -896,7 +913,7 @@ cudaError_t Frontier::descend(size_t want, unsigned long long limit, double fill
     const int shift = pshift - bits;
     if ((e = cudaMemsetAsync(hist, 0, kBins * 4, s)) != cudaSuccess) return e;
     digit_hist<<<grid_cap(n_items, 256), 256, 0, s>>>(key, idx, n_items, limit, shift, bits,
-                                                      prefix, pshift, hist);
+                                                      prefix, pshift, hist, inv);
     const int nb = 1 << bits;
     if ((e = cudaMemcpyAsync(h_hist.data(), hist, nb * 4, cudaMemcpyDeviceToHost, s)) !=
         cudaSuccess)
@@ -945,7 +962,7 @@ cudaError_t Frontier::rebuild_candidates(size_t want_total, cudaStream_t s) {
   }
   unsigned long long lo = 0, hi = kHoleKey;
   size_t below = 0, bin = 0;
-  cudaError_t e = descend(want_total, kHoleKey, 0.5, s, &lo, &hi, &below, &bin, nullptr, size);
+  cudaError_t e = descend(want_total, kHoleKey, 0.5, s, &lo, &hi, &below, &bin, nullptr, size, false);
   if (e != cudaSuccess) return e;
   const unsigned long long t = below > 0 ? lo : hi;  // massive ties: keep the boundary bin
   const size_t count = below > 0 ? below : bin;
@@ -1009,7 +1026,7 @@ cudaError_t Frontier::select_smallest(size_t want, unsigned long long limit, cud
       lo_key = hi_key = limit;
       below = bin_count = 0;
     } else if ((e = descend(want, limit, 0.5, s, &lo_key, &hi_key, &below, &bin_count, cand,
-                            cand_n)) != cudaSuccess) {
+                            cand_n, false)) != cudaSuccess) {
       return e;
     }
     // too few candidates below the limit while the pool may hold more: refill
@@ -1066,6 +1083,68 @@ cudaError_t Frontier::select_smallest(size_t want, unsigned long long limit, cud
     cand_n -= n;
   }
   tm.lap(3);
+  *n_out = n;
+  return cudaGetLastError();
+}
+
+// Drain order (memory pressure): the `want` live nodes with the LARGEST keys
+// below `limit`, i.e. the nodes nearest to being pruned, whose subtrees are
+// the shallowest. Every node below d* - eps has to be expanded before the gap
+// closes whatever the order, so expanding these first changes neither the
+// work nor the certified result, only the pool's peak size. Full-pool radix
+// descent on inverted keys (no candidate list).
+cudaError_t Frontier::select_largest(size_t want, unsigned long long limit, cudaStream_t s,
+                                     size_t* n_out) {
+  *n_out = 0;
+  if (size == 0 || want == 0) return cudaSuccess;
+  want = std::min(want, sel_cap);
+  cudaError_t e;
+  unsigned long long lo_key = 0, hi_key = limit;
+  size_t below = 0, bin_count = 0;
+  if ((e = descend(want, limit, 0.5, s, &lo_key, &hi_key, &below, &bin_count, nullptr, size,
+                   true)) != cudaSuccess)
+    return e;
+  cub::CountingInputIterator<unsigned int> it(0);
+  size_t need = 0;
+  KeyTopRange p1{key, 0ull, lo_key, limit};
+  cub::DeviceSelect::If(nullptr, need, it, sel, counter, static_cast<int>(size), p1, s);
+  if ((e = ensure_temp(need)) != cudaSuccess) return e;
+  const size_t n1 = below;
+  if (n1 > 0) cub::DeviceSelect::If(temp, need, it, sel, counter, static_cast<int>(size), p1, s);
+  size_t n2 = 0;
+  if (n1 < want && hi_key > lo_key && bin_count > 0) {
+    n2 = std::min(want - n1, bin_count);
+    if (bin_count > bsel_cap) {
+      dfree(bsel);
+      bsel = nullptr;
+      const size_t c = std::max(bin_count, 2 * bsel_cap);
+      if ((e = dmalloc(&bsel, c * 4)) != cudaSuccess) return e;
+      bsel_cap = c;
+    }
+    KeyTopRange p2{key, lo_key, hi_key, limit};
+    cub::DeviceSelect::If(temp, need, it, bsel, counter, static_cast<int>(size), p2, s);
+    if ((e = cudaMemcpyAsync(sel + n1, bsel, n2 * 4, cudaMemcpyDeviceToDevice, s)) != cudaSuccess)
+      return e;
+  }
+  const size_t n = n1 + n2;
+  if (n) {
+    mark_holes<<<grid_for(n, 256), 256, 0, s>>>(key, sel, n);
+    holes += n;
+    if (tau != 0 && cand_n) {  // the candidate list must not hold holes
+      NotHole ph{key};
+      size_t need2 = 0;
+      cub::DeviceSelect::If(nullptr, need2, cand, cand_tmp, counter, static_cast<int>(cand_n), ph,
+                            s);
+      if ((e = ensure_temp(need2)) != cudaSuccess) return e;
+      cub::DeviceSelect::If(temp, need2, cand, cand_tmp, counter, static_cast<int>(cand_n), ph,
+                            s);
+      if ((e = cudaMemcpyAsync(h_counter, counter, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+        return e;
+      if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+      std::swap(cand, cand_tmp);
+      cand_n = static_cast<size_t>(*reinterpret_cast<int*>(h_counter));
+    }
+  }
   *n_out = n;
   return cudaGetLastError();
 }
@@ -1302,7 +1381,7 @@ cudaError_t Frontier::fold_to(size_t keep_n, cudaStream_t s, double* folded_volu
   if (e != cudaSuccess || size <= keep_n) return e;
   unsigned long long lo = 0, hi = kHoleKey;
   size_t below = 0;
-  if ((e = descend(keep_n, kHoleKey, 0.9, s, &lo, &hi, &below, nullptr, nullptr, size)) !=
+  if ((e = descend(keep_n, kHoleKey, 0.9, s, &lo, &hi, &below, nullptr, nullptr, size, false)) !=
       cudaSuccess)
     return e;
   // fold every key >= tau; with massive ties below the first boundary keep the bin

@@ -106,9 +106,11 @@ struct Frontier {
   // their indices to sel, marks them holes, returns the count.
   cudaError_t descend(size_t want, unsigned long long limit, double fill, cudaStream_t s,
                       unsigned long long* lo, unsigned long long* hi, size_t* below,
-                      size_t* bin, const unsigned int* idx, size_t n_items);
+                      size_t* bin, const unsigned int* idx, size_t n_items, bool inv);
   cudaError_t rebuild_candidates(size_t want_total, cudaStream_t s);
   cudaError_t select_smallest(size_t want, unsigned long long limit, cudaStream_t s, size_t* n);
+  // drain order under memory pressure: the largest keys below limit
+  cudaError_t select_largest(size_t want, unsigned long long limit, cudaStream_t s, size_t* n);
   cudaError_t expand_selected(size_t n_sel, cudaStream_t s);
   cudaError_t expand_selected_cached(size_t n_sel, cudaStream_t s, size_t* n_cuboids);
   // rotation-split selections (rot_list) and translation-split children (trans_list)

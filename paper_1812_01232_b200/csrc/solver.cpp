@@ -465,6 +465,10 @@ struct gosma_solver {
   Frontier F;
   double total_volume = 0.0, pruned_volume = 0.0, resolved_volume = 0.0;
   double floor_lower = kInf;
+  // drain order (Frontier::select_largest) while the pool is above its
+  // high-water mark; folding (enforce_capacity) only as a last resort
+  bool drain = false;
+  unsigned long long drain_waves = 0, folds = 0;
   unsigned long long evals = 0, expanded = 0, wave = 0;
   size_t wave_nodes = 0, qcap = 0, mem_cap = 0;
   // child bounds per wave: 2 = siblings (a rotation-split parent's cuboid
@@ -598,8 +602,18 @@ int solver_init(gosma_solver* S) {
   // resolved set (sound; the reference's queue_capacity mechanism).
   size_t free_b = 0;
   free_device_memory(ctx->device, &free_b);
-  const size_t per_node = sizeof(gosma_node) + 1 + 8 + 8;
-  S->mem_cap = std::max<size_t>(free_b / 4 / per_node, 16 * S->wave_nodes);
+  // pool record + key + candidate/compaction indices; the pool may take
+  // GOSMA_POOL_FRAC (default 0.5) of the free memory (growth copies need the
+  // old arrays alongside the new ones once)
+  const size_t per_node = sizeof(gosma_node) + 1 + 8 + 8 + 12;
+  static const double pool_frac = [] {
+    const char* e = std::getenv("GOSMA_POOL_FRAC");
+    const double f = e ? std::atof(e) : 0.5;
+    return f > 0.0 && f < 0.9 ? f : 0.5;
+  }();
+  S->mem_cap = std::max<size_t>(static_cast<size_t>(pool_frac * static_cast<double>(free_b)) /
+                                    per_node,
+                                16 * S->wave_nodes);
   S->F.cap_limit = S->mem_cap;
   S->qcap = cfg.queue_capacity >= 0
                 ? std::min<size_t>(static_cast<size_t>(cfg.queue_capacity), S->mem_cap)
@@ -694,8 +708,11 @@ void gosma_solver_destroy(gosma_solver* S) {
   if (S->profile) {
     static const char* kName[8] = {"status", "select", "expand+self", "eval", "best+improve",
                                    "route", "compact", "dive"};
-    std::fprintf(stderr, "[gosma profile] waves %llu evals %llu cuboids %llu rebuilds %llu pool %zu:",
-                 S->wave, S->evals, S->cuboid_evals, S->F.rebuilds, S->F.size);
+    std::fprintf(stderr,
+                 "[gosma profile] waves %llu (drain %llu, folds %llu, budget %zu nodes) evals %llu "
+                 "cuboids %llu rebuilds %llu pool %zu:",
+                 S->wave, S->drain_waves, S->folds, S->mem_cap, S->evals, S->cuboid_evals,
+                 S->F.rebuilds, S->F.size);
     for (int k = 0; k < 8; ++k) std::fprintf(stderr, " %s %.3fs", kName[k], S->phase[k]);
     std::fprintf(stderr,
                  " | select: rebuild %.3fs descend %.3fs pick %.3fs list %.3fs (max bin %zu, "
@@ -720,17 +737,42 @@ int gosma_solver_status(gosma_solver* S, gosma_wave_status* st) {
     cudaStream_t s;
     ~LapAtExit() { S->lap(0, s); }
   } lap_at_exit{S, s};
-  // capacity folding (solver.cpp:433-447); the memory budget folds to 3/4
+  // capacity folding (solver.cpp:433-447) at the caller's queue_capacity
   const bool user_cap = S->cfg.queue_capacity >= 0 &&
                         static_cast<size_t>(S->cfg.queue_capacity) <= S->mem_cap;
-  if (S->F.live_upper_bound() > S->qcap ||
-      (!user_cap && S->F.size + 8 * S->wave_nodes > S->mem_cap)) {
-    const size_t target = user_cap ? static_cast<size_t>(S->cfg.queue_capacity)
-                                   : S->mem_cap * 3 / 4 - 8 * S->wave_nodes;
+  const size_t wave_room = 8 * S->wave_nodes;
+  if (user_cap && S->F.live_upper_bound() > S->qcap) {
     double fv = 0.0, fmin = kInf;
-    if ((e = S->F.fold_to(target, s, &fv, &fmin)) != cudaSuccess) return cuda_error(e, "fold");
+    if ((e = S->F.fold_to(S->qcap, s, &fv, &fmin)) != cudaSuccess) return cuda_error(e, "fold");
     S->resolved_volume += fv;
     S->floor_lower = std::min(S->floor_lower, fmin);
+  } else if (!user_cap) {
+    // The device memory budget: above the high-water mark the waves take the
+    // largest lower bounds below the limit (drain order: their subtrees die
+    // soonest), which bounds the pool without changing the work or the
+    // certificate; below the low-water mark best-first resumes. Folding (it
+    // caps the certified bound) happens only if the pool still overflows.
+    static const bool drain_on = [] {
+      const char* e = std::getenv("GOSMA_DRAIN");
+      return !(e && std::string(e) == "0");
+    }();
+    const size_t live = S->F.live_upper_bound();
+    if (drain_on && !S->drain && live + wave_room > S->mem_cap * 3 / 4) S->drain = true;
+    if (S->drain && live + wave_room < S->mem_cap * 9 / 20) S->drain = false;
+    if (S->F.size + wave_room > S->mem_cap) {
+      double dropped = 0.0;  // holes and stale nodes first
+      if ((e = S->F.compact(host_order_key(S->dstar()), s, &dropped)) != cudaSuccess)
+        return cuda_error(e, "compact");
+      S->pruned_volume += dropped;
+    }
+    if (S->F.size + wave_room > S->mem_cap) {
+      const size_t target = drain_on ? S->mem_cap - 2 * wave_room : S->mem_cap * 3 / 4 - wave_room;
+      double fv = 0.0, fmin = kInf;
+      if ((e = S->F.fold_to(target, s, &fv, &fmin)) != cudaSuccess) return cuda_error(e, "fold");
+      S->resolved_volume += fv;
+      S->floor_lower = std::min(S->floor_lower, fmin);
+      ++S->folds;
+    }
   }
   unsigned long long kmin = kHoleKey;
   if ((e = S->F.min_key(s, &kmin)) != cudaSuccess) return cuda_error(e, "frontier min");
@@ -763,8 +805,11 @@ int gosma_solver_expand(gosma_solver* S, double limit, unsigned long long max_ev
   size_t n_sel = 0;
   S->lap(-1, s);
   // Expand only nodes that can still matter: lower < limit (= d* - eps).
-  if ((e = S->F.select_smallest(want, host_order_key(limit), s, &n_sel)) != cudaSuccess)
+  if ((e = S->drain ? S->F.select_largest(want, host_order_key(limit), s, &n_sel)
+                    : S->F.select_smallest(want, host_order_key(limit), s, &n_sel)) !=
+      cudaSuccess)
     return cuda_error(e, "select");
+  if (S->drain) ++S->drain_waves;
   if (n_sel == 0) {
     // Nothing below the limit yet the gap is open (a resolved floor holds the
     // bound down): keep refining the live nodes, as the reference's heap would.
@@ -783,7 +828,7 @@ int gosma_solver_expand(gosma_solver* S, double limit, unsigned long long max_ev
   if ((e = S->F.ensure_kids(n_sel)) != cudaSuccess) return cuda_error(e, "child buffers");
   S->lap(1, s);
   EvalArgs a;
-  a.work = static_cast<unsigned int*>(ctx->d_work);
+  a.work = work_counter(ctx, s);
   a.skip_upper_at = S->dstar();
   if (S->cached) {
     // Translation-cached bounds: the self sums once per distinct cuboid

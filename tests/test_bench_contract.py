@@ -30,6 +30,9 @@ def test_reference_arm_prints_one_contract_line():
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
     assert d["cpu_baseline"]["kind"] in ("reference", "port") and d["cpu_baseline"]["cores"] >= 1
     assert "workload" in d["config"]
+    # the reference arm maps the reference build only, never the product library
+    assert not any("libgosma" in lib for lib in d["mapped_native"]), d["mapped_native"]
+    assert d["cpu_baseline"]["host"]["nproc"] >= 1
 
 
 def test_reference_arm_non_zero_ranks_exit_quietly():
