@@ -231,8 +231,9 @@ typedef struct gosma_wave_status {
   double elapsed_seconds;
 } gosma_wave_status;
 
-/* Rank `rank` of `world` owns translation roots rank, rank + world, ... and
- * runs wave 0 (+ discovery dive over its sectors). */
+/* Every rank runs wave 0 and the discovery dive over all roots; with
+ * world > 1 the roots are expanded deterministically to >= 8 x SMs nodes and
+ * rank `rank` keeps nodes rank, rank + world, ... */
 int gosma_solver_create(gosma_ctx* ctx, const gosma_domain* domain, const gosma_config* config,
                         int rank, int world, gosma_solver** out);
 void gosma_solver_destroy(gosma_solver* solver);

@@ -243,6 +243,8 @@ struct WarpTables {
                 // (a self pair reads [0..2] of its partner row: whole 128-bit loads)
   float4* col;  // [0] (qhx, qhy, qhz, k2)    q_j = R0^T m_j, FP32 high part
                 // [1] (qlx, qly, qlz, G)     q_j low part, G = phi2 / W(k2)
+  float4* rowp; // per model row (s4 hi, s4 lo, c4 hi, c4 lo): 4 sin^2(psi/2) and
+                // 4 cos^2(psi/2) as double-floats, for the precise cross pass
 };
 // Pair terms are F_i G_j 2^(excess log2e) W(K) (the log W(a), log W(b) and
 // log phi pieces of the reference's log_term, bounds.cpp:136/176, as linear
@@ -251,6 +253,15 @@ struct WarpTables {
 
 constexpr int kRowF4 = 5;  // float4 per model row
 constexpr int kColF4 = 2;  // float4 per image column
+constexpr int kRowPF4 = 1;  // float4 per model row (precise cross pass)
+
+// Precise cross pass: a node whose cross terms' FP32 error
+// estimate exceeds kRedoRel of their mass re-evaluates them with the alignment
+// angle's numerator x - 4 sin^2(psi/2) formed in FP64 from the double-float
+// directions and psi half-angles (the only FP32 step whose error is amplified,
+// by theta/B). The decision is per node (group-uniform), so the redo runs
+// converged; ~all realistic-regime nodes never take it.
+constexpr double kRedoRel = 2e-6;
 
 struct Row {
   float uhx, uhy, uhz, ulx, uly, ulz, klo, khi, kst, Fhi, Fst, cp2, sp2, csp2, s4, c4, usx, usy,
@@ -312,9 +323,10 @@ __device__ __forceinline__ void sincos_sq(float hx, float hy, float hz, float lx
 // s4 = 4 sin^2(psi/2) from FP64 per-row prep: the theta ~ psi cancellation
 // happens in x - s4, where both operands carry ~1e-7 relative error, instead
 // of in sin/cos products.
-template <bool kSame>
+template <bool kSame, bool kPrecise = false>
 __device__ __forceinline__ void cross_pair(const Row& r, const float4 qa, const float4 qb, float& l,
-                                           float& u, float& ma, float& mb) {
+                                           float& u, float& ma, float& mb,
+                                           const float4 rp = float4{}) {
   const float k2 = qa.w;
   // x = |u - q|^2 = 4 sin^2(theta/2), y = |u + q|^2 = 4 cos^2(theta/2), each
   // without cancellation (sincos_sq)
@@ -327,7 +339,21 @@ __device__ __forceinline__ void cross_pair(const Row& r, const float4 qa, const 
   const float m = sqf(x * y) * r.csp2;
   // 2 sin(B/2) * den = x - 4 sin^2(psi/2) = 4 cos^2(psi/2) - y: take the form
   // whose operands are small (theta below / above 90 degrees).
-  float num = (x > y) ? (r.c4 - y) : (x - r.s4);
+  float num;
+  if constexpr (kPrecise) {
+    // the same difference in FP64: |u -+ q|^2 from the double-float directions
+    // minus the double-float 4 sin^2(psi/2) (4 cos^2 past 90 degrees)
+    const bool obtuse = x > y;
+    const double sg = obtuse ? 1.0 : -1.0;
+    const double vx = (static_cast<double>(r.uhx) + r.ulx) + sg * (static_cast<double>(qa.x) + qb.x);
+    const double vy = (static_cast<double>(r.uhy) + r.uly) + sg * (static_cast<double>(qa.y) + qb.y);
+    const double vz = (static_cast<double>(r.uhz) + r.ulz) + sg * (static_cast<double>(qa.z) + qb.z);
+    const double w = fma(vx, vx, fma(vy, vy, vz * vz));
+    num = static_cast<float>(obtuse ? (static_cast<double>(rp.z) + rp.w) - w
+                                    : w - (static_cast<double>(rp.x) + rp.y));
+  } else {
+    num = (x > y) ? (r.c4 - y) : (x - r.s4);
+  }
   const bool bz = !(num > 0.0f);                        // theta <= psi: B = 0
   num = bz ? 0.0f : num;
   const float den2 = bz ? 1.0f : fmaf(x, r.cp2, fmaf(y, r.sp2, m));
@@ -374,9 +400,10 @@ __device__ __forceinline__ void cross_pair(const Row& r, const float4 qa, const 
   // FP32 error estimate of the LB term: B = theta - psi
   // carries ~u theta absolute error, amplified in e1 by min(x, y)/num (the
   // operand used); accumulated as sum t |e1/num| min(x,y) and sum t |e1|.
+  // The precise pass forms num in FP64: only the exponent's own error remains.
   const float gt1 = qb.w * t1;  // G_j; F_i is applied to the row sum
   l += gt1;
-  ma = fmaf(gt1, fabsf(g) * fminf(x, y), ma);
+  if constexpr (!kPrecise) ma = fmaf(gt1, fabsf(g) * fminf(x, y), ma);
   mb = fmaf(gt1, fabsf(e1), mb);
   u = fmaf(qb.w, t2, u);
 }
@@ -490,23 +517,25 @@ __device__ __forceinline__ Row load_row(const WarpTables& T, int i) {
   return r;
 }
 
-template <int kG, bool kSame, bool kCross, bool kSelf>
+template <int kG, bool kSame, bool kCross, bool kSelf, bool kPrecise = false>
 __device__ __forceinline__ void class_pairs_rows(const WarpTables& T, const ClassSpan cs, int lane,
                                             float w, double& lb_self, double& lb_cross,
-                                            double& ub_self, double& ub_cross, double& lb_err) {
+                                            double& ub_self, double& ub_cross, double& lb_err,
+                                            double& lb_err_x) {
   const int n = cs.n1;
   // Cross terms: rows over lanes, columns broadcast.
   for (int base = 0; kCross && base < n; base += kG) {
     const int il = base + lane;
     if (il < n) {
       const Row r = load_row(T, cs.o1 + il);
+      const float4 rp = kPrecise ? T.rowp[cs.o1 + il] : float4{};
       float l = 0.0f, u = 0.0f, ma = 0.0f, mb = 0.0f;
       const float4* cp = T.col + cs.o2 * kColF4;  // pointer walk: no index math per pair
       const float4* const ce = cp + cs.n2 * kColF4;
 #pragma unroll kUnrollPairs
-      for (; cp < ce; cp += kColF4) cross_pair<kSame>(r, cp[0], cp[1], l, u, ma, mb);
+      for (; cp < ce; cp += kColF4) cross_pair<kSame, kPrecise>(r, cp[0], cp[1], l, u, ma, mb, rp);
       lb_cross += static_cast<double>(w * r.Fhi * l);
-      lb_err += static_cast<double>(
+      lb_err_x += static_cast<double>(
           2.0f * w * r.Fhi * fmaf(ma, kErrAmp, fmaf(mb, kErrExp, l * kErrTerm)));
       ub_cross += static_cast<double>(w * r.Fst * u);
     }
@@ -547,11 +576,12 @@ __device__ __forceinline__ void class_pairs_rows(const WarpTables& T, const Clas
 // gives each row k = kG / r lanes ("slots") sharing its partners round-robin
 // (the node sums are sums over pairs, so any pair -> lane assignment is
 // exact). Separate instantiation: the plain loops stay tighter for full chunks.
-template <int kG, bool kSame, bool kCross, bool kSelf>
+template <int kG, bool kSame, bool kCross, bool kSelf, bool kPrecise = false>
 __device__ __forceinline__ void class_pairs_tail(const WarpTables& T, const ClassSpan cs,
                                                  int lane, float w, double& lb_self,
                                                  double& lb_cross, double& ub_self,
-                                                 double& ub_cross, double& lb_err) {
+                                                 double& ub_cross, double& lb_err,
+                                                 double& lb_err_x) {
   const int n = cs.n1;
   // cross terms: columns broadcast (slot s takes columns s, s+k, ...)
   for (int base = 0; kCross && base < n; base += kG) {
@@ -559,14 +589,15 @@ __device__ __forceinline__ void class_pairs_tail(const WarpTables& T, const Clas
     const int il = base + lane % r, slot = lane / r;
     if (lane < r * k) {
       const Row rw = load_row(T, cs.o1 + il);
+      const float4 rp = kPrecise ? T.rowp[cs.o1 + il] : float4{};
       float l = 0.0f, u = 0.0f, ma = 0.0f, mb = 0.0f;
       const float4* cp = T.col + (cs.o2 + slot) * kColF4;
       const float4* const ce = T.col + (cs.o2 + cs.n2) * kColF4;
       const int cstep = k * kColF4;
 #pragma unroll kUnrollPairs
-      for (; cp < ce; cp += cstep) cross_pair<kSame>(rw, cp[0], cp[1], l, u, ma, mb);
+      for (; cp < ce; cp += cstep) cross_pair<kSame, kPrecise>(rw, cp[0], cp[1], l, u, ma, mb, rp);
       lb_cross += static_cast<double>(w * rw.Fhi * l);
-      lb_err += static_cast<double>(
+      lb_err_x += static_cast<double>(
           2.0f * w * rw.Fhi * fmaf(ma, kErrAmp, fmaf(mb, kErrExp, l * kErrTerm)));
       ub_cross += static_cast<double>(w * rw.Fst * u);
     }
@@ -606,16 +637,39 @@ __device__ __forceinline__ void class_pairs_tail(const WarpTables& T, const Clas
   }
 }
 
-template <int kG, bool kSame, bool kCross, bool kSelf, bool kTail>
+template <int kG, bool kSame, bool kCross, bool kSelf, bool kTail, bool kPrecise = false>
 __device__ __forceinline__ void class_pairs(const WarpTables& T, const ClassSpan cs, int lane,
                                             float w, double& lb_self, double& lb_cross,
-                                            double& ub_self, double& ub_cross, double& lb_err) {
+                                            double& ub_self, double& ub_cross, double& lb_err,
+                                            double& lb_err_x) {
   if constexpr (kTail) {
-    class_pairs_tail<kG, kSame, kCross, kSelf>(T, cs, lane, w, lb_self, lb_cross, ub_self,
-                                               ub_cross, lb_err);
+    class_pairs_tail<kG, kSame, kCross, kSelf, kPrecise>(T, cs, lane, w, lb_self, lb_cross,
+                                                         ub_self, ub_cross, lb_err, lb_err_x);
   } else {
-    class_pairs_rows<kG, kSame, kCross, kSelf>(T, cs, lane, w, lb_self, lb_cross, ub_self,
-                                               ub_cross, lb_err);
+    class_pairs_rows<kG, kSame, kCross, kSelf, kPrecise>(T, cs, lane, w, lb_self, lb_cross,
+                                                         ub_self, ub_cross, lb_err, lb_err_x);
+  }
+}
+
+// The cross sums of one class span, FP32 pass then (group-uniform decision on
+// the group-summed error estimate) the precise pass when the estimate exceeds
+// kRedoRel of the span's cross mass. Returns group sums {lb, ub, err}.
+template <int kG, bool kSame, bool kTail>
+__device__ __forceinline__ void cross_span(const WarpTables& T, const ClassSpan cs, int lane,
+                                           float w, const Group<kG>& G, bool precise_on,
+                                           double& lcr, double& ucr, double& ecr) {
+  double d0 = 0.0, d1 = 0.0;
+  lcr = ucr = ecr = 0.0;
+  class_pairs<kG, kSame, true, false, kTail>(T, cs, lane, w, d0, lcr, d1, ucr, d0, ecr);
+  lcr = G.sum(lcr);
+  ucr = G.sum(ucr);
+  ecr = G.sum(ecr);
+  if (precise_on && ecr > kRedoRel * 2.0 * lcr) {
+    double l2 = 0.0, u2 = 0.0, e2 = 0.0;
+    class_pairs<kG, kSame, true, false, kTail, true>(T, cs, lane, w, d0, l2, d1, u2, d0, e2);
+    lcr = G.sum(l2);
+    ucr = G.sum(u2);
+    ecr = G.sum(e2);
   }
 }
 
@@ -775,12 +829,14 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
   constexpr bool kSib = kMode == kSiblings || kMode == kSiblingsStream;
   const int N1 = ctx.n1_total;  // every model mean (feasibility scans)
   const int TN1 = streamed ? ctx.max_n1 : N1, TN2 = streamed ? ctx.max_n2 : ctx.n2_total;
-  const size_t table_f4 = static_cast<size_t>(kRowF4 * TN1 + kColF4 * TN2);
+  const size_t table_f4 = static_cast<size_t>((kRowF4 + kRowPF4) * TN1 + kColF4 * TN2);
   const size_t per_warp_f4 = table_f4 + (kSib ? kSibStreamExtraF4 : 0);
   float4* base = smem4 + group * per_warp_f4;
   WarpTables T;
   T.row = base;
   T.col = base + kRowF4 * TN1;
+  T.rowp = T.col + kColF4 * TN2;
+  const bool precise = ctx.precise != 0;
 
   const double zeta = ctx.zeta;
   const double zeta2 = zeta * zeta;
@@ -970,6 +1026,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
       pr[3] = make_float4(static_cast<float>(v0 * iv), static_cast<float>(v1 * iv),
                           static_cast<float>(v2 * iv), static_cast<float>(4.0 * sp * sp));
       pr[4] = make_float4(klo, static_cast<float>(sp), static_cast<float>(cp), Fhi);
+      const double s4 = 4.0 * sp * sp, c4 = 4.0 * cp * cp;
+      const float s4h = static_cast<float>(s4), c4h = static_cast<float>(c4);
+      T.rowp[slot] = make_float4(s4h, static_cast<float>(s4 - s4h), c4h,
+                                 static_cast<float>(c4 - c4h));
     };
     if constexpr (!streamed) {
       for (int c = 0; c < ctx.n_classes; ++c) {
@@ -999,12 +1059,21 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
         G.sync();
 #ifndef GOSMA_PREP_ONLY
         const ClassSpan loc{0, cs.n1, 0, cs.n2};
+        double dz = 0.0, xl, xu, xe;
         if (same) {
-          class_pairs<kG, true, true, true, kTail>(T, loc, lane, w, lb_self, lb_cross, ub_self,
-                                                   ub_cross, lb_err);
+          class_pairs<kG, true, false, true, kTail>(T, loc, lane, w, lb_self, dz, ub_self, dz,
+                                                    lb_err, dz);
+          cross_span<kG, true, kTail>(T, loc, lane, w, G, precise, xl, xu, xe);
         } else {
-          class_pairs<kG, false, true, true, kTail>(T, loc, lane, w, lb_self, lb_cross, ub_self,
-                                                    ub_cross, lb_err);
+          class_pairs<kG, false, false, true, kTail>(T, loc, lane, w, lb_self, dz, ub_self, dz,
+                                                     lb_err, dz);
+          cross_span<kG, false, kTail>(T, loc, lane, w, G, precise, xl, xu, xe);
+        }
+        // group totals, carried by lane 0 into the final group sums
+        if (lane == 0) {
+          lb_cross += xl;
+          ub_cross += xu;
+          lb_err += xe;
         }
 #endif
       }
@@ -1034,14 +1103,14 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
         su_self += static_cast<double>(w * dsu);
         G.sync();
         const ClassSpan loc{0, cs.n1, 0, cs.n2};
-        double dl = 0.0, du = 0.0;
+        double dz = 0.0;
 #ifndef GOSMA_PREP_ONLY
         if (same) {
-          class_pairs<kG, true, false, true, kTail>(T, loc, lane, w, sl_self, dl, su_self, du,
-                                                    se_self);
+          class_pairs<kG, true, false, true, kTail>(T, loc, lane, w, sl_self, dz, su_self, dz,
+                                                    se_self, dz);
         } else {
-          class_pairs<kG, false, false, true, kTail>(T, loc, lane, w, sl_self, dl, su_self, du,
-                                                     se_self);
+          class_pairs<kG, false, false, true, kTail>(T, loc, lane, w, sl_self, dz, su_self, dz,
+                                                     se_self, dz);
         }
 #endif
         for (int ch = 0; ch < 8; ++ch) {
@@ -1051,14 +1120,11 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
           double lcr = 0.0, ucr = 0.0, ecr = 0.0;
 #ifndef GOSMA_PREP_ONLY
           if (same) {
-            class_pairs<kG, true, true, false, kTail>(T, loc, lane, w, dl, lcr, du, ucr, ecr);
+            cross_span<kG, true, kTail>(T, loc, lane, w, G, precise, lcr, ucr, ecr);
           } else {
-            class_pairs<kG, false, true, false, kTail>(T, loc, lane, w, dl, lcr, du, ucr, ecr);
+            cross_span<kG, false, kTail>(T, loc, lane, w, G, precise, lcr, ucr, ecr);
           }
 #endif
-          lcr = G.sum(lcr);
-          ucr = G.sum(ucr);
-          ecr = G.sum(ecr);
           if (lane == 0) {
             acc[3 * ch] += lcr;
             acc[3 * ch + 1] += ucr;
@@ -1121,12 +1187,13 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
         for (int c = 0; c < ctx.n_classes; ++c) {
           const ClassSpan cs = ctx.cls[c];
           const float w = static_cast<float>(ctx.cls_w[c]);
-          double dl = 0.0, du = 0.0;
+          double dz = 0.0;
           if (same) {
-            class_pairs<kG, true, false, true, kTail>(T, cs, lane, w, sl_self, dl, su_self, du, se_self);
+            class_pairs<kG, true, false, true, kTail>(T, cs, lane, w, sl_self, dz, su_self, dz,
+                                                      se_self, dz);
           } else {
-            class_pairs<kG, false, false, true, kTail>(T, cs, lane, w, sl_self, dl, su_self, du,
-                                                se_self);
+            class_pairs<kG, false, false, true, kTail>(T, cs, lane, w, sl_self, dz, su_self, dz,
+                                                       se_self, dz);
           }
         }
         sl_self = G.sum(sl_self);
@@ -1156,19 +1223,20 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
         G.sync();
         column_prep(T, ctx, lane, kG, Rcs + 9 * ch);
         G.sync();
-        double lcr = 0.0, ucr = 0.0, ecr = 0.0, dl = 0.0, du = 0.0;
+        double lcr = 0.0, ucr = 0.0, ecr = 0.0;
         for (int c = 0; c < ctx.n_classes; ++c) {
           const ClassSpan cs = ctx.cls[c];
           const float w = static_cast<float>(ctx.cls_w[c]);
+          double xl, xu, xe;
           if (same) {
-            class_pairs<kG, true, true, false, kTail>(T, cs, lane, w, dl, lcr, du, ucr, ecr);
+            cross_span<kG, true, kTail>(T, cs, lane, w, G, precise, xl, xu, xe);
           } else {
-            class_pairs<kG, false, true, false, kTail>(T, cs, lane, w, dl, lcr, du, ucr, ecr);
+            cross_span<kG, false, kTail>(T, cs, lane, w, G, precise, xl, xu, xe);
           }
+          lcr += xl;
+          ucr += xu;
+          ecr += xe;
         }
-        lcr = G.sum(lcr);
-        ucr = G.sum(ucr);
-        ecr = G.sum(ecr);
         if (lane == 0) {
           const double mass = sl_self + 2.0 * lcr;
           const double core = (sl_self - 2.0 * lcr) - ctx.lb_err_scale * (se_self + ecr) -
@@ -1215,17 +1283,31 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
 
     // ---- pair sweeps (GOSMA_PREP_ONLY: times the per-node prep alone)
 #ifndef GOSMA_PREP_ONLY
+    double xl_tot = 0.0, xu_tot = 0.0, xe_tot = 0.0;  // cross sums: group totals
     for (int c = 0; !streamed && c < ctx.n_classes; ++c) {
       const ClassSpan cs = ctx.cls[c];
       const float w = static_cast<float>(ctx.cls_w[c]);
       constexpr bool kC = kMode != kSelfOnly, kS = kMode != kCrossCached;
+      double dz = 0.0, xl = 0.0, xu = 0.0, xe = 0.0;
       if (same) {
-        class_pairs<kG, true, kC, kS, kTail>(T, cs, lane, w, lb_self, lb_cross, ub_self, ub_cross,
-                                      lb_err);
+        if (kS)
+          class_pairs<kG, true, false, true, kTail>(T, cs, lane, w, lb_self, dz, ub_self, dz,
+                                                    lb_err, dz);
+        if (kC) cross_span<kG, true, kTail>(T, cs, lane, w, G, precise, xl, xu, xe);
       } else {
-        class_pairs<kG, false, kC, kS, kTail>(T, cs, lane, w, lb_self, lb_cross, ub_self, ub_cross,
-                                       lb_err);
+        if (kS)
+          class_pairs<kG, false, false, true, kTail>(T, cs, lane, w, lb_self, dz, ub_self, dz,
+                                                     lb_err, dz);
+        if (kC) cross_span<kG, false, kTail>(T, cs, lane, w, G, precise, xl, xu, xe);
       }
+      xl_tot += xl;
+      xu_tot += xu;
+      xe_tot += xe;
+    }
+    if (lane == 0) {  // lane 0 carries the group totals into the sums below
+      lb_cross += xl_tot;
+      ub_cross += xu_tot;
+      lb_err += xe_tot;
     }
 #endif
     lb_self = G.sum(lb_self);
@@ -1271,7 +1353,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
 size_t eval_smem_per_warp(const DevCtx& ctx, int mode) {
   const bool streamed = mode == kModeStream || mode == kSiblingsStream;
   const int n1 = streamed ? ctx.max_n1 : ctx.n1_total, n2 = streamed ? ctx.max_n2 : ctx.n2_total;
-  size_t f4 = static_cast<size_t>(kRowF4 * n1 + kColF4 * n2);
+  size_t f4 = static_cast<size_t>((kRowF4 + kRowPF4) * n1 + kColF4 * n2);
   if (mode == kSiblings || mode == kSiblingsStream) f4 += kSibStreamExtraF4;
   return f4 * sizeof(float4);
 }

@@ -114,6 +114,11 @@ int ctx_upload(gosma_ctx* ctx) {
   d.lb_margin = ctx->lb_margin;
   d.lb_err_scale = 1.0;
   d.tail_chunks = 0;
+  static const bool precise_off = [] {  // GOSMA_PRECISE=0: FP32 pass only (A/B)
+    const char* e = std::getenv("GOSMA_PRECISE");
+    return e && std::string(e) == "0";
+  }();
+  d.precise = precise_off ? 0 : 1;
   for (const ClassSpan& cs : spans)
     if (cs.n1 % 32 != 0 && cs.n1 % 32 <= 16) d.tail_chunks = 1;
   ClassSpan* dspans;

@@ -48,6 +48,7 @@ struct DevCtx {
   int tail_chunks;       // some class has a last row chunk of <= 16 of 32 rows
   int max_n2;            // largest class n2
   int stream_classes;    // full mode keeps one class's table at a time (n_classes > 1)
+  int precise;           // precise cross pass for nodes whose FP32 error estimate is large
 };
 
 // Host-side master copy of one class (ClassData, objective.hpp:19-31).

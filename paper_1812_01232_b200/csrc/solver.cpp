@@ -558,6 +558,12 @@ int solver_init(gosma_solver* S) {
   const bool unit_measure = !(total_volume > 0.0);
   if (unit_measure) total_volume = static_cast<double>(S->dom.boxes.size());
   S->total_volume = total_volume;
+  // Every rank evaluates all feasible roots and runs the full discovery dive
+  // (identical, deterministic work: every rank starts from the same d*);
+  // with world > 1 the roots are then expanded deterministically to >= 8 x SMs
+  // nodes and rank r keeps nodes r, r + world, .... Volumes and
+  // evaluations of the replicated work are booked on rank 0 only.
+  const bool book = S->rank == 0;
   std::vector<gosma_node> roots;
   std::vector<double> root_vol;
   bool any_feasible = false;
@@ -574,11 +580,10 @@ int solver_init(gosma_solver* S) {
     const double v = unit_measure ? 1.0 : volume_of(n);
     const bool feas = feasible_box(m, b.c, b.h);
     any_feasible = any_feasible || feas;
-    if (static_cast<int>(k % S->world) != S->rank) continue;
     if (feas) {
       roots.push_back(n);
       root_vol.push_back(v);
-    } else {
+    } else if (book) {
       S->pruned_volume += v;
     }
   }
@@ -626,10 +631,10 @@ int solver_init(gosma_solver* S) {
   int rc = eval_host(ctx, roots, kInf, &lo, &up, &sp);
   if (rc != GOSMA_OK) return rc;
   mark("roots");
-  S->evals += roots.size();
+  unsigned long long evals = roots.size();
   if (cfg.discovery_dive) {
     const auto t0 = std::chrono::steady_clock::now();
-    rc = discovery_dive(ctx, S->dom, roots, cfg, &S->inc, &S->evals, 0.0);
+    rc = discovery_dive(ctx, S->dom, roots, cfg, &S->inc, &evals, 0.0);
     if (rc != GOSMA_OK) return rc;
     S->phase[7] += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   }
@@ -639,27 +644,71 @@ int solver_init(gosma_solver* S) {
                                     GOSMA_OK)
       return rc;
   mark("improve");
+  // route the wave's nodes (solver.cpp:396-405); returns the ones to keep
   std::vector<gosma_node> keep;
   std::vector<int8_t> ks;
   std::vector<double> kv;
-  for (size_t i = 0; i < roots.size(); ++i) {
-    gosma_node b = roots[i];
-    b.lower = lo[i];
-    if (!(b.lower < S->dstar())) {
-      S->pruned_volume += root_vol[i];
-    } else if (!splittable(b)) {
-      // resolved: FP64 bound, so zero-size domains certify exactly
-      const double l64 = lower_bound_fp64(m, Vec3(b.rc[0], b.rc[1], b.rc[2]), b.rhw,
-                                          Vec3(b.tc[0], b.tc[1], b.tc[2]),
-                                          Vec3(b.thw[0], b.thw[1], b.thw[2]), -kInf);
-      S->resolved_volume += root_vol[i];
-      S->floor_lower = std::min(S->floor_lower, std::max(l64, b.lower));
-    } else {
-      keep.push_back(b);
-      ks.push_back(sp[i]);
-      kv.push_back(root_vol[i]);
+  auto route_host = [&](const std::vector<gosma_node>& nodes, const std::vector<double>& vols) {
+    keep.clear();
+    ks.clear();
+    kv.clear();
+    for (size_t i = 0; i < nodes.size(); ++i) {
+      gosma_node b = nodes[i];
+      b.lower = lo[i];
+      if (!(b.lower < S->dstar())) {
+        if (book) S->pruned_volume += vols[i];
+      } else if (!splittable(b)) {
+        // resolved: FP64 bound, so zero-size domains certify exactly
+        const double l64 = lower_bound_fp64(m, Vec3(b.rc[0], b.rc[1], b.rc[2]), b.rhw,
+                                            Vec3(b.tc[0], b.tc[1], b.tc[2]),
+                                            Vec3(b.thw[0], b.thw[1], b.thw[2]), -kInf);
+        if (book) S->resolved_volume += vols[i];
+        S->floor_lower = std::min(S->floor_lower, std::max(l64, b.lower));
+      } else {
+        keep.push_back(b);
+        ks.push_back(sp[i]);
+        kv.push_back(vols[i]);
+      }
     }
+  };
+  route_host(roots, root_vol);
+  if (S->world > 1) {
+    // deterministic breadth-first expansion (subdivide_adaptive with the
+    // kernel's split flags) until every rank gets a share, then stripe
+    const size_t target = std::max<size_t>(8 * static_cast<size_t>(ctx->sm_count),
+                                           256 * static_cast<size_t>(S->world));
+    while (!keep.empty() && keep.size() < target) {
+      std::vector<gosma_node> kids;
+      std::vector<double> kvol;
+      kids.reserve(8 * keep.size());
+      for (size_t i = 0; i < keep.size(); ++i)
+        for (int c = 0; c < 8; ++c) {
+          gosma_node k = child_of(keep[i], ks[i], c);
+          k.lower = keep[i].lower;
+          kids.push_back(k);
+          kvol.push_back(kv[i] / 8.0);
+        }
+      if ((rc = eval_host(ctx, kids, S->dstar(), &lo, &up, &sp)) != GOSMA_OK) return rc;
+      evals += kids.size();
+      for (size_t i = 0; i < kids.size(); ++i)
+        if (up[i] < S->inc.value &&
+            (rc = improve(m, S->dom, kids[i], &S->inc, S->sma_dev.get())) != GOSMA_OK)
+          return rc;
+      route_host(kids, kvol);
+    }
+    size_t out = 0;
+    for (size_t i = 0; i < keep.size(); ++i)
+      if (static_cast<int>(i % S->world) == S->rank) {
+        keep[out] = keep[i];
+        ks[out] = ks[i];
+        kv[out] = kv[i];
+        ++out;
+      }
+    keep.resize(out);
+    ks.resize(out);
+    kv.resize(out);
   }
+  if (book) S->evals += evals;
   if (!keep.empty() &&
       (e = S->F.upload(keep.data(), ks.data(), kv.data(), keep.size(), s)) != cudaSuccess)
     return cuda_error(e, "frontier upload");

@@ -1,18 +1,21 @@
 """Frontier-sharded branch-and-bound across GPUs.
 
-One process per GPU (torchrun), one ``ShardSolver`` per rank owning the
-translation roots rank, rank+world, ... Every wave:
+One process per GPU (torchrun), one ``ShardSolver`` per rank. Every rank runs
+wave 0 and the discovery dive on all roots (the same d* everywhere), expands
+the roots deterministically to >= 8 x SMs nodes and keeps every world-th
+(SURVEY.md §8(e)). Every wave:
 
-1. each rank reports {d*_local, min(frontier min, resolved floor)};
-2. one min-allreduce (NCCL over NVLink for CUDA tensors, gloo on CPU) gives the
-   global incumbent and the global frontier minimum;
-3. certified = max(prev, min(d*, global min)) (solver.cpp:626-627); the stop
+1. each rank contributes one 5-double record {d*_local, min(frontier min,
+   resolved floor), elapsed, live nodes, evaluations} to ONE tiny all-gather
+   (NCCL over NVLink for CUDA tensors, gloo on CPU); every rank reduces the
+   records identically (min, min, max, sum, sum);
+2. certified = max(prev, min(d*, global min)) (solver.cpp:626-627); the stop
    rules (solver.cpp:629-645) are evaluated identically on every rank;
-4. the global d* is pushed into every shard (it prunes there, soundly);
-5. each shard expands its best nodes below d* - eps;
-6. every ``rebalance_every`` waves the live-frontier sizes are all-gathered and,
-   when max/min exceeds ``imbalance``, donors hand their best nodes to
-   receivers (point-to-point, deterministic pairing).
+3. the global d* is pushed into every shard (it prunes there, soundly);
+4. each shard expands its best nodes below d* - eps;
+5. every ``rebalance_every`` waves, when the gathered live-frontier sizes
+   differ by more than ``imbalance``, donors hand their best nodes to
+   receivers (point-to-point, deterministic pairing; no extra collective).
 
 The shard interface (status / set_incumbent / expand / export / import_ /
 result) is duck-typed, so the exchange logic is tested on CPU with gloo and a
@@ -70,12 +73,16 @@ class Comm:
         return t.cpu().numpy()
 
     def allgather(self, value: float):
-        t = self._t([value])
+        return self.allgather_rows([value])[:, 0]
+
+    def allgather_rows(self, values):
+        """All ranks' equal-length records as a (world, len) array (one collective)."""
+        t = self._t(values)
         if self.world == 1:
-            return t.cpu().numpy()
-        out = [torch.empty_like(t) for _ in range(self.world)]
-        dist.all_gather(out, t, group=self.group)
-        return torch.cat(out).cpu().numpy()
+            return t.cpu().numpy().reshape(1, -1)
+        out = torch.empty(self.world * t.numel(), dtype=t.dtype, device=self.device)
+        dist.all_gather_into_tensor(out, t, group=self.group)
+        return out.cpu().numpy().reshape(self.world, -1)
 
     def send_array(self, arr: np.ndarray, dst: int):
         t = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float64)).to(self.device)
@@ -103,6 +110,10 @@ class Comm:
         if k:
             for t in (nodes, split, vol):
                 dist.recv(t, src, group=self.group)
+        if self.device.type == "cuda":
+            # NCCL receives are ordered on torch's current stream only; the
+            # solver's import copies on its own stream, so wait here
+            torch.cuda.current_stream(self.device).synchronize()
         return nodes, split, vol
 
     def recv_array(self, src: int, width: int) -> np.ndarray:
@@ -177,14 +188,15 @@ def solve_sharded(shard, epsilon: float, comm: Comm, time_limit: Optional[float]
     while True:
         st = shard.status()
         local_min = min(st["frontier_min"], st["floor_lower"])
-        mins = comm.allreduce([st["best_value"], local_min], "min")
-        dstar, gmin = float(mins[0]), float(mins[1])
-        sums = comm.allreduce([float(st["live_nodes"]), float(st["bound_evaluations"])], "sum")
-        live, evals = int(sums[0]), int(sums[1])
-        elapsed = float(comm.allreduce([time.perf_counter() - t0], "max")[0])
+        rows = comm.allgather_rows([st["best_value"], local_min, time.perf_counter() - t0,
+                                    float(st["live_nodes"]), float(st["bound_evaluations"])])
+        dstar, gmin = float(rows[:, 0].min()), float(rows[:, 1].min())
+        elapsed = float(rows[:, 2].max())
+        counts = rows[:, 3]
+        live, evals = int(counts.sum()), int(rows[:, 4].sum())
         certified = max(certified, min(dstar, gmin))
         if trace:
-            tr.append((wave, evals, dstar, certified, live))
+            tr.append((wave, evals, dstar, certified, live, elapsed))
         if dstar - certified <= epsilon:
             status = "epsilon_optimal"
             break
@@ -204,7 +216,7 @@ def solve_sharded(shard, epsilon: float, comm: Comm, time_limit: Optional[float]
         shard.expand(dstar - epsilon, budget)
         wave += 1
         if comm.world > 1 and rebalance_every > 0 and wave % rebalance_every == 0:
-            counts = comm.allgather(float(shard.status()["live_nodes"]))
+            # the sizes gathered at the top of this wave (no extra collective)
             device_path = comm.device.type == "cuda" and hasattr(shard, "export_device")
             for src, dst, n in plan_rebalance(counts, imbalance):
                 n = min(n, max_migrate)

@@ -464,3 +464,85 @@ def test_scene_gap_matches_reference(gosma):
     ang = math.acos(max(-1.0, min(1.0, (np.trace(dR) - 1.0) / 2.0)))
     assert ang <= 1e-4
     assert np.linalg.norm(np.asarray(r.t) - np.array(gold["t"])) <= 1e-4
+
+
+def _shard_worker(rank, world, port, inst, eps, rebalance_every, q):
+    """One rank of a world-2 sharded solve: a real ShardSolver on cuda:0, the
+    exchange over gloo (host tensors; both ranks share the box's one GPU, and
+    no kernel of one rank waits on the other's)."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch.distributed as dist
+    import paper_1812_01232_b200 as g
+    from paper_1812_01232_b200.distributed import Comm, solve_sharded
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        mix = Mixture.from_dict(inst["mixture"])
+        ctx = g.ObjectiveContext([{"mu": mix.mu, "sigma2": mix.sigma2, "phi1": mix.phi1,
+                                   "dir": mix.dir, "kappa2": mix.kappa2, "phi2": mix.phi2}],
+                                 mix.zeta, single_mixture=True)
+        dom = g.PoseDomain(np.array(inst["rot_c"]), inst["rot_hw"], np.array(inst["boxes"]))
+        cfg = g.SolverConfig(epsilon=eps, zeta=mix.zeta, wave_nodes=4096)
+        shard = g.ShardSolver(ctx, dom, cfg, rank, world)
+        rep = solve_sharded(shard, eps, Comm(), rebalance_every=rebalance_every,
+                            imbalance=1.2, max_migrate=2048, time_limit=120)
+        st = shard.status()
+        q.put((rank, rep.status, rep.best_value, rep.global_lower, list(rep.r), list(rep.t),
+               rep.migrated_nodes, st["pruned_volume"], st["resolved_volume"],
+               shard.live_volume(), st["total_volume"]))
+        del shard
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("rebalance_every", [1, 0])
+def test_two_real_shards_certify_the_single_gpu_optimum(gosma, rebalance_every):
+    """world = 2 with real ShardSolvers (deterministic root expansion, striped
+    ownership, one all-gather per wave, node migration through export/import):
+    the sharded solve certifies the same optimum as gosma_solve and the
+    reference (certify_golden.json), both ranks report the same result, and
+    the volume ledger summed over ranks is conserved after migration."""
+    import json
+    import socket
+    import torch.multiprocessing as mp
+    G = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "certify_golden.json")))
+    inst = max((i for i in G["instances"] if i.get("classes", 1) == 1),
+               key=lambda x: x["bound_evaluations"])
+    eps = inst["epsilon"]
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx_mp = mp.get_context("spawn")
+    q = ctx_mp.Queue()
+    procs = [ctx_mp.Process(target=_shard_worker, args=(r, 2, port, inst, eps, rebalance_every, q))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(300)
+        assert p.exitcode == 0
+    res = sorted(q.get(timeout=10) for _ in range(2))
+    mix = Mixture.from_dict(inst["mixture"])
+    ctx = gosma.ObjectiveContext([{"mu": mix.mu, "sigma2": mix.sigma2, "phi1": mix.phi1,
+                                   "dir": mix.dir, "kappa2": mix.kappa2, "phi2": mix.phi2}],
+                                 mix.zeta, single_mixture=True)
+    dom = gosma.PoseDomain(np.array(inst["rot_c"]), inst["rot_hw"], np.array(inst["boxes"]))
+    one = gosma.solve(ctx, dom, gosma.SolverConfig(epsilon=eps, zeta=mix.zeta, time_limit=60))
+    assert one.status == "epsilon_optimal"
+    for rank, status, best, lower, r, t, migrated, pv, rv, lv, tv in res:
+        assert status == "epsilon_optimal"
+        assert best - lower <= eps + 1e-12
+        assert abs(best - one.best_value) <= eps + 1e-9
+        assert abs(best - inst["best_value"]) <= eps + 1e-9
+        assert lower <= inst["best_value"] + 1e-9 and inst["global_lower"] <= best + 1e-9
+        # the published pose is the incumbent's
+        assert abs(gosma.objective_value(ctx, r, t) - best) <= 1e-9
+    assert res[0][1:4] == res[1][1:4]
+    total = res[0][10]
+    ledger = sum(x[7] + x[8] + x[9] for x in res)
+    assert abs(ledger - total) <= 1e-9 * total, (ledger, total)
+    if rebalance_every:
+        assert sum(x[6] for x in res) >= 0
