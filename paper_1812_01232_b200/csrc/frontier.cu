@@ -247,21 +247,23 @@ inline unsigned grid_cap(size_t n, unsigned block) {
 
 // Histogram of digit (key >> shift) & mask among keys < limit whose bits above
 // `prefix_shift` equal `prefix` (prefix_shift 64: no prefix).
-// With `inv` set the keys are ranked from the top: key' = limit - 1 - key
-// (the drain order, largest lower bounds first).
+// With `rank` set, the slots with key < limit are ranked by the bits of
+// rank[i] (a positive double: the node volume) instead of by their key (the
+// depth-first order, smallest volumes first).
 __global__ void digit_hist(const unsigned long long* key, const unsigned int* idx, size_t n,
                            unsigned long long limit, int shift, int bits,
                            unsigned long long prefix, int prefix_shift, unsigned int* hist,
-                           bool inv) {
+                           const double* rank) {
   __shared__ unsigned int sh[kBins];
   const int nb = 1 << bits;
   for (int b = threadIdx.x; b < nb; b += blockDim.x) sh[b] = 0;
   __syncthreads();
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<size_t>(gridDim.x) * blockDim.x) {
-    unsigned long long k = idx ? key[idx[i]] : key[i];
+    const size_t slot = idx ? idx[i] : i;
+    unsigned long long k = key[slot];
     if (k >= limit) continue;
-    if (inv) k = limit - 1 - k;
+    if (rank) k = __double_as_longlong(rank[slot]);
     if (prefix_shift < 64 && (k >> prefix_shift) != prefix) continue;
     atomicAdd(&sh[(k >> shift) & static_cast<unsigned long long>(nb - 1)], 1u);
   }
@@ -279,14 +281,14 @@ struct KeyBelow {
   }
 };
 
-// Drain order: key < limit with limit - 1 - key in [lo, hi).
-struct KeyTopRange {
+// Depth-first order: key < limit with the volume's bits in [lo, hi).
+struct VolRange {
   const unsigned long long* key;
+  const double* vol;
   unsigned long long lo, hi, limit;
   __device__ __forceinline__ bool operator()(const unsigned int& i) const {
-    const unsigned long long k = key[i];
-    if (k >= limit) return false;
-    const unsigned long long r = limit - 1 - k;
+    if (key[i] >= limit) return false;
+    const unsigned long long r = __double_as_longlong(vol[i]);
     return r >= lo && r < hi;
   }
 };
@@ -751,6 +753,7 @@ void Frontier::release() {
   pmin_cap = 0;
   dfree(rec);
   rec = nullptr;
+  rec_cap = 0;
   dfree(cand);
   dfree(cand_tmp);
   cand = cand_tmp = nullptr;
@@ -893,18 +896,18 @@ cudaError_t Frontier::min_key(cudaStream_t s, unsigned long long* out) {
 cudaError_t Frontier::descend(size_t want, unsigned long long limit, double fill, cudaStream_t s,
                               unsigned long long* lo, unsigned long long* hi, size_t* below_out,
                               size_t* bin_out, const unsigned int* idx, size_t n_items,
-                              bool inv) {
+                              const double* rank) {
   // Digit schedule over the 64-bit key: 12,12,12,12,12,4 bits.
   // Every live key lies in [known_min, limit): the digits start below their
   // common high bits (one 12-bit level usually resolves a wave).
   int pshift = 64;  // bits >= pshift are fixed to `prefix` (64: none)
   unsigned long long prefix = 0;
-  if (!inv && known_min > 0 && known_min < limit) {
+  if (!rank && known_min > 0 && known_min < limit) {
     const unsigned long long x = known_min ^ (limit - 1);
     pshift = std::max(12, x ? 64 - __builtin_clzll(x) : 0);
     prefix = pshift >= 64 ? 0ull : (known_min >> pshift);
   }
-  unsigned long long lo_key = 0, hi_key = limit;
+  unsigned long long lo_key = 0, hi_key = rank ? kHoleKey : limit;
   size_t below = 0;  // count of keys < lo_key
   size_t bin = 0;    // count of keys in [lo_key, hi_key)
   cudaError_t e;
@@ -913,7 +916,7 @@ cudaError_t Frontier::descend(size_t want, unsigned long long limit, double fill
     const int shift = pshift - bits;
     if ((e = cudaMemsetAsync(hist, 0, kBins * 4, s)) != cudaSuccess) return e;
     digit_hist<<<grid_cap(n_items, 256), 256, 0, s>>>(key, idx, n_items, limit, shift, bits,
-                                                      prefix, pshift, hist, inv);
+                                                      prefix, pshift, hist, rank);
     const int nb = 1 << bits;
     if ((e = cudaMemcpyAsync(h_hist.data(), hist, nb * 4, cudaMemcpyDeviceToHost, s)) !=
         cudaSuccess)
@@ -926,9 +929,10 @@ cudaError_t Frontier::descend(size_t want, unsigned long long limit, double fill
       if (cum + h_hist[b] > want) break;
       cum += h_hist[b];
     }
+    const unsigned long long cap = rank ? kHoleKey : limit;  // ranked values are not keys
     if (b == nb) {  // everything under this prefix fits
       const unsigned long long end = pshift >= 64 ? 0ull : base + (1ull << pshift);
-      lo_key = hi_key = (end == 0 || end > limit) ? limit : end;
+      lo_key = hi_key = (end == 0 || end > cap) ? cap : end;
       below = cum;
       bin = 0;
       break;
@@ -936,7 +940,7 @@ cudaError_t Frontier::descend(size_t want, unsigned long long limit, double fill
     bin = h_hist[b];
     lo_key = base + (static_cast<unsigned long long>(b) << shift);
     const unsigned long long end = lo_key + (1ull << shift);
-    hi_key = (end == 0 || end > limit) ? limit : end;
+    hi_key = (end == 0 || end > cap) ? cap : end;
     below = cum;
     if (static_cast<double>(below) >= fill * static_cast<double>(want) || shift == 0) break;
     prefix = (pshift >= 64 ? 0ull : (prefix << bits)) | static_cast<unsigned long long>(b);
@@ -962,7 +966,7 @@ cudaError_t Frontier::rebuild_candidates(size_t want_total, cudaStream_t s) {
   }
   unsigned long long lo = 0, hi = kHoleKey;
   size_t below = 0, bin = 0;
-  cudaError_t e = descend(want_total, kHoleKey, 0.5, s, &lo, &hi, &below, &bin, nullptr, size, false);
+  cudaError_t e = descend(want_total, kHoleKey, 0.5, s, &lo, &hi, &below, &bin, nullptr, size, nullptr);
   if (e != cudaSuccess) return e;
   const unsigned long long t = below > 0 ? lo : hi;  // massive ties: keep the boundary bin
   const size_t count = below > 0 ? below : bin;
@@ -1026,7 +1030,7 @@ cudaError_t Frontier::select_smallest(size_t want, unsigned long long limit, cud
       lo_key = hi_key = limit;
       below = bin_count = 0;
     } else if ((e = descend(want, limit, 0.5, s, &lo_key, &hi_key, &below, &bin_count, cand,
-                            cand_n, false)) != cudaSuccess) {
+                            cand_n, nullptr)) != cudaSuccess) {
       return e;
     }
     // too few candidates below the limit while the pool may hold more: refill
@@ -1087,26 +1091,26 @@ cudaError_t Frontier::select_smallest(size_t want, unsigned long long limit, cud
   return cudaGetLastError();
 }
 
-// Drain order (memory pressure): the `want` live nodes with the LARGEST keys
-// below `limit`, i.e. the nodes nearest to being pruned, whose subtrees are
-// the shallowest. Every node below d* - eps has to be expanded before the gap
-// closes whatever the order, so expanding these first changes neither the
-// work nor the certified result, only the pool's peak size. Full-pool radix
-// descent on inverted keys (no candidate list).
-cudaError_t Frontier::select_largest(size_t want, unsigned long long limit, cudaStream_t s,
+// Depth-first order (memory pressure): the `want` live nodes below `limit`
+// with the SMALLEST volumes, i.e. the deepest. Every node below d* - eps has
+// to be expanded before the gap closes whatever the order (children's bounds
+// are max(core, parent)), so the order changes neither the work nor the
+// certificate, only the pool's peak size: depth-first keeps ~(8 W x depth)
+// nodes open. Full-pool radix descent on the volume bits (no candidate list).
+cudaError_t Frontier::select_deepest(size_t want, unsigned long long limit, cudaStream_t s,
                                      size_t* n_out) {
   *n_out = 0;
   if (size == 0 || want == 0) return cudaSuccess;
   want = std::min(want, sel_cap);
   cudaError_t e;
-  unsigned long long lo_key = 0, hi_key = limit;
+  unsigned long long lo_key = 0, hi_key = kHoleKey;
   size_t below = 0, bin_count = 0;
   if ((e = descend(want, limit, 0.5, s, &lo_key, &hi_key, &below, &bin_count, nullptr, size,
-                   true)) != cudaSuccess)
+                   vol)) != cudaSuccess)
     return e;
   cub::CountingInputIterator<unsigned int> it(0);
   size_t need = 0;
-  KeyTopRange p1{key, 0ull, lo_key, limit};
+  VolRange p1{key, vol, 0ull, lo_key, limit};
   cub::DeviceSelect::If(nullptr, need, it, sel, counter, static_cast<int>(size), p1, s);
   if ((e = ensure_temp(need)) != cudaSuccess) return e;
   const size_t n1 = below;
@@ -1121,7 +1125,7 @@ cudaError_t Frontier::select_largest(size_t want, unsigned long long limit, cuda
       if ((e = dmalloc(&bsel, c * 4)) != cudaSuccess) return e;
       bsel_cap = c;
     }
-    KeyTopRange p2{key, lo_key, hi_key, limit};
+    VolRange p2{key, vol, lo_key, hi_key, limit};
     cub::DeviceSelect::If(temp, need, it, bsel, counter, static_cast<int>(size), p2, s);
     if ((e = cudaMemcpyAsync(sel + n1, bsel, n2 * 4, cudaMemcpyDeviceToDevice, s)) != cudaSuccess)
       return e;
@@ -1213,7 +1217,6 @@ cudaError_t Frontier::expand_selected_cached(size_t n_sel, cudaStream_t s, size_
 
 cudaError_t Frontier::improving_children(size_t n_kids, double bound, cudaStream_t s,
                                          std::vector<ImprovingChild>* out) {
-  constexpr unsigned kRecCap = 4096;
   out->clear();
   if (n_kids == 0) return cudaSuccess;
   cudaError_t e = cudaSuccess;
@@ -1224,7 +1227,10 @@ cudaError_t Frontier::improving_children(size_t n_kids, double bound, cudaStream
     if ((e = dmalloc(&kid_pmin, kid_cap * sizeof(double))) != cudaSuccess) return e;
     pmin_cap = kid_cap;
   }
-  if (!rec && (e = dmalloc(&rec, kRecCap * sizeof(ImprovingChild))) != cudaSuccess) return e;
+  if (!rec) {
+    if ((e = dmalloc(&rec, 4096 * sizeof(ImprovingChild))) != cudaSuccess) return e;
+    rec_cap = 4096;
+  }
   size_t bytes = 0;
   cub::DeviceScan::ExclusiveScan(nullptr, bytes, kid_upper, kid_pmin, MinOp(), bound,
                                  static_cast<int>(n_kids), s);
@@ -1233,14 +1239,25 @@ cudaError_t Frontier::improving_children(size_t n_kids, double bound, cudaStream
   if ((e = cub::DeviceScan::ExclusiveScan(temp, bytes, kid_upper, kid_pmin, MinOp(), bound,
                                           static_cast<int>(n_kids), s)) != cudaSuccess)
     return e;
-  if ((e = cudaMemsetAsync(counter, 0, sizeof(unsigned long long), s)) != cudaSuccess) return e;
-  flag_records<<<grid_cap(n_kids, 256), 256, 0, s>>>(kid_upper, kid_pmin, n_kids, rec, counter,
-                                                     kRecCap);
-  if ((e = cudaMemcpyAsync(h_counter, counter, sizeof(unsigned long long),
-                           cudaMemcpyDeviceToHost, s)) != cudaSuccess)
-    return e;
-  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
-  const size_t m = std::min<size_t>(*h_counter, kRecCap);
+  // every record is kept (the list grows and the flags are re-run when a wave
+  // has more than fit), so the replay below is the reference's in-order one
+  for (int pass = 0; pass < 2; ++pass) {
+    if ((e = cudaMemsetAsync(counter, 0, sizeof(unsigned long long), s)) != cudaSuccess) return e;
+    flag_records<<<grid_cap(n_kids, 256), 256, 0, s>>>(kid_upper, kid_pmin, n_kids, rec, counter,
+                                                       static_cast<unsigned>(rec_cap));
+    if ((e = cudaMemcpyAsync(h_counter, counter, sizeof(unsigned long long),
+                             cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+      return e;
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+    if (*h_counter <= rec_cap) break;
+    dfree(rec);
+    rec = nullptr;
+    rec_cap = 0;
+    const size_t c = static_cast<size_t>(*h_counter) * 2;
+    if ((e = dmalloc(&rec, c * sizeof(ImprovingChild))) != cudaSuccess) return e;
+    rec_cap = c;
+  }
+  const size_t m = std::min<size_t>(*h_counter, rec_cap);
   out->resize(m);
   if (m && (e = cudaMemcpy(out->data(), rec, m * sizeof(ImprovingChild),
                            cudaMemcpyDeviceToHost)) != cudaSuccess)
@@ -1381,7 +1398,7 @@ cudaError_t Frontier::fold_to(size_t keep_n, cudaStream_t s, double* folded_volu
   if (e != cudaSuccess || size <= keep_n) return e;
   unsigned long long lo = 0, hi = kHoleKey;
   size_t below = 0;
-  if ((e = descend(keep_n, kHoleKey, 0.9, s, &lo, &hi, &below, nullptr, nullptr, size, false)) !=
+  if ((e = descend(keep_n, kHoleKey, 0.9, s, &lo, &hi, &below, nullptr, nullptr, size, nullptr)) !=
       cudaSuccess)
     return e;
   // fold every key >= tau; with massive ties below the first boundary keep the bin

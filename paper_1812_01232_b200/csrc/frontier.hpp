@@ -106,11 +106,11 @@ struct Frontier {
   // their indices to sel, marks them holes, returns the count.
   cudaError_t descend(size_t want, unsigned long long limit, double fill, cudaStream_t s,
                       unsigned long long* lo, unsigned long long* hi, size_t* below,
-                      size_t* bin, const unsigned int* idx, size_t n_items, bool inv);
+                      size_t* bin, const unsigned int* idx, size_t n_items, const double* rank);
   cudaError_t rebuild_candidates(size_t want_total, cudaStream_t s);
   cudaError_t select_smallest(size_t want, unsigned long long limit, cudaStream_t s, size_t* n);
-  // drain order under memory pressure: the largest keys below limit
-  cudaError_t select_largest(size_t want, unsigned long long limit, cudaStream_t s, size_t* n);
+  // depth-first order under memory pressure: the smallest volumes below limit
+  cudaError_t select_deepest(size_t want, unsigned long long limit, cudaStream_t s, size_t* n);
   cudaError_t expand_selected(size_t n_sel, cudaStream_t s);
   cudaError_t expand_selected_cached(size_t n_sel, cudaStream_t s, size_t* n_cuboids);
   // rotation-split selections (rot_list) and translation-split children (trans_list)
@@ -130,7 +130,8 @@ struct Frontier {
                                  std::vector<ImprovingChild>* out);
   double* kid_pmin = nullptr;  // exclusive prefix minimum of kid_upper
   size_t pmin_cap = 0;
-  ImprovingChild* rec = nullptr;  // device record list (kRecCap)
+  ImprovingChild* rec = nullptr;  // device record list (rec_cap entries, grown on demand)
+  size_t rec_cap = 0;
   // route children against d*, append survivors
   cudaError_t route_append(size_t n_kids, double dstar, cudaStream_t s, RouteStats* out);
   // drop holes and nodes with key >= limit; returns the dropped (non-hole) volume

@@ -1,195 +1,155 @@
 // Host FP64 objective, gradient and geometry: the thin host side of the
-// path (north star (4)) used by the local refiner (SMA), the incumbent
-// re-evaluation and gosma_objective_value. Follows the reference formulas:
-// sphere_stats.cpp:47-69 (log Z, its derivative), se3.cpp:21-31 (Rodrigues),
-// objective.cpp:160-334 (value, gradient).
+// path (north star (4)) used by the host refiner, the incumbent
+// re-evaluation and gosma_objective_value. The objective and gradient are the
+// GPU evaluator's formulation (objective_math.hpp) run serially, so host and
+// device agree to FP64 summation order.
 #include "host_math.hpp"
+
+#include "objective_math.hpp"
 
 #include <algorithm>
 #include <cmath>
 
 namespace gosma {
 
-double log_z_eval(double kappa) {
-  // sphere_stats.cpp:47-56
-  if (kappa < 1e-4) return std::log(2.0) + std::log1p(kappa * kappa / 6.0);
-  return kappa + std::log1p(-std::exp(-2.0 * kappa)) - std::log(kappa);
-}
+double log_z_eval(double kappa) { return objmath::log_z_d(kappa); }
 
-double log_z_deriv(double kappa) {
-  // sphere_stats.cpp:58-69
-  if (kappa < 1e-4) return kappa / 3.0 - kappa * kappa * kappa / 45.0;
-  if (kappa > 350.0) return 1.0 - 1.0 / kappa;
-  const double e2 = std::exp(-2.0 * kappa);
-  return (1.0 + e2) / (1.0 - e2) - 1.0 / kappa;
-}
+double log_z_deriv(double kappa) { return objmath::log_z_deriv_d(kappa); }
 
 Mat3 rotation_matrix(const Vec3& r) {
-  // se3.cpp:21-31
-  const double theta2 = r.dot(r);
-  const Mat3 K = Mat3::skew(r);
-  const Mat3 K2 = K * K;
-  double a, c;
-  if (theta2 < 1e-16) {
-    a = 1.0;
-    c = 0.5;
-  } else {
-    const double theta = std::sqrt(theta2);
-    a = std::sin(theta) / theta;
-    c = (1.0 - std::cos(theta)) / theta2;
-  }
   Mat3 R;
-  for (int i = 0; i < 9; ++i) R.m[i] = ((i % 4 == 0 ? 1.0 : 0.0) + a * K.m[i]) + c * K2.m[i];
+  objmath::rotation_and_jacobian(r[0], r[1], r[2], R.m, nullptr);
   return R;
 }
 
 Vec3 wrap_rotation_vector(const Vec3& r) {
-  // se3.cpp:50-58
+  // the same rotation with |r| <= pi
   Vec3 w = r;
-  double n = w.norm();
-  while (n > M_PI) {
-    w = w * (1.0 - 2.0 * M_PI / n);
-    n = w.norm();
-  }
+  for (double n = w.norm(); n > M_PI; n = w.norm()) w = w * (1.0 - 2.0 * M_PI / n);
   return w;
 }
 
 bool pose_feasible(const HostModel& model, const Vec3& t) {
-  // check_feasible, objective.cpp:160-166
-  for (const Vec3& mu : model.all_means) {
+  // camera centre outside every standoff ball (objective.cpp:160-166)
+  for (const Vec3& mu : model.all_means)
     if ((mu - t).norm() < model.zeta) return false;
-  }
   return true;
 }
 
 namespace {
 
-constexpr double kMargin = 64.0;  // objective.cpp:17
-
-double class_objective(const HostClass& cls, const Mat3& R, const Vec3& t) {
-  // class_objective + project_model, objective.cpp:175-223
-  const int n1 = cls.n1(), n2 = cls.n2();
-  std::vector<Vec3> v(n1);
-  std::vector<double> kap(n1), lz(n1);
-  for (int i = 0; i < n1; ++i) {
-    const Vec3 u = Vec3(cls.mu[3 * i], cls.mu[3 * i + 1], cls.mu[3 * i + 2]) - t;
-    const double d2 = u.dot(u);
-    const double d = std::sqrt(d2);
-    kap[i] = d2 / cls.sigma2[i] + 1.0;
-    v[i] = u * (kap[i] / d);
-    lz[i] = log_z_eval(kap[i]);
-  }
-  double self_sum = 0.0;
-  for (int i = 0; i < n1; ++i) {
-    self_sum += cls.phi1[i] * cls.phi1[i] * 0.5 * kap[i] / std::tanh(kap[i]);
-    for (int j = i + 1; j < n1; ++j) {
-      const double K = (v[i] + v[j]).norm();
-      if (K < kap[i] + kap[j] - kMargin) continue;
-      self_sum += 2.0 * cls.phi1[i] * cls.phi1[j] * std::exp(log_z_eval(K) - lz[i] - lz[j]);
+// The objective (and optionally its gradient) at x = (r, t) in the GPU
+// evaluator's formulation (objective_math.hpp; objgrad_block in
+// objective_kernel.cu with one partner slice): per class, rows of
+// (u_i, d_i, k_i, log Z, log Z'), the closed-form diagonal, ordered self pairs
+// i != j each adding half of the pair, cross pairs against the rotated rows;
+// gradients accumulated as vectors and mapped by J_i (jv) and Jl^T.
+double evaluate(const HostModel& model, const Vec3& r, const Vec3& t, double* grad) {
+  double R[9], Jl[9];
+  objmath::rotation_and_jacobian(r[0], r[1], r[2], R, grad ? Jl : nullptr);
+  double f = 0.0, gt[3] = {0.0, 0.0, 0.0}, cr[3] = {0.0, 0.0, 0.0};
+  std::vector<objmath::RowD> rows;
+  for (const HostClass& cls : model.classes) {
+    const double w = cls.weight;
+    const int n1 = cls.n1(), n2 = cls.n2();
+    rows.resize(n1);
+    for (int i = 0; i < n1; ++i)
+      rows[i] = objmath::make_row(cls.mu[3 * i], cls.mu[3 * i + 1], cls.mu[3 * i + 2],
+                                  cls.sigma2[i], cls.phi1[i], t[0], t[1], t[2]);
+    for (int i = 0; i < n1; ++i) {
+      const objmath::RowD& a = rows[i];
+      const double ui[3] = {a.ux * a.d, a.uy * a.d, a.uz * a.d};
+      const double vi[3] = {a.ux * a.k, a.uy * a.k, a.uz * a.k};
+      const double cu = 2.0 * a.zl * a.is2;
+      const double diag = 0.5 * a.k / std::tanh(a.k);
+      double fself = a.phi * a.phi * diag, fcross = 0.0;
+      double s[3] = {0.0, 0.0, 0.0}, su = 0.0, h[3] = {0.0, 0.0, 0.0}, hu = 0.0;
+      if (grad) {
+        const double sd = a.phi * a.phi * diag * 2.0 * (objmath::log_z_deriv_d(2.0 * a.k) - a.zl) *
+                          (-2.0 * a.is2);
+        for (int k = 0; k < 3; ++k) gt[k] += w * ui[k] * sd;
+      }
+      for (int j = 0; j < n1; ++j) {  // self pairs, this row's half
+        if (j == i) continue;
+        const objmath::RowD& b = rows[j];
+        const double e[3] = {vi[0] + b.ux * b.k, vi[1] + b.uy * b.k, vi[2] + b.uz * b.k};
+        const double K = std::sqrt(e[0] * e[0] + e[1] * e[1] + e[2] * e[2]);
+        if (K < a.k + b.k - objmath::kNegligible) continue;
+        double eK, zl;
+        objmath::pair_terms(K, a.lz + b.lz, eK, zl);
+        const double term = 2.0 * a.phi * b.phi * eK;
+        fself += 0.5 * term;
+        if (grad) {
+          if (K > 1e-12)
+            for (int k = 0; k < 3; ++k) s[k] += e[k] * (zl * term / K);
+          su += term;
+        }
+      }
+      const double wv[3] = {R[0] * vi[0] + R[1] * vi[1] + R[2] * vi[2],
+                            R[3] * vi[0] + R[4] * vi[1] + R[5] * vi[2],
+                            R[6] * vi[0] + R[7] * vi[1] + R[8] * vi[2]};
+      for (int j = 0; j < n2; ++j) {  // cross pairs
+        const double e[3] = {wv[0] + cls.b[3 * j], wv[1] + cls.b[3 * j + 1],
+                             wv[2] + cls.b[3 * j + 2]};
+        const double K = std::sqrt(e[0] * e[0] + e[1] * e[1] + e[2] * e[2]);
+        if (K < a.k + cls.kappa2[j] - objmath::kNegligible) continue;
+        double eK, zl;
+        objmath::pair_terms(K, a.lz + cls.log_z2[j], eK, zl);
+        const double term = a.phi * cls.phi2[j] * eK;
+        fcross += term;
+        if (grad) {
+          double q[3] = {0.0, 0.0, 0.0};
+          if (K > 1e-12)
+            for (int k = 0; k < 3; ++k) q[k] = e[k] / K;
+          const double sc = zl * (-2.0 * term);
+          for (int k = 0; k < 3; ++k) h[k] += q[k] * sc;
+          hu += -2.0 * term;
+          cr[0] += w * (wv[1] * q[2] - wv[2] * q[1]) * sc;
+          cr[1] += w * (wv[2] * q[0] - wv[0] * q[2]) * sc;
+          cr[2] += w * (wv[0] * q[1] - wv[1] * q[0]) * sc;
+        }
+      }
+      if (grad) {
+        double o[3];
+        objmath::jv(a, s[0], s[1], s[2], o[0], o[1], o[2]);
+        for (int k = 0; k < 3; ++k) gt[k] += w * (o[k] + ui[k] * cu * su);
+        const double p[3] = {R[0] * h[0] + R[3] * h[1] + R[6] * h[2],  // R^T h
+                             R[1] * h[0] + R[4] * h[1] + R[7] * h[2],
+                             R[2] * h[0] + R[5] * h[1] + R[8] * h[2]};
+        objmath::jv(a, p[0], p[1], p[2], o[0], o[1], o[2]);
+        for (int k = 0; k < 3; ++k) gt[k] += w * (o[k] + ui[k] * cu * hu);
+      }
+      f += w * (fself - 2.0 * fcross);
     }
   }
-  double cross_sum = 0.0;
-  for (int i = 0; i < n1; ++i) {
-    const Vec3 w = R * v[i];
-    for (int j = 0; j < n2; ++j) {
-      const double K = (w + Vec3(cls.b[3 * j], cls.b[3 * j + 1], cls.b[3 * j + 2])).norm();
-      if (K < kap[i] + cls.kappa2[j] - kMargin) continue;
-      cross_sum +=
-          cls.phi1[i] * cls.phi2[j] * std::exp(log_z_eval(K) - lz[i] - cls.log_z2[j]);
-    }
+  if (grad) {
+    for (int k = 0; k < 3; ++k) grad[k] = Jl[k] * cr[0] + Jl[3 + k] * cr[1] + Jl[6 + k] * cr[2];
+    for (int k = 0; k < 3; ++k) grad[3 + k] = gt[k];
   }
-  return self_sum - 2.0 * cross_sum;
-}
-
-Mat3 left_jacobian(const Vec3& r) {
-  // objective.cpp:240-250
-  const double theta2 = r.dot(r);
-  const Mat3 K = Mat3::skew(r);
-  const Mat3 K2 = K * K;
-  if (theta2 < 1e-12) return Mat3::identity() + K * 0.5 + K2 * (1.0 / 6.0);
-  const double theta = std::sqrt(theta2);
-  return Mat3::identity() + K * ((1.0 - std::cos(theta)) / theta2) +
-         K2 * ((theta - std::sin(theta)) / (theta2 * theta));
+  return f;
 }
 
 }  // namespace
 
 double objective_value(const HostModel& model, const Vec3& r, const Vec3& t) {
-  // objective.cpp:227-235 (+inf in place of InfeasiblePoseError)
+  // +inf in place of the reference's InfeasiblePoseError
   if (!pose_feasible(model, t)) return INFINITY;
-  const Mat3 R = rotation_matrix(r);
-  double f = 0.0;
-  for (const HostClass& cls : model.classes) f += cls.weight * class_objective(cls, R, t);
-  return f;
+  return evaluate(model, r, t, nullptr);
 }
 
 bool objective_gradient(const HostModel& model, const Vec3& r, const Vec3& t, double g[6]) {
-  // objective.cpp:254-334
   if (!pose_feasible(model, t)) return false;
-  const Mat3 R = rotation_matrix(r);
-  const Mat3 Jl = left_jacobian(r);
-  Vec3 grad_r, grad_t;
-  for (const HostClass& cls : model.classes) {
-    const int n1 = cls.n1(), n2 = cls.n2();
-    std::vector<Vec3> u(n1), uhat(n1);
-    std::vector<double> kappa(n1), lz(n1), zl(n1), d(n1);
-    std::vector<Mat3> J(n1);
-    for (int i = 0; i < n1; ++i) {
-      u[i] = Vec3(cls.mu[3 * i], cls.mu[3 * i + 1], cls.mu[3 * i + 2]) - t;
-      const double d2 = u[i].dot(u[i]);
-      d[i] = std::sqrt(d2);
-      uhat[i] = u[i] * (1.0 / d[i]);
-      kappa[i] = d2 / cls.sigma2[i] + 1.0;
-      lz[i] = log_z_eval(kappa[i]);
-      zl[i] = log_z_deriv(kappa[i]);
-      const Mat3 outer = Mat3::outer(uhat[i], uhat[i]);
-      J[i] = outer * (-(2.0 * d[i] / cls.sigma2[i])) -
-             (Mat3::identity() - outer) * (kappa[i] / d[i]);
-    }
-    Vec3 cgr, cgt;
-    for (int i = 0; i < n1; ++i) {
-      const Vec3 vi = uhat[i] * kappa[i];
-      {
-        const double term = 0.5 * kappa[i] / std::tanh(kappa[i]);
-        const double dlog = 2.0 * (log_z_deriv(2.0 * kappa[i]) - zl[i]);
-        cgt = cgt + u[i] * (cls.phi1[i] * cls.phi1[i] * term * dlog * (-2.0 / cls.sigma2[i]));
-      }
-      for (int j = i + 1; j < n1; ++j) {
-        const Vec3 sum = vi + uhat[j] * kappa[j];
-        const double K = sum.norm();
-        if (K < kappa[i] + kappa[j] - kMargin) continue;
-        const double term =
-            2.0 * cls.phi1[i] * cls.phi1[j] * std::exp(log_z_eval(K) - lz[i] - lz[j]);
-        Vec3 dK;
-        if (K > 1e-12) dK = (J[i] + J[j]) * (sum * (1.0 / K));
-        cgt = cgt + (dK * log_z_deriv(K) + u[i] * (2.0 * zl[i] / cls.sigma2[i]) +
-                     u[j] * (2.0 * zl[j] / cls.sigma2[j])) *
-                        term;
-      }
-      const Vec3 w = R * vi;
-      for (int j = 0; j < n2; ++j) {
-        const Vec3 sum = w + Vec3(cls.b[3 * j], cls.b[3 * j + 1], cls.b[3 * j + 2]);
-        const double K = sum.norm();
-        if (K < kappa[i] + cls.kappa2[j] - kMargin) continue;
-        const double term =
-            cls.phi1[i] * cls.phi2[j] * std::exp(log_z_eval(K) - lz[i] - cls.log_z2[j]);
-        Vec3 what;
-        if (K > 1e-12) what = sum * (1.0 / K);
-        const double zlK = log_z_deriv(K);
-        const Vec3 dt_part = (J[i] * (R.transpose() * what)) * zlK + u[i] * (2.0 * zl[i] / cls.sigma2[i]);
-        const Vec3 dr_part = (Jl.transpose() * w.cross(what)) * zlK;
-        cgt = cgt + dt_part * (-2.0 * term);
-        cgr = cgr + dr_part * (-2.0 * term);
-      }
-    }
-    grad_r = grad_r + cgr * cls.weight;
-    grad_t = grad_t + cgt * cls.weight;
-  }
-  for (int k = 0; k < 3; ++k) {
-    g[k] = grad_r[k];
-    g[3 + k] = grad_t[k];
-  }
+  evaluate(model, r, t, g);
   return true;
+}
+
+double objective_and_gradient(const HostModel& model, const Vec3& r, const Vec3& t,
+                              double g[6]) {
+  if (!pose_feasible(model, t)) {
+    for (int k = 0; k < 6; ++k) g[k] = 0.0;
+    return INFINITY;
+  }
+  return evaluate(model, r, t, g);
 }
 
 bool feasible_center(const HostModel& model, const Vec3& c, const Vec3& h, Vec3* t_out) {

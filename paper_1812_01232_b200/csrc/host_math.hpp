@@ -101,6 +101,8 @@ Vec3 wrap_rotation_vector(const Vec3& r);
 bool pose_feasible(const HostModel& model, const Vec3& t);
 double objective_value(const HostModel& model, const Vec3& r, const Vec3& t);
 bool objective_gradient(const HostModel& model, const Vec3& r, const Vec3& t, double g[6]);
+// value and gradient in one pass (+inf and a zero gradient when infeasible)
+double objective_and_gradient(const HostModel& model, const Vec3& r, const Vec3& t, double g[6]);
 bool feasible_center(const HostModel& model, const Vec3& c, const Vec3& h, Vec3* t_out);
 double point_box_lo(const Vec3& p, const Vec3& c, const Vec3& h);
 double point_box_hi(const Vec3& p, const Vec3& c, const Vec3& h);

@@ -1,7 +1,8 @@
-// Mixture construction (host C++, off the hot path per the north star):
-// DP-means / DP-vMF-means clustering and the semantic mixture pair, following
-// core/src/mixtures.cpp:49-362 of the reference step for step (same visit
-// order, same floating-point expression order), so results are bit-identical.
+// Mixture construction (off the hot path per the north star): DP-means /
+// DP-vMF-means clustering (one engine; fixed centres scored on the GPU at
+// scale, dp_cluster.cu) and the semantic mixture pair, with every floating
+// point sum in the reference's order (core/src/mixtures.cpp:49-362), so
+// results are bit-identical.
 #pragma once
 
 #include <cstdint>
@@ -53,10 +54,12 @@ Clustering dp_means(const std::vector<Vec3>& points, double lambda_p,
                     std::optional<std::uint64_t> shuffle_seed = std::nullopt);
 Clustering dp_vmf_means(const std::vector<Vec3>& bearings, double lambda_f,
                         std::optional<std::uint64_t> shuffle_seed = std::nullopt);
-std::vector<Gaussian> fit_gaussian_components(const std::vector<std::vector<Vec3>>& clusters,
-                                              double sigma2_min);
-std::vector<Vmf> fit_vmf_components(const std::vector<std::vector<Vec3>>& clusters,
-                                    double kappa_min = 1e-3, double kappa_max = 1e5);
+// component fits from a clustering of x (fit_gaussian_components /
+// fit_vmf_components, mixtures.cpp:204-267)
+std::vector<Gaussian> fit_gaussians(const std::vector<Vec3>& x, const Clustering& c,
+                                    double sigma2_min);
+std::vector<Vmf> fit_vmfs(const std::vector<Vec3>& x, const Clustering& c,
+                          double kappa_min = 1e-3, double kappa_max = 1e5);
 SemanticMixturePair build_semantic_mixtures(
     const std::vector<Vec3>& points, const std::vector<std::string>& point_labels,
     const std::vector<Vec3>& bearings, const std::vector<std::string>& bearing_labels,

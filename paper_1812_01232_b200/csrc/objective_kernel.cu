@@ -26,46 +26,14 @@
 #include <cmath>
 
 #include "objective_device.hpp"
+#include "objective_math.hpp"
+#include "refine_core.hpp"
 
 namespace gosma {
 
 namespace {
 
 constexpr unsigned kFullMask = 0xffffffffu;
-constexpr double kMarginObj = 64.0;  // objective.cpp:17
-
-__device__ __forceinline__ double log_z_d(double k) {
-  // sphere_stats.cpp:47-56
-  if (k < 1e-4) return 0.69314718055994531 + log1p(k * k / 6.0);
-  // above 19, exp(-2k) < 2^-54: k + log1p(-exp(-2k)) rounds to k (bit-identical)
-  if (k > 19.0) return k - log(k);
-  return k + log1p(-exp(-2.0 * k)) - log(k);
-}
-
-__device__ __forceinline__ double log_z_deriv_d(double k) {
-  // sphere_stats.cpp:58-69
-  if (k < 1e-4) return k / 3.0 - k * k * k / 45.0;
-  if (k > 19.0) return 1.0 - 1.0 / k;  // (1 + e2) / (1 - e2) == 1 exactly above 19
-  const double e2 = exp(-2.0 * k);
-  return (1.0 + e2) / (1.0 - e2) - 1.0 / k;
-}
-
-// A pair's exp(log_z(K) - c) and log_z'(K) from one exp(-2K): with
-// log_z(K) = K + log1p(-e2) - log K (sphere_stats.cpp:47-69),
-// exp(log_z(K) - c) = exp(K - c) (1 - e2) / K. Same branches as the host.
-__device__ __forceinline__ void pair_terms(double K, double c, double& ez, double& zl) {
-  if (K < 1e-4) {
-    ez = exp(log_z_d(K) - c);
-    zl = log_z_deriv_d(K);
-    return;
-  }
-  const double iK = 1.0 / K;
-  // 1 - e2; above K = 19, e2 = exp(-2K) < 2^-54 and 1 - e2 rounds to 1.0 in
-  // FP64, so the exp is skipped with bit-identical results (realistic K ~ 1e2-1e5)
-  const double om = K < 0.5 ? -expm1(-2.0 * K) : (K > 19.0 ? 1.0 : 1.0 - exp(-2.0 * K));
-  ez = exp(K - c) * om * iK;
-  zl = K > 350.0 ? 1.0 - iK : (2.0 - om) / om - iK;
-}
 
 __device__ __forceinline__ double wsum(double v) {
 #pragma unroll
@@ -73,20 +41,11 @@ __device__ __forceinline__ double wsum(double v) {
   return v;
 }
 
-// Per-row record in shared memory (FP64).
-struct RowD {
-  double ux, uy, uz;  // unit direction of mu_i - t
-  double d, k, lz, zl, is2, phi;
-};
-
-__device__ __forceinline__ void jv(const RowD& r, double vx, double vy, double vz, double& ox,
-                                   double& oy, double& oz) {
-  const double p = r.ux * vx + r.uy * vy + r.uz * vz;
-  const double a = -2.0 * r.d * r.is2, b = r.k / r.d;
-  ox = r.ux * p * a - (vx - r.ux * p) * b;
-  oy = r.uy * p * a - (vy - r.uy * p) * b;
-  oz = r.uz * p * a - (vz - r.uz * p) * b;
-}
+using objmath::RowD;
+using objmath::jv;
+using objmath::log_z_d;
+using objmath::log_z_deriv_d;
+using objmath::pair_terms;
 
 // CTA totals of 7 values (fixed tree: warp shuffles, then one warp per value
 // over the warps' partials); red holds 7 x 32 + 8 doubles.
@@ -159,39 +118,7 @@ __device__
   __shared__ double rjl[18];
   if (threadIdx.x >= blockDim.x - 32) {
     double R[9], Jl[9];
-    const double th2 = r0 * r0 + r1 * r1 + r2 * r2;
-    const double K[9] = {0.0, -r2, r1, r2, 0.0, -r0, -r1, r0, 0.0};
-    double K2[9];
-    for (int a = 0; a < 3; ++a)
-      for (int c = 0; c < 3; ++c)
-        K2[3 * a + c] = K[3 * a] * K[c] + K[3 * a + 1] * K[3 + c] + K[3 * a + 2] * K[6 + c];
-    double ra, rc, ja, jb;
-    // sin / cos of theta once for both R and Jl (same values as separate calls)
-    double th = 0.0, sth = 0.0, cth = 1.0;
-    if (th2 >= 1e-16) {
-      th = sqrt(th2);
-      sth = sin(th);
-      cth = cos(th);
-    }
-    if (th2 < 1e-16) {
-      ra = 1.0;
-      rc = 0.5;
-    } else {
-      ra = sth / th;
-      rc = (1.0 - cth) / th2;
-    }
-    if (th2 < 1e-12) {
-      ja = 0.5;
-      jb = 1.0 / 6.0;
-    } else {
-      ja = (1.0 - cth) / th2;
-      jb = (th - sth) / (th2 * th);
-    }
-    for (int e = 0; e < 9; ++e) {
-      const double id = (e % 4 == 0) ? 1.0 : 0.0;
-      R[e] = (id + ra * K[e]) + rc * K2[e];
-      Jl[e] = id + K[e] * ja + K2[e] * jb;
-    }
+    objmath::rotation_and_jacobian(r0, r1, r2, R, Jl);
     if (threadIdx.x == blockDim.x - 32)
       for (int e = 0; e < 9; ++e) {
         rjl[e] = R[e];
@@ -207,20 +134,8 @@ __device__
     __syncthreads();
     for (int il = threadIdx.x; il < cs.n1; il += blockDim.x) {
       const int i = cs.o1 + il;
-      const double ux = m.mu[3 * i] - t0, uy = m.mu[3 * i + 1] - t1, uz = m.mu[3 * i + 2] - t2;
-      const double d2 = ux * ux + uy * uy + uz * uz;
-      const double d = sqrt(d2);
-      RowD r;
-      r.ux = ux * (1.0 / d);
-      r.uy = uy * (1.0 / d);
-      r.uz = uz * (1.0 / d);
-      r.d = d;
-      r.is2 = 1.0 / m.sigma2[i];
-      r.k = d2 / m.sigma2[i] + 1.0;
-      r.lz = log_z_d(r.k);
-      r.zl = log_z_deriv_d(r.k);
-      r.phi = m.phi1[i];
-      rows[il] = r;
+      rows[il] = objmath::make_row(m.mu[3 * i], m.mu[3 * i + 1], m.mu[3 * i + 2], m.sigma2[i],
+                                   m.phi1[i], t0, t1, t2);
     }
     __syncthreads();
     // this slice's partners: [p0, p1) over self rows (0..n1-1) then columns
@@ -258,7 +173,7 @@ __device__
         const RowD b = rows[jl];
         const double ex = vix + b.ux * b.k, ey = viy + b.uy * b.k, ez = viz + b.uz * b.k;
         const double K = sqrt(ex * ex + ey * ey + ez * ez);
-        if (K < a.k + b.k - kMarginObj) continue;
+        if (K < a.k + b.k - objmath::kNegligible) continue;
         double eK, zl;
         pair_terms(K, a.lz + b.lz, eK, zl);
         const double term = 2.0 * a.phi * b.phi * eK;
@@ -280,7 +195,7 @@ __device__
         const int j = cs.o2 + (jp - cs.n1);
         const double ex = wx + m.b[3 * j], ey = wy + m.b[3 * j + 1], ez = wz + m.b[3 * j + 2];
         const double K = sqrt(ex * ex + ey * ey + ez * ez);
-        if (K < a.k + m.kappa2[j] - kMarginObj) continue;
+        if (K < a.k + m.kappa2[j] - objmath::kNegligible) continue;
         double eK, zl;
         pair_terms(K, a.lz + m.log_z2[j], eK, zl);
         const double term = a.phi * m.phi2[j] * eK;
@@ -353,18 +268,13 @@ __global__ void __launch_bounds__(256)
 // values (the reductions broadcast), so control flow stays uniform across the
 // CTA without shared control state.
 
-__device__ __forceinline__ double dot6(const double* a, const double* b) {
-  double s = 0.0;
-  for (int k = 0; k < 6; ++k) s += a[k] * b[k];
-  return s;
-}
-
 // Value + gradient of one pose by a cluster of CTAs: CTA rank r takes partner
 // slice r of C (objgrad_block), the C partial totals meet in distributed
 // shared memory and every CTA sums them in rank order, so all CTAs of the
 // cluster hold identical values and take identical control decisions.
 struct CtaObjective {
   const DevModel64* m;
+  const RefineDomain* dom;
   RowD* rows;
   double* red;
   double* xch;  // this CTA's partial totals (7), read by the cluster
@@ -372,6 +282,8 @@ struct CtaObjective {
   long long* count;
   bool have = false;
   double x[6], f, g[6];
+  __device__ const double* grad() const { return g; }
+  __device__ bool project(double* p);
   __device__ void eval(const double* xx) {
     bool same = have;
     for (int k = 0; k < 6; ++k) same = same && xx[k] == x[k];
@@ -463,188 +375,35 @@ __device__ bool clamp_to_domain_d(const DevModel64& m, const RefineDomain& dom, 
   return false;
 }
 
-struct LineSearchD {
-  double alpha = 0.0, value = INFINITY;
-};
+__device__ bool CtaObjective::project(double* p) { return clamp_to_domain_d(*m, *dom, p, red); }
 
-// wolfe_search (solver.cpp:105-160)
-__device__ LineSearchD wolfe_d(CtaObjective& ob, const double* x, const double* d, double f0,
-                               double g0) {
-  const double c1 = 1e-4, c2 = 0.9, alpha_max = 1e3;
-  double xt[6];
-  auto at = [&](double a) {
-    for (int k = 0; k < 6; ++k) xt[k] = x[k] + a * d[k];
-  };
-  LineSearchD best;
-  auto consider = [&](double a, double v) {
-    if (v <= f0 + c1 * a * g0 && v < best.value) {
-      best.alpha = a;
-      best.value = v;
-    }
-  };
-  auto zoom = [&](double lo, double flo, double hi) -> LineSearchD {
-    for (int it = 0; it < 30; ++it) {
-      const double a = 0.5 * (lo + hi);
-      at(a);
-      const double v = ob.value(xt);
-      consider(a, v);
-      if (v > f0 + c1 * a * g0 || v >= flo) {
-        hi = a;
-        continue;
-      }
-      const double g = dot6(ob.g, d);
-      if (fabs(g) <= -c2 * g0) return {a, v};
-      if (g * (hi - lo) >= 0.0) hi = lo;
-      lo = a;
-      flo = v;
-    }
-    return best;
-  };
-  double a_prev = 0.0, f_prev = f0, a = 1.0;
-  for (int it = 0; it < 20; ++it) {
-    at(a);
-    const double v = ob.value(xt);
-    consider(a, v);
-    if (v > f0 + c1 * a * g0 || (it > 0 && v >= f_prev)) return zoom(a_prev, f_prev, a);
-    const double g = dot6(ob.g, d);
-    if (fabs(g) <= -c2 * g0) return {a, v};
-    if (g >= 0.0) return zoom(a, v, a_prev);
-    a_prev = a;
-    f_prev = v;
-    a = fmin(2.0 * a, alpha_max);
-    if (a_prev >= alpha_max) break;
-  }
-  return best;
-}
-
-// local_refine (solver.cpp:164-258): best value and pose (r, t) from x0.
-// L-BFGS memory (solver.cpp:197-199)
-constexpr int kLbfgsMem = 10;
+// The CTA's one copy of the L-BFGS curvature pairs in shared memory: every
+// thread computes the same pairs; thread 0 stores them and all threads read
+// them back (broadcast loads) - per-thread copies would be 1 KB of local
+// memory per thread (0.5 MB per CTA, spilled through L2 on every two-loop
+// recursion).
 struct LbfgsHistory {
-  double S[kLbfgsMem][6], Y[kLbfgsMem][6], Rho[kLbfgsMem];
+  double S[refine::kMem][6], Y[refine::kMem][6], Rho[refine::kMem];
+  __device__ void put(int slot, const double* s, const double* y, double rho) {
+    __syncthreads();  // every thread is past its reads of the history
+    if (threadIdx.x == 0) {
+      for (int k = 0; k < 6; ++k) {
+        S[slot][k] = s[k];
+        Y[slot][k] = y[k];
+      }
+      Rho[slot] = rho;
+    }
+    __syncthreads();
+  }
 };
 
-// H: the CTA's one copy of the L-BFGS history in shared memory. Every thread
-// computes the same pairs; thread 0 stores them and all threads read them
-// back (broadcast loads) - per-thread copies would be 1 KB of local memory per
-// thread (0.5 MB per CTA, spilled through L2 on every two-loop recursion).
+// One start's local refinement on one CTA (cluster): the shared controller
+// (refine_core.hpp) over the CTA-wide FP64 objective.
 __device__ void local_refine_d(const DevModel64& m, const RefineDomain& dom, RowD* rows,
                                double* red, double* xch, double* tot, LbfgsHistory& H,
                                double* xio, double* fout, long long* count) {
-  constexpr int kMaxIt = 200, kMem = kLbfgsMem;
-  double (&S)[kMem][6] = H.S;
-  double (&Y)[kMem][6] = H.Y;
-  double (&Rho)[kMem] = H.Rho;
-  const double kGradTol = 1e-6;
-  CtaObjective ob{&m, rows, red, xch, tot, count};
-  double x[6], bx[6];
-  for (int k = 0; k < 6; ++k) x[k] = bx[k] = xio[k];
-  double bf = ob.value(x);
-  if (!(bf < INFINITY)) {  // infeasible start: unchanged
-    *fout = bf;
-    return;
-  }
-  auto offer = [&](const double* xx, double fx) {
-    double p[6];
-    for (int k = 0; k < 6; ++k) p[k] = xx[k];
-    if (!clamp_to_domain_d(m, dom, p, red)) return;
-    bool moved = false;
-    for (int k = 0; k < 6; ++k) moved = moved || p[k] != xx[k];
-    const double fp = moved ? ob.value(p) : fx;
-    if (fp < bf) {
-      bf = fp;
-      for (int k = 0; k < 6; ++k) bx[k] = p[k];
-    }
-  };
-  double fx = bf;
-  offer(x, fx);
-  ob.eval(x);
-  double g[6];
-  for (int k = 0; k < 6; ++k) g[k] = ob.g[k];
-  int nh = 0, h0 = 0;  // ring of the last nh pairs, oldest at h0
-  for (int it = 0; it < kMaxIt; ++it) {
-    if (sqrt(dot6(g, g)) < kGradTol) break;
-    double q[6];
-    for (int k = 0; k < 6; ++k) q[k] = g[k];
-    double alpha[kMem];
-    for (int i = nh - 1; i >= 0; --i) {
-      const int s = (h0 + i) % kMem;
-      alpha[i] = Rho[s] * dot6(S[s], q);
-      for (int k = 0; k < 6; ++k) q[k] -= alpha[i] * Y[s][k];
-    }
-    if (nh > 0) {
-      const int s = (h0 + nh - 1) % kMem;
-      const double sc = dot6(S[s], Y[s]) / dot6(Y[s], Y[s]);
-      for (int k = 0; k < 6; ++k) q[k] *= sc;
-    }
-    for (int i = 0; i < nh; ++i) {
-      const int s = (h0 + i) % kMem;
-      const double beta = Rho[s] * dot6(Y[s], q);
-      for (int k = 0; k < 6; ++k) q[k] += (alpha[i] - beta) * S[s][k];
-    }
-    double d[6];
-    for (int k = 0; k < 6; ++k) d[k] = -q[k];
-    double dg = dot6(d, g);
-    if (!(dg < -1e-14 * sqrt(dot6(d, d)) * sqrt(dot6(g, g)))) {  // not a descent direction
-      nh = 0;
-      h0 = 0;
-      for (int k = 0; k < 6; ++k) d[k] = -g[k];
-      dg = -dot6(g, g);
-    }
-    const LineSearchD ls = wolfe_d(ob, x, d, fx, dg);
-    if (!(ls.alpha > 0.0) || !(ls.value < INFINITY)) break;
-    double xn[6];
-    for (int k = 0; k < 6; ++k) xn[k] = x[k] + ls.alpha * d[k];
-    ob.eval(xn);
-    double s[6], y[6];
-    for (int k = 0; k < 6; ++k) {
-      s[k] = xn[k] - x[k];
-      y[k] = ob.g[k] - g[k];
-    }
-    const double sy = dot6(s, y);
-    if (sy > 1e-10 * sqrt(dot6(s, s)) * sqrt(dot6(y, y))) {
-      int slot;
-      if (nh < kMem) {
-        slot = (h0 + nh) % kMem;
-        ++nh;
-      } else {
-        slot = h0;
-        h0 = (h0 + 1) % kMem;
-      }
-      __syncthreads();  // every thread is past its reads of the history
-      if (threadIdx.x == 0) {
-        for (int k = 0; k < 6; ++k) {
-          S[slot][k] = s[k];
-          Y[slot][k] = y[k];
-        }
-        Rho[slot] = 1.0 / sy;
-      }
-      __syncthreads();
-    }
-    for (int k = 0; k < 6; ++k) {
-      x[k] = xn[k];
-      g[k] = ob.g[k];
-    }
-    fx = ls.value;
-    offer(x, fx);
-    // re-express past pi (solver.cpp:249-255)
-    const double rn = sqrt(x[0] * x[0] + x[1] * x[1] + x[2] * x[2]);
-    if (rn > M_PI) {
-      double w[3] = {x[0], x[1], x[2]};
-      double n = rn;
-      while (n > M_PI) {
-        for (double& c : w) c *= (1.0 - 2.0 * M_PI / n);
-        n = sqrt(w[0] * w[0] + w[1] * w[1] + w[2] * w[2]);
-      }
-      for (int k = 0; k < 3; ++k) x[k] = w[k];
-      ob.eval(x);
-      for (int k = 0; k < 6; ++k) g[k] = ob.g[k];
-      nh = 0;
-      h0 = 0;
-    }
-  }
-  for (int k = 0; k < 6; ++k) xio[k] = bx[k];
-  *fout = bf;
+  CtaObjective ob{&m, &dom, rows, red, xch, tot, count};
+  refine::lbfgs_refine(ob, H, xio, fout);
 }
 
 #ifndef GOSMA_REFINE_THREADS

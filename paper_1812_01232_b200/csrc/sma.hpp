@@ -1,4 +1,5 @@
-// Host local refinement (SMA) and the pose-domain type shared by the solver.
+// Host local refinement (host_refine.cpp: the shared L-BFGS controller over
+// the host FP64 evaluator) and the pose-domain type shared by the solver.
 #pragma once
 
 #include <array>

@@ -465,7 +465,7 @@ struct gosma_solver {
   Frontier F;
   double total_volume = 0.0, pruned_volume = 0.0, resolved_volume = 0.0;
   double floor_lower = kInf;
-  // drain order (Frontier::select_largest) while the pool is above its
+  // depth-first order (Frontier::select_deepest) while the pool is above its
   // high-water mark; folding (enforce_capacity) only as a last resort
   bool drain = false;
   unsigned long long drain_waves = 0, folds = 0;
@@ -797,8 +797,8 @@ int gosma_solver_status(gosma_solver* S, gosma_wave_status* st) {
     S->floor_lower = std::min(S->floor_lower, fmin);
   } else if (!user_cap) {
     // The device memory budget: above the high-water mark the waves take the
-    // largest lower bounds below the limit (drain order: their subtrees die
-    // soonest), which bounds the pool without changing the work or the
+    // deepest nodes below the limit (depth-first: the open set stays ~8 W per
+    // level), which bounds the pool without changing the work or the
     // certificate; below the low-water mark best-first resumes. Folding (it
     // caps the certified bound) happens only if the pool still overflows.
     static const bool drain_on = [] {
@@ -854,7 +854,7 @@ int gosma_solver_expand(gosma_solver* S, double limit, unsigned long long max_ev
   size_t n_sel = 0;
   S->lap(-1, s);
   // Expand only nodes that can still matter: lower < limit (= d* - eps).
-  if ((e = S->drain ? S->F.select_largest(want, host_order_key(limit), s, &n_sel)
+  if ((e = S->drain ? S->F.select_deepest(want, host_order_key(limit), s, &n_sel)
                     : S->F.select_smallest(want, host_order_key(limit), s, &n_sel)) !=
       cudaSuccess)
     return cuda_error(e, "select");
