@@ -570,14 +570,15 @@ __global__ void min_key_at_least(const unsigned long long* key, size_t n,
 }
 
 // Children whose upper bound is below the exclusive prefix minimum (records).
-__global__ void flag_records(const double* upper, const double* pmin, size_t n,
-                             ImprovingChild* out, unsigned long long* count, unsigned cap) {
+__global__ void flag_records(const double* upper, const double* pmin, const gosma_node* kids,
+                             size_t n, ImprovingChild* out, unsigned long long* count,
+                             unsigned cap) {
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<size_t>(gridDim.x) * blockDim.x) {
     const double u = upper[i];
     if (u < pmin[i]) {
       const unsigned long long k = atomicAdd(count, 1ull);
-      if (k < cap) out[k] = ImprovingChild{u, i};
+      if (k < cap) out[k] = ImprovingChild{u, i, kids[i]};
     }
   }
 }
@@ -601,17 +602,15 @@ double key_to_double(unsigned long long k) {
   return d;
 }
 
-// Child buffers for n_sel selected parents (8 children each), grown
-// geometrically on demand so small solves do not map a full wave's worth.
 // Child buffers for n_sel selected parents (8 children each): a small set
-// first, then a full wave's worth (at most two allocations per solver; a
-// finished solver parks them for the next solve on the device).
+// first, then grown on demand (at least doubling); a finished solver parks
+// them for the next solve on the device.
 cudaError_t Frontier::ensure_kids(size_t n_sel) {
   const size_t need = 8 * n_sel;
   if (need <= kid_cap) return cudaSuccess;
-  const size_t full = 8 * std::max(sel_cap, n_sel);
-  const size_t nk = need <= (size_t(1) << 16) && full > (size_t(1) << 16) ? (size_t(1) << 16)
-                                                                            : full;
+  // geometric growth from a small first block (short solves never map a
+  // full wave's worth; depth-first waves grow it further)
+  const size_t nk = std::max(need, kid_cap ? 2 * kid_cap : (size_t(1) << 16));
   void** slots[10] = {reinterpret_cast<void**>(&tidx),      reinterpret_cast<void**>(&tnodes),
                       reinterpret_cast<void**>(&tself),     reinterpret_cast<void**>(&kids),
                       reinterpret_cast<void**>(&kid_lower), reinterpret_cast<void**>(&kid_upper),
@@ -1243,8 +1242,8 @@ cudaError_t Frontier::improving_children(size_t n_kids, double bound, cudaStream
   // has more than fit), so the replay below is the reference's in-order one
   for (int pass = 0; pass < 2; ++pass) {
     if ((e = cudaMemsetAsync(counter, 0, sizeof(unsigned long long), s)) != cudaSuccess) return e;
-    flag_records<<<grid_cap(n_kids, 256), 256, 0, s>>>(kid_upper, kid_pmin, n_kids, rec, counter,
-                                                       static_cast<unsigned>(rec_cap));
+    flag_records<<<grid_cap(n_kids, 256), 256, 0, s>>>(kid_upper, kid_pmin, kids, n_kids, rec,
+                                                       counter, static_cast<unsigned>(rec_cap));
     if ((e = cudaMemcpyAsync(h_counter, counter, sizeof(unsigned long long),
                              cudaMemcpyDeviceToHost, s)) != cudaSuccess)
       return e;

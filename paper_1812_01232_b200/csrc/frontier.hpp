@@ -31,6 +31,7 @@ unsigned long long host_order_key(double v);
 struct ImprovingChild {
   double upper;
   unsigned long long index;
+  gosma_node node;  // the child itself (no per-record copy afterwards)
 };
 double key_to_double(unsigned long long k);
 

@@ -34,6 +34,7 @@ using namespace gosma;
 namespace {
 
 constexpr double kInf = std::numeric_limits<double>::infinity();
+constexpr size_t kDfsWaveFactor = 4;
 constexpr double kFloor = 1e-9;  // is_splittable floor (se3.cpp:102-105)
 
 Domain make_domain(const gosma_domain* d) {
@@ -599,8 +600,9 @@ int solver_init(gosma_solver* S) {
           ? static_cast<size_t>(cfg.wave_nodes)
           : std::min<size_t>(std::max<size_t>(300000000 / std::max<size_t>(pairs, 1), 1024),
                              1u << 21);
+  // selection arrays for depth-first waves of kDfsWaveFactor x wave_nodes
   cudaError_t e = S->F.reserve(std::max<size_t>(size_t(1) << 20, roots.size() * 2 + 16),
-                               S->wave_nodes);
+                               kDfsWaveFactor * S->wave_nodes);
   if (e != cudaSuccess) return cuda_error(e, "frontier reserve");
   mark("reserve");
   // Device memory budget for the pool: beyond it the worst nodes fold into the
@@ -789,7 +791,8 @@ int gosma_solver_status(gosma_solver* S, gosma_wave_status* st) {
   // capacity folding (solver.cpp:433-447) at the caller's queue_capacity
   const bool user_cap = S->cfg.queue_capacity >= 0 &&
                         static_cast<size_t>(S->cfg.queue_capacity) <= S->mem_cap;
-  const size_t wave_room = 8 * S->wave_nodes;
+  const size_t wave_room =
+      8 * std::max(S->wave_nodes, std::min(kDfsWaveFactor * S->wave_nodes, size_t(1) << 20));
   if (user_cap && S->F.live_upper_bound() > S->qcap) {
     double fv = 0.0, fmin = kInf;
     if ((e = S->F.fold_to(S->qcap, s, &fv, &fmin)) != cudaSuccess) return cuda_error(e, "fold");
@@ -849,7 +852,11 @@ int gosma_solver_expand(gosma_solver* S, double limit, unsigned long long max_ev
   DeviceGuard g(ctx->device);
   cudaStream_t s = ctx->stream;
   cudaError_t e;
-  size_t want = S->wave_nodes;
+  // depth-first waves take kDfsWaveFactor x as many parents: their selection
+  // scans the whole pool, which a larger wave amortises
+  size_t want = S->drain ? std::max(S->wave_nodes,
+                                    std::min(kDfsWaveFactor * S->wave_nodes, size_t(1) << 20))
+                         : S->wave_nodes;
   if (max_evals > 0) want = std::min<size_t>(want, std::max<unsigned long long>(1, (max_evals + 7) / 8));
   size_t n_sel = 0;
   S->lap(-1, s);
@@ -938,11 +945,7 @@ int gosma_solver_expand(gosma_solver* S, double limit, unsigned long long max_ev
     return cuda_error(e, "improving children");
   for (const ImprovingChild& c : S->improving) {
     if (!(c.upper < S->inc.value)) continue;
-    gosma_node b;
-    if ((e = cudaMemcpy(&b, S->F.kids + c.index, sizeof(gosma_node), cudaMemcpyDeviceToHost)) !=
-        cudaSuccess)
-      return cuda_error(e, "improving child");
-    const int rc = improve(ctx->model, S->dom, b, &S->inc, S->sma_dev.get());
+    const int rc = improve(ctx->model, S->dom, c.node, &S->inc, S->sma_dev.get());
     if (rc != GOSMA_OK) return rc;
   }
   S->lap(4, s);

@@ -19,13 +19,20 @@ seed = int(os.environ.get("SEED", "1"))
 eps = float(os.environ.get("EPS", "0.1"))
 tl = float(os.environ.get("TL", "300"))
 every = float(os.environ.get("PRINT", "5"))
+mode = os.environ.get("MODE", "plain")
 G = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "tests",
-                              "golden", "solver_golden.json")))
+                              "golden", "scenes_golden.json")))
 sc = next(s for s in G["scenes"] if s["seed"] == seed)
-m = sc["mixture"]
-cls = [{"mu": m["mu"], "sigma2": m["sigma2"], "phi1": m["phi1"], "dir": m["dir"],
-        "kappa2": m["kappa2"], "phi2": m["phi2"]}]
-ctx = g.ObjectiveContext(cls, m["zeta"], single_mixture=True)
+m = sc["semantic"] if mode == "semantic" else sc["mixture"]
+cls, o1, o2 = [], 0, 0
+for c in range(len(m["n1"])):
+    a, b = m["n1"][c], m["n2"][c]
+    cls.append({"mu": m["mu"][o1:o1 + a], "sigma2": m["sigma2"][o1:o1 + a],
+                "phi1": m["phi1"][o1:o1 + a], "dir": m["dir"][o2:o2 + b],
+                "kappa2": m["kappa2"][o2:o2 + b], "phi2": m["phi2"][o2:o2 + b],
+                "weight": m["class_weight"][c]})
+    o1, o2 = o1 + a, o2 + b
+ctx = g.ObjectiveContext(cls, m["zeta"], single_mixture=(mode != "semantic"))
 dom = g.PoseDomain(np.zeros(3), math.pi, np.array(G["torus_cover_3.5_0.5"]))
 cfg = g.SolverConfig(epsilon=eps, zeta=m["zeta"])
 t0 = time.perf_counter()
@@ -59,7 +66,7 @@ while True:
         break
     S.expand(d - eps)
 res = S.result()
-out = {"seed": seed, "eps": eps, "status": status, "seconds": time.perf_counter() - t0,
+out = {"seed": seed, "mode": mode, "eps": eps, "status": status, "seconds": time.perf_counter() - t0,
        "init_seconds": t_init, "best_value": res["value"], "global_lower": cert,
        "evals": res["bound_evaluations"], "waves": res["waves"], "r": res["r"].tolist(),
        "t": res["t"].tolist(), "last": row}
