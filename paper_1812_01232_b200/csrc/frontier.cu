@@ -1104,7 +1104,12 @@ cudaError_t Frontier::select_deepest(size_t want, unsigned long long limit, cuda
   cudaError_t e;
   unsigned long long lo_key = 0, hi_key = kHoleKey;
   size_t below = 0, bin_count = 0;
-  if ((e = descend(want, limit, 0.5, s, &lo_key, &hi_key, &below, &bin_count, nullptr, size,
+  // one histogram pass: the first 12 bits of a positive double are its
+  // exponent, and a level deeper divides the volume by 8 (three exponent
+  // steps), so the first digit already separates depths; the nodes of one
+  // depth share their volume bits, so refining the boundary bin would only
+  // cost passes (the boundary depth contributes its first nodes in pool order)
+  if ((e = descend(want, limit, 0.0, s, &lo_key, &hi_key, &below, &bin_count, nullptr, size,
                    vol)) != cudaSuccess)
     return e;
   cub::CountingInputIterator<unsigned int> it(0);
