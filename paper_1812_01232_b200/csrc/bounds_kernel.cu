@@ -36,6 +36,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 #include <vector>
@@ -243,8 +244,8 @@ struct WarpTables {
                 // (a self pair reads [0..2] of its partner row: whole 128-bit loads)
   float4* col;  // [0] (qhx, qhy, qhz, k2)    q_j = R0^T m_j, FP32 high part
                 // [1] (qlx, qly, qlz, G)     q_j low part, G = phi2 / W(k2)
-  float4* rowp; // per model row (s4 hi, s4 lo, c4 hi, c4 lo): 4 sin^2(psi/2) and
-                // 4 cos^2(psi/2) as double-floats, for the precise cross pass
+  float4* rowp; // fix-up launches: per model row (s4 hi, s4 lo, c4 hi, c4 lo),
+                // 4 sin^2(psi/2) and 4 cos^2(psi/2) as double-floats
 };
 // Pair terms are F_i G_j 2^(excess log2e) W(K) (the log W(a), log W(b) and
 // log phi pieces of the reference's log_term, bounds.cpp:136/176, as linear
@@ -253,15 +254,18 @@ struct WarpTables {
 
 constexpr int kRowF4 = 5;  // float4 per model row
 constexpr int kColF4 = 2;  // float4 per image column
-constexpr int kRowPF4 = 1;  // float4 per model row (precise cross pass)
+constexpr int kRowPF4 = 1;  // float4 per model row, fix-up launches only
 
-// Precise cross pass: a node whose cross terms' FP32 error
-// estimate exceeds kRedoRel of their mass re-evaluates them with the alignment
-// angle's numerator x - 4 sin^2(psi/2) formed in FP64 from the double-float
-// directions and psi half-angles (the only FP32 step whose error is amplified,
-// by theta/B). The decision is per node (group-uniform), so the redo runs
-// converged; ~all realistic-regime nodes never take it.
-constexpr double kRedoRel = 2e-6;
+// Precise fix-up: a node (or child) whose cross terms carry a
+// theta/B-amplified FP32 error estimate above kRedoRel of its cross mass is
+// appended to a redo list by the main pass and re-evaluated by a second
+// launch (kFixFull / kFixStream) whose cross pass forms the alignment angle's
+// numerator x - 4 sin^2(psi/2) in FP64 from the double-float directions and a
+// double-float 4 sin^2(psi/2). The main kernel only accumulates the estimate's
+// amplified part (one multiply-add per row) and appends; nodes that never
+// reach the threshold pay nothing else.
+// kRedoRel: the threshold (DevCtx::redo_rel, default 8e-5 of the cross mass;
+// profiles/r02_k1_variants.md)
 
 struct Row {
   float uhx, uhy, uhz, ulx, uly, ulz, klo, khi, kst, Fhi, Fst, cp2, sp2, csp2, s4, c4, usx, usy,
@@ -341,8 +345,8 @@ __device__ __forceinline__ void cross_pair(const Row& r, const float4 qa, const 
   // whose operands are small (theta below / above 90 degrees).
   float num;
   if constexpr (kPrecise) {
-    // the same difference in FP64: |u -+ q|^2 from the double-float directions
-    // minus the double-float 4 sin^2(psi/2) (4 cos^2 past 90 degrees)
+    // the same difference in FP64 (fix-up launches): |u -+ q|^2 from the
+    // double-float directions minus the double-float 4 sin^2 (4 cos^2) of psi/2
     const bool obtuse = x > y;
     const double sg = obtuse ? 1.0 : -1.0;
     const double vx = (static_cast<double>(r.uhx) + r.ulx) + sg * (static_cast<double>(qa.x) + qb.x);
@@ -400,7 +404,7 @@ __device__ __forceinline__ void cross_pair(const Row& r, const float4 qa, const 
   // FP32 error estimate of the LB term: B = theta - psi
   // carries ~u theta absolute error, amplified in e1 by min(x, y)/num (the
   // operand used); accumulated as sum t |e1/num| min(x,y) and sum t |e1|.
-  // The precise pass forms num in FP64: only the exponent's own error remains.
+  // (the fix-up's FP64 numerator leaves only the exponent's own error)
   const float gt1 = qb.w * t1;  // G_j; F_i is applied to the row sum
   l += gt1;
   if constexpr (!kPrecise) ma = fmaf(gt1, fabsf(g) * fminf(x, y), ma);
@@ -517,26 +521,31 @@ __device__ __forceinline__ Row load_row(const WarpTables& T, int i) {
   return r;
 }
 
-template <int kG, bool kSame, bool kCross, bool kSelf, bool kPrecise = false>
+template <int kG, bool kSame, bool kCross, bool kSelf, bool kPrecise>
 __device__ __forceinline__ void class_pairs_rows(const WarpTables& T, const ClassSpan cs, int lane,
                                             float w, double& lb_self, double& lb_cross,
                                             double& ub_self, double& ub_cross, double& lb_err,
-                                            double& lb_err_x) {
+                                            float& lb_amp) {
   const int n = cs.n1;
   // Cross terms: rows over lanes, columns broadcast.
   for (int base = 0; kCross && base < n; base += kG) {
     const int il = base + lane;
     if (il < n) {
       const Row r = load_row(T, cs.o1 + il);
-      const float4 rp = kPrecise ? T.rowp[cs.o1 + il] : float4{};
+      float4 rp{};
+      if constexpr (kPrecise) rp = T.rowp[cs.o1 + il];
       float l = 0.0f, u = 0.0f, ma = 0.0f, mb = 0.0f;
       const float4* cp = T.col + cs.o2 * kColF4;  // pointer walk: no index math per pair
       const float4* const ce = cp + cs.n2 * kColF4;
 #pragma unroll kUnrollPairs
       for (; cp < ce; cp += kColF4) cross_pair<kSame, kPrecise>(r, cp[0], cp[1], l, u, ma, mb, rp);
       lb_cross += static_cast<double>(w * r.Fhi * l);
-      lb_err_x += static_cast<double>(
-          2.0f * w * r.Fhi * fmaf(ma, kErrAmp, fmaf(mb, kErrExp, l * kErrTerm)));
+      const float amp = 2.0f * w * r.Fhi * ma * kErrAmp;
+      lb_err += static_cast<double>(
+          fmaf(2.0f * w * r.Fhi, fmaf(mb, kErrExp, l * kErrTerm), amp));
+#ifndef GOSMA_NO_AMP
+      lb_amp += amp;
+#endif
       ub_cross += static_cast<double>(w * r.Fst * u);
     }
   }
@@ -576,12 +585,12 @@ __device__ __forceinline__ void class_pairs_rows(const WarpTables& T, const Clas
 // gives each row k = kG / r lanes ("slots") sharing its partners round-robin
 // (the node sums are sums over pairs, so any pair -> lane assignment is
 // exact). Separate instantiation: the plain loops stay tighter for full chunks.
-template <int kG, bool kSame, bool kCross, bool kSelf, bool kPrecise = false>
+template <int kG, bool kSame, bool kCross, bool kSelf, bool kPrecise>
 __device__ __forceinline__ void class_pairs_tail(const WarpTables& T, const ClassSpan cs,
                                                  int lane, float w, double& lb_self,
                                                  double& lb_cross, double& ub_self,
                                                  double& ub_cross, double& lb_err,
-                                                 double& lb_err_x) {
+                                                 float& lb_amp) {
   const int n = cs.n1;
   // cross terms: columns broadcast (slot s takes columns s, s+k, ...)
   for (int base = 0; kCross && base < n; base += kG) {
@@ -589,16 +598,22 @@ __device__ __forceinline__ void class_pairs_tail(const WarpTables& T, const Clas
     const int il = base + lane % r, slot = lane / r;
     if (lane < r * k) {
       const Row rw = load_row(T, cs.o1 + il);
-      const float4 rp = kPrecise ? T.rowp[cs.o1 + il] : float4{};
+      float4 rp{};
+      if constexpr (kPrecise) rp = T.rowp[cs.o1 + il];
       float l = 0.0f, u = 0.0f, ma = 0.0f, mb = 0.0f;
       const float4* cp = T.col + (cs.o2 + slot) * kColF4;
       const float4* const ce = T.col + (cs.o2 + cs.n2) * kColF4;
       const int cstep = k * kColF4;
 #pragma unroll kUnrollPairs
-      for (; cp < ce; cp += cstep) cross_pair<kSame, kPrecise>(rw, cp[0], cp[1], l, u, ma, mb, rp);
+      for (; cp < ce; cp += cstep)
+        cross_pair<kSame, kPrecise>(rw, cp[0], cp[1], l, u, ma, mb, rp);
       lb_cross += static_cast<double>(w * rw.Fhi * l);
-      lb_err_x += static_cast<double>(
-          2.0f * w * rw.Fhi * fmaf(ma, kErrAmp, fmaf(mb, kErrExp, l * kErrTerm)));
+      const float amp = 2.0f * w * rw.Fhi * ma * kErrAmp;
+      lb_err += static_cast<double>(
+          fmaf(2.0f * w * rw.Fhi, fmaf(mb, kErrExp, l * kErrTerm), amp));
+#ifndef GOSMA_NO_AMP
+      lb_amp += amp;
+#endif
       ub_cross += static_cast<double>(w * rw.Fst * u);
     }
   }
@@ -637,39 +652,17 @@ __device__ __forceinline__ void class_pairs_tail(const WarpTables& T, const Clas
   }
 }
 
-template <int kG, bool kSame, bool kCross, bool kSelf, bool kTail, bool kPrecise = false>
+template <int kG, bool kSame, bool kCross, bool kSelf, bool kTail, bool kPrecise>
 __device__ __forceinline__ void class_pairs(const WarpTables& T, const ClassSpan cs, int lane,
                                             float w, double& lb_self, double& lb_cross,
                                             double& ub_self, double& ub_cross, double& lb_err,
-                                            double& lb_err_x) {
+                                            float& lb_amp) {
   if constexpr (kTail) {
     class_pairs_tail<kG, kSame, kCross, kSelf, kPrecise>(T, cs, lane, w, lb_self, lb_cross,
-                                                         ub_self, ub_cross, lb_err, lb_err_x);
+                                                         ub_self, ub_cross, lb_err, lb_amp);
   } else {
     class_pairs_rows<kG, kSame, kCross, kSelf, kPrecise>(T, cs, lane, w, lb_self, lb_cross,
-                                                         ub_self, ub_cross, lb_err, lb_err_x);
-  }
-}
-
-// The cross sums of one class span, FP32 pass then (group-uniform decision on
-// the group-summed error estimate) the precise pass when the estimate exceeds
-// kRedoRel of the span's cross mass. Returns group sums {lb, ub, err}.
-template <int kG, bool kSame, bool kTail>
-__device__ __forceinline__ void cross_span(const WarpTables& T, const ClassSpan cs, int lane,
-                                           float w, const Group<kG>& G, bool precise_on,
-                                           double& lcr, double& ucr, double& ecr) {
-  double d0 = 0.0, d1 = 0.0;
-  lcr = ucr = ecr = 0.0;
-  class_pairs<kG, kSame, true, false, kTail>(T, cs, lane, w, d0, lcr, d1, ucr, d0, ecr);
-  lcr = G.sum(lcr);
-  ucr = G.sum(ucr);
-  ecr = G.sum(ecr);
-  if (precise_on && ecr > kRedoRel * 2.0 * lcr) {
-    double l2 = 0.0, u2 = 0.0, e2 = 0.0;
-    class_pairs<kG, kSame, true, false, kTail, true>(T, cs, lane, w, d0, l2, d1, u2, d0, e2);
-    lcr = G.sum(l2);
-    ucr = G.sum(u2);
-    ecr = G.sum(e2);
+                                                         ub_self, ub_cross, lb_err, lb_amp);
   }
 }
 
@@ -733,12 +726,14 @@ enum {
   kCrossCached = 2,
   kSiblings = 3,
   kModeStream = 4,
-  kSiblingsStream = 5  // siblings mode of a multi-class context, one class's table at a time
+  kSiblingsStream = 5,  // siblings mode of a multi-class context, one class's table at a time
+  kFixFull = 6,         // precise fix-up of redo-list entries (single class)
+  kFixStream = 7        // precise fix-up, multi-class context
 };
 // per-group extra shared memory of the siblings modes: the 8 children's R
 // (72 doubles, computed by 8 lanes at once) and (streamed) their {lb, ub,
-// err} cross sums (24 doubles)
-constexpr int kSibStreamExtraF4 = (72 + 24) * 8 / 16;
+// err, amplified err} cross sums (32 doubles)
+constexpr int kSibStreamExtraF4 = (72 + 32) * 8 / 16;
 
 // Rodrigues R0 = rotation_matrix(rc) (se3.cpp:21-31), FP64.
 __device__ __forceinline__ void rodrigues(double rc0, double rc1, double rc2, double R[9]) {
@@ -825,19 +820,40 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
   const Group<kG> G{gm, gbase, &gscratch};
   // class-streamed full mode (multi-class contexts): the table holds one
   // class's rows and columns at a time, so it is sized by the largest class
-  constexpr bool streamed = kMode == kModeStream || kMode == kSiblingsStream;
+  // fix-up launches run the full (or class-streamed) mode on redo-list
+  // entries with the FP64-numerator cross pass
+  constexpr bool kFix = kMode == kFixFull || kMode == kFixStream;
+  constexpr bool streamed =
+      kMode == kModeStream || kMode == kSiblingsStream || kMode == kFixStream;
   constexpr bool kSib = kMode == kSiblings || kMode == kSiblingsStream;
   const int N1 = ctx.n1_total;  // every model mean (feasibility scans)
   const int TN1 = streamed ? ctx.max_n1 : N1, TN2 = streamed ? ctx.max_n2 : ctx.n2_total;
-  const size_t table_f4 = static_cast<size_t>((kRowF4 + kRowPF4) * TN1 + kColF4 * TN2);
+  const size_t table_f4 =
+      static_cast<size_t>(kRowF4 * TN1 + kColF4 * TN2 + (kFix ? kRowPF4 * TN1 : 0));
   const size_t per_warp_f4 = table_f4 + (kSib ? kSibStreamExtraF4 : 0);
   float4* base = smem4 + group * per_warp_f4;
   WarpTables T;
   T.row = base;
   T.col = base + kRowF4 * TN1;
-  T.rowp = T.col + kColF4 * TN2;
-  const bool precise = ctx.precise != 0;
-
+  T.rowp = kFix ? T.col + kColF4 * TN2 : nullptr;  // (a constant outside the fix-up)
+  // redo-list append (main launches): the evaluated node's record, re-read
+  // from memory so no node coordinate stays live through the pair loops;
+  // child >= 0: rotation child `child` of the (parent) record
+  auto redo = [&](long long rec, int child, long long slot) {
+    const unsigned long long k = atomicAdd(args.redo_count, 1ull);
+    if (static_cast<long long>(k) >= args.redo_cap) return;
+    const double* in = args.nodes + 11 * rec;
+    double* o = args.redo_nodes + 11 * k;
+    for (int q = 0; q < 11; ++q) o[q] = in[q];
+    if (child >= 0) {  // subdivide_adaptive's rotation child (se3.cpp:124-131)
+      const double h = 0.5 * in[3];
+      o[0] = in[0] + h * ((child & 4) ? 1 : -1);
+      o[1] = in[1] + h * ((child & 2) ? 1 : -1);
+      o[2] = in[2] + h * ((child & 1) ? 1 : -1);
+      o[3] = h;
+    }
+    args.redo_slot[k] = slot;
+  };
   const double zeta = ctx.zeta;
   const double zeta2 = zeta * zeta;
   const long long n_items = args.n_dev ? *args.n_dev : args.n;
@@ -974,6 +990,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
     // ---- per-row prep: kappa interval, psi_t, projections; row i of the
     // context into table slot `slot`
     double lb_self = 0.0, lb_cross = 0.0, ub_self = 0.0, ub_cross = 0.0, lb_err = 0.0;
+    float lb_amp = 0.0f;  // the theta/B-amplified part of the cross terms' error estimate
     double st_max = 0.0;
     auto prep_row = [&](int i, int slot, float& dsl, float& dsu) {
       const double m0 = ctx.mu[3 * i], m1 = ctx.mu[3 * i + 1], m2 = ctx.mu[3 * i + 2];
@@ -1026,10 +1043,12 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
       pr[3] = make_float4(static_cast<float>(v0 * iv), static_cast<float>(v1 * iv),
                           static_cast<float>(v2 * iv), static_cast<float>(4.0 * sp * sp));
       pr[4] = make_float4(klo, static_cast<float>(sp), static_cast<float>(cp), Fhi);
-      const double s4 = 4.0 * sp * sp, c4 = 4.0 * cp * cp;
-      const float s4h = static_cast<float>(s4), c4h = static_cast<float>(c4);
-      T.rowp[slot] = make_float4(s4h, static_cast<float>(s4 - s4h), c4h,
-                                 static_cast<float>(c4 - c4h));
+      if constexpr (kFix) {
+        const double s4 = 4.0 * sp * sp, c4 = 4.0 * cp * cp;
+        const float s4h = static_cast<float>(s4), c4h = static_cast<float>(c4);
+        T.rowp[slot] = make_float4(s4h, static_cast<float>(s4 - s4h), c4h,
+                                   static_cast<float>(c4 - c4h));
+      }
     };
     if constexpr (!streamed) {
       for (int c = 0; c < ctx.n_classes; ++c) {
@@ -1043,7 +1062,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
           ub_self += static_cast<double>(w * dsu);
         }
       }
-    } else if constexpr (kMode == kModeStream) {
+    } else if constexpr (kMode == kModeStream || kMode == kFixStream) {
       // one class at a time: rows, columns, then its pairs
       for (int c = 0; c < ctx.n_classes; ++c) {
         const ClassSpan cs = ctx.cls[c];
@@ -1059,21 +1078,12 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
         G.sync();
 #ifndef GOSMA_PREP_ONLY
         const ClassSpan loc{0, cs.n1, 0, cs.n2};
-        double dz = 0.0, xl, xu, xe;
         if (same) {
-          class_pairs<kG, true, false, true, kTail>(T, loc, lane, w, lb_self, dz, ub_self, dz,
-                                                    lb_err, dz);
-          cross_span<kG, true, kTail>(T, loc, lane, w, G, precise, xl, xu, xe);
+          class_pairs<kG, true, true, true, kTail, kFix>(T, loc, lane, w, lb_self, lb_cross,
+                                                         ub_self, ub_cross, lb_err, lb_amp);
         } else {
-          class_pairs<kG, false, false, true, kTail>(T, loc, lane, w, lb_self, dz, ub_self, dz,
-                                                     lb_err, dz);
-          cross_span<kG, false, kTail>(T, loc, lane, w, G, precise, xl, xu, xe);
-        }
-        // group totals, carried by lane 0 into the final group sums
-        if (lane == 0) {
-          lb_cross += xl;
-          ub_cross += xu;
-          lb_err += xe;
+          class_pairs<kG, false, true, true, kTail, kFix>(T, loc, lane, w, lb_self, lb_cross,
+                                                          ub_self, ub_cross, lb_err, lb_amp);
         }
 #endif
       }
@@ -1083,13 +1093,13 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
       // rows (with the children's shared psi_r) and self sums, then per child
       // its columns and cross sums, accumulated per child in shared memory
       double* const Rcs = reinterpret_cast<double*>(base + table_f4);  // [8][9]
-      double* const acc = Rcs + 72;                                      // [8][3]
+      double* const acc = Rcs + 72;                                      // [8][4]
       const double hr = 0.5 * rhw;
       for (int ch = lane; ch < 8; ch += kG) {
         const int sx = (ch & 4) ? 1 : -1, sy = (ch & 2) ? 1 : -1, sz = (ch & 1) ? 1 : -1;
         rodrigues(rc0 + hr * sx, rc1 + hr * sy, rc2 + hr * sz, Rcs + 9 * ch);
       }
-      for (int k = lane; k < 24; k += kG) acc[k] = 0.0;
+      for (int k = lane; k < 32; k += kG) acc[k] = 0.0;
       double sl_self = 0.0, su_self = 0.0, se_self = 0.0;
       for (int c = 0; c < ctx.n_classes; ++c) {
         const ClassSpan cs = ctx.cls[c];
@@ -1103,14 +1113,14 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
         su_self += static_cast<double>(w * dsu);
         G.sync();
         const ClassSpan loc{0, cs.n1, 0, cs.n2};
-        double dz = 0.0;
+        double dl = 0.0, du = 0.0;
 #ifndef GOSMA_PREP_ONLY
         if (same) {
-          class_pairs<kG, true, false, true, kTail>(T, loc, lane, w, sl_self, dz, su_self, dz,
-                                                    se_self, dz);
+          class_pairs<kG, true, false, true, kTail, false>(T, loc, lane, w, sl_self, dl, su_self,
+                                                           du, se_self, lb_amp);
         } else {
-          class_pairs<kG, false, false, true, kTail>(T, loc, lane, w, sl_self, dz, su_self, dz,
-                                                     se_self, dz);
+          class_pairs<kG, false, false, true, kTail, false>(T, loc, lane, w, sl_self, dl, su_self,
+                                                            du, se_self, lb_amp);
         }
 #endif
         for (int ch = 0; ch < 8; ++ch) {
@@ -1118,17 +1128,25 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
           column_prep_span(T, ctx, lane, kG, Rcs + 9 * ch, cs.o2, cs.n2);
           G.sync();
           double lcr = 0.0, ucr = 0.0, ecr = 0.0;
+          float acr = 0.0f;
 #ifndef GOSMA_PREP_ONLY
           if (same) {
-            cross_span<kG, true, kTail>(T, loc, lane, w, G, precise, lcr, ucr, ecr);
+            class_pairs<kG, true, true, false, kTail, false>(T, loc, lane, w, dl, lcr, du, ucr,
+                                                             ecr, acr);
           } else {
-            cross_span<kG, false, kTail>(T, loc, lane, w, G, precise, lcr, ucr, ecr);
+            class_pairs<kG, false, true, false, kTail, false>(T, loc, lane, w, dl, lcr, du, ucr,
+                                                              ecr, acr);
           }
 #endif
+          lcr = G.sum(lcr);
+          ucr = G.sum(ucr);
+          ecr = G.sum(ecr);
+          const double acr_sum = G.sum(static_cast<double>(acr));
           if (lane == 0) {
-            acc[3 * ch] += lcr;
-            acc[3 * ch + 1] += ucr;
-            acc[3 * ch + 2] += ecr;
+            acc[4 * ch] += lcr;
+            acc[4 * ch + 1] += ucr;
+            acc[4 * ch + 2] += ecr;
+            acc[4 * ch + 3] += acr_sum;
           }
         }
       }
@@ -1154,7 +1172,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
           args.lower[slot] = INFINITY;
           args.upper[slot] = INFINITY;
         } else {
-          const double lcr = acc[3 * ch], ucr = acc[3 * ch + 1], ecr = acc[3 * ch + 2];
+          const double lcr = acc[4 * ch], ucr = acc[4 * ch + 1], ecr = acc[4 * ch + 2];
           const double mass = sl_self + 2.0 * lcr;
           const double core = (sl_self - 2.0 * lcr) - ctx.lb_err_scale * (se_self + ecr) -
                               ctx.lb_margin * mass;
@@ -1163,6 +1181,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
           if (!(lo >= args.skip_upper_at) && have_center) up = su_self - 2.0 * ucr;
           args.lower[slot] = lo;
           args.upper[slot] = up;
+          if (args.redo_count && acc[4 * ch + 3] > ctx.redo_rel * 2.0 * lcr) redo(node, ch, slot);
         }
       }
       G.sync();
@@ -1187,13 +1206,13 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
         for (int c = 0; c < ctx.n_classes; ++c) {
           const ClassSpan cs = ctx.cls[c];
           const float w = static_cast<float>(ctx.cls_w[c]);
-          double dz = 0.0;
+          double dl = 0.0, du = 0.0;
           if (same) {
-            class_pairs<kG, true, false, true, kTail>(T, cs, lane, w, sl_self, dz, su_self, dz,
-                                                      se_self, dz);
+            class_pairs<kG, true, false, true, kTail, false>(T, cs, lane, w, sl_self, dl, su_self,
+                                                             du, se_self, lb_amp);
           } else {
-            class_pairs<kG, false, false, true, kTail>(T, cs, lane, w, sl_self, dz, su_self, dz,
-                                                       se_self, dz);
+            class_pairs<kG, false, false, true, kTail, false>(T, cs, lane, w, sl_self, dl,
+                                                              su_self, du, se_self, lb_amp);
           }
         }
         sl_self = G.sum(sl_self);
@@ -1223,20 +1242,23 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
         G.sync();
         column_prep(T, ctx, lane, kG, Rcs + 9 * ch);
         G.sync();
-        double lcr = 0.0, ucr = 0.0, ecr = 0.0;
+        double lcr = 0.0, ucr = 0.0, ecr = 0.0, dl = 0.0, du = 0.0;
+        float acr = 0.0f;
         for (int c = 0; c < ctx.n_classes; ++c) {
           const ClassSpan cs = ctx.cls[c];
           const float w = static_cast<float>(ctx.cls_w[c]);
-          double xl, xu, xe;
           if (same) {
-            cross_span<kG, true, kTail>(T, cs, lane, w, G, precise, xl, xu, xe);
+            class_pairs<kG, true, true, false, kTail, false>(T, cs, lane, w, dl, lcr, du, ucr, ecr,
+                                                             acr);
           } else {
-            cross_span<kG, false, kTail>(T, cs, lane, w, G, precise, xl, xu, xe);
+            class_pairs<kG, false, true, false, kTail, false>(T, cs, lane, w, dl, lcr, du, ucr,
+                                                              ecr, acr);
           }
-          lcr += xl;
-          ucr += xu;
-          ecr += xe;
         }
+        lcr = G.sum(lcr);
+        ucr = G.sum(ucr);
+        ecr = G.sum(ecr);
+        const double acr_sum = G.sum(static_cast<double>(acr));
         if (lane == 0) {
           const double mass = sl_self + 2.0 * lcr;
           const double core = (sl_self - 2.0 * lcr) - ctx.lb_err_scale * (se_self + ecr) -
@@ -1246,6 +1268,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
           if (!(lo >= args.skip_upper_at) && have_center) up = su_self - 2.0 * ucr;
           args.lower[slot] = lo;
           args.upper[slot] = up;
+          if (args.redo_count && acr_sum > ctx.redo_rel * 2.0 * lcr) redo(node, ch, slot);
         }
         G.sync();
       }
@@ -1270,8 +1293,9 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
           o[0] = o[1] = o[2] = 0.0;
           o[3] = 1.0;  // infeasible
         } else {
-          args.lower[node] = INFINITY;
-          args.upper[node] = INFINITY;
+          const long long out = kFix ? args.out_slot[node] : node;
+          args.lower[out] = INFINITY;
+          args.upper[out] = INFINITY;
         }
       }
       G.sync();
@@ -1283,31 +1307,17 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
 
     // ---- pair sweeps (GOSMA_PREP_ONLY: times the per-node prep alone)
 #ifndef GOSMA_PREP_ONLY
-    double xl_tot = 0.0, xu_tot = 0.0, xe_tot = 0.0;  // cross sums: group totals
     for (int c = 0; !streamed && c < ctx.n_classes; ++c) {
       const ClassSpan cs = ctx.cls[c];
       const float w = static_cast<float>(ctx.cls_w[c]);
       constexpr bool kC = kMode != kSelfOnly, kS = kMode != kCrossCached;
-      double dz = 0.0, xl = 0.0, xu = 0.0, xe = 0.0;
       if (same) {
-        if (kS)
-          class_pairs<kG, true, false, true, kTail>(T, cs, lane, w, lb_self, dz, ub_self, dz,
-                                                    lb_err, dz);
-        if (kC) cross_span<kG, true, kTail>(T, cs, lane, w, G, precise, xl, xu, xe);
+        class_pairs<kG, true, kC, kS, kTail, kFix>(T, cs, lane, w, lb_self, lb_cross, ub_self,
+                                                   ub_cross, lb_err, lb_amp);
       } else {
-        if (kS)
-          class_pairs<kG, false, false, true, kTail>(T, cs, lane, w, lb_self, dz, ub_self, dz,
-                                                     lb_err, dz);
-        if (kC) cross_span<kG, false, kTail>(T, cs, lane, w, G, precise, xl, xu, xe);
+        class_pairs<kG, false, kC, kS, kTail, kFix>(T, cs, lane, w, lb_self, lb_cross, ub_self,
+                                                    ub_cross, lb_err, lb_amp);
       }
-      xl_tot += xl;
-      xu_tot += xu;
-      xe_tot += xe;
-    }
-    if (lane == 0) {  // lane 0 carries the group totals into the sums below
-      lb_cross += xl_tot;
-      ub_cross += xu_tot;
-      lb_err += xe_tot;
     }
 #endif
     lb_self = G.sum(lb_self);
@@ -1315,6 +1325,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
     ub_self = G.sum(ub_self);
     ub_cross = G.sum(ub_cross);
     lb_err = G.sum(lb_err);
+    double amp_sum = 0.0;
+    if constexpr (!kFix && kMode != kSelfOnly) amp_sum = G.sum(static_cast<double>(lb_amp));
     if (kMode == kSelfOnly) {
       if (lane == 0) {
         double* o = args.self_out + 4 * node;
@@ -1341,8 +1353,12 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
       const double lo = core < parent_lower ? parent_lower : core;  // std::max(core, lower)
       double up = INFINITY;
       if (!(lo >= args.skip_upper_at) && have_center) up = ub_self - 2.0 * ub_cross;
-      args.lower[node] = lo;
-      args.upper[node] = up;
+      const long long out = kFix ? args.out_slot[node] : node;
+      args.lower[out] = lo;
+      args.upper[out] = up;
+      if constexpr (!kFix) {
+        if (args.redo_count && amp_sum > ctx.redo_rel * 2.0 * lb_cross) redo(node, -1, node);
+      }
     }
     G.sync();
   }
@@ -1351,9 +1367,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
 }  // namespace
 
 size_t eval_smem_per_warp(const DevCtx& ctx, int mode) {
-  const bool streamed = mode == kModeStream || mode == kSiblingsStream;
+  const bool streamed = mode == kModeStream || mode == kSiblingsStream || mode == kFixStream;
   const int n1 = streamed ? ctx.max_n1 : ctx.n1_total, n2 = streamed ? ctx.max_n2 : ctx.n2_total;
-  size_t f4 = static_cast<size_t>((kRowF4 + kRowPF4) * n1 + kColF4 * n2);
+  size_t f4 = static_cast<size_t>(kRowF4 * n1 + kColF4 * n2);
+  if (mode == kFixFull || mode == kFixStream) f4 += static_cast<size_t>(kRowPF4 * n1);
   if (mode == kSiblings || mode == kSiblingsStream) f4 += kSibStreamExtraF4;
   return f4 * sizeof(float4);
 }
@@ -1481,11 +1498,9 @@ cudaError_t launch_group(const DevCtx& ctx, const EvalArgs& a, int sm_count,
 }
 
 template <int kMode>
-cudaError_t launch_mode(const DevCtx& ctx, const EvalArgs& a, int sm_count,
-                        cudaStream_t stream) {
-  if (a.n <= 0) return cudaSuccess;
-  if (!a.work) return cudaErrorMemoryAllocation;  // no node counter for this stream
-  switch (group_lanes(ctx, kMode)) {
+cudaError_t launch_dispatch(const DevCtx& ctx, const EvalArgs& a, int sm_count,
+                            cudaStream_t stream, int lanes) {
+  switch (lanes) {
     case kCtaGroup:
       return launch_group<kMode, kCtaGroup, false>(ctx, a, sm_count, stream);
     case 1:
@@ -1498,6 +1513,46 @@ cudaError_t launch_mode(const DevCtx& ctx, const EvalArgs& a, int sm_count,
       return ctx.tail_chunks ? launch_group<kMode, 32, true>(ctx, a, sm_count, stream)
                              : launch_group<kMode, 32, false>(ctx, a, sm_count, stream);
   }
+}
+
+template <int kMode>
+cudaError_t launch_mode(const DevCtx& ctx, const EvalArgs& a, int sm_count,
+                        cudaStream_t stream) {
+  if (a.n <= 0) return cudaSuccess;
+  if (!a.work) return cudaErrorMemoryAllocation;  // no node counter for this stream
+  const bool fix = kMode != kSelfOnly && a.redo_count && ctx.precise;
+  EvalArgs m = a;
+  if (!fix) {
+    m.redo_count = nullptr;
+  } else {
+    const cudaError_t e = cudaMemsetAsync(a.redo_count, 0, sizeof(unsigned long long), stream);
+    if (e != cudaSuccess) return e;
+  }
+  cudaError_t e = launch_dispatch<kMode>(ctx, m, sm_count, stream, group_lanes(ctx, kMode));
+  if (e != cudaSuccess || !fix) return e;
+  static const bool stats = std::getenv("GOSMA_REDO_STATS") != nullptr;
+  if (stats) {  // diagnostics: how many items the fix-up re-evaluates
+    unsigned long long k = 0;
+    cudaMemcpyAsync(&k, a.redo_count, sizeof(k), cudaMemcpyDeviceToHost, stream);
+    cudaStreamSynchronize(stream);
+    std::fprintf(stderr, "[gosma] mode %d: %llu of %lld items to the precise fix-up\n", kMode, k,
+                 a.n);
+  }
+  // the redo list, re-evaluated with the FP64 numerator (its count stays on
+  // the device: the grid is sized for the capacity, idle groups exit at once)
+  EvalArgs f{};
+  f.nodes = a.redo_nodes;
+  f.n = a.redo_cap;
+  f.n_dev = reinterpret_cast<const long long*>(a.redo_count);
+  f.out_slot = a.redo_slot;
+  f.skip_upper_at = a.skip_upper_at;
+  f.lower = a.lower;
+  f.upper = a.upper;
+  f.split_rot = nullptr;
+  f.work = a.work;
+  return ctx.stream_classes ? launch_dispatch<kFixStream>(ctx, f, sm_count, stream,
+                                              group_lanes(ctx, kFixStream))
+                : launch_dispatch<kFixFull>(ctx, f, sm_count, stream, group_lanes(ctx, kFixFull));
 }
 
 }  // namespace

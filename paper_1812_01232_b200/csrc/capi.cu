@@ -26,15 +26,51 @@ int cuda_error(cudaError_t e, const char* where) {
   return set_error(GOSMA_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
 }
 
+namespace {
+gosma_ctx::StreamScratch* stream_scratch(gosma_ctx* ctx, cudaStream_t s) {
+  for (auto& ws : ctx->work_slots)
+    if (ws.stream == s) return &ws;
+  gosma_ctx::StreamScratch ws;
+  ws.stream = s;
+  if (cudaMalloc(&ws.work, sizeof(unsigned int)) != cudaSuccess) return nullptr;
+  ctx->work_slots.push_back(ws);
+  return &ctx->work_slots.back();
+}
+}  // namespace
+
 unsigned int* work_counter(gosma_ctx* ctx, cudaStream_t s) {
   if (s == ctx->stream || s == nullptr) return static_cast<unsigned int*>(ctx->d_work);
   std::lock_guard<std::mutex> lk(ctx->work_mu);
-  for (const auto& ws : ctx->work_slots)
-    if (ws.first == s) return static_cast<unsigned int*>(ws.second);
-  void* p = nullptr;
-  if (cudaMalloc(&p, sizeof(unsigned int)) != cudaSuccess) return nullptr;
-  ctx->work_slots.emplace_back(s, p);
-  return static_cast<unsigned int*>(p);
+  gosma_ctx::StreamScratch* ws = stream_scratch(ctx, s);
+  return ws ? static_cast<unsigned int*>(ws->work) : nullptr;
+}
+
+cudaError_t attach_redo(gosma_ctx* ctx, cudaStream_t s, long long n_out, EvalArgs* a) {
+  if (s == nullptr) s = ctx->stream;
+  std::lock_guard<std::mutex> lk(ctx->work_mu);
+  gosma_ctx::StreamScratch* ws = stream_scratch(ctx, s);
+  if (!ws) return cudaErrorMemoryAllocation;
+  if (n_out > ws->redo_cap) {
+    cudaFree(ws->redo_count);
+    cudaFree(ws->redo_nodes);
+    cudaFree(ws->redo_slot);
+    ws->redo_count = nullptr;
+    ws->redo_nodes = nullptr;
+    ws->redo_slot = nullptr;
+    ws->redo_cap = 0;
+    const long long cap = std::max<long long>(n_out, 1024);
+    cudaError_t e;
+    if ((e = cudaMalloc(&ws->redo_count, sizeof(unsigned long long))) != cudaSuccess ||
+        (e = cudaMalloc(&ws->redo_nodes, cap * 11 * sizeof(double))) != cudaSuccess ||
+        (e = cudaMalloc(&ws->redo_slot, cap * sizeof(long long))) != cudaSuccess)
+      return e;
+    ws->redo_cap = cap;
+  }
+  a->redo_count = ws->redo_count;
+  a->redo_nodes = ws->redo_nodes;
+  a->redo_slot = ws->redo_slot;
+  a->redo_cap = ws->redo_cap;
+  return cudaSuccess;
 }
 
 namespace {
@@ -119,6 +155,12 @@ int ctx_upload(gosma_ctx* ctx) {
     return e && std::string(e) == "0";
   }();
   d.precise = precise_off ? 0 : 1;
+  static const double redo_rel = [] {  // GOSMA_REDO_REL: fix-up threshold (A/B)
+    const char* e = std::getenv("GOSMA_REDO_REL");
+    const double v = e ? std::atof(e) : 0.0;
+    return v > 0.0 ? v : 8e-5;
+  }();
+  d.redo_rel = redo_rel;
   for (const ClassSpan& cs : spans)
     if (cs.n1 % 32 != 0 && cs.n1 % 32 <= 16) d.tail_chunks = 1;
   ClassSpan* dspans;
@@ -164,7 +206,12 @@ void ctx_free_device(gosma_ctx* ctx) {
   ctx->d_work = nullptr;
   {
     std::lock_guard<std::mutex> lk(ctx->work_mu);
-    for (auto& ws : ctx->work_slots) cudaFree(ws.second);
+    for (auto& ws : ctx->work_slots) {
+      cudaFree(ws.work);
+      cudaFree(ws.redo_count);
+      cudaFree(ws.redo_nodes);
+      cudaFree(ws.redo_slot);
+    }
     ctx->work_slots.clear();
   }
   cudaFree(ctx->d_cache_nodes);
@@ -411,7 +458,8 @@ int gosma_eval_bounds_device(gosma_ctx* ctx, const gosma_node* d_nodes, size_t n
   a.upper = d_upper;
   a.split_rot = d_split;
   a.work = work_counter(ctx, s);
-  const cudaError_t e = launch_eval_bounds(ctx->dev, a, ctx->sm_count, s);
+  cudaError_t e = attach_redo(ctx, s, static_cast<long long>(n), &a);
+  if (e == cudaSuccess) e = launch_eval_bounds(ctx->dev, a, ctx->sm_count, s);
   if (e != cudaSuccess) return cuda_error(e, "eval_bounds launch");
   return GOSMA_OK;
 }
@@ -454,6 +502,8 @@ int gosma_eval_children_device(gosma_ctx* ctx, const gosma_node* d_parents, cons
   a.upper = d_upper;
   a.split_rot = d_child_split;
   a.work = work_counter(ctx, s);
+  if ((e = attach_redo(ctx, s, static_cast<long long>(8 * n), &a)) != cudaSuccess)
+    return cuda_error(e, "redo list");
   EvalArgs b = a;
   b.nodes = reinterpret_cast<const double*>(d_parents);
   b.n = static_cast<long long>(n);
@@ -513,6 +563,8 @@ int gosma_eval_bounds_cached_device(gosma_ctx* ctx, const gosma_node* d_nodes, s
   a.upper = d_upper;
   a.split_rot = d_split;
   a.tindex = d_tindex;
+  if ((e = attach_redo(ctx, s, static_cast<long long>(n), &a)) != cudaSuccess)
+    return cuda_error(e, "redo list");
   if ((e = launch_eval_cross_cached(ctx->dev, a, ctx->sm_count, s)) != cudaSuccess)
     return cuda_error(e, "cross kernel");
   return GOSMA_OK;

@@ -51,10 +51,19 @@ struct gosma_ctx {
   double lb_margin = gosma::kDefaultLbMargin;
   std::vector<void*> owned;
   void* d_work = nullptr;  // persistent-warp node counter of launches on `stream`
-  // one node counter per caller stream (the kernels' persistent warps claim
+  // per caller stream: a node counter (the kernels' persistent warps claim
   // nodes from it; two launches in flight on different streams must not share
-  // one): work_counter() hands them out, ctx_free_device releases them
-  std::vector<std::pair<cudaStream_t, void*>> work_slots;
+  // one) and the precise fix-up's redo list; work_counter() / attach_redo()
+  // hand them out, ctx_free_device releases them
+  struct StreamScratch {
+    cudaStream_t stream = nullptr;
+    void* work = nullptr;
+    unsigned long long* redo_count = nullptr;
+    double* redo_nodes = nullptr;
+    long long* redo_slot = nullptr;
+    long long redo_cap = 0;
+  };
+  std::vector<StreamScratch> work_slots;
   std::mutex work_mu;
   gosma_node* d_cache_nodes = nullptr;  // translation-cached mode scratch
   double* d_cache_self = nullptr;
@@ -87,6 +96,10 @@ namespace gosma {
 // The node counter of bound-kernel launches on stream s (launches on one
 // stream are ordered, so they may share it; other streams get their own).
 unsigned int* work_counter(gosma_ctx* ctx, cudaStream_t s);
+// Points a's redo list (precise fix-up) at the stream's buffers, grown to hold
+// n_out entries (one per output slot, so it never overflows). Not during
+// stream capture (it may allocate): captured callers leave it unset.
+cudaError_t attach_redo(gosma_ctx* ctx, cudaStream_t s, long long n_out, EvalArgs* a);
 int set_error(int code, const std::string& msg);
 int cuda_error(cudaError_t e, const char* where);
 }  // namespace gosma

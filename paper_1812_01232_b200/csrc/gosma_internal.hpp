@@ -48,7 +48,8 @@ struct DevCtx {
   int tail_chunks;       // some class has a last row chunk of <= 16 of 32 rows
   int max_n2;            // largest class n2
   int stream_classes;    // full mode keeps one class's table at a time (n_classes > 1)
-  int precise;           // precise cross pass for nodes whose FP32 error estimate is large
+  int precise;           // precise fix-up for nodes whose FP32 error estimate is large
+  double redo_rel;       // fix-up threshold: amplified estimate / cross mass
 };
 
 // Host-side master copy of one class (ClassData, objective.hpp:19-31).
@@ -81,6 +82,15 @@ struct EvalArgs {
   const int* item_index = nullptr;  // optional work list: item -> node slot (or selection k)
   const unsigned int* sel = nullptr;  // siblings mode: selection k -> pool slot
   const long long* n_dev = nullptr;   // item count in device memory (<= n, which sizes the grid)
+  // precise fix-up: nodes whose cross-term error estimate has a
+  // large theta/B-amplified part are appended here by the main pass (node
+  // record + output slot) and re-evaluated by a second launch with the
+  // alignment angle's numerator in FP64; null: no fix-up
+  unsigned long long* redo_count = nullptr;
+  double* redo_nodes = nullptr;      // 11 doubles per entry
+  long long* redo_slot = nullptr;    // output slot of each entry
+  long long redo_cap = 0;
+  const long long* out_slot = nullptr;  // fix-up launches: item -> output slot
 };
 
 cudaError_t launch_eval_bounds(const DevCtx& ctx, const EvalArgs& a, int sm_count,

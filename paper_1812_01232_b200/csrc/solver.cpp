@@ -885,6 +885,8 @@ int gosma_solver_expand(gosma_solver* S, double limit, unsigned long long max_ev
   S->lap(1, s);
   EvalArgs a;
   a.work = work_counter(ctx, s);
+  if ((e = attach_redo(ctx, s, static_cast<long long>(n_kids), &a)) != cudaSuccess)
+    return cuda_error(e, "redo list");
   a.skip_upper_at = S->dstar();
   if (S->cached) {
     // Translation-cached bounds: the self sums once per distinct cuboid
