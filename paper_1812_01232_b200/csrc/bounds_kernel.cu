@@ -327,7 +327,7 @@ __device__ __forceinline__ void sincos_sq(float hx, float hy, float hz, float lx
 // s4 = 4 sin^2(psi/2) from FP64 per-row prep: the theta ~ psi cancellation
 // happens in x - s4, where both operands carry ~1e-7 relative error, instead
 // of in sin/cos products.
-template <bool kSame, bool kPrecise = false>
+template <bool kSame, bool kPrecise = false, bool kExact = true>
 __device__ __forceinline__ void cross_pair(const Row& r, const float4 qa, const float4 qb, float& l,
                                            float& u, float& ma, float& mb,
                                            const float4 rp = float4{}) {
@@ -395,11 +395,15 @@ __device__ __forceinline__ void cross_pair(const Row& r, const float4 qa, const 
   float t2 = ex2f(e2) * rK2;
   // exact paths (one rarely-taken branch): K's interior minimum
   // (cos B < -klo/k2, i.e. c2 k2 + 2 klo < 2 k2) or small K
-  const bool s1 = e1 > kNegligibleLog2 && (fmaf(c2, k2, r.klo2) < k2 + k2 || !(K1 > 15.0f));
-  const bool s2 = e2 > kNegligibleLog2 && !(K2 > 15.0f);
-  if (s1 | s2) {
-    if (s1) t1 = cross_lb_exact(r.klo, r.khi, k2, 4.0f - c2, c2, K1, e1);
-    if (s2) t2 = ex2f(e2 + log2w(K2));
+  // (kExact = false: the node's concentrations exclude every case below
+  // from non-negligible terms, see exact_needed)
+  if constexpr (kExact) {
+    const bool s1 = e1 > kNegligibleLog2 && (fmaf(c2, k2, r.klo2) < k2 + k2 || !(K1 > 15.0f));
+    const bool s2 = e2 > kNegligibleLog2 && !(K2 > 15.0f);
+    if (s1 | s2) {
+      if (s1) t1 = cross_lb_exact(r.klo, r.khi, k2, 4.0f - c2, c2, K1, e1);
+      if (s2) t2 = ex2f(e2 + log2w(K2));
+    }
   }
   // FP32 error estimate of the LB term: B = theta - psi
   // carries ~u theta absolute error, amplified in e1 by min(x, y)/num (the
@@ -424,7 +428,7 @@ __device__ __noinline__ float self_lb_exact(float alo, float ahi, float blo, flo
   return ex2f(e1 + log2w(sqf(fmaxf(m, 0.0f))));
 }
 
-template <bool kSame>
+template <bool kSame, bool kExact = true>
 __device__ __forceinline__ void self_pair(const float4& a0, const float4& a1, const float4& a2,
                                           const float4& a3, const float4* pa, const float4* pb,
                                           float& l, float& u, float& me) {
@@ -482,11 +486,13 @@ __device__ __forceinline__ void self_pair(const float4& a0, const float4& a1, co
   float t1 = ex2f(e1) * rKhh;
   float t2 = ex2f(e2) * rK2;
   // exact paths (one rarely-taken branch, as in cross_pair)
-  const bool x1 = e1 > kNegligibleLog2 && (c2 < 2.0f || !(Khh > 15.0f));
-  const bool x2 = e2 > kNegligibleLog2 && !(K2 > 15.0f);
-  if (x1 | x2) {
-    if (x1) t1 = self_lb_exact(pa[4].x, ahi, pb[4].x, bhi, c2, K2hh, e1);
-    if (x2) t2 = ex2f(e2 + log2w(K2));
+  if constexpr (kExact) {
+    const bool x1 = e1 > kNegligibleLog2 && (c2 < 2.0f || !(Khh > 15.0f));
+    const bool x2 = e2 > kNegligibleLog2 && !(K2 > 15.0f);
+    if (x1 | x2) {
+      if (x1) t1 = self_lb_exact(pa[4].x, ahi, pb[4].x, bhi, c2, K2hh, e1);
+      if (x2) t2 = ex2f(e2 + log2w(K2));
+    }
   }
   const float ft1 = b1.y * t1;  // F_j (Flo); 2 F_i is applied to the row sum
   l += ft1;
@@ -521,7 +527,7 @@ __device__ __forceinline__ Row load_row(const WarpTables& T, int i) {
   return r;
 }
 
-template <int kG, bool kSame, bool kCross, bool kSelf, bool kPrecise>
+template <int kG, bool kSame, bool kCross, bool kSelf, bool kPrecise, bool kExact>
 __device__ __forceinline__ void class_pairs_rows(const WarpTables& T, const ClassSpan cs, int lane,
                                             float w, double& lb_self, double& lb_cross,
                                             double& ub_self, double& ub_cross, double& lb_err,
@@ -538,7 +544,7 @@ __device__ __forceinline__ void class_pairs_rows(const WarpTables& T, const Clas
       const float4* cp = T.col + cs.o2 * kColF4;  // pointer walk: no index math per pair
       const float4* const ce = cp + cs.n2 * kColF4;
 #pragma unroll kUnrollPairs
-      for (; cp < ce; cp += kColF4) cross_pair<kSame, kPrecise>(r, cp[0], cp[1], l, u, ma, mb, rp);
+      for (; cp < ce; cp += kColF4) cross_pair<kSame, kPrecise, kExact>(r, cp[0], cp[1], l, u, ma, mb, rp);
       lb_cross += static_cast<double>(w * r.Fhi * l);
       const float amp = 2.0f * w * r.Fhi * ma * kErrAmp;
       lb_err += static_cast<double>(
@@ -568,11 +574,11 @@ __device__ __forceinline__ void class_pairs_rows(const WarpTables& T, const Clas
       for (int d = dfull; d > 0; --d) {
         pb += kRowF4;
         pb = pb == rend ? rbeg : pb;
-        self_pair<kSame>(a0, a1, a2, a3, pa, pb, l, u, me);
+        self_pair<kSame, kExact>(a0, a1, a2, a3, pa, pb, l, u, me);
       }
       if (even && il < n / 2) {
         const int j = i + n / 2;
-        self_pair<kSame>(a0, a1, a2, a3, pa, T.row + j * kRowF4, l, u, me);
+        self_pair<kSame, kExact>(a0, a1, a2, a3, pa, T.row + j * kRowF4, l, u, me);
       }
       lb_self += static_cast<double>(2.0f * w * a1.y * l);
       lb_err += static_cast<double>(2.0f * w * a1.y * fmaf(me, kErrExp, l * kErrTerm));
@@ -585,7 +591,7 @@ __device__ __forceinline__ void class_pairs_rows(const WarpTables& T, const Clas
 // gives each row k = kG / r lanes ("slots") sharing its partners round-robin
 // (the node sums are sums over pairs, so any pair -> lane assignment is
 // exact). Separate instantiation: the plain loops stay tighter for full chunks.
-template <int kG, bool kSame, bool kCross, bool kSelf, bool kPrecise>
+template <int kG, bool kSame, bool kCross, bool kSelf, bool kPrecise, bool kExact>
 __device__ __forceinline__ void class_pairs_tail(const WarpTables& T, const ClassSpan cs,
                                                  int lane, float w, double& lb_self,
                                                  double& lb_cross, double& ub_self,
@@ -606,7 +612,7 @@ __device__ __forceinline__ void class_pairs_tail(const WarpTables& T, const Clas
       const int cstep = k * kColF4;
 #pragma unroll kUnrollPairs
       for (; cp < ce; cp += cstep)
-        cross_pair<kSame, kPrecise>(rw, cp[0], cp[1], l, u, ma, mb, rp);
+        cross_pair<kSame, kPrecise, kExact>(rw, cp[0], cp[1], l, u, ma, mb, rp);
       lb_cross += static_cast<double>(w * rw.Fhi * l);
       const float amp = 2.0f * w * rw.Fhi * ma * kErrAmp;
       lb_err += static_cast<double>(
@@ -639,11 +645,11 @@ __device__ __forceinline__ void class_pairs_tail(const WarpTables& T, const Clas
       for (int d = 1 + slot; d <= dfull; d += k) {
         pb += step;
         pb = pb >= rend ? pb - n * kRowF4 : pb;
-        self_pair<kSame>(a0, a1, a2, a3, pa, pb, l, u, me);
+        self_pair<kSame, kExact>(a0, a1, a2, a3, pa, pb, l, u, me);
       }
       if (even && slot == 0 && il < n / 2) {
         const int j = i + n / 2;
-        self_pair<kSame>(a0, a1, a2, a3, pa, T.row + j * kRowF4, l, u, me);
+        self_pair<kSame, kExact>(a0, a1, a2, a3, pa, T.row + j * kRowF4, l, u, me);
       }
       lb_self += static_cast<double>(2.0f * w * a1.y * l);
       lb_err += static_cast<double>(2.0f * w * a1.y * fmaf(me, kErrExp, l * kErrTerm));
@@ -656,14 +662,44 @@ template <int kG, bool kSame, bool kCross, bool kSelf, bool kTail, bool kPrecise
 __device__ __forceinline__ void class_pairs(const WarpTables& T, const ClassSpan cs, int lane,
                                             float w, double& lb_self, double& lb_cross,
                                             double& ub_self, double& ub_cross, double& lb_err,
-                                            float& lb_amp) {
+                                            float& lb_amp, bool exact) {
+  // the fast loop copies only for groups of >= 16 lanes (classes of > 24
+  // rows): short loops gain nothing from them and lose to the larger code
+  exact = exact || kG < 16;
   if constexpr (kTail) {
-    class_pairs_tail<kG, kSame, kCross, kSelf, kPrecise>(T, cs, lane, w, lb_self, lb_cross,
-                                                         ub_self, ub_cross, lb_err, lb_amp);
+    if (exact)
+      class_pairs_tail<kG, kSame, kCross, kSelf, kPrecise, true>(
+          T, cs, lane, w, lb_self, lb_cross, ub_self, ub_cross, lb_err, lb_amp);
+    else
+      class_pairs_tail<kG, kSame, kCross, kSelf, kPrecise, false>(
+          T, cs, lane, w, lb_self, lb_cross, ub_self, ub_cross, lb_err, lb_amp);
   } else {
-    class_pairs_rows<kG, kSame, kCross, kSelf, kPrecise>(T, cs, lane, w, lb_self, lb_cross,
-                                                         ub_self, ub_cross, lb_err, lb_amp);
+    if (exact)
+      class_pairs_rows<kG, kSame, kCross, kSelf, kPrecise, true>(
+          T, cs, lane, w, lb_self, lb_cross, ub_self, ub_cross, lb_err, lb_amp);
+    else
+      class_pairs_rows<kG, kSame, kCross, kSelf, kPrecise, false>(
+          T, cs, lane, w, lb_self, lb_cross, ub_self, ub_cross, lb_err, lb_amp);
   }
+}
+
+// Whether a node's terms can take the rare exact paths (small K, the cross
+// LB's interior K minimum, the self LB's corner maximum past 90 degrees) with
+// a value that matters. Those cases need cos B < 0, cos A < 0 or K <= 15;
+// with every row's kappa_lo >= 90 (kappa_hi and kappa at t* are larger) and
+// kappa_lo k2 / (kappa_lo + k2) >= 45 for the smallest image concentration,
+// each of them forces the pair's exponent below -64 (log2: |excess| >=
+// ab (1 - cos) / (a + b) >= ab / (a + b), times log2 e), where a term is at
+// most 2^-64 of its F_i G_j W(K) prefactor, i.e. below 1e-13 of the node's
+// |term| mass even for kappa2 / kappa1 ratios of 1e5: skipping the exact W(K)
+// for such terms moves the bound by far less than the 2e-7 mass margin.
+// Group-uniform (one vote), so the fast loops never diverge.
+#ifndef GOSMA_EXACT_KLO
+#define GOSMA_EXACT_KLO 90.0f
+#endif
+__device__ __forceinline__ bool exact_needed_row(float klo_min, float k2_min) {
+  constexpr float kLo = GOSMA_EXACT_KLO, kH = 0.5f * GOSMA_EXACT_KLO;
+  return !(klo_min >= kLo && klo_min * k2_min >= kH * (klo_min + k2_min));
 }
 
 // Half-angle of psi_trans (se3.cpp:72-92) for a mean outside the cuboid: the
@@ -856,7 +892,11 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
   };
   const double zeta = ctx.zeta;
   const double zeta2 = zeta * zeta;
-  const long long n_items = args.n_dev ? *args.n_dev : args.n;
+  // fix-up launches: the count stays on the device (it may exceed the list's
+  // capacity, whose overflow keeps its FP32 bounds); an empty list exits
+  // before any work-counter traffic
+  const long long n_items = args.n_dev ? min(*args.n_dev, args.n) : args.n;
+  if (n_items <= 0) return;
   for (;;) {
     long long node = 0;
     if (lane == 0) node = static_cast<long long>(atomicAdd(args.work, 1u));
@@ -992,6 +1032,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
     double lb_self = 0.0, lb_cross = 0.0, ub_self = 0.0, ub_cross = 0.0, lb_err = 0.0;
     float lb_amp = 0.0f;  // the theta/B-amplified part of the cross terms' error estimate
     double st_max = 0.0;
+    float klo_min = INFINITY;  // smallest kappa_lo over this lane's rows (exact_needed_row)
     auto prep_row = [&](int i, int slot, float& dsl, float& dsu) {
       const double m0 = ctx.mu[3 * i], m1 = ctx.mu[3 * i + 1], m2 = ctx.mu[3 * i + 2];
       const double is2 = ctx.inv_s2[i];
@@ -1003,6 +1044,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
       const double dhi2 = (a0 + h0) * (a0 + h0) + (a1 + h1) * (a1 + h1) + (a2 + h2) * (a2 + h2);
       const float klo = static_cast<float>(dlo2 * is2 + 1.0);
       const float khi = static_cast<float>(dhi2 * is2 + 1.0);
+      klo_min = fminf(klo_min, klo);
       const double un2 = u0 * u0 + u1 * u1 + u2 * u2;
       double c0 = 1.0, c1 = 0.0, c2 = 0.0;  // UnitX when the mean is at the centre
       if (un2 > 1e-24) {
@@ -1069,8 +1111,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
         const float w = static_cast<float>(ctx.cls_w[c]);
         float dsl = 0.0f, dsu = 0.0f;
         G.sync();  // the previous class's pairs are done with the table
+        klo_min = INFINITY;
         for (int il = lane; il < cs.n1; il += kG) prep_row(cs.o1 + il, il, dsl, dsu);
         if (infeasible) continue;  // (rows still feed the split decision)
+        const bool exact = G.any(exact_needed_row(klo_min, ctx.min_k2));
         lb_self += static_cast<double>(w * dsl);
         lb_err += static_cast<double>(w * dsl * kErrTerm);
         ub_self += static_cast<double>(w * dsu);
@@ -1080,10 +1124,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
         const ClassSpan loc{0, cs.n1, 0, cs.n2};
         if (same) {
           class_pairs<kG, true, true, true, kTail, kFix>(T, loc, lane, w, lb_self, lb_cross,
-                                                         ub_self, ub_cross, lb_err, lb_amp);
+                                                         ub_self, ub_cross, lb_err, lb_amp, exact);
         } else {
           class_pairs<kG, false, true, true, kTail, kFix>(T, loc, lane, w, lb_self, lb_cross,
-                                                          ub_self, ub_cross, lb_err, lb_amp);
+                                                          ub_self, ub_cross, lb_err, lb_amp, exact);
         }
 #endif
       }
@@ -1106,8 +1150,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
         const float w = static_cast<float>(ctx.cls_w[c]);
         float dsl = 0.0f, dsu = 0.0f;
         G.sync();  // the previous class's pairs are done with the table
+        klo_min = INFINITY;
         for (int il = lane; il < cs.n1; il += kG) prep_row(cs.o1 + il, il, dsl, dsu);
         if (infeasible) continue;  // (rows still feed the split decision)
+        const bool exact = G.any(exact_needed_row(klo_min, ctx.min_k2));
         sl_self += static_cast<double>(w * dsl);
         se_self += static_cast<double>(w * dsl * kErrTerm);
         su_self += static_cast<double>(w * dsu);
@@ -1117,10 +1163,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
 #ifndef GOSMA_PREP_ONLY
         if (same) {
           class_pairs<kG, true, false, true, kTail, false>(T, loc, lane, w, sl_self, dl, su_self,
-                                                           du, se_self, lb_amp);
+                                                           du, se_self, lb_amp, exact);
         } else {
           class_pairs<kG, false, false, true, kTail, false>(T, loc, lane, w, sl_self, dl, su_self,
-                                                            du, se_self, lb_amp);
+                                                            du, se_self, lb_amp, exact);
         }
 #endif
         for (int ch = 0; ch < 8; ++ch) {
@@ -1132,10 +1178,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
 #ifndef GOSMA_PREP_ONLY
           if (same) {
             class_pairs<kG, true, true, false, kTail, false>(T, loc, lane, w, dl, lcr, du, ucr,
-                                                             ecr, acr);
+                                                             ecr, acr, exact);
           } else {
             class_pairs<kG, false, true, false, kTail, false>(T, loc, lane, w, dl, lcr, du, ucr,
-                                                              ecr, acr);
+                                                              ecr, acr, exact);
           }
 #endif
           lcr = G.sum(lcr);
@@ -1189,6 +1235,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
     }
     // split decision (subdivide_adaptive, se3.cpp:107-121)
     st_max = G.max(st_max);
+    // whole-table modes: every row is prepared, one decision for the node
+    const bool exact = streamed || G.any(exact_needed_row(klo_min, ctx.min_k2));
     if constexpr (kMode == kSiblings) {
       // one cuboid, 8 rotation children: self sums once, then per child
       const double hr = 0.5 * rhw;
@@ -1209,10 +1257,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
           double dl = 0.0, du = 0.0;
           if (same) {
             class_pairs<kG, true, false, true, kTail, false>(T, cs, lane, w, sl_self, dl, su_self,
-                                                             du, se_self, lb_amp);
+                                                             du, se_self, lb_amp, exact);
           } else {
             class_pairs<kG, false, false, true, kTail, false>(T, cs, lane, w, sl_self, dl,
-                                                              su_self, du, se_self, lb_amp);
+                                                              su_self, du, se_self, lb_amp, exact);
           }
         }
         sl_self = G.sum(sl_self);
@@ -1249,10 +1297,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
           const float w = static_cast<float>(ctx.cls_w[c]);
           if (same) {
             class_pairs<kG, true, true, false, kTail, false>(T, cs, lane, w, dl, lcr, du, ucr, ecr,
-                                                             acr);
+                                                             acr, exact);
           } else {
             class_pairs<kG, false, true, false, kTail, false>(T, cs, lane, w, dl, lcr, du, ucr,
-                                                              ecr, acr);
+                                                              ecr, acr, exact);
           }
         }
         lcr = G.sum(lcr);
@@ -1313,10 +1361,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
       constexpr bool kC = kMode != kSelfOnly, kS = kMode != kCrossCached;
       if (same) {
         class_pairs<kG, true, kC, kS, kTail, kFix>(T, cs, lane, w, lb_self, lb_cross, ub_self,
-                                                   ub_cross, lb_err, lb_amp);
+                                                   ub_cross, lb_err, lb_amp, exact);
       } else {
         class_pairs<kG, false, kC, kS, kTail, kFix>(T, cs, lane, w, lb_self, lb_cross, ub_self,
-                                                    ub_cross, lb_err, lb_amp);
+                                                    ub_cross, lb_err, lb_amp, exact);
       }
     }
 #endif

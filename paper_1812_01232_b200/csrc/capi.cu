@@ -161,6 +161,9 @@ int ctx_upload(gosma_ctx* ctx) {
     return v > 0.0 ? v : 8e-5;
   }();
   d.redo_rel = redo_rel;
+  d.min_k2 = INFINITY;  // K1's exact-path gate (exact_needed_row)
+  for (const HostClass& c : hm.classes)
+    for (double k : c.kappa2) d.min_k2 = std::min(d.min_k2, static_cast<float>(k));
   for (const ClassSpan& cs : spans)
     if (cs.n1 % 32 != 0 && cs.n1 % 32 <= 16) d.tail_chunks = 1;
   ClassSpan* dspans;

@@ -50,6 +50,7 @@ struct DevCtx {
   int stream_classes;    // full mode keeps one class's table at a time (n_classes > 1)
   int precise;           // precise fix-up for nodes whose FP32 error estimate is large
   double redo_rel;       // fix-up threshold: amplified estimate / cross mass
+  float min_k2;          // smallest image concentration (K1's exact-path gate)
 };
 
 // Host-side master copy of one class (ClassData, objective.hpp:19-31).
