@@ -320,6 +320,21 @@ __device__ __forceinline__ void sincos_sq(float hx, float hy, float hz, float lx
 #endif
 }
 
+// x = |u - v|^2 alone, from the double-float difference, and y = 4 - x: the
+// fast loop copies (kExact = false), whose nodes have every psi <= pi/2 and
+// concentrations that make the theta-near-pi terms negligible, so y's
+// absolute (not relative) precision never reaches a non-negligible term.
+#ifndef GOSMA_XONLY
+#define GOSMA_XONLY 1
+#endif
+__device__ __forceinline__ void sin_sq(float hx, float hy, float hz, float lx, float ly, float lz,
+                                       float gx, float gy, float gz, float mx, float my,
+                                       float mz, float& x, float& y) {
+  const float dx = (hx - gx) + (lx - mx), dy = (hy - gy) + (ly - my), dz = (hz - gz) + (lz - mz);
+  x = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+  y = fmaxf(4.0f - x, 0.0f);  // x may round past 4 for antipodal directions
+}
+
 // One cross pair (model row i x image column j). The alignment angle
 // B = max(0, theta - psi_t - psi_r) (alignment_angle_B, bounds.cpp:143-156)
 // enters as 2 sin(B/2) = (x - s4) / (2 sin(theta/2) cos(psi/2) + 2 cos(theta/2) sin(psi/2))
@@ -334,8 +349,12 @@ __device__ __forceinline__ void cross_pair(const Row& r, const float4 qa, const 
   const float k2 = qa.w;
   // x = |u - q|^2 = 4 sin^2(theta/2), y = |u + q|^2 = 4 cos^2(theta/2), each
   // without cancellation (sincos_sq)
+  constexpr bool kX = !kExact && GOSMA_XONLY;
   float x, y;
-  sincos_sq(r.uhx, r.uhy, r.uhz, r.ulx, r.uly, r.ulz, qa.x, qa.y, qa.z, qb.x, qb.y, qb.z, x, y);
+  if constexpr (kX)
+    sin_sq(r.uhx, r.uhy, r.uhz, r.ulx, r.uly, r.ulz, qa.x, qa.y, qa.z, qb.x, qb.y, qb.z, x, y);
+  else
+    sincos_sq(r.uhx, r.uhy, r.uhz, r.ulx, r.uly, r.ulz, qa.x, qa.y, qa.z, qb.x, qb.y, qb.z, x, y);
   // With sg = 2 sin(theta/2) = sqrt(x), gm = 2 cos(theta/2) = sqrt(y):
   //   den^2 = (sg cp + gm sp)^2 = x cp^2 + y sp^2 + 2 sg gm cp sp
   //   c2    = (gm cp + sg sp)^2 = y cp^2 + x sp^2 + 2 sg gm cp sp = 2(1 + cos B)
@@ -355,6 +374,8 @@ __device__ __forceinline__ void cross_pair(const Row& r, const float4 qa, const 
     const double w = fma(vx, vx, fma(vy, vy, vz * vz));
     num = static_cast<float>(obtuse ? (static_cast<double>(rp.z) + rp.w) - w
                                     : w - (static_cast<double>(rp.x) + rp.y));
+  } else if constexpr (kX) {
+    num = x - r.s4;  // x carries its relative precision on both sides of 90 deg
   } else {
     num = (x > y) ? (r.c4 - y) : (x - r.s4);
   }
@@ -411,7 +432,7 @@ __device__ __forceinline__ void cross_pair(const Row& r, const float4 qa, const 
   // (the fix-up's FP64 numerator leaves only the exponent's own error)
   const float gt1 = qb.w * t1;  // G_j; F_i is applied to the row sum
   l += gt1;
-  if constexpr (!kPrecise) ma = fmaf(gt1, fabsf(g) * fminf(x, y), ma);
+  if constexpr (!kPrecise) ma = fmaf(gt1, fabsf(g) * (kX ? x : fminf(x, y)), ma);
   mb = fmaf(gt1, fabsf(e1), mb);
   u = fmaf(qb.w, t2, u);
 }
@@ -439,7 +460,10 @@ __device__ __forceinline__ void self_pair(const float4& a0, const float4& a1, co
   // spread angle A = min(pi, theta + psi_i + psi_j) (bounds.cpp:108-124);
   // directions are double-float (high part in [0], low part in [2])
   float x, y;  // |u_i - u_j|^2, |u_i + u_j|^2
-  sincos_sq(a0.x, a0.y, a0.z, a2.x, a2.y, a2.z, b0.x, b0.y, b0.z, b2.x, b2.y, b2.z, x, y);
+  if constexpr (!kExact && GOSMA_XONLY)
+    sin_sq(a0.x, a0.y, a0.z, a2.x, a2.y, a2.z, b0.x, b0.y, b0.z, b2.x, b2.y, b2.z, x, y);
+  else
+    sincos_sq(a0.x, a0.y, a0.z, a2.x, a2.y, a2.z, b0.x, b0.y, b0.z, b2.x, b2.y, b2.z, x, y);
   const float sij = fmaf(a1.z, b1.w, a1.w * b1.z);   // sin((psi_i+psi_j)/2)
   const float cij = fmaf(a1.w, b1.w, -a1.z * b1.z);  // cos((psi_i+psi_j)/2)
   // With sg = sqrt(x) = 2 sin(theta/2), gm = sqrt(y) = 2 cos(theta/2):
@@ -683,23 +707,40 @@ __device__ __forceinline__ void class_pairs(const WarpTables& T, const ClassSpan
   }
 }
 
-// Whether a node's terms can take the rare exact paths (small K, the cross
-// LB's interior K minimum, the self LB's corner maximum past 90 degrees) with
-// a value that matters. Those cases need cos B < 0, cos A < 0 or K <= 15;
-// with every row's kappa_lo >= 90 (kappa_hi and kappa at t* are larger) and
-// kappa_lo k2 / (kappa_lo + k2) >= 45 for the smallest image concentration,
-// each of them forces the pair's exponent below -64 (log2: |excess| >=
-// ab (1 - cos) / (a + b) >= ab / (a + b), times log2 e), where a term is at
-// most 2^-64 of its F_i G_j W(K) prefactor, i.e. below 1e-13 of the node's
-// |term| mass even for kappa2 / kappa1 ratios of 1e5: skipping the exact W(K)
-// for such terms moves the bound by far less than the 2e-7 mass margin.
-// Group-uniform (one vote), so the fast loops never diverge.
-#ifndef GOSMA_EXACT_KLO
-#define GOSMA_EXACT_KLO 90.0f
+// Whether a node's terms can skip the rare exact paths (small K, the cross
+// LB's interior K minimum, the self LB's corner maximum past 90 degrees) and
+// take the fast loop copies (no exact branches, x-only angles via sin_sq).
+// Every skipped case is shown to leave the pair's log2 exponent below -64,
+// i.e. the term at most 2^-64 of its F_i G_j W(K) prefactor (below 1e-13 of
+// the node's |term| mass even for kappa2 / kappa1 ratios of 1e5), so skipping
+// it moves the bound by far less than the 2e-7 mass margin. With
+// |excess| = ab (1 - cos) 2 / (K + a + b) >= ab (1 - cos) / (a + b) and
+// L = log2 e:
+//  * cross LB interior K minimum (cos B < -kappa_lo / k2):
+//    |e| > L ab (1 + a/b) / (a + b) = L kappa_lo, so kappa_lo >= 45;
+//  * K <= 15 (cross LB / UB, self LB / UB): |a - b| <= 15 and ab c <= 225
+//    force 1 - cos >= 2 - 113/ab and |e| >= L (4ab - 225) / (15 + a + b),
+//    above 64 once both concentrations are >= 30 (kappa_lo, kappa_hi,
+//    kappa at t* >= 45 here, the partner within 15 of it);
+//  * self LB corner maximum (cos A < 0): |e| >= L H(kappa_hi_i, kappa_hi_j),
+//    so kappa_hi >= 90 (H = ab / (a + b));
+//  * sin_sq's y = 4 - x has absolute, not relative, precision: it matters only
+//    for theta near pi, where B >= pi - psi gives |e| >= L H(kappa_lo, k2)
+//    (1 + cos psi) = L H 2 cos^2(psi/2) (and the UB / self terms at
+//    theta ~ pi have |e| >= 2 L H): H(kappa_lo, min k2) min(1, 2 cp^2) >= 45,
+//    with cp = 0 exempt (psi clamped at pi: every cross pair has B = 0).
+// Per row a score >= 1 when all hold; the node decision is one vote over its
+// rows (group-uniform: the fast loops never diverge inside a group).
+// GOSMA_FAST_SCALE scales the thresholds (A/B builds).
+#ifndef GOSMA_FAST_SCALE
+#define GOSMA_FAST_SCALE 1.0f
 #endif
-__device__ __forceinline__ bool exact_needed_row(float klo_min, float k2_min) {
-  constexpr float kLo = GOSMA_EXACT_KLO, kH = 0.5f * GOSMA_EXACT_KLO;
-  return !(klo_min >= kLo && klo_min * k2_min >= kH * (klo_min + k2_min));
+__device__ __forceinline__ float fast_score(float klo, float khi, float kst, float k2_min,
+                                            double cp) {
+  constexpr float kA = 1.0f / (45.0f * GOSMA_FAST_SCALE), kB = 1.0f / (90.0f * GOSMA_FAST_SCALE);
+  const float h = klo * k2_min / (klo + k2_min);
+  const float c = cp > 0.0 ? fminf(1.0f, static_cast<float>(2.0 * cp * cp)) : 1.0f;
+  return fminf(fminf(fminf(klo, kst), h * c) * kA, khi * kB);
 }
 
 // Half-angle of psi_trans (se3.cpp:72-92) for a mean outside the cuboid: the
@@ -1032,7 +1073,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
     double lb_self = 0.0, lb_cross = 0.0, ub_self = 0.0, ub_cross = 0.0, lb_err = 0.0;
     float lb_amp = 0.0f;  // the theta/B-amplified part of the cross terms' error estimate
     double st_max = 0.0;
-    float klo_min = INFINITY;  // smallest kappa_lo over this lane's rows (exact_needed_row)
+    // smallest fast_score over this lane's rows (exact_needed)
+    float fscore = INFINITY;
     auto prep_row = [&](int i, int slot, float& dsl, float& dsu) {
       const double m0 = ctx.mu[3 * i], m1 = ctx.mu[3 * i + 1], m2 = ctx.mu[3 * i + 2];
       const double is2 = ctx.inv_s2[i];
@@ -1044,7 +1086,6 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
       const double dhi2 = (a0 + h0) * (a0 + h0) + (a1 + h1) * (a1 + h1) + (a2 + h2) * (a2 + h2);
       const float klo = static_cast<float>(dlo2 * is2 + 1.0);
       const float khi = static_cast<float>(dhi2 * is2 + 1.0);
-      klo_min = fminf(klo_min, klo);
       const double un2 = u0 * u0 + u1 * u1 + u2 * u2;
       double c0 = 1.0, c1 = 0.0, c2 = 0.0;  // UnitX when the mean is at the centre
       if (un2 > 1e-24) {
@@ -1067,6 +1108,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
       const double v0 = m0 - ts0, v1 = m1 - ts1, v2 = m2 - ts2;
       const double vn2 = v0 * v0 + v1 * v1 + v2 * v2;
       const float kst = static_cast<float>(vn2 * is2 + 1.0);
+      fscore = fminf(fscore, fast_score(klo, khi, kst, ctx.min_k2, cp));
       const double iv = rsqrt(vn2);
       const float phi = static_cast<float>(ctx.phi1[i]);
       dsl += diag_term(phi, klo);
@@ -1111,10 +1153,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
         const float w = static_cast<float>(ctx.cls_w[c]);
         float dsl = 0.0f, dsu = 0.0f;
         G.sync();  // the previous class's pairs are done with the table
-        klo_min = INFINITY;
+        fscore = INFINITY;
         for (int il = lane; il < cs.n1; il += kG) prep_row(cs.o1 + il, il, dsl, dsu);
         if (infeasible) continue;  // (rows still feed the split decision)
-        const bool exact = G.any(exact_needed_row(klo_min, ctx.min_k2));
+        const bool exact = G.any(!(fscore >= 1.0f));
         lb_self += static_cast<double>(w * dsl);
         lb_err += static_cast<double>(w * dsl * kErrTerm);
         ub_self += static_cast<double>(w * dsu);
@@ -1150,10 +1192,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
         const float w = static_cast<float>(ctx.cls_w[c]);
         float dsl = 0.0f, dsu = 0.0f;
         G.sync();  // the previous class's pairs are done with the table
-        klo_min = INFINITY;
+        fscore = INFINITY;
         for (int il = lane; il < cs.n1; il += kG) prep_row(cs.o1 + il, il, dsl, dsu);
         if (infeasible) continue;  // (rows still feed the split decision)
-        const bool exact = G.any(exact_needed_row(klo_min, ctx.min_k2));
+        const bool exact = G.any(!(fscore >= 1.0f));
         sl_self += static_cast<double>(w * dsl);
         se_self += static_cast<double>(w * dsl * kErrTerm);
         su_self += static_cast<double>(w * dsu);
@@ -1236,7 +1278,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
     // split decision (subdivide_adaptive, se3.cpp:107-121)
     st_max = G.max(st_max);
     // whole-table modes: every row is prepared, one decision for the node
-    const bool exact = streamed || G.any(exact_needed_row(klo_min, ctx.min_k2));
+    const bool exact = streamed || G.any(!(fscore >= 1.0f));
     if constexpr (kMode == kSiblings) {
       // one cuboid, 8 rotation children: self sums once, then per child
       const double hr = 0.5 * rhw;

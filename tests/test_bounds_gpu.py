@@ -272,6 +272,7 @@ def test_config2_batch_properties(gosma):
                                            s.cuda_stream)
     s.synchronize()
     lo, up, sp = d_lo.cpu().numpy(), d_up.cpu().numpy(), d_sp.cpu().numpy()
+    assert not np.isnan(lo).any() and not np.isnan(up).any()
     f = np.isfinite(lo)
     assert f.mean() > 0.99
     assert np.all(np.isfinite(up[f]))
@@ -284,7 +285,10 @@ def test_config2_batch_properties(gosma):
                                            d_up.data_ptr(), d_sp.data_ptr(), float("inf"),
                                            s.cuda_stream)
     s.synchronize()
-    assert np.array_equal(d_lo.cpu().numpy(), lo) and np.array_equal(d_up.cpu().numpy(), up)
+    lo2, up2 = d_lo.cpu().numpy(), d_up.cpu().numpy()
+    bad = np.flatnonzero((lo2 != lo) | (up2 != up))
+    assert len(bad) == 0, (f"{len(bad)} nodes differ, e.g. {bad[:4]}: "
+                           f"{lo[bad[:4]]} vs {lo2[bad[:4]]}, {up[bad[:4]]} vs {up2[bad[:4]]}")
     assert np.array_equal(d_sp.cpu().numpy(), sp)
     # sampled parity against the oracle
     rng = np.random.default_rng(0)
@@ -328,8 +332,8 @@ def _cached_vs_full(gosma, classes, zeta, nodes, tboxes, tindex, skip=float("inf
 @pytest.mark.parametrize("n1,n2,ncls", [(8, 6, 1), (64, 32, 1), (33, 17, 3)])
 def test_translation_cached_mode_equals_full(gosma, n1, n2, ncls):
     """Self terms once per translation cuboid (rotation-split siblings share it),
-    cross terms per node: the same bounds as the full kernel, to FP32 rounding
-    (1e-7 of the mass, far below TOL_RAW)."""
+    cross terms per node: the same bounds as the full kernel, to the raw FP32
+    tolerance."""
     from paper_1812_01232_b200 import synth
     classes = synth.mixture(n1, n2, "realistic", seed=n1 + 5 * n2, n_classes=ncls)
     base = synth.nodes(400, seed=n1 * n2).view(np.float64).reshape(-1, 11)
@@ -351,13 +355,14 @@ def test_translation_cached_mode_equals_full(gosma, n1, n2, ncls):
     rlo, rup, lm, um, _ = Oracle(mix).eval_bounds(nodes, threads=8)
     d = np.abs(lo[f] - clo[f])
     print(f"cached vs full: max |dLB|/scale {np.max(d / scale):.3e}, /mass {np.max(d / lm[f]):.3e}")
-    # Equal up to FP32 rounding: the modes may take different copies of the
-    # pair loops (K1's exact-path gate decides per class when classes are
-    # streamed, per node otherwise), which the compiler contracts differently.
-    assert np.all(d <= 1e-7 * lm[f])
+    # The modes may take different copies of the pair loops (K1's fast-path
+    # vote is per class when classes are streamed, per node otherwise), whose
+    # FP32 error estimates differ, so a node can reach the precise fix-up in
+    # one mode only: they agree to the raw FP32 tolerance.
+    assert np.all(d <= TOL_RAW * lm[f])
     fu = np.isfinite(up)
     assert np.array_equal(fu, np.isfinite(cup))
-    assert np.all(np.abs(up[fu] - cup[fu]) <= 1e-7 * um[fu] + 1e-12)
+    assert np.all(np.abs(up[fu] - cup[fu]) <= TOL_UB * um[fu] + 1e-12)
     assert np.array_equal(sp, csp)
     # and against the FP64 oracle (certified LB sound, UB within TOL_UB)
     ff = np.isfinite(rlo)
