@@ -163,6 +163,11 @@ struct Group {
       return __syncthreads_or(b) != 0;
     }
   }
+  // OR of 2-bit flags over the group (two votes: __reduce_or_sync with a
+  // partial mask serialises the groups of a warp)
+  __device__ __forceinline__ unsigned bor2(unsigned v) const {
+    return (any((v & 1u) != 0u) ? 1u : 0u) | (any((v & 2u) != 0u) ? 2u : 0u);
+  }
   __device__ __forceinline__ double sum(double v) const {
     if constexpr (kG <= 32) {
 #pragma unroll
@@ -682,27 +687,43 @@ __device__ __forceinline__ void class_pairs_tail(const WarpTables& T, const Clas
   }
 }
 
+template <int kG, bool kSame, bool kCross, bool kSelf, bool kTail, bool kPrecise, bool kExact>
+__device__ __forceinline__ void class_pairs_part(const WarpTables& T, const ClassSpan cs, int lane,
+                                                 float w, double& lb_self, double& lb_cross,
+                                                 double& ub_self, double& ub_cross,
+                                                 double& lb_err, float& lb_amp) {
+  if constexpr (kTail)
+    class_pairs_tail<kG, kSame, kCross, kSelf, kPrecise, kExact>(
+        T, cs, lane, w, lb_self, lb_cross, ub_self, ub_cross, lb_err, lb_amp);
+  else
+    class_pairs_rows<kG, kSame, kCross, kSelf, kPrecise, kExact>(
+        T, cs, lane, w, lb_self, lb_cross, ub_self, ub_cross, lb_err, lb_amp);
+}
+
+// exact: bit 0 the cross loop needs the exact-path copy, bit 1 the self loop
+// (FastScore); the cross sums come first, as in class_pairs_rows.
 template <int kG, bool kSame, bool kCross, bool kSelf, bool kTail, bool kPrecise>
 __device__ __forceinline__ void class_pairs(const WarpTables& T, const ClassSpan cs, int lane,
                                             float w, double& lb_self, double& lb_cross,
                                             double& ub_self, double& ub_cross, double& lb_err,
-                                            float& lb_amp, bool exact) {
+                                            float& lb_amp, unsigned exact) {
   // the fast loop copies only for groups of >= 16 lanes (classes of > 24
   // rows): short loops gain nothing from them and lose to the larger code
-  exact = exact || kG < 16;
-  if constexpr (kTail) {
-    if (exact)
-      class_pairs_tail<kG, kSame, kCross, kSelf, kPrecise, true>(
+  if (kG < 16) exact = 3u;
+  if constexpr (kCross) {
+    if (exact & 1u)
+      class_pairs_part<kG, kSame, true, false, kTail, kPrecise, true>(
           T, cs, lane, w, lb_self, lb_cross, ub_self, ub_cross, lb_err, lb_amp);
     else
-      class_pairs_tail<kG, kSame, kCross, kSelf, kPrecise, false>(
+      class_pairs_part<kG, kSame, true, false, kTail, kPrecise, false>(
           T, cs, lane, w, lb_self, lb_cross, ub_self, ub_cross, lb_err, lb_amp);
-  } else {
-    if (exact)
-      class_pairs_rows<kG, kSame, kCross, kSelf, kPrecise, true>(
+  }
+  if constexpr (kSelf) {
+    if (exact & 2u)
+      class_pairs_part<kG, kSame, false, true, kTail, kPrecise, true>(
           T, cs, lane, w, lb_self, lb_cross, ub_self, ub_cross, lb_err, lb_amp);
     else
-      class_pairs_rows<kG, kSame, kCross, kSelf, kPrecise, false>(
+      class_pairs_part<kG, kSame, false, true, kTail, kPrecise, false>(
           T, cs, lane, w, lb_self, lb_cross, ub_self, ub_cross, lb_err, lb_amp);
   }
 }
@@ -729,19 +750,28 @@ __device__ __forceinline__ void class_pairs(const WarpTables& T, const ClassSpan
 //    (1 + cos psi) = L H 2 cos^2(psi/2) (and the UB / self terms at
 //    theta ~ pi have |e| >= 2 L H): H(kappa_lo, min k2) min(1, 2 cp^2) >= 45,
 //    with cp = 0 exempt (psi clamped at pi: every cross pair has B = 0).
-// Per row a score >= 1 when all hold; the node decision is one vote over its
-// rows (group-uniform: the fast loops never diverge inside a group).
+// Per row two scores, >= 1 when the cross (resp. self) conditions hold; the
+// node decisions are one vote each over its rows (group-uniform: the fast
+// loops never diverge inside a group).
 // GOSMA_FAST_SCALE scales the thresholds (A/B builds).
 #ifndef GOSMA_FAST_SCALE
 #define GOSMA_FAST_SCALE 1.0f
 #endif
-__device__ __forceinline__ float fast_score(float klo, float khi, float kst, float k2_min,
-                                            double cp) {
-  constexpr float kA = 1.0f / (45.0f * GOSMA_FAST_SCALE), kB = 1.0f / (90.0f * GOSMA_FAST_SCALE);
-  const float h = klo * k2_min / (klo + k2_min);
-  const float c = cp > 0.0 ? fminf(1.0f, static_cast<float>(2.0 * cp * cp)) : 1.0f;
-  return fminf(fminf(fminf(klo, kst), h * c) * kA, khi * kB);
-}
+struct FastScore {
+  float cross = INFINITY, self = INFINITY;
+  __device__ __forceinline__ void add(float klo, float khi, float kst, float k2_min, double cp) {
+    constexpr float kA = 1.0f / (45.0f * GOSMA_FAST_SCALE), kB = 1.0f / (90.0f * GOSMA_FAST_SCALE);
+    const float h = klo * k2_min / (klo + k2_min);
+    const float c = cp > 0.0 ? fminf(1.0f, static_cast<float>(2.0 * cp * cp)) : 1.0f;
+    cross = fminf(cross, fminf(fminf(klo, kst), h * c) * kA);
+    self = fminf(self, fminf(kst * kA, khi * kB));
+  }
+  __device__ __forceinline__ void reset() { cross = self = INFINITY; }
+  // this lane's rows: bit 0 the cross loop needs the exact copy, bit 1 the self loop
+  __device__ __forceinline__ unsigned need() const {
+    return (cross >= 1.0f ? 0u : 1u) | (self >= 1.0f ? 0u : 2u);
+  }
+};
 
 // Half-angle of psi_trans (se3.cpp:72-92) for a mean outside the cuboid: the
 // vertex with the largest angle to the centre direction has the smallest
@@ -1073,8 +1103,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
     double lb_self = 0.0, lb_cross = 0.0, ub_self = 0.0, ub_cross = 0.0, lb_err = 0.0;
     float lb_amp = 0.0f;  // the theta/B-amplified part of the cross terms' error estimate
     double st_max = 0.0;
-    // smallest fast_score over this lane's rows (exact_needed)
-    float fscore = INFINITY;
+    FastScore fs;  // fast-loop eligibility of this lane's rows
     auto prep_row = [&](int i, int slot, float& dsl, float& dsu) {
       const double m0 = ctx.mu[3 * i], m1 = ctx.mu[3 * i + 1], m2 = ctx.mu[3 * i + 2];
       const double is2 = ctx.inv_s2[i];
@@ -1108,7 +1137,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
       const double v0 = m0 - ts0, v1 = m1 - ts1, v2 = m2 - ts2;
       const double vn2 = v0 * v0 + v1 * v1 + v2 * v2;
       const float kst = static_cast<float>(vn2 * is2 + 1.0);
-      fscore = fminf(fscore, fast_score(klo, khi, kst, ctx.min_k2, cp));
+      fs.add(klo, khi, kst, ctx.min_k2, cp);
       const double iv = rsqrt(vn2);
       const float phi = static_cast<float>(ctx.phi1[i]);
       dsl += diag_term(phi, klo);
@@ -1153,10 +1182,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
         const float w = static_cast<float>(ctx.cls_w[c]);
         float dsl = 0.0f, dsu = 0.0f;
         G.sync();  // the previous class's pairs are done with the table
-        fscore = INFINITY;
+        fs.reset();
         for (int il = lane; il < cs.n1; il += kG) prep_row(cs.o1 + il, il, dsl, dsu);
         if (infeasible) continue;  // (rows still feed the split decision)
-        const bool exact = G.any(!(fscore >= 1.0f));
+        const unsigned exact = kG < 16 ? 3u : G.bor2(fs.need());
         lb_self += static_cast<double>(w * dsl);
         lb_err += static_cast<double>(w * dsl * kErrTerm);
         ub_self += static_cast<double>(w * dsu);
@@ -1192,10 +1221,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
         const float w = static_cast<float>(ctx.cls_w[c]);
         float dsl = 0.0f, dsu = 0.0f;
         G.sync();  // the previous class's pairs are done with the table
-        fscore = INFINITY;
+        fs.reset();
         for (int il = lane; il < cs.n1; il += kG) prep_row(cs.o1 + il, il, dsl, dsu);
         if (infeasible) continue;  // (rows still feed the split decision)
-        const bool exact = G.any(!(fscore >= 1.0f));
+        const unsigned exact = kG < 16 ? 3u : G.bor2(fs.need());
         sl_self += static_cast<double>(w * dsl);
         se_self += static_cast<double>(w * dsl * kErrTerm);
         su_self += static_cast<double>(w * dsu);
@@ -1278,7 +1307,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
     // split decision (subdivide_adaptive, se3.cpp:107-121)
     st_max = G.max(st_max);
     // whole-table modes: every row is prepared, one decision for the node
-    const bool exact = streamed || G.any(!(fscore >= 1.0f));
+    const unsigned exact = (streamed || kG < 16) ? 3u : G.bor2(fs.need());
     if constexpr (kMode == kSiblings) {
       // one cuboid, 8 rotation children: self sums once, then per child
       const double hr = 0.5 * rhw;
