@@ -269,7 +269,7 @@ constexpr int kRowPF4 = 1;  // float4 per model row, fix-up launches only
 // double-float 4 sin^2(psi/2). The main kernel only accumulates the estimate's
 // amplified part (one multiply-add per row) and appends; nodes that never
 // reach the threshold pay nothing else.
-// kRedoRel: the threshold (DevCtx::redo_rel, default 8e-5 of the cross mass;
+// kRedoRel: the threshold (DevCtx::redo_rel, default 1.2e-4 of the cross mass;
 // profiles/r02_k1_variants.md)
 
 struct Row {

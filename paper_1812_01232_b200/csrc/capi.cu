@@ -158,7 +158,7 @@ int ctx_upload(gosma_ctx* ctx) {
   static const double redo_rel = [] {  // GOSMA_REDO_REL: fix-up threshold (A/B)
     const char* e = std::getenv("GOSMA_REDO_REL");
     const double v = e ? std::atof(e) : 0.0;
-    return v > 0.0 ? v : 8e-5;
+    return v > 0.0 ? v : 1.2e-4;
   }();
   d.redo_rel = redo_rel;
   d.min_k2 = INFINITY;  // K1's exact-path gate (exact_needed_row)

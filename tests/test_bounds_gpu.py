@@ -5,12 +5,12 @@ Tolerance. Pair terms are FP32 (FP64 sums), so
 agreement is stated relative to the node's |term| mass M (sum of |pair
 contributions|, from the oracle):
   * raw FP32 core (ctx.set_lb_margin(-1)):  |LB - LB_ref| <= 1e-5 M
-    (north_star's FP32 tolerance; nodes whose cross-term error estimate
-    exceeds 2e-6 of their cross mass are re-evaluated with the alignment
-    angle's numerator in FP64, the one FP32 step amplified by theta/B),
+    (north_star's FP32 tolerance; nodes whose theta/B-amplified cross-term
+    error estimate exceeds 1.2e-4 of their cross mass -- 0.03% of configs[1]
+    nodes -- are re-evaluated with the alignment angle's numerator in FP64),
   * certified LB (default): the kernel subtracts its own per-term FP32 error
     estimate + 2e-7 M, so  LB <= LB_ref (sound)  and  LB >= LB_ref - 1e-4 M
-    (the estimate's theta/B-amplified part is at most 8e-5 of the cross mass
+    (the estimate's theta/B-amplified part is at most 1.2e-4 of the cross mass
     -- larger sends the node through the FP64 fix-up -- plus the exponent and
     rounding parts; measured <= 2.4e-5 M on the 1M configs[1] nodes;
     DESIGN.md §5),
