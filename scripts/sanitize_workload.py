@@ -1,5 +1,5 @@
 """Small workload touching every kernel family, for compute-sanitizer runs
-(memcheck / racecheck / synccheck / initcheck; profiles/r02_sanitizer.md):
+(memcheck / racecheck / synccheck / initcheck; see DESIGN.md §10 for why no run is kept):
 K1 in its full, class-streamed, translation-cached and siblings modes (with
 tail chunks and CTA groups), the precise cross pass, the frontier (select,
 expand, route, compaction, depth-first selection), the device dive beam, the
