@@ -687,6 +687,11 @@ __device__ __forceinline__ void class_pairs_tail(const WarpTables& T, const Clas
   }
 }
 
+#ifndef GOSMA_FAST_MIN_G
+#define GOSMA_FAST_MIN_G 16
+#endif
+constexpr int kFastMinG = GOSMA_FAST_MIN_G;
+
 template <int kG, bool kSame, bool kCross, bool kSelf, bool kTail, bool kPrecise, bool kExact>
 __device__ __forceinline__ void class_pairs_part(const WarpTables& T, const ClassSpan cs, int lane,
                                                  float w, double& lb_self, double& lb_cross,
@@ -707,9 +712,9 @@ __device__ __forceinline__ void class_pairs(const WarpTables& T, const ClassSpan
                                             float w, double& lb_self, double& lb_cross,
                                             double& ub_self, double& ub_cross, double& lb_err,
                                             float& lb_amp, unsigned exact) {
-  // the fast loop copies only for groups of >= 16 lanes (classes of > 24
-  // rows): short loops gain nothing from them and lose to the larger code
-  if (kG < 16) exact = 3u;
+  // the fast loop copies only for groups of >= kFastMinG lanes (classes of
+  // > 24 rows): short loops gain nothing from them and lose to the larger code
+  if (kG < kFastMinG) exact = 3u;
   if constexpr (kCross) {
     if (exact & 1u)
       class_pairs_part<kG, kSame, true, false, kTail, kPrecise, true>(
@@ -914,8 +919,14 @@ __device__ __forceinline__ void column_prep_span(const WarpTables& T, const DevC
 #ifndef GOSMA_MIN_BLOCKS
 #define GOSMA_MIN_BLOCKS 7
 #endif
+// CTAs per SM the register allocation targets (72 registers at 7). The
+// class-streamed siblings mode (semantic solves) runs best at 5 (96
+// registers: its per-class / per-child loops otherwise rematerialise the
+// table addresses; 8 x (8x4) siblings 2.04 -> 1.93 ms, 8 x (32x16) 15.6 ->
+// 14.6 ms); every other mode loses at 5 or 6 (profiles/r02_k1_variants.md).
+constexpr int min_blocks_for(int mode) { return mode == kSiblingsStream ? 5 : GOSMA_MIN_BLOCKS; }
 template <int kMode, int kG, bool kTail>
-__global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
+__global__ void __launch_bounds__(kWarpsPerCta * 32, min_blocks_for(kMode))
     eval_bounds_kernel(const DevCtx ctx, const EvalArgs args) {
   extern __shared__ float4 smem4[];
   __shared__ GroupScratch gscratch;
@@ -1185,7 +1196,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
         fs.reset();
         for (int il = lane; il < cs.n1; il += kG) prep_row(cs.o1 + il, il, dsl, dsu);
         if (infeasible) continue;  // (rows still feed the split decision)
-        const unsigned exact = kG < 16 ? 3u : G.bor2(fs.need());
+        const unsigned exact = kG < kFastMinG ? 3u : G.bor2(fs.need());
         lb_self += static_cast<double>(w * dsl);
         lb_err += static_cast<double>(w * dsl * kErrTerm);
         ub_self += static_cast<double>(w * dsu);
@@ -1224,7 +1235,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
         fs.reset();
         for (int il = lane; il < cs.n1; il += kG) prep_row(cs.o1 + il, il, dsl, dsu);
         if (infeasible) continue;  // (rows still feed the split decision)
-        const unsigned exact = kG < 16 ? 3u : G.bor2(fs.need());
+        const unsigned exact = kG < kFastMinG ? 3u : G.bor2(fs.need());
         sl_self += static_cast<double>(w * dsl);
         se_self += static_cast<double>(w * dsl * kErrTerm);
         su_self += static_cast<double>(w * dsu);
@@ -1307,7 +1318,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GOSMA_MIN_BLOCKS)
     // split decision (subdivide_adaptive, se3.cpp:107-121)
     st_max = G.max(st_max);
     // whole-table modes: every row is prepared, one decision for the node
-    const unsigned exact = (streamed || kG < 16) ? 3u : G.bor2(fs.need());
+    const unsigned exact = (streamed || kG < kFastMinG) ? 3u : G.bor2(fs.need());
     if constexpr (kMode == kSiblings) {
       // one cuboid, 8 rotation children: self sums once, then per child
       const double hr = 0.5 * rhw;
