@@ -691,6 +691,7 @@ __device__ __forceinline__ void class_pairs_tail(const WarpTables& T, const Clas
 #define GOSMA_FAST_MIN_G 16
 #endif
 constexpr int kFastMinG = GOSMA_FAST_MIN_G;
+constexpr int kSibFastMinG = 8;  // the class-streamed siblings mode (semantic solves)
 
 template <int kG, bool kSame, bool kCross, bool kSelf, bool kTail, bool kPrecise, bool kExact>
 __device__ __forceinline__ void class_pairs_part(const WarpTables& T, const ClassSpan cs, int lane,
@@ -707,14 +708,16 @@ __device__ __forceinline__ void class_pairs_part(const WarpTables& T, const Clas
 
 // exact: bit 0 the cross loop needs the exact-path copy, bit 1 the self loop
 // (FastScore); the cross sums come first, as in class_pairs_rows.
-template <int kG, bool kSame, bool kCross, bool kSelf, bool kTail, bool kPrecise>
+template <int kG, bool kSame, bool kCross, bool kSelf, bool kTail, bool kPrecise,
+          int kMinG = kFastMinG>
 __device__ __forceinline__ void class_pairs(const WarpTables& T, const ClassSpan cs, int lane,
                                             float w, double& lb_self, double& lb_cross,
                                             double& ub_self, double& ub_cross, double& lb_err,
                                             float& lb_amp, unsigned exact) {
-  // the fast loop copies only for groups of >= kFastMinG lanes (classes of
-  // > 24 rows): short loops gain nothing from them and lose to the larger code
-  if (kG < kFastMinG) exact = 3u;
+  // the fast loop copies only for groups of >= kMinG lanes (classes of > 24
+  // rows in the full modes): short loops gain nothing from them and lose to
+  // the larger code; the class-streamed siblings mode gains at 8 lanes too
+  if (kG < kMinG) exact = 3u;
   if constexpr (kCross) {
     if (exact & 1u)
       class_pairs_part<kG, kSame, true, false, kTail, kPrecise, true>(
@@ -1235,7 +1238,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, min_blocks_for(kMode))
         fs.reset();
         for (int il = lane; il < cs.n1; il += kG) prep_row(cs.o1 + il, il, dsl, dsu);
         if (infeasible) continue;  // (rows still feed the split decision)
-        const unsigned exact = kG < kFastMinG ? 3u : G.bor2(fs.need());
+        const unsigned exact = kG < kSibFastMinG ? 3u : G.bor2(fs.need());
         sl_self += static_cast<double>(w * dsl);
         se_self += static_cast<double>(w * dsl * kErrTerm);
         su_self += static_cast<double>(w * dsu);
@@ -1244,10 +1247,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, min_blocks_for(kMode))
         double dl = 0.0, du = 0.0;
 #ifndef GOSMA_PREP_ONLY
         if (same) {
-          class_pairs<kG, true, false, true, kTail, false>(T, loc, lane, w, sl_self, dl, su_self,
+          class_pairs<kG, true, false, true, kTail, false, kSibFastMinG>(T, loc, lane, w, sl_self, dl, su_self,
                                                            du, se_self, lb_amp, exact);
         } else {
-          class_pairs<kG, false, false, true, kTail, false>(T, loc, lane, w, sl_self, dl, su_self,
+          class_pairs<kG, false, false, true, kTail, false, kSibFastMinG>(T, loc, lane, w, sl_self, dl, su_self,
                                                             du, se_self, lb_amp, exact);
         }
 #endif
@@ -1259,10 +1262,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, min_blocks_for(kMode))
           float acr = 0.0f;
 #ifndef GOSMA_PREP_ONLY
           if (same) {
-            class_pairs<kG, true, true, false, kTail, false>(T, loc, lane, w, dl, lcr, du, ucr,
+            class_pairs<kG, true, true, false, kTail, false, kSibFastMinG>(T, loc, lane, w, dl, lcr, du, ucr,
                                                              ecr, acr, exact);
           } else {
-            class_pairs<kG, false, true, false, kTail, false>(T, loc, lane, w, dl, lcr, du, ucr,
+            class_pairs<kG, false, true, false, kTail, false, kSibFastMinG>(T, loc, lane, w, dl, lcr, du, ucr,
                                                               ecr, acr, exact);
           }
 #endif

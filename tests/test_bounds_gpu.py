@@ -491,11 +491,21 @@ def test_children_branch_and_bound_equals_explicit_children(gosma, n1, n2, ncls)
     lo, up, cs = d_lo.cpu().numpy(), d_up.cpu().numpy(), d_cs.cpu().numpy()
     assert np.array_equal(np.isinf(lo), np.isinf(klo))
     f = np.isfinite(klo)
-    scale = np.abs(klo[f]) + np.abs(kup[f]) + 1.0
-    assert np.all(np.abs(lo[f] - klo[f]) <= 1e-12 * scale)
     fu = np.isfinite(kup)
     assert np.array_equal(fu, np.isfinite(up))
-    assert np.all(np.abs(up[fu] - kup[fu]) <= 1e-12 * (np.abs(kup[fu]) + 1.0))
+    if ncls == 1:
+        # same loop copies, same FP32 terms: equal up to FP64 summation order
+        scale = np.abs(klo[f]) + np.abs(kup[f]) + 1.0
+        assert np.all(np.abs(lo[f] - klo[f]) <= 1e-12 * scale)
+        assert np.all(np.abs(up[fu] - kup[fu]) <= 1e-12 * (np.abs(kup[fu]) + 1.0))
+    else:
+        # the class-streamed siblings mode may take the fast loop copies at
+        # 8-lane groups where the full kernel keeps the exact ones (and send
+        # other nodes through the precise fix-up): equal to the FP32 tolerance
+        mix = Mixture(**synth.to_mixture_arrays(classes, 0.5))
+        _, _, lm, um, _ = Oracle(mix).eval_bounds(kids, threads=8)
+        assert np.all(np.abs(lo[f] - klo[f]) <= TOL_RAW * lm[f] + 1e-12)
+        assert np.all(np.abs(up[fu] - kup[fu]) <= TOL_UB * um[fu] + 1e-12)
     assert np.array_equal(cs, ksp)
 
 
