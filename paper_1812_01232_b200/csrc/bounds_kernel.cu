@@ -783,9 +783,12 @@ struct FastScore {
 
 // Half-angle of psi_trans (se3.cpp:72-92) for a mean outside the cuboid: the
 // vertex with the largest angle to the centre direction has the smallest
-// cosine c_hat . v_hat. FP32 picks the candidates (every vertex within 1e-6 of
-// the best cosine), FP64 evaluates them: returns sin and cos of half the
-// angle as |c_hat - v_hat|/2 and |c_hat + v_hat|/2.
+// cosine c_hat . v_hat. FP32 ranks the vertices, FP64 evaluates the FP32 best
+// and (rarely) every other vertex within 1e-6 of it, keeping the largest
+// FP64 angle (first vertex on exact ties): returns sin and cos of half the
+// angle as |c_hat - v_hat|/2 and |c_hat + v_hat|/2. The best vertex is
+// evaluated with its signs as data, so lanes with different best vertices
+// share one FP64 evaluation instead of diverging over all eight.
 __device__ __forceinline__ void psi_trans_half(double u0, double u1, double u2, double h0,
                                                double h1, double h2, double c0, double c1,
                                                double c2, double& st, double& ct) {
@@ -797,6 +800,7 @@ __device__ __forceinline__ void psi_trans_half(double u0, double u1, double u2, 
               fc2 = static_cast<float>(c2);
   float cosv[8];
   float best = 2.0f;
+  int sb = 0;
 #pragma unroll
   for (int s = 0; s < 8; ++s) {
     const float vx = fu0 - ((s & 4) ? fh0 : -fh0);
@@ -804,23 +808,35 @@ __device__ __forceinline__ void psi_trans_half(double u0, double u1, double u2, 
     const float vz = fu2 - ((s & 1) ? fh2 : -fh2);
     const float rv = rsqf(fmaf(vx, vx, fmaf(vy, vy, vz * vz)));
     cosv[s] = fmaf(fc0, vx, fmaf(fc1, vy, fc2 * vz)) * rv;
-    best = fminf(best, cosv[s]);
+    if (cosv[s] < best) {
+      best = cosv[s];
+      sb = s;
+    }
   }
-  double bs = -1.0, bc = 0.0;
+  // FP64 squared half-chords |c - w|^2, |c + w|^2 of vertex s
+  auto chord = [&](int s, double& sd, double& pd) {
+    const double vx = u0 - ((s & 4) ? h0 : -h0);
+    const double vy = u1 - ((s & 2) ? h1 : -h1);
+    const double vz = u2 - ((s & 1) ? h2 : -h2);
+    const double iv = rsqrt(vx * vx + vy * vy + vz * vz);
+    const double wx = vx * iv, wy = vy * iv, wz = vz * iv;
+    const double ex = c0 - wx, ey = c1 - wy, ez = c2 - wz;
+    sd = ex * ex + ey * ey + ez * ez;
+    const double px = c0 + wx, py = c1 + wy, pz = c2 + wz;
+    pd = px * px + py * py + pz * pz;
+  };
+  double bs, bc;
+  chord(sb, bs, bc);
+  int bsi = sb;
 #pragma unroll
   for (int s = 0; s < 8; ++s) {
-    if (cosv[s] <= best + 1e-6f) {
-      const double vx = u0 - ((s & 4) ? h0 : -h0);
-      const double vy = u1 - ((s & 2) ? h1 : -h1);
-      const double vz = u2 - ((s & 1) ? h2 : -h2);
-      const double iv = rsqrt(vx * vx + vy * vy + vz * vz);
-      const double wx = vx * iv, wy = vy * iv, wz = vz * iv;
-      const double ex = c0 - wx, ey = c1 - wy, ez = c2 - wz;
-      const double sd = ex * ex + ey * ey + ez * ez;
-      if (sd > bs) {
+    if (s != sb && cosv[s] <= best + 1e-6f) {  // FP32 near-tie: decide in FP64
+      double sd, pd;
+      chord(s, sd, pd);
+      if (sd > bs || (sd == bs && s < bsi)) {
         bs = sd;
-        const double px = c0 + wx, py = c1 + wy, pz = c2 + wz;
-        bc = px * px + py * py + pz * pz;
+        bc = pd;
+        bsi = s;
       }
     }
   }
