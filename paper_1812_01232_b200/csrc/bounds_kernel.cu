@@ -196,6 +196,16 @@ struct Group {
       return fmax(fmax(sh->d[0], sh->d[1]), fmax(sh->d[2], sh->d[3]));
     }
   }
+  // value of lane k of this warp's part of the group (kG > 32: of this warp)
+  __device__ __forceinline__ double shfl(double v, int k) const {
+    if constexpr (kG == 1) {
+      return v;
+    } else if constexpr (kG <= 32) {
+      return __shfl_sync(gm, v, k, kG);
+    } else {
+      return __shfl_sync(kFull, v, k);
+    }
+  }
   // value of group lane 0
   __device__ __forceinline__ long long bcast0(long long v) const {
     if constexpr (kG == 1) {
@@ -866,17 +876,16 @@ enum {
 // err, amplified err} cross sums (32 doubles)
 constexpr int kSibStreamExtraF4 = (72 + 32) * 8 / 16;
 
-// Rodrigues R0 = rotation_matrix(rc) (se3.cpp:21-31), FP64.
-__device__ __forceinline__ void rodrigues(double rc0, double rc1, double rc2, double R[9]) {
-  const double th2 = rc0 * rc0 + rc1 * rc1 + rc2 * rc2;
+// Rodrigues R0 = rotation_matrix(rc) (se3.cpp:21-31), FP64, from sin and
+// cos of theta = |rc| (unused when theta^2 < 1e-16).
+__device__ __forceinline__ void rodrigues_sc(double rc0, double rc1, double rc2, double th2,
+                                             double s, double co, double R[9]) {
   double a, c;
   if (th2 < 1e-16) {
     a = 1.0;
     c = 0.5;
   } else {
     const double th = sqrt(th2);
-    double s, co;
-    sincos(th, &s, &co);
     a = s / th;
     c = (1.0 - co) / th2;
   }
@@ -888,6 +897,13 @@ __device__ __forceinline__ void rodrigues(double rc0, double rc1, double rc2, do
       const double k2 = K[3 * r] * K[cix] + K[3 * r + 1] * K[3 + cix] + K[3 * r + 2] * K[6 + cix];
       R[3 * r + cix] = ((r == cix ? 1.0 : 0.0) + a * K[3 * r + cix]) + c * k2;
     }
+}
+
+__device__ __forceinline__ void rodrigues(double rc0, double rc1, double rc2, double R[9]) {
+  const double th2 = rc0 * rc0 + rc1 * rc1 + rc2 * rc2;
+  double s = 0.0, co = 1.0;
+  if (!(th2 < 1e-16)) sincos(sqrt(th2), &s, &co);
+  rodrigues_sc(rc0, rc1, rc2, th2, s, co, R);
 }
 
 // Half-angle of psi_t + psi_r per row (B = 0 once the sum reaches pi) from the
@@ -1066,9 +1082,22 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, min_blocks_for(kMode))
     double R[9];
     double s_r = 0.0, c_r = 1.0;
     if (!kSib) {
-      rodrigues(rc0, rc1, rc2, R);
       const double psi_r = fmin(sqrt(3.0) * rhw, M_PI);
-      sincos(0.5 * psi_r, &s_r, &c_r);
+      const double th2 = rc0 * rc0 + rc1 * rc1 + rc2 * rc2;
+      if constexpr (kG == 1) {
+        rodrigues(rc0, rc1, rc2, R);
+        sincos(0.5 * psi_r, &s_r, &c_r);
+      } else {
+        // one FP64 sincos for both angles: even lanes theta = |rc| (Rodrigues),
+        // odd lanes psi_r / 2, exchanged with a shuffle
+        const bool odd = (lane & 1) != 0;
+        double s1, c1;
+        sincos(odd ? 0.5 * psi_r : (th2 < 1e-16 ? 0.0 : sqrt(th2)), &s1, &c1);
+        const double sr0 = G.shfl(s1, 0), cr0 = G.shfl(c1, 0);
+        s_r = G.shfl(s1, 1);
+        c_r = G.shfl(c1, 1);
+        rodrigues_sc(rc0, rc1, rc2, th2, sr0, cr0, R);
+      }
     } else {
       // the 8 rotation children share psi_r (their half-width 0.5 rhw): the
       // rows are prepared once with it (psi_t + psi_r half-angles)
