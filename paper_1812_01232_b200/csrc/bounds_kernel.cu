@@ -163,10 +163,11 @@ struct Group {
       return __syncthreads_or(b) != 0;
     }
   }
-  // OR of 2-bit flags over the group (two votes: __reduce_or_sync with a
-  // partial mask serialises the groups of a warp)
-  __device__ __forceinline__ unsigned bor2(unsigned v) const {
-    return (any((v & 1u) != 0u) ? 1u : 0u) | (any((v & 2u) != 0u) ? 2u : 0u);
+  // OR of 3-bit flags over the group (one vote per bit: __reduce_or_sync
+  // with a partial mask serialises the groups of a warp)
+  __device__ __forceinline__ unsigned bor3(unsigned v) const {
+    return (any((v & 1u) != 0u) ? 1u : 0u) | (any((v & 2u) != 0u) ? 2u : 0u) |
+           (any((v & 4u) != 0u) ? 4u : 0u);
   }
   __device__ __forceinline__ double sum(double v) const {
     if constexpr (kG <= 32) {
@@ -357,14 +358,14 @@ __device__ __forceinline__ void sin_sq(float hx, float hy, float hz, float lx, f
 // s4 = 4 sin^2(psi/2) from FP64 per-row prep: the theta ~ psi cancellation
 // happens in x - s4, where both operands carry ~1e-7 relative error, instead
 // of in sin/cos products.
-template <bool kSame, bool kPrecise = false, bool kExact = true>
+template <bool kSame, bool kPrecise = false, bool kExact = true, bool kXo = !kExact>
 __device__ __forceinline__ void cross_pair(const Row& r, const float4 qa, const float4 qb, float& l,
                                            float& u, float& ma, float& mb,
                                            const float4 rp = float4{}) {
   const float k2 = qa.w;
   // x = |u - q|^2 = 4 sin^2(theta/2), y = |u + q|^2 = 4 cos^2(theta/2), each
   // without cancellation (sincos_sq)
-  constexpr bool kX = !kExact && GOSMA_XONLY;
+  constexpr bool kX = kXo && GOSMA_XONLY;
   float x, y;
   if constexpr (kX)
     sin_sq(r.uhx, r.uhy, r.uhz, r.ulx, r.uly, r.ulz, qa.x, qa.y, qa.z, qb.x, qb.y, qb.z, x, y);
@@ -566,7 +567,8 @@ __device__ __forceinline__ Row load_row(const WarpTables& T, int i) {
   return r;
 }
 
-template <int kG, bool kSame, bool kCross, bool kSelf, bool kPrecise, bool kExact>
+template <int kG, bool kSame, bool kCross, bool kSelf, bool kPrecise, bool kExact,
+          bool kXo = !kExact>
 __device__ __forceinline__ void class_pairs_rows(const WarpTables& T, const ClassSpan cs, int lane,
                                             float w, double& lb_self, double& lb_cross,
                                             double& ub_self, double& ub_cross, double& lb_err,
@@ -583,7 +585,7 @@ __device__ __forceinline__ void class_pairs_rows(const WarpTables& T, const Clas
       const float4* cp = T.col + cs.o2 * kColF4;  // pointer walk: no index math per pair
       const float4* const ce = cp + cs.n2 * kColF4;
 #pragma unroll kUnrollPairs
-      for (; cp < ce; cp += kColF4) cross_pair<kSame, kPrecise, kExact>(r, cp[0], cp[1], l, u, ma, mb, rp);
+      for (; cp < ce; cp += kColF4) cross_pair<kSame, kPrecise, kExact, kXo>(r, cp[0], cp[1], l, u, ma, mb, rp);
       lb_cross += static_cast<double>(w * r.Fhi * l);
       const float amp = 2.0f * w * r.Fhi * ma * kErrAmp;
       lb_err += static_cast<double>(
@@ -630,7 +632,8 @@ __device__ __forceinline__ void class_pairs_rows(const WarpTables& T, const Clas
 // gives each row k = kG / r lanes ("slots") sharing its partners round-robin
 // (the node sums are sums over pairs, so any pair -> lane assignment is
 // exact). Separate instantiation: the plain loops stay tighter for full chunks.
-template <int kG, bool kSame, bool kCross, bool kSelf, bool kPrecise, bool kExact>
+template <int kG, bool kSame, bool kCross, bool kSelf, bool kPrecise, bool kExact,
+          bool kXo = !kExact>
 __device__ __forceinline__ void class_pairs_tail(const WarpTables& T, const ClassSpan cs,
                                                  int lane, float w, double& lb_self,
                                                  double& lb_cross, double& ub_self,
@@ -651,7 +654,7 @@ __device__ __forceinline__ void class_pairs_tail(const WarpTables& T, const Clas
       const int cstep = k * kColF4;
 #pragma unroll kUnrollPairs
       for (; cp < ce; cp += cstep)
-        cross_pair<kSame, kPrecise, kExact>(rw, cp[0], cp[1], l, u, ma, mb, rp);
+        cross_pair<kSame, kPrecise, kExact, kXo>(rw, cp[0], cp[1], l, u, ma, mb, rp);
       lb_cross += static_cast<double>(w * rw.Fhi * l);
       const float amp = 2.0f * w * rw.Fhi * ma * kErrAmp;
       lb_err += static_cast<double>(
@@ -703,21 +706,24 @@ __device__ __forceinline__ void class_pairs_tail(const WarpTables& T, const Clas
 constexpr int kFastMinG = GOSMA_FAST_MIN_G;
 constexpr int kSibFastMinG = 8;  // the class-streamed siblings mode (semantic solves)
 
-template <int kG, bool kSame, bool kCross, bool kSelf, bool kTail, bool kPrecise, bool kExact>
+template <int kG, bool kSame, bool kCross, bool kSelf, bool kTail, bool kPrecise, bool kExact,
+          bool kXo = !kExact>
 __device__ __forceinline__ void class_pairs_part(const WarpTables& T, const ClassSpan cs, int lane,
                                                  float w, double& lb_self, double& lb_cross,
                                                  double& ub_self, double& ub_cross,
                                                  double& lb_err, float& lb_amp) {
   if constexpr (kTail)
-    class_pairs_tail<kG, kSame, kCross, kSelf, kPrecise, kExact>(
+    class_pairs_tail<kG, kSame, kCross, kSelf, kPrecise, kExact, kXo>(
         T, cs, lane, w, lb_self, lb_cross, ub_self, ub_cross, lb_err, lb_amp);
   else
-    class_pairs_rows<kG, kSame, kCross, kSelf, kPrecise, kExact>(
+    class_pairs_rows<kG, kSame, kCross, kSelf, kPrecise, kExact, kXo>(
         T, cs, lane, w, lb_self, lb_cross, ub_self, ub_cross, lb_err, lb_amp);
 }
 
-// exact: bit 0 the cross loop needs the exact-path copy, bit 1 the self loop
-// (FastScore); the cross sums come first, as in class_pairs_rows.
+// exact: bit 0 the cross loop needs the exact-path copy, bit 1 the self loop,
+// bit 2 the cross loop's fast copy must keep the sign-selected angles (a row's
+// psi too large for x-only; FastScore); the cross sums come first, as in
+// class_pairs_rows.
 template <int kG, bool kSame, bool kCross, bool kSelf, bool kTail, bool kPrecise,
           int kMinG = kFastMinG>
 __device__ __forceinline__ void class_pairs(const WarpTables& T, const ClassSpan cs, int lane,
@@ -727,10 +733,13 @@ __device__ __forceinline__ void class_pairs(const WarpTables& T, const ClassSpan
   // the fast loop copies only for groups of >= kMinG lanes (classes of > 24
   // rows in the full modes): short loops gain nothing from them and lose to
   // the larger code; the class-streamed siblings mode gains at 8 lanes too
-  if (kG < kMinG) exact = 3u;
+  if (kG < kMinG) exact = 7u;
   if constexpr (kCross) {
     if (exact & 1u)
       class_pairs_part<kG, kSame, true, false, kTail, kPrecise, true>(
+          T, cs, lane, w, lb_self, lb_cross, ub_self, ub_cross, lb_err, lb_amp);
+    else if (exact & 4u)
+      class_pairs_part<kG, kSame, true, false, kTail, kPrecise, false, false>(
           T, cs, lane, w, lb_self, lb_cross, ub_self, ub_cross, lb_err, lb_amp);
     else
       class_pairs_part<kG, kSame, true, false, kTail, kPrecise, false>(
@@ -768,26 +777,33 @@ __device__ __forceinline__ void class_pairs(const WarpTables& T, const ClassSpan
 //    (1 + cos psi) = L H 2 cos^2(psi/2) (and the UB / self terms at
 //    theta ~ pi have |e| >= 2 L H): H(kappa_lo, min k2) min(1, 2 cp^2) >= 45,
 //    with cp = 0 exempt (psi clamped at pi: every cross pair has B = 0).
-// Per row two scores, >= 1 when the cross (resp. self) conditions hold; the
-// node decisions are one vote each over its rows (group-uniform: the fast
-// loops never diverge inside a group).
+// Per row three scores, >= 1 when the cross loop may skip the exact paths
+// (kappa_lo, kappa at t* >= 45), when its fast copy may use x-only angles
+// (H(kappa_lo, min k2) min(1, 2 cos^2(psi/2)) >= 45), and when the self loop
+// may take its fast copy (kappa_hi >= 90, kappa at t* >= 45); the node
+// decisions are one vote each over its rows (group-uniform: the loops never
+// diverge inside a group). Nodes failing only the x-only score (psi near pi,
+// e.g. rotation-level-1 cubes) run the fast cross copy with sign-selected
+// angles.
 // GOSMA_FAST_SCALE scales the thresholds (A/B builds).
 #ifndef GOSMA_FAST_SCALE
 #define GOSMA_FAST_SCALE 1.0f
 #endif
 struct FastScore {
-  float cross = INFINITY, self = INFINITY;
+  float cross = INFINITY, self = INFINITY, xonly = INFINITY;
   __device__ __forceinline__ void add(float klo, float khi, float kst, float k2_min, double cp) {
     constexpr float kA = 1.0f / (45.0f * GOSMA_FAST_SCALE), kB = 1.0f / (90.0f * GOSMA_FAST_SCALE);
     const float h = klo * k2_min / (klo + k2_min);
     const float c = cp > 0.0 ? fminf(1.0f, static_cast<float>(2.0 * cp * cp)) : 1.0f;
-    cross = fminf(cross, fminf(fminf(klo, kst), h * c) * kA);
+    cross = fminf(cross, fminf(klo, kst) * kA);
+    xonly = fminf(xonly, h * c * kA);
     self = fminf(self, fminf(kst * kA, khi * kB));
   }
-  __device__ __forceinline__ void reset() { cross = self = INFINITY; }
-  // this lane's rows: bit 0 the cross loop needs the exact copy, bit 1 the self loop
+  __device__ __forceinline__ void reset() { cross = self = xonly = INFINITY; }
+  // this lane's rows: bit 0 the cross loop needs the exact copy, bit 1 the
+  // self loop, bit 2 the cross loop's fast copy needs the sign-selected angles
   __device__ __forceinline__ unsigned need() const {
-    return (cross >= 1.0f ? 0u : 1u) | (self >= 1.0f ? 0u : 2u);
+    return (cross >= 1.0f ? 0u : 1u) | (self >= 1.0f ? 0u : 2u) | (xonly >= 1.0f ? 0u : 4u);
   }
 };
 
@@ -1244,7 +1260,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, min_blocks_for(kMode))
         fs.reset();
         for (int il = lane; il < cs.n1; il += kG) prep_row(cs.o1 + il, il, dsl, dsu);
         if (infeasible) continue;  // (rows still feed the split decision)
-        const unsigned exact = kG < kFastMinG ? 3u : G.bor2(fs.need());
+        const unsigned exact = kG < kFastMinG ? 7u : G.bor3(fs.need());
         lb_self += static_cast<double>(w * dsl);
         lb_err += static_cast<double>(w * dsl * kErrTerm);
         ub_self += static_cast<double>(w * dsu);
@@ -1283,7 +1299,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, min_blocks_for(kMode))
         fs.reset();
         for (int il = lane; il < cs.n1; il += kG) prep_row(cs.o1 + il, il, dsl, dsu);
         if (infeasible) continue;  // (rows still feed the split decision)
-        const unsigned exact = kG < kSibFastMinG ? 3u : G.bor2(fs.need());
+        const unsigned exact = kG < kSibFastMinG ? 7u : G.bor3(fs.need());
         sl_self += static_cast<double>(w * dsl);
         se_self += static_cast<double>(w * dsl * kErrTerm);
         su_self += static_cast<double>(w * dsu);
@@ -1366,7 +1382,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, min_blocks_for(kMode))
     // split decision (subdivide_adaptive, se3.cpp:107-121)
     st_max = G.max(st_max);
     // whole-table modes: every row is prepared, one decision for the node
-    const unsigned exact = (streamed || kG < kFastMinG) ? 3u : G.bor2(fs.need());
+    const unsigned exact = (streamed || kG < kFastMinG) ? 7u : G.bor3(fs.need());
     if constexpr (kMode == kSiblings) {
       // one cuboid, 8 rotation children: self sums once, then per child
       const double hr = 0.5 * rhw;
