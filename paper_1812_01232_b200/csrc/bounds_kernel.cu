@@ -735,15 +735,19 @@ __device__ __forceinline__ void class_pairs(const WarpTables& T, const ClassSpan
   // the larger code; the class-streamed siblings mode gains at 8 lanes too
   if (kG < kMinG) exact = 7u;
   if constexpr (kCross) {
-    if (exact & 1u)
+    // (8-lane groups: no sign-selected fast copy; its code cost the
+    // class-streamed siblings mode 3% there)
+    if (exact & 1u || (kG < 16 && (exact & 4u))) {
       class_pairs_part<kG, kSame, true, false, kTail, kPrecise, true>(
           T, cs, lane, w, lb_self, lb_cross, ub_self, ub_cross, lb_err, lb_amp);
-    else if (exact & 4u)
-      class_pairs_part<kG, kSame, true, false, kTail, kPrecise, false, false>(
-          T, cs, lane, w, lb_self, lb_cross, ub_self, ub_cross, lb_err, lb_amp);
-    else
+    } else if (exact & 4u) {
+      if constexpr (kG >= 16)
+        class_pairs_part<kG, kSame, true, false, kTail, kPrecise, false, false>(
+            T, cs, lane, w, lb_self, lb_cross, ub_self, ub_cross, lb_err, lb_amp);
+    } else {
       class_pairs_part<kG, kSame, true, false, kTail, kPrecise, false>(
           T, cs, lane, w, lb_self, lb_cross, ub_self, ub_cross, lb_err, lb_amp);
+    }
   }
   if constexpr (kSelf) {
     if (exact & 2u)
