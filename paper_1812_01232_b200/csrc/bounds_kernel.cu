@@ -1579,8 +1579,10 @@ namespace {
 //  1  tiny mixtures (5 n1 + 2 n2 <= 48 table float4, e.g. up to 6x6): one lane
 //     runs a whole node - 4.8x at 2x2, 2x at 4x4 over 8-lane groups;
 //  8  up to 24 rows per class (8x8 .. 24x20: 1.2-2x over 16 / 32 lanes);
-//  16 up to 32 rows; 32 beyond; a whole CTA (4 warps sharing one node's
-//     tables) for large mixtures whose tables would cap residency.
+//  32 beyond (since the fast loop copies, 32 beats 16 lanes at 25-32 rows:
+//     32x32 5.85 -> 5.33 ms, 8 x (32x16) 32.7 -> 28.0 ms; 16 stays
+//     selectable); a whole CTA (4 warps sharing one node's tables) for large
+//     mixtures whose tables would cap residency.
 // Each choice also keeps the CTA's tables within a shared-memory budget.
 // GOSMA_GROUP forces a size (A/B runs).
 int group_lanes(const DevCtx& ctx, int mode) {
@@ -1598,7 +1600,6 @@ int group_lanes(const DevCtx& ctx, int mode) {
   const long long pairs_bound = n1 * (n1 - 1) / 2 + n1 * n2;  // exact for one class
   if (core <= 48 * 16 && pairs_bound <= 64 && table * groups_per_cta <= 160 * 1024) return 1;
   if (ctx.max_n1 <= 24 && table * kWarpsPerCta * 4 <= 64 * 1024) return 8;
-  if (ctx.max_n1 <= 32 && table * kWarpsPerCta * 2 <= 64 * 1024) return 16;
   if (ctx.max_n1 >= 64 && table > 10 * 1024) return kCtaGroup;
   return 32;
 }
