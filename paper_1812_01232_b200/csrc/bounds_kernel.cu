@@ -811,6 +811,19 @@ struct FastScore {
   }
 };
 
+// 1/sqrt(x) in FP64 for x in the normal float range (squared distances of
+// scene geometry): the MUFU float estimate and two branch-free Newton steps
+// (2^-22 -> 2^-43 -> ~1 ulp). The libdevice rsqrt carries a special-case
+// branch whose reconvergence points stalled the prologue's warps
+// (profiles/r02_k1_variants.md).
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double y = static_cast<double>(rsqf(static_cast<float>(x)));
+  const double hx = 0.5 * x;
+  y = y * fma(-hx * y, y, 1.5);
+  y = y * fma(-hx * y, y, 1.5);
+  return y;
+}
+
 // Half-angle of psi_trans (se3.cpp:72-92) for a mean outside the cuboid: the
 // vertex with the largest angle to the centre direction has the smallest
 // cosine c_hat . v_hat. FP32 ranks the vertices, FP64 evaluates the FP32 best
@@ -848,7 +861,7 @@ __device__ __forceinline__ void psi_trans_half(double u0, double u1, double u2, 
     const double vx = u0 - ((s & 4) ? h0 : -h0);
     const double vy = u1 - ((s & 2) ? h1 : -h1);
     const double vz = u2 - ((s & 1) ? h2 : -h2);
-    const double iv = rsqrt(vx * vx + vy * vy + vz * vz);
+    const double iv = rsqrt_nr(vx * vx + vy * vy + vz * vz);
     const double wx = vx * iv, wy = vy * iv, wz = vz * iv;
     const double ex = c0 - wx, ey = c1 - wy, ez = c2 - wz;
     sd = ex * ex + ey * ey + ez * ez;
@@ -870,8 +883,8 @@ __device__ __forceinline__ void psi_trans_half(double u0, double u1, double u2, 
       }
     }
   }
-  st = 0.5 * sqrt(bs);
-  ct = 0.5 * sqrt(bc);
+  st = bs > 0.0 ? 0.5 * bs * rsqrt_nr(bs) : 0.0;
+  ct = bc > 0.0 ? 0.5 * bc * rsqrt_nr(bc) : 0.0;
 }
 
 // kMode: kModeFull = every term per node; kSelfOnly = per distinct translation
@@ -905,9 +918,9 @@ __device__ __forceinline__ void rodrigues_sc(double rc0, double rc1, double rc2,
     a = 1.0;
     c = 0.5;
   } else {
-    const double th = sqrt(th2);
-    a = s / th;
-    c = (1.0 - co) / th2;
+    const double ith = rsqrt_nr(th2);  // 1 / theta
+    a = s * ith;
+    c = (1.0 - co) * (ith * ith);
   }
   const double K[9] = {0.0, -rc2, rc1, rc2, 0.0, -rc0, -rc1, rc0, 0.0};
 #pragma unroll
@@ -922,7 +935,7 @@ __device__ __forceinline__ void rodrigues_sc(double rc0, double rc1, double rc2,
 __device__ __forceinline__ void rodrigues(double rc0, double rc1, double rc2, double R[9]) {
   const double th2 = rc0 * rc0 + rc1 * rc1 + rc2 * rc2;
   double s = 0.0, co = 1.0;
-  if (!(th2 < 1e-16)) sincos(sqrt(th2), &s, &co);
+  if (!(th2 < 1e-16)) sincos(th2 * rsqrt_nr(th2), &s, &co);
   rodrigues_sc(rc0, rc1, rc2, th2, s, co, R);
 }
 
@@ -1112,7 +1125,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, min_blocks_for(kMode))
         // odd lanes psi_r / 2, exchanged with a shuffle
         const bool odd = (lane & 1) != 0;
         double s1, c1;
-        sincos(odd ? 0.5 * psi_r : (th2 < 1e-16 ? 0.0 : sqrt(th2)), &s1, &c1);
+        sincos(odd ? 0.5 * psi_r : (th2 < 1e-16 ? 0.0 : th2 * rsqrt_nr(th2)), &s1, &c1);
         const double sr0 = G.shfl(s1, 0), cr0 = G.shfl(c1, 0);
         s_r = G.shfl(s1, 1);
         c_r = G.shfl(c1, 1);
@@ -1197,7 +1210,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, min_blocks_for(kMode))
       const double un2 = u0 * u0 + u1 * u1 + u2 * u2;
       double c0 = 1.0, c1 = 0.0, c2 = 0.0;  // UnitX when the mean is at the centre
       if (un2 > 1e-24) {
-        const double inv = rsqrt(un2);
+        const double inv = rsqrt_nr(un2);
         c0 = u0 * inv;
         c1 = u1 * inv;
         c2 = u2 * inv;
@@ -1217,7 +1230,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, min_blocks_for(kMode))
       const double vn2 = v0 * v0 + v1 * v1 + v2 * v2;
       const float kst = static_cast<float>(vn2 * is2 + 1.0);
       fs.add(klo, khi, kst, ctx.min_k2, cp);
-      const double iv = rsqrt(vn2);
+      const double iv = rsqrt_nr(vn2);
       const float phi = static_cast<float>(ctx.phi1[i]);
       dsl += diag_term(phi, klo);
       dsu += diag_term(phi, kst);
