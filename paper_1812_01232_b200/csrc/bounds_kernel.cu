@@ -870,16 +870,21 @@ __device__ __forceinline__ void psi_trans_half(double u0, double u1, double u2, 
   };
   double bs, bc;
   chord(sb, bs, bc);
-  int bsi = sb;
+  bool tie = false;
 #pragma unroll
-  for (int s = 0; s < 8; ++s) {
-    if (s != sb && cosv[s] <= best + 1e-6f) {  // FP32 near-tie: decide in FP64
-      double sd, pd;
-      chord(s, sd, pd);
-      if (sd > bs || (sd == bs && s < bsi)) {
-        bs = sd;
-        bc = pd;
-        bsi = s;
+  for (int s = 0; s < 8; ++s) tie |= (s != sb) & (cosv[s] <= best + 1e-6f);
+  if (tie) {  // FP32 near-ties (rare): decide in FP64, one branch for all
+    int bsi = sb;
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      if (s != sb && cosv[s] <= best + 1e-6f) {
+        double sd, pd;
+        chord(s, sd, pd);
+        if (sd > bs || (sd == bs && s < bsi)) {
+          bs = sd;
+          bc = pd;
+          bsi = s;
+        }
       }
     }
   }
