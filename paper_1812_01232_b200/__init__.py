@@ -572,6 +572,10 @@ class ShardSolver:
         nodes = torch.empty(max_nodes * NODE_DTYPE.itemsize, dtype=torch.uint8, device=device)
         split = torch.empty(max_nodes, dtype=torch.int8, device=device)
         vol = torch.empty(max_nodes, dtype=torch.float64, device=device)
+        # the solver writes them on its own stream: let torch's stream finish
+        # any work on the recycled allocations first (the export itself
+        # synchronises its stream before returning)
+        torch.cuda.current_stream(device).synchronize()
         n = C.c_size_t(0)
         _check(lib.gosma_solver_export_device(self._h, max_nodes, nodes.data_ptr(),
                                               split.data_ptr(), vol.data_ptr(), C.byref(n)),
