@@ -997,7 +997,12 @@ __device__ __forceinline__ void column_prep_span(const WarpTables& T, const DevC
 // registers: its per-class / per-child loops otherwise rematerialise the
 // table addresses; 8 x (8x4) siblings 2.04 -> 1.93 ms, 8 x (32x16) 15.6 ->
 // 14.6 ms); every other mode loses at 5 or 6 (profiles/r02_k1_variants.md).
-constexpr int min_blocks_for(int mode) { return mode == kSiblingsStream ? 5 : GOSMA_MIN_BLOCKS; }
+#ifndef GOSMA_SIB_MIN_BLOCKS
+#define GOSMA_SIB_MIN_BLOCKS 5
+#endif
+constexpr int min_blocks_for(int mode) {
+  return mode == kSiblingsStream ? GOSMA_SIB_MIN_BLOCKS : GOSMA_MIN_BLOCKS;
+}
 template <int kMode, int kG, bool kTail>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, min_blocks_for(kMode))
     eval_bounds_kernel(const DevCtx ctx, const EvalArgs args) {
