@@ -9,9 +9,10 @@
 // plus subdivide_adaptive's split decision (se3.cpp:107-121), fused because
 // it reuses psi_trans.
 //
-// Work decomposition: one warp per node (persistent warps, dynamic node
-// counter). Lanes first build per-component tables for the node in shared
-// memory, then sweep the pair terms:
+// Work decomposition: one lane group per node (1, 8 or 32 lanes, or a whole
+// CTA for large mixtures; persistent groups, dynamic node counter). Lanes
+// first build per-component tables for the node in shared memory, then sweep
+// the pair terms:
 //   cross (i, j): the lane owns model row i (registers), the image column j
 //                 is a shared-memory broadcast;
 //   self  (i, j): circulant schedule (i, i+d mod n) — every unordered pair
@@ -26,11 +27,14 @@
 // formulas). This keeps FP32 accurate at concentrations of 1e4-1e5, where
 // log Z(K) - log Z(a) - log Z(b) would cancel catastrophically. For K > 15,
 // W(K) = 1/K to FP32 precision, so exp(... + log W(K)) = 2^(...) * rsqrt(K^2):
-// a pair costs 7 MUFU ops (2 sqrt, 2 rsqrt, 1 rcp, 2 ex2). The rare exact
+// a pair costs 6 MUFU ops (1 sqrt, 2 rsqrt, 1 rcp, 2 ex2). The rare exact
 // paths (K <= 15, the interior K minimum of the cross LB, the corner maximum
 // of the self LB when cos A < 0) run only for terms that survive FP32
-// underflow. Terms are FP32; per-row partial sums flush to FP64; per-node sums
-// are FP64 warp reductions.
+// underflow, and only in the exact loop copies: per node, group votes over
+// per-row scores send the cross and self loops to copies without them
+// (FastScore). Terms are FP32; per-row partial sums flush to FP64; per-node
+// sums are FP64 group reductions; a precise fix-up launch re-evaluates the
+// few nodes whose FP32 error estimate is large (kFixFull / kFixStream).
 #include <cuda_runtime.h>
 
 #include <atomic>
