@@ -217,6 +217,35 @@ def test_bound_soundness_sampling(gosma):
     assert checked > 2000
 
 
+@pytest.mark.parametrize("n1,n2", [(64, 32), (41, 36)])
+def test_bound_soundness_sampling_fast_copies(gosma, n1, n2):
+    """LB <= f(pose) at feasible interior poses on realistic mixtures, where
+    K1 runs its fast loop copies (x-only and sign-selected cross, fast self)
+    on most nodes: rotation levels 1-6, so every copy is exercised."""
+    from paper_1812_01232_b200 import synth
+    classes = synth.mixture(n1, n2, "realistic", seed=n1 + n2)
+    ctx = gosma.ObjectiveContext(classes, 0.5)
+    o = Oracle(Mixture(**synth.to_mixture_arrays(classes, 0.5)))
+    nodes = synth.nodes(300, seed=n1).view(np.float64).reshape(-1, 11)
+    lo, up = gosma.evaluate_branch_batch(ctx, nodes)
+    rng = np.random.default_rng(n2)
+    checked = 0
+    for k in range(len(nodes)):
+        if math.isinf(lo[k]):
+            continue
+        assert lo[k] <= up[k] + 1e-9 * abs(up[k]) + 1e-9
+        b = nodes[k]
+        for _ in range(6):
+            r = b[0:3] + rng.uniform(-b[3], b[3], 3)
+            t = b[4:7] + rng.uniform(-1, 1, 3) * b[7:10]
+            f = o.objective(r, t)
+            if math.isinf(f):
+                continue
+            assert lo[k] <= f + 1e-9 * abs(f)
+            checked += 1
+    assert checked > 1000
+
+
 def test_children_keep_parent_floor(gosma):
     # test_bounds.cpp:355-373
     rng = np.random.default_rng(66)
