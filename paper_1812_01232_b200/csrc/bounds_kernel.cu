@@ -815,13 +815,13 @@ struct FastScore {
   }
 };
 
-// 1/sqrt(x) in FP64 for x in the normal float range (squared distances of
-// scene geometry): the MUFU float estimate and two branch-free Newton steps
-// (2^-22 -> 2^-43 -> ~1 ulp). The libdevice rsqrt carries a special-case
-// branch whose reconvergence points stalled the prologue's warps
-// (profiles/r02_k1_variants.md).
+// 1/sqrt(x) in FP64 for normal x > 0: the MUFU FP64 estimate
+// (rsqrt.approx.f64, full exponent range) and two branch-free Newton steps.
+// The libdevice rsqrt carries a special-case branch whose reconvergence
+// points stalled the prologue's warps (profiles/r02_k1_variants.md).
 __device__ __forceinline__ double rsqrt_nr(double x) {
-  double y = static_cast<double>(rsqf(static_cast<float>(x)));
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
   const double hx = 0.5 * x;
   y = y * fma(-hx * y, y, 1.5);
   y = y * fma(-hx * y, y, 1.5);
