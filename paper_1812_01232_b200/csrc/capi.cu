@@ -585,7 +585,15 @@ int gosma_eval_bounds(gosma_ctx* ctx, const gosma_node* nodes, size_t n, double 
   // stream) and D2H of chunk k-1 (copy-out stream) overlap the bound kernel on
   // chunk k (compute stream). Overlap needs pinned host buffers; pageable ones
   // still work (the copies then serialise).
-  const size_t chunk = std::min<size_t>(n, static_cast<size_t>(1) << 17);
+  // chunk of 2^19 nodes (46 MB of nodes per slot): 1M-node batches run
+  // 64k, 128k, 256k, 512k chunks; e2e 8.22e7 (2^17) -> 8.40e7 (2^19) ->
+  // 8.33e7 (2^20) bounds/s on the configs[1] batch. GOSMA_CHUNK_LOG2 (A/B).
+  static const int chunk_log2 = [] {
+    const char* e = std::getenv("GOSMA_CHUNK_LOG2");
+    const int v = e ? std::atoi(e) : 19;
+    return v >= 12 && v <= 24 ? v : 19;
+  }();
+  const size_t chunk = std::min<size_t>(n, static_cast<size_t>(1) << chunk_log2);
   if ((e = ctx->scratch.reserve(2 * chunk)) != cudaSuccess) return cuda_error(e, "scratch");
   constexpr size_t kSmall = 8192;
   if (n <= kSmall) {
