@@ -38,7 +38,7 @@ for c in range(len(m["n1"])):
     o1, o2 = o1 + a, o2 + b
 ctx = g.ObjectiveContext(cls, m["zeta"], single_mixture=(mode != "semantic"))
 dom = g.PoseDomain(np.zeros(3), math.pi, np.array(G["torus_cover_3.5_0.5"]))
-cfg = g.SolverConfig(epsilon=eps, zeta=m["zeta"])
+cfg = g.SolverConfig(epsilon=eps, zeta=m["zeta"], wave_nodes=int(os.environ.get("WAVE", "0")))
 t0 = time.perf_counter()
 S = g.ShardSolver(ctx, dom, cfg)
 t_init = time.perf_counter() - t0
