@@ -709,6 +709,10 @@ __device__ __forceinline__ void class_pairs_tail(const WarpTables& T, const Clas
 #endif
 constexpr int kFastMinG = GOSMA_FAST_MIN_G;
 constexpr int kSibFastMinG = 8;  // the class-streamed siblings mode (semantic solves)
+#ifndef GOSMA_STREAM_FAST_MIN_G
+#define GOSMA_STREAM_FAST_MIN_G 16
+#endif
+constexpr int kStreamFastMinG = GOSMA_STREAM_FAST_MIN_G;  // class-streamed full mode
 
 template <int kG, bool kSame, bool kCross, bool kSelf, bool kTail, bool kPrecise, bool kExact,
           bool kXo = !kExact>
@@ -1291,7 +1295,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, min_blocks_for(kMode))
         fs.reset();
         for (int il = lane; il < cs.n1; il += kG) prep_row(cs.o1 + il, il, dsl, dsu);
         if (infeasible) continue;  // (rows still feed the split decision)
-        const unsigned exact = kG < kFastMinG ? 7u : G.bor3(fs.need());
+        const unsigned exact = kG < kStreamFastMinG ? 7u : G.bor3(fs.need());
         lb_self += static_cast<double>(w * dsl);
         lb_err += static_cast<double>(w * dsl * kErrTerm);
         ub_self += static_cast<double>(w * dsu);
@@ -1300,10 +1304,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, min_blocks_for(kMode))
 #ifndef GOSMA_PREP_ONLY
         const ClassSpan loc{0, cs.n1, 0, cs.n2};
         if (same) {
-          class_pairs<kG, true, true, true, kTail, kFix>(T, loc, lane, w, lb_self, lb_cross,
+          class_pairs<kG, true, true, true, kTail, kFix, kStreamFastMinG>(T, loc, lane, w, lb_self, lb_cross,
                                                          ub_self, ub_cross, lb_err, lb_amp, exact);
         } else {
-          class_pairs<kG, false, true, true, kTail, kFix>(T, loc, lane, w, lb_self, lb_cross,
+          class_pairs<kG, false, true, true, kTail, kFix, kStreamFastMinG>(T, loc, lane, w, lb_self, lb_cross,
                                                           ub_self, ub_cross, lb_err, lb_amp, exact);
         }
 #endif
