@@ -243,8 +243,10 @@ int gosma_solver_status(gosma_solver* solver, gosma_wave_status* status);
 /* An incumbent value found elsewhere (another rank): prunes, carries no pose. */
 int gosma_solver_set_incumbent(gosma_solver* solver, double value);
 /* One wave: expand the best nodes with lower < limit (normally d* - eps),
- * bound the children, update the incumbent (+SMA), route. max_evals > 0 caps
- * the children evaluated. */
+ * bound the children, update the incumbent (+SMA), route. Children whose
+ * lower bound is >= min(limit, d*) are finished: they join the certificate's
+ * floor instead of the frontier, so later calls must not raise the limit
+ * (d* - eps never rises). max_evals > 0 caps the children evaluated. */
 int gosma_solver_expand(gosma_solver* solver, double limit, unsigned long long max_evals);
 /* Frontier rebalancing: remove up to max_nodes of the best live nodes into
  * host buffers / add nodes received from another rank. */

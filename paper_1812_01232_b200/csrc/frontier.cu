@@ -407,8 +407,14 @@ __global__ void cuboid_counts(const int8_t* split, const unsigned int* sel, size
 }
 
 // Route evaluated children (solver.cpp:396-405).
+// finish: children with a bound >= finish (the wave's limit d* - eps) are
+// finished for the certificate: no wave will expand them, and their only
+// effect on it is the minimum bound among those still below d* -- which is
+// the minimum over all of them, since pruning removes the largest first. They
+// go to the floor like unsplittable children instead of the pool (the
+// certificate min(d*, frontier min, floor) is unchanged).
 __global__ void route(gosma_node* kids, const double* lower, const int8_t* split,
-                      const double* kid_vol, size_t n, double dstar, int* keep,
+                      const double* kid_vol, size_t n, double dstar, double finish, int* keep,
                       RouteStats* stats) {
   const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
   double pv = 0.0, rv = 0.0;
@@ -419,7 +425,7 @@ __global__ void route(gosma_node* kids, const double* lower, const int8_t* split
     kids[i].lower = lo;
     if (!(lo < dstar)) {
       pv = kid_vol[i];
-    } else if (split[i] < 0) {
+    } else if (split[i] < 0 || !(lo < finish)) {
       rv = kid_vol[i];
       fl = order_key(lo);
     } else {
@@ -1271,7 +1277,7 @@ cudaError_t Frontier::improving_children(size_t n_kids, double bound, cudaStream
   return cudaSuccess;
 }
 
-cudaError_t Frontier::route_append(size_t n_kids, double dstar, cudaStream_t s,
+cudaError_t Frontier::route_append(size_t n_kids, double dstar, double finish, cudaStream_t s,
                                    RouteStats* out) {
   SubTimer tm(this, s);
   cudaError_t e;
@@ -1285,7 +1291,7 @@ cudaError_t Frontier::route_append(size_t n_kids, double dstar, cudaStream_t s,
   tm.lap(4);
   if (n_kids) {
     route<<<grid_for(n_kids, 256), 256, 0, s>>>(kids, kid_lower, kid_split, kid_vol, n_kids,
-                                                dstar, keep, stats);
+                                                dstar, finish, keep, stats);
     size_t need = 0;
     cub::CountingInputIterator<unsigned int> it(0);
     cub::DeviceSelect::Flagged(nullptr, need, it, keep, kept_idx, counter,

@@ -133,8 +133,10 @@ struct Frontier {
   size_t pmin_cap = 0;
   ImprovingChild* rec = nullptr;  // device record list (rec_cap entries, grown on demand)
   size_t rec_cap = 0;
-  // route children against d*, append survivors
-  cudaError_t route_append(size_t n_kids, double dstar, cudaStream_t s, RouteStats* out);
+  // route children against d* (prune) and finish (bound >= finish: to the
+  // floor with the unsplittable ones), append survivors
+  cudaError_t route_append(size_t n_kids, double dstar, double finish, cudaStream_t s,
+                           RouteStats* out);
   // drop holes and nodes with key >= limit; returns the dropped (non-hole) volume
   cudaError_t compact(unsigned long long limit, cudaStream_t s, double* dropped_volume);
   // keep the `keep_n` smallest keys (capacity folding); returns folded volume

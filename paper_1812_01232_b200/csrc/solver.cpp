@@ -952,7 +952,14 @@ int gosma_solver_expand(gosma_solver* S, double limit, unsigned long long max_ev
   }
   S->lap(4, s);
   RouteStats rs;
-  if ((e = S->F.route_append(n_kids, S->dstar(), s, &rs)) != cudaSuccess)
+  // children already finished for the certificate (bound >= limit = d* - eps)
+  // go to the floor instead of the pool (GOSMA_FINISH=0: keep them, A/B)
+  static const bool finish_on = [] {
+    const char* v = std::getenv("GOSMA_FINISH");
+    return !(v && std::string(v) == "0");
+  }();
+  const double finish = finish_on ? std::min(limit, S->dstar()) : kInf;
+  if ((e = S->F.route_append(n_kids, S->dstar(), finish, s, &rs)) != cudaSuccess)
     return cuda_error(e, "route");
   S->pruned_volume += rs.pruned_volume;
   S->resolved_volume += rs.resolved_volume;
