@@ -618,9 +618,11 @@ int solver_init(gosma_solver* S) {
     const double f = e ? std::atof(e) : 0.5;
     return f > 0.0 && f < 0.9 ? f : 0.5;
   }();
+  // (at least 64 waves' parents: a depth-first wave needs room for 32 W
+  // children, twice over for the fold target below)
   S->mem_cap = std::max<size_t>(static_cast<size_t>(pool_frac * static_cast<double>(free_b)) /
                                     per_node,
-                                16 * S->wave_nodes);
+                                64 * S->wave_nodes);
   S->F.cap_limit = S->mem_cap;
   S->qcap = cfg.queue_capacity >= 0
                 ? std::min<size_t>(static_cast<size_t>(cfg.queue_capacity), S->mem_cap)
@@ -818,7 +820,10 @@ int gosma_solver_status(gosma_solver* S, gosma_wave_status* st) {
       S->pruned_volume += dropped;
     }
     if (S->F.size + wave_room > S->mem_cap) {
-      const size_t target = drain_on ? S->mem_cap - 2 * wave_room : S->mem_cap * 3 / 4 - wave_room;
+      const size_t target = drain_on && S->mem_cap > 4 * wave_room
+                                ? S->mem_cap - 2 * wave_room
+                                : (S->mem_cap * 3 / 4 > 2 * wave_room ? S->mem_cap * 3 / 4 - wave_room
+                                                                      : S->mem_cap / 2);
       double fv = 0.0, fmin = kInf;
       if ((e = S->F.fold_to(target, s, &fv, &fmin)) != cudaSuccess) return cuda_error(e, "fold");
       S->resolved_volume += fv;

@@ -615,3 +615,31 @@ def test_discovery_dive_incumbent_matches_reference(gosma):
         # can only be lower; the dive's incumbent must match it where the
         # reference's loop did not improve on its own dive
         assert r.best_value <= ref["best_value"] + 1e-6 * abs(ref["best_value"]), (m["n1"], r.best_value, ref["best_value"])
+
+
+def _drain_probe(mode):
+    import json, os, subprocess, sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, GOSMA_POOL_FRAC="1e-9", GOSMA_PROFILE="1", MODE=mode, WAVE="256")
+    r = subprocess.run([sys.executable, os.path.join(root, "scripts", "drain_probe.py")],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = [l for l in r.stdout.splitlines() if l.startswith("{")][-1]
+    prof = [l for l in (r.stdout + r.stderr).splitlines() if "drain" in l and "folds" in l]
+    return json.loads(line), prof
+
+
+def test_depth_first_and_folds_under_a_tiny_pool_budget(gosma):
+    """GOSMA_POOL_FRAC=1e-9 caps the pool at 64 waves' parents (16384 nodes):
+    the waves go depth-first and the pool still folds. The volume ledger holds
+    every wave, the certified bound never decreases, and the 2x2 certify
+    instance ends sound (d* the reference's, LB below it) -- certified, or
+    with the queue exhausted when folding capped the certificate."""
+    res, prof = _drain_probe("ledger")
+    assert res["ledger_worst_rel"] <= 1e-9 and res["monotone"]
+    assert prof and " drain 0," not in prof[-1]  # depth-first waves ran
+    res, prof = _drain_probe("certify")
+    assert prof and " drain 0," not in prof[-1]
+    assert res["status"] in ("epsilon_optimal", "queue_exhausted")
+    assert abs(res["best_value"] - res["golden_best"]) <= res["epsilon"]
+    assert res["global_lower"] <= res["golden_best"] + 1e-9
