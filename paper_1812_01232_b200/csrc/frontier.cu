@@ -293,6 +293,20 @@ struct VolRange {
   }
 };
 
+// Live node below the limit (holes carry kHoleKey, which no limit reaches).
+struct KeyBelowLimit {
+  const unsigned long long* key;
+  unsigned long long limit;
+  __device__ __forceinline__ bool operator()(const unsigned int& i) const {
+    return key[i] < limit;
+  }
+};
+
+__global__ void iota_u32(unsigned int* out, unsigned int first, size_t n) {
+  const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+  if (i < n) out[i] = first + static_cast<unsigned int>(i);
+}
+
 // Appended children (slot < end, read on the device) whose key is below tau.
 struct NewCandidate {
   const unsigned long long* key;
@@ -765,6 +779,11 @@ void Frontier::release() {
   cand_n = cand_cap = 0;
   tau = 0;
   known_min = 0;
+  dfree(dstk);
+  dstk = nullptr;
+  dstk_cap = 0;
+  drop_deep();
+  deep_active = false;
   dfree(stats);
   dfree(counter);
   dfree(temp);
@@ -846,6 +865,7 @@ cudaError_t Frontier::grow(size_t need, cudaStream_t s) {
 
 cudaError_t Frontier::upload(const gosma_node* h_nodes, const int8_t* h_split,
                              const double* h_vol, size_t n, cudaStream_t s) {
+  drop_deep();
   cudaError_t e;
   if ((e = grow(size + n, s)) != cudaSuccess) return e;
   std::vector<unsigned long long> k(n);
@@ -1020,6 +1040,8 @@ struct SubTimer {
 
 cudaError_t Frontier::select_smallest(size_t want, unsigned long long limit, cudaStream_t s,
                                       size_t* n_out) {
+  deep_active = false;  // best-first again: the depth-first stack is refilled next time
+  drop_deep();
   SubTimer tm(this, s);
   *n_out = 0;
   if (size == 0 || want == 0) return cudaSuccess;
@@ -1102,11 +1124,13 @@ cudaError_t Frontier::select_smallest(size_t want, unsigned long long limit, cud
 // are max(core, parent)), so the order changes neither the work nor the
 // certificate, only the pool's peak size: depth-first keeps ~(8 W x depth)
 // nodes open. Full-pool radix descent on the volume bits (no candidate list).
-cudaError_t Frontier::select_deepest(size_t want, unsigned long long limit, cudaStream_t s,
-                                     size_t* n_out) {
+// The want_total deepest live nodes below the limit (one pool scan) into
+// out[0 .. *n_out): the smallest volumes; the boundary depth contributes its
+// first nodes in pool order.
+cudaError_t Frontier::deep_scan(size_t want_total, unsigned long long limit, cudaStream_t s,
+                                unsigned int* out, size_t* n_out) {
   *n_out = 0;
-  if (size == 0 || want == 0) return cudaSuccess;
-  want = std::min(want, sel_cap);
+  if (size == 0 || want_total == 0) return cudaSuccess;
   cudaError_t e;
   unsigned long long lo_key = 0, hi_key = kHoleKey;
   size_t below = 0, bin_count = 0;
@@ -1115,19 +1139,19 @@ cudaError_t Frontier::select_deepest(size_t want, unsigned long long limit, cuda
   // steps), so the first digit already separates depths; the nodes of one
   // depth share their volume bits, so refining the boundary bin would only
   // cost passes (the boundary depth contributes its first nodes in pool order)
-  if ((e = descend(want, limit, 0.0, s, &lo_key, &hi_key, &below, &bin_count, nullptr, size,
-                   vol)) != cudaSuccess)
+  if ((e = descend(want_total, limit, 0.0, s, &lo_key, &hi_key, &below, &bin_count, nullptr,
+                   size, vol)) != cudaSuccess)
     return e;
   cub::CountingInputIterator<unsigned int> it(0);
   size_t need = 0;
   VolRange p1{key, vol, 0ull, lo_key, limit};
-  cub::DeviceSelect::If(nullptr, need, it, sel, counter, static_cast<int>(size), p1, s);
+  cub::DeviceSelect::If(nullptr, need, it, out, counter, static_cast<int>(size), p1, s);
   if ((e = ensure_temp(need)) != cudaSuccess) return e;
   const size_t n1 = below;
-  if (n1 > 0) cub::DeviceSelect::If(temp, need, it, sel, counter, static_cast<int>(size), p1, s);
+  if (n1 > 0) cub::DeviceSelect::If(temp, need, it, out, counter, static_cast<int>(size), p1, s);
   size_t n2 = 0;
-  if (n1 < want && hi_key > lo_key && bin_count > 0) {
-    n2 = std::min(want - n1, bin_count);
+  if (n1 < want_total && hi_key > lo_key && bin_count > 0) {
+    n2 = std::min(want_total - n1, bin_count);
     if (bin_count > bsel_cap) {
       dfree(bsel);
       bsel = nullptr;
@@ -1137,10 +1161,62 @@ cudaError_t Frontier::select_deepest(size_t want, unsigned long long limit, cuda
     }
     VolRange p2{key, vol, lo_key, hi_key, limit};
     cub::DeviceSelect::If(temp, need, it, bsel, counter, static_cast<int>(size), p2, s);
-    if ((e = cudaMemcpyAsync(sel + n1, bsel, n2 * 4, cudaMemcpyDeviceToDevice, s)) != cudaSuccess)
+    if ((e = cudaMemcpyAsync(out + n1, bsel, n2 * 4, cudaMemcpyDeviceToDevice, s)) != cudaSuccess)
       return e;
   }
-  const size_t n = n1 + n2;
+  *n_out = n1 + n2;
+  return cudaGetLastError();
+}
+
+cudaError_t Frontier::select_deepest(size_t want, unsigned long long limit, cudaStream_t s,
+                                     size_t* n_out) {
+  *n_out = 0;
+  deep_active = true;
+  if (size == 0 || want == 0) return cudaSuccess;
+  want = std::min(want, sel_cap);
+  cudaError_t e;
+  static const bool use_stack = [] {  // GOSMA_DEEP_STACK=0: scan every wave (A/B)
+    const char* v = std::getenv("GOSMA_DEEP_STACK");
+    return !(v && std::string(v) == "0");
+  }();
+  size_t n = 0;
+  if (!use_stack) {
+    if ((e = deep_scan(want, limit, s, sel, &n)) != cudaSuccess) return e;
+  } else {
+    for (int attempt = 0; attempt < 4 && n == 0; ++attempt) {
+      if (!dstk_ok || dstk_n == 0) {
+        // refill: the 8 waves' worth deepest live nodes (one pool scan)
+        const size_t fill = 8 * want;
+        const size_t cap_need = fill + 32 * want;  // room for the pushed children
+        if (cap_need > dstk_cap) {
+          dfree(dstk);
+          dstk = nullptr;
+          dstk_cap = 0;
+          if ((e = dmalloc(&dstk, cap_need * 4)) != cudaSuccess) return e;
+          dstk_cap = cap_need;
+        }
+        ++deep_fills;
+        if ((e = deep_scan(fill, limit, s, dstk, &dstk_n)) != cudaSuccess) return e;
+        dstk_ok = true;
+        if (dstk_n == 0) break;  // nothing live below the limit
+      }
+      // pop the top window (the most recently pushed, i.e. deepest, nodes);
+      // entries that became holes or stale since they were pushed drop out
+      const size_t w = std::min(want, dstk_n);
+      KeyBelowLimit pk{key, limit};
+      size_t need = 0;
+      cub::DeviceSelect::If(nullptr, need, dstk + (dstk_n - w), sel, counter,
+                            static_cast<int>(w), pk, s);
+      if ((e = ensure_temp(need)) != cudaSuccess) return e;
+      cub::DeviceSelect::If(temp, need, dstk + (dstk_n - w), sel, counter, static_cast<int>(w),
+                            pk, s);
+      if ((e = cudaMemcpyAsync(h_counter, counter, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+        return e;
+      if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+      n = static_cast<size_t>(*reinterpret_cast<int*>(h_counter));
+      dstk_n -= w;
+    }
+  }
   if (n) {
     mark_holes<<<grid_for(n, 256), 256, 0, s>>>(key, sel, n);
     holes += n;
@@ -1180,6 +1256,7 @@ cudaError_t Frontier::gather_selected(size_t n, cudaStream_t s, gosma_node* out_
 
 cudaError_t Frontier::upload_device(const gosma_node* d_nodes, const int8_t* d_split,
                                     const double* d_vol, size_t n, cudaStream_t s) {
+  drop_deep();
   cudaError_t e;
   if ((e = grow(size + n, s)) != cudaSuccess) return e;
   e = cudaMemcpyAsync(nodes + size, d_nodes, n * sizeof(gosma_node), cudaMemcpyDeviceToDevice, s);
@@ -1324,9 +1401,21 @@ cudaError_t Frontier::route_append(size_t n_kids, double dstar, double finish, c
   tm.lap(5);
   *out = *h_stats;
   if (n_kids) {
-    size += static_cast<size_t>(*reinterpret_cast<int*>(h_counter));
+    const size_t kept = static_cast<size_t>(*reinterpret_cast<int*>(h_counter));
+    // depth-first waves: the kept children (the deepest nodes) go on top of
+    // the stack, so the next wave pops them without a pool scan
+    if (deep_active && dstk_ok && kept) {
+      if (dstk_n + kept <= dstk_cap) {
+        iota_u32<<<grid_for(kept, 256), 256, 0, s>>>(dstk + dstk_n,
+                                                     static_cast<unsigned int>(size), kept);
+        dstk_n += kept;
+      } else {
+        drop_deep();
+      }
+    }
+    size += kept;
     kids_total += n_kids;
-    kids_kept += static_cast<size_t>(*reinterpret_cast<int*>(h_counter));
+    kids_kept += kept;
     if (tau != 0) cand_n += static_cast<size_t>(*reinterpret_cast<int*>(h_counter + 1));
   }
   return cudaGetLastError();
@@ -1336,6 +1425,7 @@ cudaError_t Frontier::route_append(size_t n_kids, double dstar, double finish, c
 // holes (their volume is returned), then the live tail is moved into the head
 // holes; no reallocation, traffic proportional to the moved nodes.
 cudaError_t Frontier::compact(unsigned long long limit, cudaStream_t s, double* dropped) {
+  drop_deep();  // slots move
   *dropped = 0.0;
   if (size == 0) return cudaSuccess;
   cudaError_t e;
@@ -1401,6 +1491,7 @@ cudaError_t Frontier::live_volume(cudaStream_t s, double* out) {
 
 cudaError_t Frontier::fold_to(size_t keep_n, cudaStream_t s, double* folded_volume,
                               double* folded_min) {
+  drop_deep();  // slots move
   *folded_volume = 0.0;
   *folded_min = INFINITY;
   double none = 0.0;

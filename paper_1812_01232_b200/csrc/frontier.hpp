@@ -62,6 +62,16 @@ struct Frontier {
   size_t cand_n = 0, cand_cap = 0;
   unsigned long long tau = 0;
   unsigned long long rebuilds = 0;  // candidate-list rebuilds (profiling)
+  // depth-first stack (select_deepest): pool indices of deep live nodes, the
+  // kept children of each depth-first wave pushed on top, so a wave pops the
+  // deepest nodes without scanning the pool; refilled by one scan when short,
+  // dropped whenever pool indices move (compaction, folds, imports) or the
+  // waves go best-first again
+  unsigned int* dstk = nullptr;
+  size_t dstk_n = 0, dstk_cap = 0;
+  bool dstk_ok = false, deep_active = false;
+  unsigned long long deep_fills = 0;  // stack refills (profiling)
+  void drop_deep() { dstk_ok = false; dstk_n = 0; }
   bool prof = false;                // synchronising sub-phase timers
   double t_sub[6] = {0, 0, 0, 0, 0, 0};  // rebuild, descend, pick, list; grow, route
   size_t max_bin = 0, max_cand = 0;
@@ -112,6 +122,8 @@ struct Frontier {
   cudaError_t select_smallest(size_t want, unsigned long long limit, cudaStream_t s, size_t* n);
   // depth-first order under memory pressure: the smallest volumes below limit
   cudaError_t select_deepest(size_t want, unsigned long long limit, cudaStream_t s, size_t* n);
+  cudaError_t deep_scan(size_t want_total, unsigned long long limit, cudaStream_t s,
+                        unsigned int* out, size_t* n_out);
   cudaError_t expand_selected(size_t n_sel, cudaStream_t s);
   cudaError_t expand_selected_cached(size_t n_sel, cudaStream_t s, size_t* n_cuboids);
   // rotation-split selections (rot_list) and translation-split children (trans_list)
